@@ -1,0 +1,417 @@
+"""CPU tests pinning the oracle (oracle/) to things other than itself.
+
+Pins, per DESIGN.md section 3:
+  * published values: Random123 Philox KAT (tests/golden/philox_kat.txt);
+  * worked examples: tests/golden/worked_examples.json (hand-worked with exact
+    rationals), MAPE examples (Eq. 1);
+  * an independent implementation: oracle/micro.py (pure Python, exact
+    Fractions, SSE-reduction criterion, depth-first growth, decimal ln);
+  * library routines: sklearn DecisionTreeRegressor on tie-free data,
+    decimal ln, Python big-int mulhi;
+  * invariants / closed forms: fits-exactly, range, constant target,
+    node bound 2D-1, leaf row partition, forest mean, prefix forests,
+    twin-row CV = 0, LOO cardinality, fold partitions, F rule.
+"""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from oracle import micro
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ RNG ---
+def _kat():
+    rows = []
+    for line in open(os.path.join(GOLD, "philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        rows.append((v[0:4], v[4:6], v[6:10]))
+    return rows
+
+
+@pytest.mark.parametrize("ctr,key,out", _kat())
+def test_philox_kat(ctr, key, out):
+    assert [int(x) for x in oracle.philox(ctr, key)] == out
+    assert micro.philox(ctr, key) == out
+
+
+def test_draw_and_mulhi():
+    rnd = random.Random(1)
+    for _ in range(2000):
+        u = rnd.getrandbits(64)
+        m = rnd.randrange(1, 1 << 40)
+        assert oracle.mulhi64(u, m) == (u * m) >> 64
+    for i in range(50):
+        k0, k1, c1, c2, c3 = (rnd.getrandbits(32) for _ in range(5))
+        assert oracle.draw(k0, k1, c1, c2, c3, i) == micro.draw([k0, k1], c1, c2, c3, i)
+    for task in range(5):
+        for t in range(5):
+            assert list(oracle.tree_key(7104, task, t)) == micro.tree_key(7104, task, t)
+
+
+# ------------------------------------------------------- target + F rule ---
+def test_ln_correctly_rounded():
+    rnd = random.Random(3)
+    vals = [1.0, 2.0, math.e, 0.5, 1e-300, 1e300, 7.0, 1000.0, 100000.0]
+    vals += [10 ** rnd.uniform(-3, 9) for _ in range(3000)]
+    for v in vals:
+        assert oracle.ln(v) == micro.ln_cr(v), v
+
+
+def test_quantize_F_rule_closed_form():
+    # n = 4, M = 7 -> e(M) = 3, ceil(log2 4) = 2 -> F = 62 - 2 - 3 = 57 (R7)
+    t, tq, F = oracle.quantize([1.0, 2.0, 6.0, 7.0], 0)
+    assert F == 57
+    assert list(tq) == [1 << 57, 2 << 57, 6 << 57, 7 << 57]
+    # M exactly a power of two: e(8) = 3
+    _, _, F = oracle.quantize([8.0, -1.0, 0.5], 0)
+    assert F == 62 - 2 - 3
+    _, _, F = oracle.quantize([0.0, 0.0], 0)
+    assert F == 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_quantize_vs_exact(seed):
+    X, y = datagen.tiny(37, 2, seed)
+    for target in (0, 1):
+        yy = y if target == 1 else y - 1.3
+        t, tq, F = oracle.quantize(yy, target)
+        t2, tq2, F2 = micro.quantize(list(yy), target)
+        assert F == F2 and list(tq) == tq2 and list(t) == t2
+        # |sum| bound that makes int64 sums exact: n * max|tq| <= 2^62
+        assert len(yy) * int(np.abs(tq).max()) <= 1 << 62
+
+
+# ----------------------------------------------------------------- folds ---
+@pytest.mark.parametrize("n,k", [(189, 10), (168, 10), (10, 10), (23, 4), (7, 2)])
+def test_plain_folds_partition(n, k):
+    y = np.ones(n)
+    f = oracle.make_folds(y, k, 3, seed=5)
+    for rep in range(3):
+        counts = np.bincount(f[rep], minlength=k)
+        assert counts.sum() == n and counts.min() >= n // k and counts.max() <= n // k + 1
+        assert sorted(counts.tolist(), reverse=True) == counts.tolist()  # first n mod k folds larger
+    assert not np.array_equal(f[0], f[1]) or n <= 2
+
+
+def test_plain_folds_loo():
+    # k = n is leave-one-out
+    f = oracle.make_folds(np.ones(13), 13, 1, seed=2)
+    assert sorted(f[0].tolist()) == list(range(13))
+
+
+def test_custom_split_example_S372():
+    # 30 short + 30 medium + 30 long + 5 pinned, k = 5 -> 6 of each class per test fold
+    rnd = np.random.default_rng(0)
+    y = np.concatenate([rnd.uniform(1, 999, 30), rnd.uniform(1000, 99999, 30),
+                        rnd.uniform(100001, 1e6, 30), [5e7, 6e7, 7e7, 8e7, 9e7]])
+    rnd.shuffle(y)
+    f = oracle.make_folds(y, 5, 2, seed=11, custom=True)
+    cls = np.where(y < 1000, 0, np.where(y < 100000, 1, 2))
+    top5 = np.argsort(-y, kind="stable")[:5]
+    for rep in range(2):
+        assert (f[rep][top5] == -1).all() and (f[rep] == -1).sum() == 5
+        for fold in range(5):
+            m = f[rep] == fold
+            assert [int((cls[m] == c).sum()) for c in range(3)] == [6, 6, 6]
+
+
+def test_custom_split_balance_and_errors():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    f = oracle.make_folds(y, 10, 4, seed=3, custom=True)
+    cls = np.where(y < 1000, 0, np.where(y < 100000, 1, 2))
+    top5 = np.argsort(-y, kind="stable")[:5]
+    for rep in range(4):
+        assert (f[rep][top5] == -1).all()
+        sizes = np.bincount(f[rep][f[rep] >= 0], minlength=10)
+        assert sizes.max() - sizes.min() <= 1
+        for c in range(3):
+            per = [int(((f[rep] == fold) & (cls == c) & (f[rep] >= 0)).sum()) for fold in range(10)]
+            assert max(per) - min(per) <= 2
+    with pytest.raises(oracle.OracleError):
+        oracle.make_folds(np.ones(6), 5, 1, seed=0, custom=True)  # S:371 TooFewSamples
+
+
+# ------------------------------------------------------- worked examples ---
+def test_worked_examples():
+    ex = json.load(open(os.path.join(GOLD, "worked_examples.json")))
+    A = ex["A"]
+    f = oracle.fit(np.array(A["X"], float), np.array(A["y"], float), ntree=1, mtry=2,
+                   bootstrap=False, leaf_rows=True)
+    t = f.trees[0]
+    assert f.F == A["F"]
+    assert t.feature.tolist() == A["feature"]
+    assert t.thr_value.tolist() == A["thr_value"]
+    assert t.thr_index.tolist() == A["thr_index"]
+    assert t.left.tolist() == A["left"]
+    assert t.leaf_value.tolist() == A["leaf_value"]
+    assert t.leaf_of_row.tolist() == A["leaf_of_row"]
+    assert oracle.predict(f, np.array([A["query"]]))[0] == A["query_pred"]
+    B = ex["B"]
+    t = oracle.fit(np.array(B["X"], float), np.array(B["y"], float), ntree=1, mtry=1,
+                   bootstrap=False).trees[0]
+    for key in ("feature", "thr_value", "thr_index", "left", "leaf_value"):
+        assert getattr(t, key).tolist() == B[key], key
+    Cx = ex["C"]
+    t = oracle.fit(np.array(Cx["X"], float), np.array(Cx["y"], float), ntree=1, mtry=1,
+                   bootstrap=False).trees[0]
+    assert t.feature.tolist() == Cx["feature"] and t.leaf_value.tolist() == Cx["leaf_value"]
+
+
+def test_example_A_root_gains_exact():
+    # exact SSE reductions of the six root candidates (Appendix C) from the micro oracle
+    from fractions import Fraction
+    ex = json.load(open(os.path.join(GOLD, "worked_examples.json")))["A"]
+    X, y = ex["X"], ex["y"]
+    w = [1] * 4
+    S2W = Fraction(16 ** 2, 4)
+    tot = sum(Fraction(v) ** 2 for v in y)
+    for name, G in ex["root_candidates_G"].items():
+        f, thr = int(name[1]), int(name[-1])
+        L = [i for i in range(4) if X[i][f] <= thr]
+        R = [i for i in range(4) if X[i][f] > thr]
+        red = micro.sse(list(range(4)), w, y) - micro.sse(L, w, y) - micro.sse(R, w, y)
+        # SSE reduction = G - S^2/W
+        assert red == Fraction(G) - S2W
+        assert tot - micro.sse(list(range(4)), w, y) == S2W
+
+
+# ------------------------------------- independent micro implementation ---
+CASES = [  # n, p, mtry, distinct, bootstrap, max_depth, target, hist
+    (14, 3, 2, 5, True, -1, 0, False),
+    (12, 4, 4, None, False, -1, 1, False),
+    (20, 2, 1, 3, True, -1, 0, False),
+    (25, 3, 3, 4, True, 3, 1, False),
+    (18, 3, 2, None, True, -1, 0, True),
+    (22, 2, 2, 6, False, -1, 0, True),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("seed", range(8))
+def test_oracle_equals_micro(case, seed):
+    n, p, m, dist, boot, md, target, hist = case
+    X, y = datagen.tiny(n, p, seed, distinct=dist)
+    fo = oracle.fit(X, y, ntree=3, mtry=m, seed=seed, bootstrap=boot, max_depth=md,
+                    target=target, split_mode=1 if hist else 0)
+    for t in range(3):
+        tr = fo.trees[t]
+        mt, F = micro.fit_tree(X, y, t, m, seed=seed, boot=boot, target=target, max_depth=md,
+                               hist=hist)
+        assert F == fo.F
+        for key in ("feature", "thr_index", "thr_value", "left"):
+            assert getattr(tr, key).tolist() == mt[key], key
+        # leaf value: oracle = fl(d(S)/d(W)) 2^-F; micro = exact S/W rounded once
+        a, b = tr.leaf_value, np.array(mt["leaf_value"])
+        np.testing.assert_allclose(a, b, rtol=2.3e-16, atol=0)
+        for nd in mt["nodes"]:
+            if nd.gain_exact_best is not None:  # chosen split maximises the exact SSE reduction
+                assert nd.gain_exact_chosen >= nd.gain_exact_best * (1 - 1e-12)
+
+
+def test_cv_task_keys_match_micro():
+    # CV task (rep, fold) trees use key (seed, task, t) and the task's training rows
+    X, y = datagen.tiny(16, 3, 4, distinct=6)
+    fids = oracle.make_folds(y, 4, 1, seed=9)
+    fm, pred = oracle.cv_grid(X, y, 4, 1, [2], [2], fold_ids=fids, seed=9, want_pred=True)
+    for fold in range(4):
+        tr = [i for i in range(16) if fids[0][i] != fold]
+        te = [i for i in range(16) if fids[0][i] == fold]
+        s = np.zeros(len(te))
+        for t in range(2):
+            mt, F = micro.fit_tree(X, y, t, 2, seed=9, task=fold, train_rows=tr)
+            # traverse micro tree
+            for j, r in enumerate(te):
+                i = 0
+                while mt["feature"][i] >= 0:
+                    i = mt["left"][i] if X[r][mt["feature"][i]] <= mt["thr_value"][i] else mt["left"][i] + 1
+                s[j] += mt["leaf_value"][i]
+        np.testing.assert_allclose(pred[0, 0, 0, te], s / 2, rtol=1e-14)
+        ex = float(micro.mape_exact(y[te], pred[0, 0, 0, te]))
+        assert abs(fm[0, 0, 0, fold] - ex) <= 1e-12 * max(ex, 1e-300)
+
+
+# ----------------------------------------------------------- invariants ---
+def _unique_rows(X, y):
+    _, idx = np.unique(X, axis=0, return_index=True)
+    idx = np.sort(idx)
+    return X[idx], y[idx]
+
+
+@pytest.mark.parametrize("target", [0, 1])
+def test_fits_exactly(target):
+    X, y = _unique_rows(*datagen.paper_shaped(189, "V100", "time"))
+    f = oracle.fit(X, y, ntree=1, mtry=X.shape[1], bootstrap=False, target=target)
+    t, tq, F = oracle.quantize(y, target)
+    tr = f.trees[0]
+    got = np.array([tr.predict_row(x) for x in X])
+    want = np.ldexp(tq.astype(np.float64), -F)
+    assert np.array_equal(got, want)
+    # number of leaves = number of rows (every row isolated)
+    assert int((tr.feature < 0).sum()) == X.shape[0]
+
+
+def test_range_property():
+    X, y = datagen.paper_shaped(189, "P100", "power")
+    f = oracle.fit(X, y, ntree=20, mtry=4, seed=1)
+    Q = datagen.paper_shaped(300, "P100", "power", seed=5)[0]
+    yh = oracle.predict(f, Q)
+    assert yh.min() >= y.min() and yh.max() <= y.max()  # P:748 / P:479
+
+
+def test_constant_target_single_leaf():
+    X, _ = datagen.tiny(30, 4, 0)
+    f = oracle.fit(X, np.full(30, 3.25), ntree=5, mtry=2, seed=3)
+    for t in f.trees:
+        assert t.n_nodes == 1 and t.feature[0] == -1 and t.leaf_value[0] == 3.25
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_node_bound_leaf_partition_depth(seed):
+    X, y = datagen.paper_shaped(189, "TitanXp", "time", seed=seed + 100)
+    for md in (-1, 4):
+        f = oracle.fit(X, y, ntree=6, mtry=3, seed=seed, leaf_rows=True, max_depth=md, target=1)
+        for t in f.trees:
+            inbag = np.nonzero(t.leaf_of_row >= 0)[0]
+            Xin = X[inbag]
+            D = len(np.unique(Xin, axis=0)) if md < 0 else len(inbag)
+            assert t.n_nodes <= 2 * len(inbag) - 1
+            leaves = set(np.nonzero(t.feature < 0)[0].tolist())
+            assert set(t.leaf_of_row[inbag].tolist()) == leaves  # every leaf holds >= 1 in-bag row
+            for r in inbag:  # each in-bag row routes to its recorded leaf
+                i = 0
+                while t.feature[i] >= 0:
+                    i = int(t.left[i]) + (0 if X[r, t.feature[i]] <= t.thr_value[i] else 1)
+                assert i == t.leaf_of_row[r]
+            if md >= 0:
+                assert t.max_depth() <= md
+            del D
+
+
+def test_bootstrap_distinct_fraction():
+    # E[distinct]/n = 1 - (1 - 1/n)^n (closed form), statistical
+    X, y = datagen.tiny(170, 2, 1)
+    f = oracle.fit(X, y, ntree=400, mtry=1, seed=17, leaf_rows=True, max_depth=0)
+    frac = np.mean([(t.leaf_of_row >= 0).mean() for t in f.trees])
+    expect = 1 - (1 - 1 / 170) ** 170
+    assert abs(frac - expect) < 0.004
+
+
+def test_forest_mean_and_prefix():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    f16 = oracle.fit(X, y, ntree=16, mtry=3, seed=5, target=1)
+    f8 = oracle.fit(X, y, ntree=8, mtry=3, seed=5, target=1)
+    shard = oracle.fit(X, y, ntree=16, mtry=3, seed=5, target=1, tree_begin=8, tree_end=16)
+    for a, b in zip(f8.trees + shard.trees, f16.trees):
+        assert a.feature.tolist() == b.feature.tolist() and a.leaf_value.tolist() == b.leaf_value.tolist()
+    Q = datagen.paper_shaped(50, "K20", "time", seed=9)[0]
+    yh = oracle.predict(f16, Q)
+    man = []
+    for q in Q:
+        acc = 0.0
+        for t in f16.trees:  # sequential, in tree order (Python's sum() is compensated)
+            acc += t.predict_row(q)
+        man.append(math.exp(acc / 16))
+    np.testing.assert_allclose(yh, man, rtol=1e-15)
+    # T = 1 forest is the tree
+    f1 = oracle.Forest([f16.trees[3]], f16.F, 0)
+    assert oracle.predict(f1, Q[:5]).tolist() == [f16.trees[3].predict_row(q) for q in Q[:5]]
+
+
+def test_forest_mean_two_leaves_S289():
+    mk = lambda v: oracle.Tree(np.array([-1], np.int32), np.zeros(1, np.uint32), np.zeros(1),
+                               np.zeros(1, np.uint32), np.array([v]))
+    assert oracle.predict(oracle.Forest([mk(4.0), mk(6.0)], 0, 0), np.zeros((1, 3)))[0] == 5.0
+    assert oracle.predict(oracle.Forest([mk(7.0)], 0, 0), np.ones((2, 3))).tolist() == [7.0, 7.0]
+
+
+def test_mape_examples():
+    g = json.load(open(os.path.join(GOLD, "mape_examples.json")))
+    for c in g["cases"]:
+        assert oracle.mape(c["y"], c["yhat"]) == pytest.approx(c["mape"], abs=1e-12)
+
+
+# ------------------------------------------------------------------- CV ---
+def test_twin_row_cv_is_zero():
+    X, y = datagen.tiny(20, 3, 8)
+    X = np.round(X * 1000)
+    _, y = _unique_rows(X, y)
+    X, _ = _unique_rows(X, y)
+    n = X.shape[0]
+    y = np.round(y * 64) / 64 + 1  # on the 2^-F grid, positive
+    X2 = np.concatenate([X, X])
+    y2 = np.concatenate([y, y])
+    f = np.zeros((1, 2 * n), np.int32)
+    f[0, :n] = np.arange(n) % 4
+    f[0, n:] = (np.arange(n) + 1) % 4
+    fm = oracle.cv_grid(X2, y2, 4, 1, [3], [3], fold_ids=f, bootstrap=False, seed=1)
+    assert (fm == 0.0).all()
+
+
+def test_cv_grid_prefix_and_duplicate_mtry():
+    X, y = datagen.paper_shaped(60, "K20", "time", seed=3)
+    big = oracle.cv_grid(X, y, 5, 2, [2, 4], [3, 12, 3], target=1, seed=4)
+    small = oracle.cv_grid(X, y, 5, 2, [2], [3], target=1, seed=4)
+    assert np.array_equal(big[0, 0], small[0, 0])
+    assert np.array_equal(big[0], big[2])
+    assert np.isfinite(big).all()
+
+
+def test_cv_loo_and_shards():
+    X, y = datagen.tiny(12, 2, 3)
+    fm, pred = oracle.cv_grid(X, y, 12, 1, [3], [2], seed=2, want_pred=True)
+    assert np.isfinite(pred).all() and fm.shape == (1, 1, 1, 12)
+    part = oracle.cv_grid(X, y, 12, 1, [3], [2], seed=2, task_begin=3, task_end=7)
+    assert np.array_equal(part[0, 0, 0, 3:7], fm[0, 0, 0, 3:7])
+    assert np.isnan(part[0, 0, 0, :3]).all()
+
+
+def test_errors():
+    X = np.ones((3, 2))
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit(np.zeros((0, 2)), np.zeros(0))
+    assert e.value.code == 2
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit(np.array([[np.nan, 1.0]]), np.ones(1), mtry=1)
+    assert e.value.code == 3
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.fit(X, np.array([1.0, -1.0, 2.0]), mtry=1, target=1)
+    assert e.value.code == 4
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.cv_grid(X, np.ones(3), 4, 1, [1], [1])
+    assert e.value.code == 6
+
+
+# ------------------------------------------------- hist mode + library ---
+def test_hist_equals_exact_when_few_distinct():
+    X, y = datagen.tiny(300, 5, 2, distinct=40)
+    fe = oracle.fit(X, y, ntree=4, mtry=3, seed=6, leaf_rows=True)
+    fh = oracle.fit(X, y, ntree=4, mtry=3, seed=6, leaf_rows=True, split_mode=1)
+    for a, b in zip(fe.trees, fh.trees):
+        for key in ("feature", "thr_index", "left", "leaf_value", "leaf_of_row"):
+            assert getattr(a, key).tolist() == getattr(b, key).tolist(), key
+
+
+def test_sklearn_structure_advisory():
+    sk = pytest.importorskip("sklearn.tree")
+    rnd = np.random.default_rng(4)
+    n = 60
+    X = np.stack([rnd.permutation(n), rnd.permutation(n)], 1).astype(np.float64)  # fp32-exact, tie-free
+    y = rnd.normal(size=n) * 10 + 50
+    tr = oracle.fit(X, y, ntree=1, mtry=2, bootstrap=False, leaf_rows=True).trees[0]
+    reg = sk.DecisionTreeRegressor(max_features=None, random_state=0).fit(X, y)
+    # identical partition of the training rows into leaves
+    a = tr.leaf_of_row
+    b = reg.apply(X)
+    pairs = set(zip(a.tolist(), b.tolist()))
+    assert len(pairs) == len(set(a.tolist())) == len(set(b.tolist()))
+    np.testing.assert_allclose([tr.predict_row(x) for x in X], reg.predict(X), rtol=1e-12)
