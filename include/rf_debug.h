@@ -1,0 +1,21 @@
+/*
+ * rf_debug.h -- test hooks of librfgpu.so (parity tests only; not part of the
+ * modelling API).  Same conventions as rf.h: device pointers, stream as void*.
+ */
+#ifndef RF_DEBUG_H
+#define RF_DEBUG_H
+#include <stdint.h>
+#include "rf.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* dout[i] = ln(dy[i]) correctly rounded to binary64, dy[i] > 0 finite
+   (the target transform of P:631-632 as read in DESIGN.md R20). */
+RF_API rf_status rf_debug_ln_dev(const double* dy, double* dout, uint64_t n, void* stream);
+/* Philox4x32-10 (R14): for each i, dctr_key[6i..6i+5] =
+   (c0, c1, c2, c3, k0, k1) -> dout[4i..4i+3]. */
+RF_API rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, uint64_t n, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,823 @@
+// api.cu -- the C ABI of librfgpu.so (include/rf.h): argument validation,
+// device memory, orchestration of the kernels, host<->device copies.
+// Every compute step runs in this library's CUDA kernels; there is no CPU
+// fallback (without a device every call returns RF_E_CUDA).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/rf.h"
+#include "../../include/rf_debug.h"
+#include "common.cuh"
+#include "cv.cuh"
+#include "large_tree.cuh"
+#include "predict.cuh"
+#include "prep.cuh"
+#include "small_tree.cuh"
+#include "host_util.cuh"
+
+struct rf_forest {
+  int device = 0;
+  uint32_t ntree = 0, p = 0, target = 0;
+  int32_t F = 0;
+  uint64_t total_nodes = 0;
+  rf::Node16* nodes = nullptr;   // device
+  uint32_t* thr_index = nullptr; // device
+  uint64_t* tree_off = nullptr;  // device [ntree + 1]
+  std::vector<uint64_t> h_tree_off;
+  int32_t* leaf_of_row = nullptr;  // device [ntree][n_rows] (debug fits)
+  uint64_t n_rows = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+thread_local std::vector<ProfRec> g_prof;
+thread_local bool g_prof_on = false;
+using rf::ProfScope;
+using rf::Scratch;
+
+rf_status fail(rf_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+rf_status cuda_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) return fail(RF_E_OOM, std::string(where) + ": out of device memory");
+  return fail(RF_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                              \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+cudaStream_t host_stream(int device) {
+  static thread_local std::vector<cudaStream_t> streams;
+  if ((int)streams.size() <= device) streams.resize(device + 1, nullptr);
+  if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  return streams[device];
+}
+
+rf_status check_device() {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess || cnt == 0) return fail(RF_E_CUDA, "no CUDA device available (no CPU fallback)");
+  return RF_OK;
+}
+
+rf_status check_params(const rf_params* prm, uint32_t p, uint32_t* mtry_out) {
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  if (prm->struct_size != sizeof(rf_params)) return fail(RF_E_ARG, "rf_params.struct_size mismatch");
+  if (p == 0) return fail(RF_E_ARG, "p must be >= 1");
+  if (p > (uint32_t)rf::kSmallMaxP && p > 4096) return fail(RF_E_ARG, "p too large");
+  if (prm->min_samples_split < 2) return fail(RF_E_ARG, "min_samples_split must be >= 2");
+  if (prm->max_depth < -1) return fail(RF_E_ARG, "max_depth must be >= -1");
+  if (prm->split_mode > 1 || prm->target > 1) return fail(RF_E_ARG, "bad split_mode/target");
+  uint32_t m = prm->mtry ? prm->mtry : std::max<uint32_t>(1, p / 3);
+  if (m > p) return fail(RF_E_ARG, "mtry must be <= p");
+  if (mtry_out) *mtry_out = m;
+  return RF_OK;
+}
+
+rf_status read_err(const int* derr, cudaStream_t s) {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, s), "err flag");
+  CK(cudaStreamSynchronize(s), "sync");
+  if (h & rf::kErrNonFinite) return fail(RF_E_NONFINITE, "non-finite value in X or y");
+  if (h & rf::kErrNonPositive) return fail(RF_E_NONPOSITIVE_Y, "y <= 0 (LOG target or CV / MAPE)");
+  if (h & rf::kErrOverflow) return fail(RF_E_OVERFLOW, "kernel size limit exceeded");
+  return RF_OK;
+}
+
+// dataset on device: canonical X, t_q, F, presort
+rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, int target,
+                  int require_pos, bool need_sort, rf::DevData& d, Scratch& sc, cudaStream_t s) {
+  d.n = (int)n;
+  d.p = (int)p;
+  CK(sc.alloc(&d.X, n * p), "alloc X");
+  CK(sc.alloc(&d.tq, n), "alloc tq");
+  CK(sc.alloc(&d.F, 1), "alloc F");
+  CK(sc.alloc(&d.err, 1), "alloc err");
+  CK(cudaMemsetAsync(d.err, 0, sizeof(int), s), "memset");
+  double* t;
+  CK(sc.alloc(&t, n + 2), "alloc t");
+  {
+    ProfScope ps("prep", s);
+    CK(rf::prep_targets(dX, dy, (int)n, (int)p, target, require_pos, d, t, s), "prep");
+  }
+  if (need_sort) {
+    CK(sc.alloc(&d.order, n * p), "alloc order");
+    CK(sc.alloc(&d.grank, n * p), "alloc grank");
+    size_t wsb = rf::presort_ws_bytes((int)n, (int)p);
+    void* ws = nullptr;
+    if (wsb) CK(sc.alloc(reinterpret_cast<char**>(&ws), wsb), "alloc presort ws");
+    ProfScope ps("presort", s);
+    CK(rf::presort(d, ws, wsb, s), "presort");
+  }
+  return RF_OK;
+}
+
+int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
+
+int resident_warps(size_t smem_block, int wpb) {
+  int per_sm = (int)std::min<size_t>(32, (227 * 1024) / std::max<size_t>(smem_block, 1));
+  per_sm = std::min(per_sm, 64 / std::max(wpb, 1));
+  return 148 * per_sm * wpb;
+}
+
+struct GridPlan {
+  std::vector<int> mtry_distinct;
+  std::vector<int> mtry_map;  // requested index -> distinct index
+};
+
+GridPlan plan_mtry(const uint32_t* mtrys, uint32_t n_mtry) {
+  GridPlan g;
+  for (uint32_t i = 0; i < n_mtry; ++i) {
+    int m = (int)mtrys[i];
+    auto it = std::find(g.mtry_distinct.begin(), g.mtry_distinct.end(), m);
+    if (it == g.mtry_distinct.end()) {
+      g.mtry_map.push_back((int)g.mtry_distinct.size());
+      g.mtry_distinct.push_back(m);
+    } else {
+      g.mtry_map.push_back((int)(it - g.mtry_distinct.begin()));
+    }
+  }
+  return g;
+}
+
+// Core of CV: fills fold_mape/pred (partial_rows == null) or per-row partial sums.
+rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                  uint32_t k, uint32_t reps, const int32_t* dfold_in, const uint32_t* ntrees,
+                  uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry, double* dfold_mape,
+                  double* dpred, double* dpartial_rows, cudaStream_t s) {
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (k < 2 || k > n) return fail(RF_E_TOO_FEW, "need 2 <= k <= n");
+  if (reps == 0) return fail(RF_E_ARG, "repeats must be >= 1");
+  if (n_ntree == 0 || n_ntree > 16 || n_mtry == 0 || n_mtry > (uint32_t)rf::kMaxMtry)
+    return fail(RF_E_ARG, "grid sizes: 1..16 ntree values, 1..16 mtry values");
+  if (n > 0x7FFFFFFF) return fail(RF_E_ARG, "n too large");
+  rf_status st = check_params(prm, p, nullptr);
+  if (st) return st;
+  int Tmax = 0;
+  for (uint32_t i = 0; i < n_ntree; ++i) {
+    if (ntrees[i] == 0) return fail(RF_E_ARG, "ntree values must be >= 1");
+    Tmax = std::max(Tmax, (int)ntrees[i]);
+  }
+  for (uint32_t i = 0; i < n_mtry; ++i)
+    if (mtrys[i] == 0 || mtrys[i] > p) return fail(RF_E_ARG, "mtry values must be in 1..p");
+  int tree_lo = 0, tree_hi = Tmax;
+  if (prm->tree_begin || prm->tree_end) {
+    if (!dpartial_rows) return fail(RF_E_ARG, "tree sharding needs rf_cv_partial_dev");
+    tree_lo = (int)prm->tree_begin;
+    tree_hi = (int)std::min<uint32_t>(prm->tree_end, (uint32_t)Tmax);
+    if (tree_lo > tree_hi) return fail(RF_E_ARG, "tree_begin > tree_end");
+  }
+  const int ntask_all = (int)(reps * k);
+  int task_lo = 0, task_hi = ntask_all;
+  if (prm->task_begin || prm->task_end) {
+    task_lo = (int)prm->task_begin;
+    task_hi = (int)std::min<uint32_t>(prm->task_end, (uint32_t)ntask_all);
+    if (task_lo > task_hi) return fail(RF_E_ARG, "task_begin > task_end");
+  }
+  Scratch sc(s);
+  rf::DevData d;
+  st = prepare(dX, dy, n, p, prm->target, 1, true, d, sc, s);
+  if (st) return st;
+
+  const int32_t* dfold = dfold_in;
+  if (!dfold) {
+    int32_t* f;
+    CK(sc.alloc(&f, (size_t)n * reps), "alloc folds");
+    size_t wsb = rf::make_folds_ws_bytes((int)n, (int)reps, 0);
+    char* ws = nullptr;
+    if (wsb) CK(sc.alloc(&ws, wsb), "alloc folds ws");
+    CK(rf::make_folds(dy, (int)n, (int)k, (int)reps, prm->seed, 0, f, ws, wsb, s), "folds");
+    dfold = f;
+  }
+
+  const size_t n_out = (size_t)n_mtry * n_ntree * reps * k;
+  if (dfold_mape) CK(cudaMemsetAsync(dfold_mape, 0xFF, n_out * sizeof(double), s), "memset mape");
+  if (dpred) CK(cudaMemsetAsync(dpred, 0xFF, (size_t)n_mtry * n_ntree * reps * n * sizeof(double), s), "memset pred");
+  if (dpartial_rows)
+    CK(cudaMemsetAsync(dpartial_rows, 0, (size_t)n_mtry * n_ntree * reps * n * sizeof(double), s), "memset partial");
+  const int ntask = task_hi - task_lo;
+  if (ntask == 0 || tree_hi == tree_lo) return read_err(d.err, s);
+
+  rf::TaskData td;
+  td.ntask = ntask; td.task0 = task_lo; td.n = (int)n; td.p = (int)p;
+  CK(sc.alloc(&td.tr_rows, (size_t)ntask * n), "alloc tasks");
+  CK(sc.alloc(&td.te_rows, (size_t)ntask * n), "alloc tasks");
+  CK(sc.alloc(&td.loc, (size_t)ntask * n), "alloc tasks");
+  CK(sc.alloc(&td.ntr, ntask), "alloc tasks");
+  CK(sc.alloc(&td.nte, ntask), "alloc tasks");
+  {
+    ProfScope ps("tasks", s);
+    CK(rf::build_tasks(dfold, (int)k, d.order, d.grank, td, s), "tasks");
+  }
+  std::vector<int32_t> hntr(ntask), hnte(ntask);
+  CK(cudaMemcpyAsync(hntr.data(), td.ntr, ntask * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaMemcpyAsync(hnte.data(), td.nte, ntask * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  st = read_err(d.err, s);  // synchronises
+  if (st) return st;
+  int ntr_max = 0, nte_max = 0;
+  for (int i = 0; i < ntask; ++i) {
+    if (hnte[i] == 0) return fail(RF_E_TOO_FEW, "empty test fold");
+    if (hntr[i] == 0) return fail(RF_E_TOO_FEW, "empty training set");
+    ntr_max = std::max(ntr_max, hntr[i]);
+    nte_max = std::max(nte_max, hnte[i]);
+  }
+  if (ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode != RF_SPLIT_EXACT)
+    return rf::cv_large(dX, d, td, dfold, prm, k, reps, ntrees, n_ntree, mtrys, n_mtry, tree_lo,
+                        tree_hi, ntr_max, nte_max, dfold_mape, dpred, dpartial_rows, s, sc, g_err);
+
+  td.ntr_stride = ntr_max;
+  CK(sc.alloc(&td.ord, (size_t)ntask * p * ntr_max), "alloc ord");
+  CK(sc.alloc(&td.lrank, (size_t)ntask * p * ntr_max), "alloc lrank");
+  {
+    ProfScope ps("task_orders", s);
+    CK(rf::build_task_orders_u8(d.order, d.grank, td, s), "task orders");
+  }
+
+  GridPlan gp = plan_mtry(mtrys, n_mtry);
+  const int nmd = (int)gp.mtry_distinct.size();
+
+  rf::SmallArgs a;
+  memset(&a, 0, sizeof a);
+  a.X = d.X; a.n = (int)n; a.p = (int)p; a.tq = d.tq; a.dF = d.F; a.grank = d.grank;
+  a.ntask = ntask; a.task0 = task_lo; a.row_stride = (int)n; a.ntr_stride = ntr_max;
+  a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
+  a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = ntr_max; a.nte_max = nte_max;
+  a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
+  a.max_depth = prm->max_depth; a.n_mtry = nmd;
+  for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
+  a.tree_lo = tree_lo; a.tree_hi = tree_hi;
+  a.err = d.err;
+  // trees per warp job: divides every prefix boundary so prefix sums align with jobs
+  int g = 0;
+  for (uint32_t i = 0; i < n_ntree; ++i) g = gcd_i(g, (int)ntrees[i]);
+  if (tree_lo) g = gcd_i(g, tree_lo);
+  if (tree_hi != Tmax) g = gcd_i(g, tree_hi);
+  a.wpb = 4;
+  size_t smem = 0;
+  for (; a.wpb >= 1; a.wpb >>= 1) {
+    smem = rf::small_tree_smem_bytes(a, 0);
+    if (smem <= 227 * 1024) break;
+  }
+  if (a.wpb == 0) return fail(RF_E_UNSUPPORTED, "small-tree kernel: shared memory budget exceeded");
+  const int T = tree_hi - tree_lo;
+  const int resident = resident_warps(smem, a.wpb);
+  int Cw = 1;
+  for (int c = 16; c >= 1; --c) {
+    if (g % c) continue;
+    long long jobs = (long long)nmd * ntask * ((T + c - 1) / c);
+    if (jobs >= 2LL * resident || c == 1) { Cw = c; break; }
+  }
+  a.Cw = Cw;
+  a.nsub = (T + Cw - 1) / Cw;
+  double* partial;
+  CK(sc.alloc(&partial, (size_t)nmd * ntask * a.nsub * nte_max), "alloc partial");
+  a.partial = partial;
+  {
+    ProfScope ps("small_tree", s);
+    CK(rf::launch_small_tree(a, s), "small_tree kernel");
+  }
+  // score every distinct mtry, then copy blocks for duplicates
+  double* mape_d = nullptr;
+  double* pred_d = nullptr;
+  double* rows_d = nullptr;
+  const size_t blk_mape = (size_t)n_ntree * reps * k, blk_rows = (size_t)n_ntree * reps * n;
+  if (dfold_mape) CK(sc.alloc(&mape_d, nmd * blk_mape), "alloc");
+  if (dpred) CK(sc.alloc(&pred_d, nmd * blk_rows), "alloc");
+  if (dpartial_rows) CK(sc.alloc(&rows_d, nmd * blk_rows), "alloc");
+  if (pred_d) CK(cudaMemsetAsync(pred_d, 0xFF, nmd * blk_rows * 8, s), "memset");
+  if (mape_d) CK(cudaMemsetAsync(mape_d, 0xFF, nmd * blk_mape * 8, s), "memset");
+  if (rows_d) CK(cudaMemsetAsync(rows_d, 0, nmd * blk_rows * 8, s), "memset");
+  rf::ScoreArgs sa;
+  memset(&sa, 0, sizeof sa);
+  sa.partial = partial; sa.n_mtry = nmd; sa.ntask = ntask; sa.nsub = a.nsub; sa.nte_max = nte_max;
+  sa.Cw = Cw; sa.tree_lo = tree_lo; sa.te_rows = td.te_rows; sa.nte = td.nte; sa.n = (int)n;
+  sa.k = (int)k; sa.reps = (int)reps; sa.task0 = task_lo; sa.n_ntree = (int)n_ntree;
+  for (uint32_t i = 0; i < n_ntree; ++i) sa.ntrees[i] = (int)ntrees[i];
+  sa.target = (int)prm->target; sa.y = dy;
+  sa.fold_mape = mape_d ? mape_d : nullptr;
+  sa.pred = pred_d;
+  sa.partial_rows = rows_d;
+  if (!mape_d && !rows_d) return read_err(d.err, s);
+  if (!sa.fold_mape) {
+    CK(sc.alloc(&mape_d, nmd * blk_mape), "alloc");
+    sa.fold_mape = mape_d;
+  }
+  {
+    ProfScope ps("score", s);
+    CK(rf::score_cv(sa, s), "score");
+  }
+  for (uint32_t i = 0; i < n_mtry; ++i) {
+    const int di = gp.mtry_map[i];
+    if (dfold_mape)
+      CK(cudaMemcpyAsync(dfold_mape + i * blk_mape, mape_d + di * blk_mape, blk_mape * 8,
+                         cudaMemcpyDeviceToDevice, s), "copy");
+    if (dpred)
+      CK(cudaMemcpyAsync(dpred + i * blk_rows, pred_d + di * blk_rows, blk_rows * 8,
+                         cudaMemcpyDeviceToDevice, s), "copy");
+    if (dpartial_rows)
+      CK(cudaMemcpyAsync(dpartial_rows + i * blk_rows, rows_d + di * blk_rows, blk_rows * 8,
+                         cudaMemcpyDeviceToDevice, s), "copy");
+  }
+  // task-range outputs outside the shard stay NaN (memset 0xFF above)
+  return RF_OK;
+}
+
+// gather per-tree node blocks (stride cap) into the flat forest
+__global__ void k_compact_nodes(const rf::Node16* __restrict__ in, const uint32_t* __restrict__ tin,
+                                const uint64_t* __restrict__ off, int T, uint64_t cap,
+                                rf::Node16* out, uint32_t* tout) {
+  const int t = blockIdx.y;
+  if (t >= T) return;
+  const uint64_t cnt = off[t + 1] - off[t];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    out[off[t] + i] = in[t * cap + i];
+    tout[off[t] + i] = tin[t * cap + i];
+  }
+}
+
+rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                   bool debug, cudaStream_t s, rf_forest** out) {
+  *out = nullptr;
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (n > 0x7FFFFFFF) return fail(RF_E_ARG, "n too large");
+  uint32_t mtry = 0;
+  rf_status st = check_params(prm, p, &mtry);
+  if (st) return st;
+  if (prm->ntree == 0) return fail(RF_E_ARG, "ntree must be >= 1");
+  int tree_lo = 0, tree_hi = (int)prm->ntree;
+  if (prm->tree_begin || prm->tree_end) {
+    tree_lo = (int)prm->tree_begin;
+    tree_hi = (int)std::min(prm->tree_end, prm->ntree);
+    if (tree_lo >= tree_hi) return fail(RF_E_ARG, "empty tree range");
+  }
+  const int T = tree_hi - tree_lo;
+  Scratch sc(s);
+  rf::DevData d;
+  st = prepare(dX, dy, n, p, prm->target, prm->target == RF_TARGET_LOG, true, d, sc, s);
+  if (st) return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+
+  const bool small = n <= (uint64_t)rf::kSmallMaxRows && p <= (uint32_t)rf::kSmallMaxP &&
+                     prm->split_mode == RF_SPLIT_EXACT;
+  rf::Node16* nodes_w = nullptr;
+  uint32_t* tidx_w = nullptr;
+  uint32_t* nn_d = nullptr;
+  int32_t* lor = nullptr;
+  uint64_t cap = 0;
+  if (debug) CK(cudaMalloc(&lor, (size_t)T * n * sizeof(int32_t)), "alloc leaf_of_row");
+  if (small) {
+    rf::TaskData td;
+    td.ntask = 1; td.task0 = 0; td.n = (int)n; td.p = (int)p; td.ntr_stride = (int)n;
+    CK(sc.alloc(&td.tr_rows, n), "alloc");
+    CK(sc.alloc(&td.te_rows, n), "alloc");
+    CK(sc.alloc(&td.loc, n), "alloc");
+    CK(sc.alloc(&td.ntr, 1), "alloc");
+    CK(sc.alloc(&td.nte, 1), "alloc");
+    CK(sc.alloc(&td.ord, (size_t)p * n), "alloc");
+    CK(sc.alloc(&td.lrank, (size_t)p * n), "alloc");
+    CK(rf::build_tasks(nullptr, 1, d.order, d.grank, td, s), "tasks");
+    CK(rf::build_task_orders_u8(d.order, d.grank, td, s), "task orders");
+    cap = 2 * n - 1;
+    CK(sc.alloc(&nodes_w, (size_t)T * cap), "alloc nodes");
+    CK(sc.alloc(&tidx_w, (size_t)T * cap), "alloc nodes");
+    CK(sc.alloc(&nn_d, (size_t)T), "alloc nodes");
+    rf::SmallArgs a;
+    memset(&a, 0, sizeof a);
+    a.X = d.X; a.n = (int)n; a.p = (int)p; a.tq = d.tq; a.dF = d.F; a.grank = d.grank;
+    a.ntask = 1; a.task0 = 0; a.row_stride = (int)n; a.ntr_stride = (int)n;
+    a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
+    a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = (int)n; a.nte_max = 0;
+    a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
+    a.max_depth = prm->max_depth; a.n_mtry = 1; a.mtrys[0] = (int)mtry;
+    a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
+    a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;
+    a.cap = (uint32_t)cap; a.leaf_of_row = lor; a.err = d.err;
+    size_t smem = 0;
+    for (; a.wpb >= 1; a.wpb >>= 1) {
+      smem = rf::small_tree_smem_bytes(a, 0);
+      if (smem <= 227 * 1024) break;
+    }
+    if (a.wpb == 0) { cudaFree(lor); return fail(RF_E_UNSUPPORTED, "shared memory budget"); }
+    ProfScope ps("small_tree_fit", s);
+    cudaError_t e = rf::launch_small_tree(a, s);
+    if (e != cudaSuccess) { cudaFree(lor); return cuda_fail(e, "small_tree fit"); }
+  } else {
+    rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,
+                                 &cap, lor, g_err);
+    if (ls) { cudaFree(lor); return ls; }
+  }
+  std::vector<uint32_t> hnn(T);
+  CK(cudaMemcpyAsync(hnn.data(), nn_d, T * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  int32_t hF = 0;
+  CK(cudaMemcpyAsync(&hF, d.F, 4, cudaMemcpyDeviceToHost, s), "d2h");
+  st = read_err(d.err, s);
+  if (st) { cudaFree(lor); return st; }
+  rf_forest* f = new rf_forest();
+  f->device = dev; f->ntree = (uint32_t)T; f->p = p; f->target = prm->target; f->F = hF;
+  f->h_tree_off.resize(T + 1);
+  f->h_tree_off[0] = 0;
+  for (int t = 0; t < T; ++t) f->h_tree_off[t + 1] = f->h_tree_off[t] + hnn[t];
+  f->total_nodes = f->h_tree_off[T];
+  f->leaf_of_row = lor;
+  f->n_rows = n;
+  cudaError_t e = cudaMalloc(&f->nodes, f->total_nodes * sizeof(rf::Node16));
+  if (e == cudaSuccess) e = cudaMalloc(&f->thr_index, f->total_nodes * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&f->tree_off, (T + 1) * sizeof(uint64_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(f->tree_off, f->h_tree_off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    dim3 grid((unsigned)std::min<uint64_t>((cap + 255) / 256, 64), (unsigned)T);
+    k_compact_nodes<<<grid, 256, 0, s>>>(nodes_w, tidx_w, f->tree_off, T, cap, f->nodes, f->thr_index);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    rf_forest_free(f);
+    return cuda_fail(e, "forest assembly");
+  }
+  *out = f;
+  return RF_OK;
+}
+
+}  // namespace
+
+namespace rf {
+bool prof_enabled() { return g_prof_on; }
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back(ProfRec{name, a, b}); }
+}  // namespace rf
+
+// ======================================================================= ABI
+extern "C" {
+
+void rf_params_default(rf_params* prm) {
+  if (!prm) return;
+  memset(prm, 0, sizeof *prm);
+  prm->struct_size = sizeof(rf_params);
+  prm->ntree = 100;
+  prm->mtry = 0;
+  prm->min_samples_split = 2;
+  prm->max_depth = -1;
+  prm->bootstrap = 1;
+  prm->split_mode = RF_SPLIT_EXACT;
+  prm->target = RF_TARGET_IDENTITY;
+  prm->seed = 0;
+  prm->device = 0;
+}
+
+const char* rf_last_error(void) { return g_err.c_str(); }
+
+void rf_forest_free(rf_forest* f) {
+  if (!f) return;
+  cudaFree(f->nodes);
+  cudaFree(f->thr_index);
+  cudaFree(f->tree_off);
+  cudaFree(f->leaf_of_row);
+  delete f;
+}
+
+rf_status rf_fit_dev(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                     void* stream, rf_forest** out) {
+  if (!out) return fail(RF_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (rf_status st = check_device()) return st;
+  try {
+    return fit_core(dX, n, p, dy, prm, false, static_cast<cudaStream_t>(stream), out);
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+static rf_status fit_host(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                          bool debug, rf_forest** out) {
+  if (!out) return fail(RF_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (rf_status st = check_device()) return st;
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (!X || !y) return fail(RF_E_ARG, "NULL input");
+  CK(cudaSetDevice(prm->device), "set device");
+  cudaStream_t s = host_stream(prm->device);
+  try {
+    Scratch sc(s);
+    double *dX, *dy;
+    CK(sc.alloc(&dX, n * p), "alloc");
+    CK(sc.alloc(&dy, n), "alloc");
+    CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+    CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+    return fit_core(dX, n, p, dy, prm, debug, s, out);
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+rf_status rf_fit(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                 rf_forest** out) {
+  return fit_host(X, n, p, y, prm, false, out);
+}
+
+rf_status rf_fit_debug(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                       rf_forest** out) {
+  return fit_host(X, n, p, y, prm, true, out);
+}
+
+static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, uint32_t p, double* dout,
+                              int mode, cudaStream_t s) {
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  if (p != f->p) return fail(RF_E_ARITY, "p differs from the forest's");
+  if (n == 0) return RF_OK;
+  Scratch sc(s);
+  int* err;
+  CK(sc.alloc(&err, 1), "alloc");
+  CK(cudaMemsetAsync(err, 0, 4, s), "memset");
+  CK(rf::check_finite(dX, n * p, err, s), "check");
+  {
+    ProfScope ps("predict", s);
+    CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s),
+       "predict");
+  }
+  return read_err(err, s);
+}
+
+rf_status rf_predict_dev(const rf_forest* f, const double* dX, uint64_t n, uint32_t p, double* dyhat,
+                         void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  return predict_core(f, dX, n, p, dyhat, f->target == RF_TARGET_LOG ? 2 : 1,
+                      static_cast<cudaStream_t>(stream));
+}
+
+rf_status rf_predict_partial_dev(const rf_forest* f, const double* dX, uint64_t n, uint32_t p,
+                                 double* dpartial, void* stream) {
+  if (rf_status st = check_device()) return st;
+  return predict_core(f, dX, n, p, dpartial, 0, static_cast<cudaStream_t>(stream));
+}
+
+rf_status rf_predict_finalize_dev(const double* dpartial, uint64_t n, uint32_t ntree_total, uint32_t target,
+                                  double* dyhat, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (ntree_total == 0) return fail(RF_E_ARG, "ntree_total must be >= 1");
+  CK(rf::predict_finalize(dpartial, (long long)n, (int)ntree_total, (int)target, dyhat,
+                          static_cast<cudaStream_t>(stream)), "finalize");
+  return RF_OK;
+}
+
+rf_status rf_predict(const rf_forest* f, const double* X, uint64_t n, uint32_t p, double* yhat) {
+  if (rf_status st = check_device()) return st;
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  if (p != f->p) return fail(RF_E_ARITY, "p differs from the forest's");
+  if (n == 0) return RF_OK;
+  CK(cudaSetDevice(f->device), "set device");
+  cudaStream_t s = host_stream(f->device);
+  Scratch sc(s);
+  double *dX, *dy;
+  CK(sc.alloc(&dX, n * p), "alloc");
+  CK(sc.alloc(&dy, n), "alloc");
+  CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+  rf_status st = predict_core(f, dX, n, p, dy, f->target == RF_TARGET_LOG ? 2 : 1, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(yhat, dy, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
+rf_status rf_make_folds_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
+                            uint32_t custom, int32_t* dfold_ids, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (k < 2 || (!custom && k > n) || (custom && (n < 5 || n - 5 < k)))
+    return fail(RF_E_TOO_FEW, "too few rows for k folds");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Scratch sc(s);
+  size_t wsb = rf::make_folds_ws_bytes((int)n, (int)repeats, (int)custom);
+  char* ws = nullptr;
+  if (wsb) CK(sc.alloc(&ws, wsb), "alloc");
+  cudaError_t e = rf::make_folds(dy, (int)n, (int)k, (int)repeats, seed, (int)custom, dfold_ids, ws, wsb, s);
+  if (e == cudaErrorNotSupported) return fail(RF_E_UNSUPPORTED, "custom split limited to n <= 4096");
+  CK(e, "folds");
+  return RF_OK;
+}
+
+rf_status rf_make_folds(const double* y, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
+                        uint32_t custom, int32_t* fold_ids) {
+  if (rf_status st = check_device()) return st;
+  cudaStream_t s = host_stream(0);
+  Scratch sc(s);
+  double* dy;
+  int32_t* df;
+  CK(sc.alloc(&dy, std::max<uint64_t>(n, 1)), "alloc");
+  CK(sc.alloc(&df, std::max<uint64_t>(n * repeats, 1)), "alloc");
+  if (n) CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+  rf_status st = rf_make_folds_dev(dy, n, k, repeats, seed, custom, df, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(fold_ids, df, n * repeats * 4, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
+rf_status rf_cross_validate_grid_dev(const double* dX, uint64_t n, uint32_t p, const double* dy,
+                                     const rf_params* prm, uint32_t k, uint32_t repeats,
+                                     const int32_t* dfold_ids, const uint32_t* ntrees, uint32_t n_ntree,
+                                     const uint32_t* mtrys, uint32_t n_mtry, double* dfold_mape,
+                                     double* dpred, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!dfold_mape) return fail(RF_E_ARG, "fold_mape is NULL");
+  try {
+    return cv_core(dX, n, p, dy, prm, k, repeats, dfold_ids, ntrees, n_ntree, mtrys, n_mtry, dfold_mape,
+                   dpred, nullptr, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+rf_status rf_cross_validate_grid(const double* X, uint64_t n, uint32_t p, const double* y,
+                                 const rf_params* prm, uint32_t k, uint32_t repeats,
+                                 const int32_t* fold_ids, const uint32_t* ntrees, uint32_t n_ntree,
+                                 const uint32_t* mtrys, uint32_t n_mtry, double* fold_mape, double* pred) {
+  if (rf_status st = check_device()) return st;
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  CK(cudaSetDevice(prm->device), "set device");
+  cudaStream_t s = host_stream(prm->device);
+  Scratch sc(s);
+  double *dX, *dy, *dm, *dp = nullptr;
+  int32_t* df = nullptr;
+  const size_t nm = (size_t)n_mtry * n_ntree * repeats * k, np_ = (size_t)n_mtry * n_ntree * repeats * n;
+  CK(sc.alloc(&dX, n * p), "alloc");
+  CK(sc.alloc(&dy, n), "alloc");
+  CK(sc.alloc(&dm, nm), "alloc");
+  if (pred) CK(sc.alloc(&dp, np_), "alloc");
+  CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+  CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+  if (fold_ids) {
+    CK(sc.alloc(&df, n * repeats), "alloc");
+    CK(cudaMemcpyAsync(df, fold_ids, n * repeats * 4, cudaMemcpyHostToDevice, s), "h2d");
+  }
+  rf_status st = rf_cross_validate_grid_dev(dX, n, p, dy, prm, k, repeats, df, ntrees, n_ntree, mtrys,
+                                            n_mtry, dm, dp, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(fold_mape, dm, nm * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  if (pred) CK(cudaMemcpyAsync(pred, dp, np_ * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
+rf_status rf_cross_validate(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                            uint32_t k, uint32_t repeats, const int32_t* fold_ids, double* fold_mape) {
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  uint32_t m = 0;
+  if (rf_status st = check_params(prm, p, &m)) return st;
+  uint32_t nt = prm->ntree;
+  return rf_cross_validate_grid(X, n, p, y, prm, k, repeats, fold_ids, &nt, 1, &m, 1, fold_mape, nullptr);
+}
+
+rf_status rf_cv_partial_dev(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                            uint32_t k, uint32_t repeats, const int32_t* dfold_ids, const uint32_t* ntrees,
+                            uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry, double* dpartial,
+                            void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!dpartial) return fail(RF_E_ARG, "partial is NULL");
+  try {
+    return cv_core(dX, n, p, dy, prm, k, repeats, dfold_ids, ntrees, n_ntree, mtrys, n_mtry, nullptr, nullptr,
+                   dpartial, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+rf_status rf_cv_finalize_dev(const double* dy, uint64_t n, uint32_t target, uint32_t k, uint32_t repeats,
+                             const int32_t* dfold_ids, const uint32_t* ntrees, uint32_t n_ntree,
+                             uint32_t n_mtry, const double* dreduced, double* dfold_mape, double* dpred,
+                             void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (n_ntree == 0 || n_ntree > 16) return fail(RF_E_ARG, "1..16 ntree values");
+  if (!dfold_ids) return fail(RF_E_ARG, "fold ids required");
+  std::vector<int> nt(ntrees, ntrees + n_ntree);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dpred) CK(cudaMemsetAsync(dpred, 0xFF, (size_t)n_mtry * n_ntree * repeats * n * 8, s), "memset");
+  CK(rf::finalize_cv(dreduced, dy, dfold_ids, (int)n, (int)k, (int)repeats, (int)n_mtry, (int)n_ntree,
+                     nt.data(), (int)target, dfold_mape, dpred, s), "finalize");
+  return RF_OK;
+}
+
+rf_status rf_forest_info(const rf_forest* f, uint32_t* ntree, uint64_t* total_nodes, int32_t* F, uint32_t* p,
+                         uint32_t* target) {
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  if (ntree) *ntree = f->ntree;
+  if (total_nodes) *total_nodes = f->total_nodes;
+  if (F) *F = f->F;
+  if (p) *p = f->p;
+  if (target) *target = f->target;
+  return RF_OK;
+}
+
+rf_status rf_forest_export(const rf_forest* f, int32_t* feature, uint32_t* left, double* value,
+                           uint32_t* thr_index, uint64_t* tree_off) {
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  CK(cudaSetDevice(f->device), "set device");
+  std::vector<rf::Node16> h(f->total_nodes);
+  CK(cudaMemcpy(h.data(), f->nodes, f->total_nodes * sizeof(rf::Node16), cudaMemcpyDeviceToHost), "d2h");
+  for (uint64_t i = 0; i < f->total_nodes; ++i) {
+    if (feature) feature[i] = h[i].feat;
+    if (left) left[i] = h[i].left;
+    if (value) value[i] = h[i].v;
+  }
+  if (thr_index)
+    CK(cudaMemcpy(thr_index, f->thr_index, f->total_nodes * 4, cudaMemcpyDeviceToHost), "d2h");
+  if (tree_off) memcpy(tree_off, f->h_tree_off.data(), (f->ntree + 1) * 8);
+  return RF_OK;
+}
+
+rf_status rf_forest_export_leaf_rows(const rf_forest* f, int32_t* leaf_of_row) {
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  if (!f->leaf_of_row) return fail(RF_E_ARG, "forest was not grown with rf_fit_debug");
+  CK(cudaSetDevice(f->device), "set device");
+  CK(cudaMemcpy(leaf_of_row, f->leaf_of_row, (size_t)f->ntree * f->n_rows * 4, cudaMemcpyDeviceToHost), "d2h");
+  return RF_OK;
+}
+
+rf_status rf_forest_import(const int32_t* feature, const uint32_t* left, const double* value,
+                           const uint32_t* thr_index, const uint64_t* tree_off, uint32_t ntree, uint32_t p,
+                           int32_t F, uint32_t target, int32_t device, rf_forest** out) {
+  if (!out) return fail(RF_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (rf_status st = check_device()) return st;
+  if (ntree == 0 || !tree_off || !feature || !left || !value) return fail(RF_E_ARG, "bad arrays");
+  CK(cudaSetDevice(device), "set device");
+  rf_forest* f = new rf_forest();
+  f->device = device; f->ntree = ntree; f->p = p; f->F = F; f->target = target;
+  f->h_tree_off.assign(tree_off, tree_off + ntree + 1);
+  f->total_nodes = tree_off[ntree];
+  std::vector<rf::Node16> h(f->total_nodes);
+  for (uint64_t i = 0; i < f->total_nodes; ++i) { h[i].feat = feature[i]; h[i].left = left[i]; h[i].v = value[i]; }
+  cudaError_t e = cudaMalloc(&f->nodes, std::max<uint64_t>(1, f->total_nodes) * sizeof(rf::Node16));
+  if (e == cudaSuccess) e = cudaMalloc(&f->thr_index, std::max<uint64_t>(1, f->total_nodes) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&f->tree_off, (ntree + 1) * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(f->nodes, h.data(), f->total_nodes * sizeof(rf::Node16), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && thr_index) e = cudaMemcpy(f->thr_index, thr_index, f->total_nodes * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(f->tree_off, tree_off, (ntree + 1) * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { rf_forest_free(f); return cuda_fail(e, "import"); }
+  *out = f;
+  return RF_OK;
+}
+
+void rf_set_profiling(int on) {
+  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+  g_prof_on = on != 0;
+}
+
+uint32_t rf_last_profile(const char** names, double* ms, uint32_t* launches, uint32_t cap) {
+  std::vector<std::string> order;
+  std::vector<double> tot;
+  std::vector<uint32_t> cnt;
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    auto it = std::find(order.begin(), order.end(), std::string(r.name));
+    size_t i = it - order.begin();
+    if (it == order.end()) { order.push_back(r.name); tot.push_back(0.0); cnt.push_back(0); }
+    tot[i] += t;
+    cnt[i] += 1;
+  }
+  uint32_t m = (uint32_t)std::min<size_t>(cap, order.size());
+  static thread_local std::vector<std::string> keep;
+  keep = order;
+  for (uint32_t i = 0; i < m; ++i) {
+    if (names) names[i] = keep[i].c_str();
+    if (ms) ms[i] = tot[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  return m;
+}
+
+rf_status rf_debug_ln_dev(const double* dy, double* dout, uint64_t n, void* stream) {
+  if (rf_status st = check_device()) return st;
+  CK(rf::device_ln(dy, dout, (int)n, static_cast<cudaStream_t>(stream)), "ln");
+  return RF_OK;
+}
+
+rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, uint64_t n, void* stream) {
+  if (rf_status st = check_device()) return st;
+  CK(rf::device_philox(dctr_key, dout, (int)n, static_cast<cudaStream_t>(stream)), "philox");
+  return RF_OK;
+}
+
+}  // extern "C"

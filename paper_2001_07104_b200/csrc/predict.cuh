@@ -1,0 +1,14 @@
+// predict.cuh -- forest inference launchers.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace rf {
+// mode 0: un-divided sum (tree-shard partial); 1: mean; 2: exp(mean) (LOG)
+cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
+                           long long n, int p, int mode, double* out, cudaStream_t s);
+cudaError_t predict_finalize(const double* partial, long long n, int T, int target, double* out,
+                             cudaStream_t s);
+cudaError_t check_finite(const double* X, size_t total, int* err, cudaStream_t s);
+}  // namespace rf

@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: tree structures bit-exact (split feature,
+threshold index, threshold value, child ids, leaf values, leaf row sets);
+fold ids and ln bit-exact; predictions and fold MAPE within 1e-9 relative
+(north_star), the summation order being the only difference.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2001_07104_b200 as rfg  # noqa: E402
+
+RTOL = 1e-9
+
+
+def _cuda(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+# ------------------------------------------------------------ primitives --
+def test_philox_device_kat(golden_dir):
+    rows = []
+    for line in open(f"{golden_dir}/philox_kat.txt"):
+        if line.startswith("#") or not line.strip():
+            continue
+        rows.append([int(x, 16) for x in line.split()])
+    rnd = np.random.default_rng(0)
+    extra = rnd.integers(0, 2 ** 32, size=(200, 6), dtype=np.uint64)
+    inp = np.concatenate([np.array([r[:6] for r in rows], np.uint64), extra])
+    out = rfg.debug_philox(torch.tensor(inp.astype(np.int64), device="cuda")).cpu().numpy()
+    for i, r in enumerate(rows):
+        assert out[i].tolist() == r[6:]
+    for i in range(len(rows), len(inp)):
+        c = inp[i]
+        assert out[i].tolist() == [int(v) for v in oracle.philox(c[:4], c[4:])]
+
+
+def test_ln_device_bit_exact():
+    rnd = np.random.default_rng(1)
+    y = np.concatenate([10 ** rnd.uniform(-5, 9, 20000), rnd.uniform(0.5, 2.0, 5000), [1.0, 2.0, np.e, 1e-310]])
+    got = rfg.debug_ln(_cuda(y)).cpu().numpy()
+    want = np.array([oracle.ln(v) for v in y])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("n,k,custom", [(189, 10, False), (168, 10, False), (10, 10, False), (23, 4, False),
+                                        (5000, 10, False), (189, 10, True), (95, 5, True)])
+def test_folds_bit_exact(n, k, custom):
+    if custom:
+        y = datagen.paper_shaped(n, "K20", "time")[1] if n == 189 else 10 ** np.random.default_rng(3).uniform(1, 7, n)
+    else:
+        y = np.ones(n)
+    g = rfg.make_folds(y, k, 5, seed=77, custom=custom)
+    o = oracle.make_folds(y, k, 5, seed=77, custom=custom)
+    assert np.array_equal(g, o)
+    gd = rfg.make_folds(_cuda(y), k, 5, seed=77, custom=custom).cpu().numpy()
+    assert np.array_equal(gd, o)
+
+
+# ---------------------------------------------------------------- fit ---
+def _compare_forest(gf, of, X):
+    e = gf.export()
+    off = e["tree_off"]
+    assert e["ntree"] == len(of.trees)
+    assert e["F"] == of.F
+    lr = gf.leaf_rows() if gf.n_rows else None
+    for t, tr in enumerate(of.trees):
+        a, b = int(off[t]), int(off[t + 1])
+        feat = e["feature"][a:b]
+        assert b - a == tr.n_nodes, f"tree {t}: {b - a} vs {tr.n_nodes} nodes"
+        assert np.array_equal(feat, tr.feature), f"tree {t} features"
+        internal = feat >= 0
+        assert np.array_equal(e["left"][a:b][internal], tr.left[internal]), f"tree {t} children"
+        assert np.array_equal(e["thr_index"][a:b][internal], tr.thr_index[internal]), f"tree {t} thr index"
+        assert np.array_equal(e["value"][a:b][internal].view(np.int64), tr.thr_value[internal].view(np.int64))
+        assert np.array_equal(e["value"][a:b][~internal].view(np.int64), tr.leaf_value[~internal].view(np.int64)), \
+            f"tree {t} leaf values"
+        if lr is not None and tr.leaf_of_row is not None:
+            assert np.array_equal(lr[t], tr.leaf_of_row), f"tree {t} leaf rows"
+
+
+FIT_CASES = [
+    # name, data fn, kwargs
+    ("paper_time_m12", lambda: datagen.paper_shaped(189, "K20", "time"), dict(mtry=12, target=1)),
+    ("paper_time_m3", lambda: datagen.paper_shaped(189, "V100", "time"), dict(mtry=3, target=1)),
+    ("paper_power", lambda: datagen.paper_shaped(168, "P100", "power"), dict(mtry=4)),
+    ("ties", lambda: datagen.tiny(200, 5, 3, distinct=6), dict(mtry=2)),
+    ("noboot", lambda: datagen.tiny(120, 4, 5), dict(mtry=4, bootstrap=False)),
+    ("depth3", lambda: datagen.paper_shaped(189, "TitanXp", "time"), dict(mtry=5, max_depth=3, target=1)),
+    ("mss5", lambda: datagen.tiny(150, 6, 8, distinct=20), dict(mtry=3, min_samples_split=5)),
+    ("n255", lambda: datagen.tiny(255, 3, 9), dict(mtry=1)),
+    ("n2", lambda: (np.array([[0.0], [1.0]]), np.array([1.0, 3.0])), dict(mtry=1)),
+    ("const", lambda: (datagen.tiny(40, 3, 1)[0], np.full(40, 2.5)), dict(mtry=2)),
+    ("negzero", lambda: (np.array([[-0.0, 1], [0.0, 2], [1, 3], [2, 1]]), np.array([1.0, 2, 3, 4])), dict(mtry=2)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", FIT_CASES, ids=[c[0] for c in FIT_CASES])
+def test_fit_structures_bit_exact(name, data, kw):
+    X, y = data()
+    of = oracle.fit(X, y, ntree=24, seed=11, leaf_rows=True, **kw)
+    gf = rfg.fit(X, y, ntree=24, seed=11, debug=True, **kw)
+    _compare_forest(gf, of, X)
+
+
+def test_fit_many_seeds_paper_shaped():
+    X, y = datagen.paper_shaped(189, "GTX1650", "time")
+    for seed in range(6):
+        of = oracle.fit(X, y, ntree=64, seed=seed, mtry=3, target=1, leaf_rows=True)
+        gf = rfg.fit(X, y, ntree=64, seed=seed, mtry=3, target=1, debug=True)
+        _compare_forest(gf, of, X)
+
+
+def test_fit_tree_shard_is_prefix():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    full = rfg.fit(X, y, ntree=32, seed=4, mtry=3, target=1).export()
+    part = rfg.fit(X, y, ntree=32, seed=4, mtry=3, target=1, tree_begin=8, tree_end=20).export()
+    a, b = int(full["tree_off"][8]), int(full["tree_off"][20])
+    assert np.array_equal(part["feature"], full["feature"][a:b])
+    assert np.array_equal(part["value"].view(np.int64), full["value"][a:b].view(np.int64))
+
+
+def test_fit_device_path_matches_host():
+    X, y = datagen.paper_shaped(168, "V100", "power")
+    h = rfg.fit(X, y, ntree=16, seed=2, mtry=4).export()
+    d = rfg.fit(_cuda(X), _cuda(y), ntree=16, seed=2, mtry=4)
+    torch.cuda.synchronize()
+    d = d.export()
+    for key in ("feature", "left", "thr_index"):
+        assert np.array_equal(h[key], d[key])
+    assert np.array_equal(h["value"].view(np.int64), d["value"].view(np.int64))
+
+
+# ------------------------------------------------------------ predict ---
+@pytest.mark.parametrize("target", [0, 1])
+def test_predict_parity(target):
+    X, y = datagen.paper_shaped(189, "P100", "time")
+    Q = datagen.paper_shaped(500, "P100", "time", seed=123)[0]
+    of = oracle.fit(X, y, ntree=50, seed=3, mtry=4, target=target)
+    gf = rfg.fit(X, y, ntree=50, seed=3, mtry=4, target=target)
+    want = oracle.predict(of, Q)
+    got = rfg.predict(gf, Q)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=0)
+    got_d = rfg.predict(gf, _cuda(Q)).cpu().numpy()
+    np.testing.assert_allclose(got_d, want, rtol=RTOL, atol=0)
+    # partial + finalize (tree-shard combine) equals predict
+    part = rfg.predict_partial(gf, _cuda(Q))
+    fin = rfg.predict_finalize(part, 50, target).cpu().numpy()
+    np.testing.assert_allclose(fin, want, rtol=RTOL, atol=0)
+
+
+def test_predict_fits_exactly():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    _, idx = np.unique(X, axis=0, return_index=True)
+    X, y = X[np.sort(idx)], y[np.sort(idx)]
+    gf = rfg.fit(X, y, ntree=1, mtry=12, bootstrap=False)
+    _, tq, F = oracle.quantize(y, 0)
+    assert np.array_equal(rfg.predict(gf, X), np.ldexp(tq.astype(np.float64), -F))
+
+
+# ----------------------------------------------------------------- CV ---
+CV_CASES = [
+    ("c1_paper", lambda: datagen.paper_shaped(189, "K20", "time"), dict(k=10, reps=1, ntrees=[20], mtrys=[12], target=1)),
+    ("grid_power", lambda: datagen.paper_shaped(168, "V100", "power"),
+     dict(k=10, reps=2, ntrees=[8, 16, 32], mtrys=[12, 3, 3], target=0)),
+    ("k2", lambda: datagen.tiny(90, 3, 4), dict(k=2, reps=2, ntrees=[5, 10], mtrys=[1, 3], target=0)),
+    ("loo", lambda: datagen.tiny(30, 2, 5), dict(k=30, reps=1, ntrees=[6], mtrys=[2], target=1)),
+    ("ties", lambda: datagen.tiny(150, 4, 6, distinct=5), dict(k=5, reps=3, ntrees=[12], mtrys=[2], target=1)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", CV_CASES, ids=[c[0] for c in CV_CASES])
+def test_cv_parity(name, data, kw):
+    X, y = data()
+    fm_o, pr_o = oracle.cv_grid(X, y, kw["k"], kw["reps"], kw["ntrees"], kw["mtrys"], target=kw["target"],
+                                seed=9, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, kw["k"], kw["reps"], kw["ntrees"], kw["mtrys"], target=kw["target"],
+                                         seed=9, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+
+
+def test_cv_custom_split_and_device_path():
+    X, y = datagen.paper_shaped(189, "TitanXp", "time")
+    f = oracle.make_folds(y, 10, 3, seed=5, custom=True)
+    fm_o = oracle.cv_grid(X, y, 10, 3, [16, 32], [12, 3], fold_ids=f, target=1, seed=5)
+    fm_g = rfg.cross_validate_grid(_cuda(X), _cuda(y), 10, 3, [16, 32], [12, 3],
+                                   fold_ids=_cuda(f, torch.int32), target=1, seed=5).cpu().numpy()
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+
+
+def test_cv_task_shard():
+    X, y = datagen.paper_shaped(168, "K20", "power")
+    full = rfg.cross_validate_grid(X, y, 10, 2, [8], [4], seed=1)
+    part = rfg.cross_validate_grid(X, y, 10, 2, [8], [4], seed=1, task_begin=5, task_end=13)
+    flat_f, flat_p = full.reshape(-1), part.reshape(-1)
+    assert np.array_equal(flat_p[5:13], flat_f[5:13])
+    assert np.isnan(flat_p[:5]).all() and np.isnan(flat_p[13:]).all()
+
+
+def test_cv_tree_shard_partial_finalize():
+    X, y = datagen.paper_shaped(189, "V100", "time")
+    Xd, yd = _cuda(X), _cuda(y)
+    folds = rfg.make_folds(yd, 10, 2, seed=3)
+    ntrees, mtrys = [16, 32], [3, 12]
+    tot = None
+    for lo, hi in [(0, 8), (8, 16), (16, 32)]:
+        part = rfg.cv_partial(Xd, yd, 10, 2, folds, ntrees, mtrys, tree_begin=lo, tree_end=hi, target=1, seed=3)
+        tot = part if tot is None else tot + part
+    fm = rfg.cv_finalize(yd, 10, 2, folds, ntrees, len(mtrys), tot, target=1).cpu().numpy()
+    want = oracle.cv_grid(X, y, 10, 2, ntrees, mtrys, fold_ids=folds.cpu().numpy(), target=1, seed=3)
+    np.testing.assert_allclose(fm, want, rtol=RTOL, atol=0)
+
+
+def test_cv_full_study_config_sampled():
+    """Full study config (30 reps x 10 folds x 1024 trees x mtry {12,3,3}) on one dataset;
+    the oracle recomputes a sample of tasks (trees are keyed by (task, tree), R15)."""
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    folds = oracle.make_folds(y, 10, 30, seed=7104, custom=True)
+    nt, mt = [128, 256, 512, 1024], [12, 3, 3]
+    fm_g = rfg.cross_validate_grid(X, y, 10, 30, nt, mt, fold_ids=folds, target=1, seed=7104)
+    assert np.isfinite(fm_g).all()
+    for task in (0, 157, 299):
+        fm_o = oracle.cv_grid(X, y, 10, 30, nt, [12, 3], fold_ids=folds, target=1, seed=7104,
+                              task_begin=task, task_end=task + 1)
+        rep, fold = divmod(task, 10)
+        np.testing.assert_allclose(fm_g[[0, 1], :, rep, fold], fm_o[:, :, rep, fold], rtol=RTOL, atol=0)
+    assert np.array_equal(fm_g[1], fm_g[2])
+
+
+# -------------------------------------------------------------- errors ---
+def test_errors():
+    X, y = datagen.tiny(20, 3, 1)
+    with pytest.raises(rfg.RFError) as e:
+        rfg.fit(np.zeros((0, 3)), np.zeros(0))
+    assert e.value.code == rfg.E_EMPTY
+    Xn = X.copy()
+    Xn[3, 1] = np.nan
+    with pytest.raises(rfg.RFError) as e:
+        rfg.fit(Xn, y, ntree=2)
+    assert e.value.code == rfg.E_NONFINITE
+    with pytest.raises(rfg.RFError) as e:
+        rfg.fit(X, y - 10, ntree=2, target=1)
+    assert e.value.code == rfg.E_NONPOSITIVE_Y
+    f = rfg.fit(X, y, ntree=2)
+    with pytest.raises(rfg.RFError) as e:
+        rfg.predict(f, np.zeros((3, 4)))
+    assert e.value.code == rfg.E_ARITY
+    with pytest.raises(rfg.RFError) as e:
+        rfg.cross_validate_grid(X, y, 25, 1, [2], [1])
+    assert e.value.code == rfg.E_TOO_FEW
+    with pytest.raises(rfg.RFError) as e:
+        rfg.cross_validate_grid(X, y - 10, 4, 1, [2], [1])
+    assert e.value.code == rfg.E_NONPOSITIVE_Y
