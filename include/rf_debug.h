@@ -15,6 +15,10 @@ RF_API rf_status rf_debug_ln_dev(const double* dy, double* dout, uint64_t n, voi
 /* Philox4x32-10 (R14): for each i, dctr_key[6i..6i+5] =
    (c0, c1, c2, c3, k0, k1) -> dout[4i..4i+3]. */
 RF_API rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, uint64_t n, void* stream);
+/* Cumulative counters of this process: kernel launches issued by the library
+   (host count) and candidate splits evaluated by the split-search kernels on
+   the current device (device counter; this call synchronises the device). */
+RF_API rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates);
 #ifdef __cplusplus
 }
 #endif

@@ -34,7 +34,7 @@ ABI_SYMBOLS = [
     "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
     "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_last_profile", "rf_set_profiling",
-    "rf_debug_ln_dev", "rf_debug_philox_dev",
+    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters",
 ]
 
 
@@ -92,6 +92,7 @@ def lib():
             "rf_set_profiling": ([C.c_int], None),
             "rf_debug_ln_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_philox_dev": ([P, P, u64, P], C.c_int),
+            "rf_debug_counters": ([P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -342,6 +343,21 @@ def last_profile():
     cnt = np.zeros(cap, np.uint32)
     m = lib().rf_last_profile(C.cast(names, C.c_void_p), _ptr(ms), _ptr(cnt), cap)
     return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(m)}
+
+
+def counters():
+    """(kernel launches issued by the library, candidate splits evaluated on this device)."""
+    a, c = C.c_uint64(), C.c_uint64()
+    _check(lib().rf_debug_counters(C.byref(a), C.byref(c)))
+    return a.value, c.value
+
+
+def launch_count():
+    return counters()[0]
+
+
+def candidate_count():
+    return counters()[1]
 
 
 def debug_ln(y):

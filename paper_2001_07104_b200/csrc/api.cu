@@ -3,6 +3,7 @@
 // Every compute step runs in this library's CUDA kernels; there is no CPU
 // fallback (without a device every call returns RF_E_CUDA).
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -262,6 +263,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
   a.err = d.err;
+  a.cand = rf::candidate_counter();
   // trees per warp job: divides every prefix boundary so prefix sums align with jobs
   int g = 0;
   for (uint32_t i = 0; i < n_ntree; ++i) g = gcd_i(g, (int)ntrees[i]);
@@ -409,6 +411,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
     a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;
     a.cap = (uint32_t)cap; a.leaf_of_row = lor; a.err = d.err;
+    a.cand = rf::candidate_counter();
     size_t smem = 0;
     for (; a.wpb >= 1; a.wpb >>= 1) {
       smem = rf::small_tree_smem_bytes(a, 0);
@@ -445,6 +448,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   if (e == cudaSuccess) {
     dim3 grid((unsigned)std::min<uint64_t>((cap + 255) / 256, 64), (unsigned)T);
     k_compact_nodes<<<grid, 256, 0, s>>>(nodes_w, tidx_w, f->tree_off, T, cap, f->nodes, f->thr_index);
+    rf::note_launch();
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -459,6 +463,19 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
 }  // namespace
 
 namespace rf {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+unsigned long long* candidate_counter() {
+  static unsigned long long* ptrs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ptrs[dev]) {
+    if (cudaMalloc(&ptrs[dev], sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(ptrs[dev], 0, sizeof(unsigned long long));
+  }
+  return ptrs[dev];
+}
 bool prof_enabled() { return g_prof_on; }
 void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back(ProfRec{name, a, b}); }
 }  // namespace rf
@@ -811,6 +828,16 @@ uint32_t rf_last_profile(const char** names, double* ms, uint32_t* launches, uin
 rf_status rf_debug_ln_dev(const double* dy, double* dout, uint64_t n, void* stream) {
   if (rf_status st = check_device()) return st;
   CK(rf::device_ln(dy, dout, (int)n, static_cast<cudaStream_t>(stream)), "ln");
+  return RF_OK;
+}
+
+rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates) {
+  if (launches) *launches = rf::g_launches.load();
+  if (candidates) {
+    *candidates = 0;
+    unsigned long long* c = rf::candidate_counter();
+    if (c) CK(cudaMemcpy(candidates, c, 8, cudaMemcpyDeviceToHost), "counter");
+  }
   return RF_OK;
 }
 

@@ -8,6 +8,7 @@
 // Scoring: MAPE, Eq. 1, in percent, on raw targets.
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include "common.cuh"
+#include "host_util.cuh"
 #include "cv.cuh"
 
 namespace rf {
@@ -306,11 +307,13 @@ cudaError_t make_folds(const double* dy, int n, int k, int reps, uint64_t seed, 
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_folds_custom_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_folds_custom_small<<<reps, 256, smem, s>>>(dy, n, k, seed, dfold);
+    note_launch();
     return cudaGetLastError();
   }
   if (n <= kFoldSmallMax) {
     size_t smem = (size_t)n * 8;
     k_folds_plain_small<<<reps, 256, smem, s>>>(n, k, seed, dfold);
+    note_launch();
     return cudaGetLastError();
   }
   const size_t total = (size_t)n * reps;
@@ -323,17 +326,21 @@ cudaError_t make_folds(const double* dy, int n, int k, int reps, uint64_t seed, 
   char* temp = reinterpret_cast<char*>(offs + reps + 1);
   size_t temp_bytes = ws_bytes - (size_t)(temp - w);
   k_fold_keys<<<148 * 8, 256, 0, s>>>(n, reps, seed, kin, vin);
+  note_launch();
   k_seg_off<<<(reps + 1 + 127) / 128, 128, 0, s>>>(offs, reps, n);
+  note_launch();
   cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout,
                                                            (int64_t)total, reps, offs, offs + 1, 0, 64, s);
   if (e != cudaSuccess) return e;
   k_fold_scatter<<<148 * 8, 256, 0, s>>>(vout, n, k, reps, dfold);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t build_tasks(const int32_t* dfold, int k, const uint32_t*, const uint32_t*, TaskData& t,
                         cudaStream_t s) {
   k_tasks<<<t.ntask, 256, 0, s>>>(dfold, t.n, k, t.task0, t.tr_rows, t.te_rows, t.loc, t.ntr, t.nte);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -342,12 +349,14 @@ cudaError_t build_task_orders_u8(const uint32_t* order, const uint32_t* grank, T
   const int warps = t.ntask * t.p;
   k_task_orders_u8<<<(warps * 32 + 255) / 256, 256, 0, s>>>(order, grank, t.loc, t.n, t.p, t.ntask,
                                                            t.ntr_stride, t.ord, t.lrank);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t score_cv(const ScoreArgs& a, cudaStream_t s) {
   const int warps = a.n_mtry * a.n_ntree * a.ntask;
   k_score<<<(warps * 32 + 127) / 128, 128, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -361,6 +370,7 @@ cudaError_t finalize_cv(const double* reduced, const double* y, const int32_t* f
   a.fold_mape = fold_mape; a.pred = pred;
   const int warps = n_mtry * n_ntree * reps * k;
   k_finalize<<<(warps * 32 + 127) / 128, 128, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 

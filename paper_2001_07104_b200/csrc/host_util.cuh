@@ -29,6 +29,11 @@ struct Scratch {
   }
 };
 
+// count of this library's kernel launches (rf_debug_counters); defined in api.cu
+void note_launch(int n = 1);
+// device counter of evaluated candidate splits (algorithmic work of the split search)
+unsigned long long* candidate_counter();
+
 // per-kernel event timing (enabled by rf_set_profiling); defined in api.cu
 bool prof_enabled();
 void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b);

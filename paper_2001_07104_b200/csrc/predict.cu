@@ -7,6 +7,7 @@
 // tree order.  The forest (C1/C2: ~2 MB) stays L1/L2-resident; rows are read
 // with 8-byte loads.  Tuned variants live beside it (predict_kernel_*).
 #include "common.cuh"
+#include "host_util.cuh"
 #include "predict.cuh"
 
 namespace rf {
@@ -60,6 +61,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
   long long blocks = (n + 255) / 256;
   if (blocks > 148LL * 64) blocks = 148LL * 64;
   k_predict<<<(unsigned)blocks, 256, 0, s>>>(nodes, tree_off, T, X, n, p, mode, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -69,6 +71,7 @@ cudaError_t predict_finalize(const double* partial, long long n, int T, int targ
   long long blocks = (n + 255) / 256;
   if (blocks > 148LL * 16) blocks = 148LL * 16;
   k_pred_finalize<<<(unsigned)blocks, 256, 0, s>>>(partial, n, T, target, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -77,6 +80,7 @@ cudaError_t check_finite(const double* X, size_t total, int* err, cudaStream_t s
   size_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_check_finite<<<(unsigned)blocks, 256, 0, s>>>(X, total, err);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 //     radix sort of order-preserving u64 keys + a per-feature rank scan.
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include "common.cuh"
+#include "host_util.cuh"
 #include "ddlog.cuh"
 #include "prep.cuh"
 
@@ -172,9 +173,12 @@ cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int t
   const size_t total = (size_t)n * p;
   int gx = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
   k_prep_X<<<gx > 0 ? gx : 1, 256, 0, s>>>(dX, d.X, total, d.err);
+  note_launch();
   int gy = std::min((n + 255) / 256, 148 * 8);
   k_prep_y<<<gy > 0 ? gy : 1, 256, 0, s>>>(dy, scratch_t, n, target, require_pos, maxbits, d.err);
+  note_launch();
   k_quant<<<gy > 0 ? gy : 1, 256, 0, s>>>(scratch_t, n, maxbits, d.tq, d.F);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -203,6 +207,7 @@ cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_presort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_presort_small<<<p, 256, smem, s>>>(d.X, n, p, d.order, d.grank);
+    note_launch();
     return cudaGetLastError();
   }
   const size_t total = (size_t)n * p;
@@ -214,11 +219,14 @@ cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
   char* temp = reinterpret_cast<char*>(offs + p + 1);
   size_t temp_bytes = ws_bytes - (size_t)(temp - w);
   k_make_keys<<<148 * 8, 256, 0, s>>>(d.X, n, p, kin, vin);
+  note_launch();
   k_seg_offsets<<<(p + 1 + 127) / 128, 128, 0, s>>>(offs, p, n);
+  note_launch();
   cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, d.order,
                                                            (int64_t)total, p, offs, offs + 1, 0, 64, s);
   if (e != cudaSuccess) return e;
   k_rank_sorted<<<p, 1024, 0, s>>>(kout, d.order, n, d.grank);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -235,11 +243,13 @@ __global__ void k_philox(const uint32_t* in, uint32_t* out, int n) {
 cudaError_t device_philox(const uint32_t* ctr_key, uint32_t* out, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   k_philox<<<(n + 127) / 128, 128, 0, s>>>(ctr_key, out, n);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t device_ln(const double* dy, double* dout, int n, cudaStream_t s) {
   k_ln<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, s>>>(dy, dout, n);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -14,16 +14,21 @@
 //   leaf if depth cap, < min_split distinct rows, constant t_q or no
 //   candidate (R11); leaf value fl(S/W) 2^-F (R13).
 //
-// Layout per warp (shared memory): in-bag row lists of every feature, each
-// node-grouped and x-sorted (u8 local row ids), a position -> open-node map,
-// node tables of the current and the next level.  Per level: m search passes
-// (lane-serial runs of K = ceil(N/32) positions + one warp scan; node sums
-// recovered as global prefix minus the node's base), one mark pass (go-left
-// flags, child sums, child constancy), p stable in-place partition passes
-// (ballot-free: lane-serial counts + warp scan).
+// Per level the warp runs three lane-serial passes (each lane owns a
+// contiguous chunk; lane totals are combined by one warp scan):
+//   search    over (node, drawn feature, position) in node-major order, so a
+//             node's candidates are contiguous: node bests need no atomics --
+//             nodes inside a lane's chunk are resolved by that lane, nodes on
+//             chunk borders by one segmented warp reduction;
+//   mark      go-left flags, left sums, child constancy;
+//   partition all p feature lists, stable, ping-pong buffers.
+// fl(a / W) for the integer weights W <= 255 uses a table of y = RN(1/W) and
+// one Markstein correction q + fma(a - W q) y, which returns exactly RN(a/W)
+// (Markstein's theorem).
 //
 // CV mode routes the task's test rows level by level and accumulates their
 // leaf values per warp job; fit mode writes BFS-ordered 16-byte nodes.
+#include "host_util.cuh"
 #include "small_tree.cuh"
 
 namespace rf {
@@ -43,48 +48,44 @@ struct Carve {
 };
 
 struct CtaSmem {
-  uint8_t* ord;     // [p][ntr_max]
-  uint8_t* lrank;   // [p][ntr_max]
-  int64_t* tq;      // [ntr_max]
-  double* xte;      // [nte_max][p]
+  uint8_t* ord;    // [p][ntr_max] local rows in x order
+  uint8_t* lrank;  // [p][ntr_max] dense rank of x among training rows, by local row
+  int64_t* tq;     // [ntr_max]
+  double* rcp;     // [256] RN(1/w)
+  double* xte;     // [nte_max][p]
 };
 
-struct NodeSet {  // one level of open nodes
+struct NodeSet {  // open nodes of one level
   uint8_t* start;
   uint8_t* len;
-  uint32_t* W;
+  uint16_t* W;
   int64_t* S;
   uint64_t* heap;
-  uint32_t* bfs;
+  uint16_t* bfs;
 };
 
 struct WarpSmem {
   uint8_t* w;       // [ntr_max] bootstrap multiplicities
-  uint8_t* list;    // [p][ntr_max]
-  uint8_t* pnode;   // [ntr_max]
-  uint8_t* pnode2;  // [ntr_max]
+  uint8_t* listA;   // [p][ntr_max]
+  uint8_t* listB;   // [p][ntr_max]
+  uint8_t* pnA;     // [ntr_max] position -> open node
+  uint8_t* pnB;
   uint8_t* side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
-  uint32_t* baseW;
-  int64_t* baseS;
-  uint8_t* feat;    // [NMAX][p]
-  unsigned long long* bestKey;
-  uint32_t* bestF;
-  uint32_t* bestPos;
-  unsigned long long* passKey;
-  uint32_t* passPos;
-  uint8_t* split;
-  double* thr;
-  uint32_t* thrIdx;
-  uint32_t* WL;
-  int64_t* SL;
-  int64_t* tqfL;
-  int64_t* tqfR;
-  uint8_t* nc;      // bit0: left child non-constant, bit1: right
-  uint8_t* chOpen;  // [NMAX][2]
-  double* chVal;    // [NMAX][2]
-  uint32_t* baseL;
+  uint8_t* feat;    // [NM][p] drawn features (partial Fisher-Yates)
+  unsigned long long* bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
+  uint32_t* baux;   // best (feature << 8 | position); bit 31 = split
+  uint32_t* bW;     // search: prefix base of W; mark: left W
+  uint64_t* bS;     // search: prefix base of S; mark: left S
+  uint32_t* nc;     // bit0 left child non-constant, bit1 right
+  uint8_t* chOpen;  // [NM][2] open index of the children or kNone
+  double* chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
+  uint16_t* baseL;  // exclusive prefix of left counts over split nodes
+  uint16_t* chBase; // BFS id of the left child
+  uint32_t* thrIdx; // fit mode: threshold rank
 };
+
+constexpr uint8_t kNone = 0xFF;
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
 
@@ -92,46 +93,41 @@ __host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_m
   s.ord = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.lrank = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.tq = c.take<int64_t>(ntr_max, 16);
+  s.rcp = c.take<double>(256, 16);
   s.xte = c.take<double>((size_t)nte_max * p, 16);
 }
 
 __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
   s.start = c.take<uint8_t>(NM, 4);
   s.len = c.take<uint8_t>(NM, 4);
-  s.W = c.take<uint32_t>(NM, 4);
+  s.W = c.take<uint16_t>(NM, 4);
   s.S = c.take<int64_t>(NM, 8);
   s.heap = c.take<uint64_t>(NM, 8);
-  s.bfs = c.take<uint32_t>(NM, 4);
+  s.bfs = c.take<uint16_t>(NM, 4);
 }
 
-__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool need_feat) {
+__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool need_feat,
+                                           bool fit) {
   const int NM = nmax_of(ntr_max);
   s.w = c.take<uint8_t>((ntr_max + 3) / 4 * 4, 16);
-  s.list = c.take<uint8_t>((size_t)p * ntr_max, 16);
-  s.pnode = c.take<uint8_t>(ntr_max, 4);
-  s.pnode2 = c.take<uint8_t>(ntr_max, 4);
+  s.listA = c.take<uint8_t>((size_t)p * ntr_max, 16);
+  s.listB = c.take<uint8_t>((size_t)p * ntr_max, 16);
+  s.pnA = c.take<uint8_t>(ntr_max, 4);
+  s.pnB = c.take<uint8_t>(ntr_max, 4);
   s.side = c.take<uint8_t>(ntr_max, 4);
   carve_nodeset(c, s.cur, NM);
   carve_nodeset(c, s.nxt, NM);
-  s.baseW = c.take<uint32_t>(NM, 4);
-  s.baseS = c.take<int64_t>(NM, 8);
   s.feat = need_feat ? c.take<uint8_t>((size_t)NM * p, 4) : nullptr;
-  s.bestKey = c.take<unsigned long long>(NM, 8);
-  s.bestF = c.take<uint32_t>(NM, 4);
-  s.bestPos = c.take<uint32_t>(NM, 4);
-  s.passKey = c.take<unsigned long long>(NM, 8);
-  s.passPos = c.take<uint32_t>(NM, 4);
-  s.split = c.take<uint8_t>(NM, 4);
-  s.thr = c.take<double>(NM, 8);
-  s.thrIdx = c.take<uint32_t>(NM, 4);
-  s.WL = c.take<uint32_t>(NM, 4);
-  s.SL = c.take<int64_t>(NM, 8);
-  s.tqfL = c.take<int64_t>(NM, 8);
-  s.tqfR = c.take<int64_t>(NM, 8);
-  s.nc = c.take<uint8_t>((NM + 3) / 4 * 4, 4);
+  s.bkey = c.take<unsigned long long>(NM, 8);
+  s.baux = c.take<uint32_t>(NM, 4);
+  s.bW = c.take<uint32_t>(NM, 4);
+  s.bS = c.take<uint64_t>(NM, 8);
+  s.nc = c.take<uint32_t>(NM, 4);
   s.chOpen = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chVal = c.take<double>((size_t)NM * 2, 8);
-  s.baseL = c.take<uint32_t>(NM, 4);
+  s.baseL = c.take<uint16_t>(NM, 4);
+  s.chBase = c.take<uint16_t>(NM, 4);
+  s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : nullptr;
 }
 
 // ---------------------------------------------------------------- warp ops --
@@ -140,19 +136,19 @@ __device__ __forceinline__ uint32_t wscan_u32(uint32_t v, uint32_t& total) {
   uint32_t x = v;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
     if (lane >= d) x += y;
   }
   total = __shfl_sync(0xffffffffu, x, 31);
   return x - v;
 }
 
-__device__ __forceinline__ int64_t wscan_i64(int64_t v, int64_t& total) {
+__device__ __forceinline__ uint64_t wscan_u64(uint64_t v, uint64_t& total) {
   const int lane = threadIdx.x & 31;
-  int64_t x = v;
+  uint64_t x = v;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
     if (lane >= d) x += y;
   }
   total = __shfl_sync(0xffffffffu, x, 31);
@@ -176,14 +172,24 @@ __device__ __forceinline__ int64_t wmax_i64(int64_t v) {
 }
 
 __device__ __forceinline__ double leaf_value(int64_t S, uint32_t W, int F) {
-  return scalbn(__ddiv_rn(__ll2double_rn(S), __ll2double_rn((long long)W)), -F);
+  return scalbn(__ddiv_rn(__ll2double_rn(S), __uint2double_rn(W)), -F);
 }
 
-constexpr uint8_t kNone = 0xFF;
+// RN(a / w) for an integer 1 <= w <= 255 with y = RN(1/w): one Markstein correction
+__device__ __forceinline__ double div_small(double a, double dw, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-dw, q, a);
+  return __fma_rn(r, y, q);
+}
+
+// total order of candidates: key (G bits + 1) descending, aux (feature, position) ascending
+__device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsigned long long k2, uint32_t a2) {
+  return k1 > k2 || (k1 == k2 && a1 < a2);
+}
 
 // -------------------------------------------------------------- the kernel --
-// KM: max positions per lane (ceil(n_tr/32)); TM: max test rows per lane.
-template <bool kFit, int KM, int TM>
+// TM: max test rows per lane.
+template <bool kFit, int TM>
 __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   bid /= cta_per_mt;
   const int tl = bid % a.ntask;
   const int mi = bid / a.ntask;
-  const int mtry = a.mtrys[mi];
-  const bool need_feat = mtry < p;
+  const int m = a.mtrys[mi];
+  const bool need_feat = m < p;
   bool any_feat = false;
   for (int i = 0; i < a.n_mtry; ++i) any_feat |= (a.mtrys[i] < p);
 
@@ -208,13 +214,13 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max);
   WarpSmem ws;
   {
-    size_t cta_bytes = (cv.off + 15) / 16 * 16;
+    const size_t cta_bytes = (cv.off + 15) / 16 * 16;
     Carve cw(nullptr);
     WarpSmem dummy;
-    carve_warp(cw, dummy, p, ntr_max, any_feat);
-    size_t per_warp = (cw.off + 15) / 16 * 16;
+    carve_warp(cw, dummy, p, ntr_max, any_feat, kFit);
+    const size_t per_warp = (cw.off + 15) / 16 * 16;
     Carve mine(smem + cta_bytes + per_warp * warp);
-    carve_warp(mine, ws, p, ntr_max, any_feat);
+    carve_warp(mine, ws, p, ntr_max, any_feat, kFit);
   }
 
   const int ntr = a.ntr[tl];
@@ -227,15 +233,16 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     const uint8_t* go = a.ord + (size_t)tl * p * a.ntr_stride;
     const uint8_t* gr = a.lrank + (size_t)tl * p * a.ntr_stride;
     for (int i = threadIdx.x; i < p * ntr; i += blockDim.x) {
-      int f = i / ntr, j = i - f * ntr;
+      const int f = i / ntr, j = i - f * ntr;
       cs.ord[f * ntr_max + j] = go[(size_t)f * a.ntr_stride + j];
       cs.lrank[f * ntr_max + j] = gr[(size_t)f * a.ntr_stride + j];
     }
     for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) cs.rcp[i] = i ? __ddiv_rn(1.0, (double)i) : 0.0;
     if (!kFit) {
       const uint32_t* te_rows = a.te_rows + (size_t)tl * a.row_stride;
       for (int i = threadIdx.x; i < nte * p; i += blockDim.x) {
-        int r = i / p, f = i - r * p;
+        const int r = i / p, f = i - r * p;
         cs.xte[i] = a.X[(size_t)te_rows[r] * p + f];
       }
     }
@@ -248,7 +255,8 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   const int t_end = min(t_begin + a.Cw, a.tree_hi);
   const int task = a.task0 + tl;
 
-  double acc[TM];  // test row lane + 32 s
+  uint32_t ncand = 0;  // candidate splits evaluated by this lane
+  double acc[TM];      // test row lane + 32 s
 #pragma unroll
   for (int s = 0; s < TM; ++s) acc[s] = 0.0;
 
@@ -265,10 +273,10 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       for (int b = lane; b < nblk; b += 32) {
         uint64_t d0, d1;
         philox_pair(k0, k1, (uint32_t)b, 0u, 0u, kTagBoot, d0, d1);
-        uint32_t i0 = (uint32_t)mulhi64(d0, (uint64_t)ntr);
+        const uint32_t i0 = (uint32_t)mulhi64(d0, (uint64_t)ntr);
         atomicAdd(reinterpret_cast<uint32_t*>(ws.w) + (i0 >> 2), 1u << ((i0 & 3) * 8));
         if (2 * b + 1 < ntr) {
-          uint32_t i1 = (uint32_t)mulhi64(d1, (uint64_t)ntr);
+          const uint32_t i1 = (uint32_t)mulhi64(d1, (uint64_t)ntr);
           atomicAdd(reinterpret_cast<uint32_t*>(ws.w) + (i1 >> 2), 1u << ((i1 & 3) * 8));
         }
       }
@@ -285,9 +293,9 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     int64_t S = 0, mn = INT64_MAX, mx = INT64_MIN;
     uint32_t D = 0;
     for (int i = lane; i < ntr; i += 32) {
-      uint32_t wv = ws.w[i];
+      const uint32_t wv = ws.w[i];
       if (wv) {
-        int64_t v = cs.tq[i];
+        const int64_t v = cs.tq[i];
         S += (int64_t)wv * v;
         mn = v < mn ? v : mn;
         mx = v > mx ? v : mx;
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     uint32_t tcur = 0;  // packed: test row s -> open node (byte s), 0xFF = finished
     const bool root_leaf = (a.max_depth == 0) || ((int)D < a.min_split) || (mn == mx);
     if (root_leaf) {
-      double v = leaf_value(S, Wroot, F);
+      const double v = leaf_value(S, Wroot, F);
 #pragma unroll
       for (int s = 0; s < TM; ++s)
         if (lane + 32 * s < nte) acc[s] += v;
@@ -322,22 +330,27 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     }
 
     // ---- in-bag lists: stable compaction of the presorted orders by w > 0
+    uint8_t* L = ws.listA;
+    uint8_t* L2 = ws.listB;
+    uint8_t* pn = ws.pnA;
+    uint8_t* pn2 = ws.pnB;
+    NodeSet cur = ws.cur, nxt = ws.nxt;
     for (int f = 0; f < p; ++f) {
       uint32_t off = 0;
       for (int c = 0; c < ntr; c += 32) {
-        int j = c + lane;
+        const int j = c + lane;
         uint8_t r = 0;
         bool keep = false;
         if (j < ntr) { r = cs.ord[f * ntr_max + j]; keep = ws.w[r] != 0; }
-        unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) ws.list[f * ntr_max + off + __popc(bal & lanemask_lt())] = r;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) L[f * ntr_max + off + __popc(bal & lanemask_lt())] = r;
         off += __popc(bal);
       }
     }
-    for (int i = lane; i < (int)D; i += 32) ws.pnode[i] = 0;
+    for (int i = lane; i < (int)D; i += 32) pn[i] = 0;
     if (lane == 0) {
-      ws.cur.start[0] = 0; ws.cur.len[0] = (uint8_t)D; ws.cur.W[0] = Wroot; ws.cur.S[0] = S;
-      ws.cur.heap[0] = 1ull; ws.cur.bfs[0] = 0;
+      cur.start[0] = 0; cur.len[0] = (uint8_t)D; cur.W[0] = (uint16_t)Wroot; cur.S[0] = S;
+      cur.heap[0] = 1ull; cur.bfs[0] = 0;
     }
     __syncwarp();
 
@@ -347,40 +360,35 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     int depth = 0;
 
     while (nOpen > 0) {
-      const int K = (N + 31) >> 5;
-      const int pbeg = lane * K;
-      const int pend = min(pbeg + K, N);  // this lane's positions [pbeg, pend)
-
-      // (a) node bases (prefix trick), reset best, (b) feature draws
+      // ---------------- (a) per node: prefix bases, reset best, feature draws
       {
         uint32_t carryW = 0;
-        int64_t carryS = 0;
+        uint64_t carryS = 0;
         for (int b0 = 0; b0 < nOpen; b0 += 32) {
-          int k = b0 + lane;
-          bool act = k < nOpen;
-          uint32_t Wk = act ? ws.cur.W[k] : 0u;
-          int64_t Sk = act ? ws.cur.S[k] : 0;
+          const int k = b0 + lane;
+          const bool act = k < nOpen;
+          const uint32_t Wk = act ? cur.W[k] : 0u;
+          const uint64_t Sk = act ? (uint64_t)cur.S[k] : 0ull;
           uint32_t tW;
-          int64_t tS;
-          uint32_t eW = wscan_u32(Wk, tW);
-          int64_t eS = wscan_i64(Sk, tS);
+          uint64_t tS;
+          const uint32_t eW = wscan_u32(Wk, tW);
+          const uint64_t eS = wscan_u64(Sk, tS);
           if (act) {
-            ws.baseW[k] = carryW + eW;
-            ws.baseS[k] = carryS + eS;
-            ws.bestKey[k] = 0ull;
-            ws.bestF[k] = 0u;
-            ws.bestPos[k] = 0u;
+            ws.bW[k] = carryW + eW;  // prefix of W over earlier open nodes
+            ws.bS[k] = carryS + eS;
+            ws.bkey[k] = 0ull;
+            ws.baux[k] = 0x7FFFFFFFu;
             if (need_feat) {
               uint8_t* fp = ws.feat + (size_t)k * p;
               for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
-              const uint64_t h = ws.cur.heap[k];
+              const uint64_t h = cur.heap[k];
               const uint32_t hlo = (uint32_t)h, hhi = (uint32_t)(h >> 32);
-              for (int j = 0; j < mtry; j += 2) {
+              for (int j = 0; j < m; j += 2) {
                 uint64_t d0, d1;
                 philox_pair(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
                 int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
                 uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
-                if (j + 1 < mtry) {
+                if (j + 1 < m) {
                   r = j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1));
                   tmp = fp[j + 1]; fp[j + 1] = fp[r]; fp[r] = tmp;
                 }
@@ -393,192 +401,248 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       }
       __syncwarp();
 
-      // (d) search passes: one per drawn-feature slot j
-      for (int j = 0; j < mtry; ++j) {
-        for (int k = lane; k < nOpen; k += 32) { ws.passKey[k] = 0ull; ws.passPos[k] = 0xFFFFFFFFu; }
-        // pass 1: lane totals; first element's (node, rank) for the left neighbour lane
-        uint32_t lw = 0;
-        int64_t ls = 0;
-        uint32_t fn = kNone, frk = 0;
-        for (int pos = pbeg; pos < pend; ++pos) {
-          int k = ws.pnode[pos];
-          int f = need_feat ? ws.feat[(size_t)k * p + j] : j;
-          uint8_t r = ws.list[f * ntr_max + pos];
-          uint32_t w_ = ws.w[r];
-          lw += w_;
-          ls += (int64_t)w_ * cs.tq[r];
-          if (pos == pbeg) { fn = (uint32_t)k; frk = cs.lrank[f * ntr_max + r]; }
-        }
-        uint32_t totW;
-        int64_t totS;
-        uint32_t cW = wscan_u32(lw, totW);
-        int64_t cS = wscan_i64(ls, totS);
-        uint32_t nfn = __shfl_down_sync(0xffffffffu, fn, 1);
-        uint32_t nfrk = __shfl_down_sync(0xffffffffu, frk, 1);
-        if (lane == 31) nfn = kNone;
-        __syncwarp();
-        // pass 2: prefix sums, candidates at distinct-value boundaries, per-run best -> atomicMax
-        unsigned long long gk[KM];
-        unsigned long long runKey = 0ull;
-        int runNode = -1;
-#pragma unroll
-        for (int i = 0; i < KM; ++i) {
-          gk[i] = 0ull;
-          const int pos = pbeg + i;
-          if (pos < pend) {
-            int k = ws.pnode[pos];
-            int f = need_feat ? ws.feat[(size_t)k * p + j] : j;
-            uint8_t r = ws.list[f * ntr_max + pos];
-            uint32_t w_ = ws.w[r];
-            cW += w_;
-            cS += (int64_t)w_ * cs.tq[r];
-            uint32_t nk, nrk;
-            if (pos + 1 < pend) {
-              nk = ws.pnode[pos + 1];
-              nrk = (nk == (uint32_t)k) ? cs.lrank[f * ntr_max + ws.list[f * ntr_max + pos + 1]] : 0u;
-            } else {
-              nk = nfn;
-              nrk = nfrk;
-            }
-            if (nk == (uint32_t)k && nrk != cs.lrank[f * ntr_max + r]) {
-              uint32_t WLv = cW - ws.baseW[k];
-              int64_t SLv = cS - ws.baseS[k];
-              double G = split_gain((int64_t)WLv, SLv, (int64_t)(ws.cur.W[k] - WLv), ws.cur.S[k] - SLv);
-              gk[i] = (unsigned long long)__double_as_longlong(G) + 1ull;
-            }
-            if (k != runNode) {
-              if (runKey) atomicMax(&ws.passKey[runNode], runKey);
-              runNode = k;
-              runKey = 0ull;
-            }
-            runKey = gk[i] > runKey ? gk[i] : runKey;
-          }
-        }
-        if (runKey) atomicMax(&ws.passKey[runNode], runKey);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < KM; ++i)
-          if (gk[i]) {
-            int k = ws.pnode[pbeg + i];
-            if (gk[i] == ws.passKey[k]) atomicMin(&ws.passPos[k], (uint32_t)(pbeg + i));
-          }
-        __syncwarp();
-        for (int k = lane; k < nOpen; k += 32) {
-          unsigned long long pk = ws.passKey[k];
-          if (pk) {
-            uint32_t f = need_feat ? ws.feat[(size_t)k * p + j] : (uint32_t)j;
-            unsigned long long bk = ws.bestKey[k];
-            if (pk > bk || (pk == bk && f < ws.bestF[k])) {
-              ws.bestKey[k] = pk;
-              ws.bestF[k] = f;
-              ws.bestPos[k] = ws.passPos[k];
-            }
-          }
-        }
-        __syncwarp();
-      }
-
-      // (e) decisions; first-row targets of the children for the constancy test
-      for (int k = lane; k < nOpen; k += 32) {
-        bool sp = ws.bestKey[k] != 0ull;
-        ws.split[k] = sp;
-        if (sp) {
-          int f = ws.bestF[k];
-          ws.tqfL[k] = cs.tq[ws.list[f * ntr_max + ws.cur.start[k]]];
-          ws.tqfR[k] = cs.tq[ws.list[f * ntr_max + ws.bestPos[k] + 1]];
-        }
-      }
-      for (int k4 = lane; k4 < (nOpen + 3) / 4; k4 += 32) reinterpret_cast<uint32_t*>(ws.nc)[k4] = 0u;
-      __syncwarp();
-
-      // (f) mark pass: go-left flags, left sums at the chosen boundary, child constancy, threshold
+      // ---------------- (b) search pass over (node, feature slot, position), node-major
       {
+        const int E = m * N;
+        const int Kc = (E + 31) >> 5;
+        const int e0 = min(lane * Kc, E), e1 = min(e0 + Kc, E);
+        int k = 0, j = 0, i = 0, st = 0, ln = 1, f = 0;
+        auto locate = [&](int e) {
+          k = pn[min(e / m, N - 1)];
+          st = cur.start[k];
+          ln = cur.len[k];
+          const int off = e - m * st;
+          j = off / ln;
+          i = off - j * ln;
+          f = need_feat ? ws.feat[(size_t)k * p + j] : j;
+        };
+        auto advance = [&]() {
+          if (++i == ln) {
+            i = 0;
+            if (++j == m) {
+              j = 0;
+              ++k;
+              st = cur.start[k];
+              ln = cur.len[k];
+            }
+            f = need_feat ? ws.feat[(size_t)k * p + j] : j;
+          }
+        };
+        // pass 1: lane totals
         uint32_t lw = 0;
-        int64_t ls = 0;
-        for (int pos = pbeg; pos < pend; ++pos) {
-          int k = ws.pnode[pos];
-          if (!ws.split[k]) continue;
-          int f = ws.bestF[k];
-          uint8_t r = ws.list[f * ntr_max + pos];
-          uint32_t w_ = ws.w[r];
-          lw += w_;
-          ls += (int64_t)w_ * cs.tq[r];
-          bool left = pos <= (int)ws.bestPos[k];
-          ws.side[r] = left ? 1 : 0;
-          int64_t ref = left ? ws.tqfL[k] : ws.tqfR[k];
-          if (cs.tq[r] != ref)  // child not constant (two bits per node byte: word atomics)
-            atomicOr(reinterpret_cast<unsigned int*>(ws.nc + (k & ~3)), (left ? 1u : 2u) << ((k & 3) * 8));
+        uint64_t ls = 0;
+        if (e0 < e1) {
+          locate(e0);
+          for (int e = e0; e < e1; ++e) {
+            const uint8_t r = L[f * ntr_max + st + i];
+            const uint32_t wv = ws.w[r];
+            lw += wv;
+            ls += (uint64_t)((int64_t)wv * cs.tq[r]);
+            if (e + 1 < e1) advance();
+          }
         }
         uint32_t tW;
-        int64_t tS;
+        uint64_t tS;
         uint32_t cW = wscan_u32(lw, tW);
-        int64_t cS = wscan_i64(ls, tS);
-        for (int pos = pbeg; pos < pend; ++pos) {
-          int k = ws.pnode[pos];
-          if (!ws.split[k]) continue;
-          int f = ws.bestF[k];
-          uint8_t r = ws.list[f * ntr_max + pos];
-          uint32_t w_ = ws.w[r];
-          cW += w_;
-          cS += (int64_t)w_ * cs.tq[r];
-          if (pos == (int)ws.bestPos[k]) {
-            // prefix over split nodes only; made node-relative in (g)
-            ws.WL[k] = cW;
-            ws.SL[k] = cS;
-            uint8_t rb = ws.list[f * ntr_max + pos + 1];
-            uint32_t ga = tr_rows[r], gb = tr_rows[rb];
-            double xa = a.X[(size_t)ga * p + f], xb = a.X[(size_t)gb * p + f];
-            ws.thr[k] = midpoint_thr(xa, xb);
-            if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
+        uint64_t cS = wscan_u64(ls, tS);
+        // pass 2: prefix sums, candidates, best per node run
+        int hk = -1, rk = -1;  // head node, current run node
+        unsigned long long hkey = 0ull, rkey = 0ull;
+        uint32_t haux = 0x7FFFFFFFu, raux = 0x7FFFFFFFu;
+        if (e0 < e1) {
+          locate(e0);
+          hk = k;
+          rk = k;
+          uint32_t Wk = cur.W[k];
+          int64_t Sk = cur.S[k];
+          uint32_t segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
+          uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
+          uint8_t r = L[f * ntr_max + st + i];
+          for (int e = e0; e < e1; ++e) {
+            const uint32_t wv = ws.w[r];
+            cW += wv;
+            cS += (uint64_t)((int64_t)wv * cs.tq[r]);
+            uint8_t rn = 0;
+            if (i + 1 < ln) {
+              rn = L[f * ntr_max + st + i + 1];
+              if (cs.lrank[f * ntr_max + r] != cs.lrank[f * ntr_max + rn]) {
+                const uint32_t WL = cW - segW;
+                const int64_t SL = (int64_t)(cS - segS);
+                const uint32_t WR = Wk - WL;
+                const int64_t SR = Sk - SL;
+                const double dSL = __ll2double_rn(SL), dSR = __ll2double_rn(SR);
+                const double gl = div_small(__dmul_rn(dSL, dSL), (double)WL, cs.rcp[WL]);
+                const double gr = div_small(__dmul_rn(dSR, dSR), (double)WR, cs.rcp[WR]);
+                const unsigned long long key =
+                    (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull;
+                const uint32_t aux = ((uint32_t)f << 8) | (uint32_t)(st + i);
+                ++ncand;
+                if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
+              }
+            }
+            if (e + 1 < e1) {
+              const int pk = k;
+              advance();
+              if (k != pk) {
+                // the run of node pk ended inside this lane: head run or a complete node
+                if (pk == hk) { hkey = rkey; haux = raux; }
+                else { ws.bkey[pk] = rkey; ws.baux[pk] = raux; }
+                rkey = 0ull; raux = 0x7FFFFFFFu;
+                rk = k;
+                Wk = cur.W[k];
+                Sk = cur.S[k];
+              }
+              if (i == 0) {  // new segment (feature slot or node)
+                segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
+                segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
+                r = L[f * ntr_max + st];
+              } else {
+                r = rn;
+              }
+            }
           }
+          if (rk == hk) { hkey = rkey; haux = raux; }
+        }
+        // nodes on chunk borders: segmented suffix reduction of the head partials
+        unsigned long long vkey = hkey;
+        uint32_t vaux = haux;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int ok = __shfl_down_sync(0xffffffffu, hk, d);
+          const unsigned long long okey = __shfl_down_sync(0xffffffffu, vkey, d);
+          const uint32_t oaux = __shfl_down_sync(0xffffffffu, vaux, d);
+          if (lane + d < 32 && hk >= 0 && ok == hk && better(okey, oaux, vkey, vaux)) { vkey = okey; vaux = oaux; }
+        }
+        const int prev_tail = __shfl_up_sync(0xffffffffu, rk, 1);
+        const unsigned long long prev_tkey = __shfl_up_sync(0xffffffffu, rkey, 1);
+        const uint32_t prev_taux = __shfl_up_sync(0xffffffffu, raux, 1);
+        const int prev_head = __shfl_up_sync(0xffffffffu, hk, 1);
+        const int next_head = __shfl_down_sync(0xffffffffu, hk, 1);
+        if (hk >= 0) {
+          // the first lane whose head is hk writes it, merging the previous lane's tail run
+          if (lane == 0 || prev_head != hk) {
+            if (lane > 0 && prev_tail == hk && better(prev_tkey, prev_taux, vkey, vaux)) {
+              vkey = prev_tkey; vaux = prev_taux;
+            }
+            ws.bkey[hk] = vkey;
+            ws.baux[hk] = vaux;
+          }
+          // a tail run that does not continue into the next lane is a complete node
+          if (rk != hk && !(lane < 31 && next_head == rk)) { ws.bkey[rk] = rkey; ws.baux[rk] = raux; }
         }
       }
       __syncwarp();
 
-      // (g) children, node emission, next-level tables
-      int nSplitTotal = 0, nOpenNext = 0, Nnext = 0;
+      // ---------------- (c) decisions and thresholds
+      for (int k = lane; k < nOpen; k += 32) {
+        const unsigned long long key = ws.bkey[k];
+        ws.nc[k] = 0u;
+        ws.bW[k] = 0u;
+        ws.bS[k] = 0ull;
+        if (key) {
+          const uint32_t aux = ws.baux[k];
+          const int f = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
+          const uint8_t ra = L[f * ntr_max + bp], rb = L[f * ntr_max + bp + 1];
+          const uint32_t ga = tr_rows[ra], gb = tr_rows[rb];
+          const double thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
+          ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
+          ws.baux[k] = aux | 0x80000000u;  // split flag
+          if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
+        }
+      }
+      __syncwarp();
+
+      // ---------------- (d) mark pass: go-left flags, left sums, child constancy
       {
-        uint32_t carryW = 0, carrySplit = 0, carryOpen = 0, carryPos = 0, carryL = 0;
-        int64_t carryS = 0;
+        const int Kp = (N + 31) >> 5;
+        const int p0 = min(lane * Kp, N), p1 = min(p0 + Kp, N);
+        int rk = -1;
+        uint32_t rw = 0, rnc = 0;
+        uint64_t rs = 0;
+        int64_t tqL = 0, tqR = 0;
+        int f = 0, bp = 0;
+        bool sp = false;
+        for (int pos = p0; pos < p1; ++pos) {
+          const int k = pn[pos];
+          if (k != rk) {
+            if (rk >= 0 && sp) {
+              atomicAdd(&ws.bW[rk], rw);
+              atomicAdd(reinterpret_cast<unsigned long long*>(&ws.bS[rk]), (unsigned long long)rs);
+              if (rnc) atomicOr(&ws.nc[rk], rnc);
+            }
+            rk = k; rw = 0; rs = 0; rnc = 0;
+            const uint32_t aux = ws.baux[k];
+            sp = (aux & 0x80000000u) != 0;
+            if (sp) {
+              f = (int)((aux >> 8) & 0xFFu);
+              bp = (int)(aux & 0xFFu);
+              tqL = cs.tq[L[f * ntr_max + cur.start[k]]];
+              tqR = cs.tq[L[f * ntr_max + bp + 1]];
+            }
+          }
+          if (!sp) continue;
+          const uint8_t r = L[f * ntr_max + pos];
+          const bool left = pos <= bp;
+          ws.side[r] = left ? 1 : 0;
+          const int64_t tv = cs.tq[r];
+          if (left) {
+            const uint32_t wv = ws.w[r];
+            rw += wv;
+            rs += (uint64_t)((int64_t)wv * tv);
+            if (tv != tqL) rnc |= 1u;
+          } else if (tv != tqR) {
+            rnc |= 2u;
+          }
+        }
+        if (rk >= 0 && sp) {
+          atomicAdd(&ws.bW[rk], rw);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&ws.bS[rk]), (unsigned long long)rs);
+          if (rnc) atomicOr(&ws.nc[rk], rnc);
+        }
+      }
+      __syncwarp();
+
+      // ---------------- (e) children, node emission, next-level tables
+      int nSplitTotal = 0, nOpenNext = 0, Nnext = 0, NL = 0;
+      {
+        uint32_t carrySplit = 0, carryOpen = 0, carryPos = 0, carryL = 0;
         for (int b0 = 0; b0 < nOpen; b0 += 32) {
-          int k = b0 + lane;
-          bool act = k < nOpen;
-          bool sp = act && ws.split[k];
-          uint32_t tW, tSp, tOpen, tPos, tL;
-          int64_t tS;
-          uint32_t eW = wscan_u32(sp ? ws.cur.W[k] : 0u, tW);
-          int64_t eS = wscan_i64(sp ? ws.cur.S[k] : 0, tS);
-          uint32_t eSp = wscan_u32(sp ? 1u : 0u, tSp);
+          const int k = b0 + lane;
+          const bool act = k < nOpen;
+          const uint32_t aux = act ? ws.baux[k] : 0u;
+          const bool sp = act && (aux & 0x80000000u);
           uint32_t WLv = 0, WRv = 0, lenL = 0, lenR = 0, nl = 0;
           int64_t SLv = 0, SRv = 0;
           bool openL = false, openR = false;
           if (sp) {
-            WLv = ws.WL[k] - (carryW + eW);
-            SLv = ws.SL[k] - (carryS + eS);
-            WRv = ws.cur.W[k] - WLv;
-            SRv = ws.cur.S[k] - SLv;
-            nl = ws.bestPos[k] - ws.cur.start[k] + 1;
+            WLv = ws.bW[k];
+            SLv = (int64_t)ws.bS[k];
+            WRv = cur.W[k] - WLv;
+            SRv = cur.S[k] - SLv;
+            nl = (aux & 0xFFu) - cur.start[k] + 1;
             lenL = nl;
-            lenR = ws.cur.len[k] - nl;
+            lenR = cur.len[k] - nl;
             const bool capd = (a.max_depth >= 0) && (depth + 1 >= a.max_depth);
-            const uint8_t ncb = ws.nc[k];
-            openL = !capd && (int)lenL >= a.min_split && (ncb & 1);
-            openR = !capd && (int)lenR >= a.min_split && (ncb & 2);
+            const uint32_t ncb = ws.nc[k];
+            openL = !capd && (int)lenL >= a.min_split && (ncb & 1u);
+            openR = !capd && (int)lenR >= a.min_split && (ncb & 2u);
           }
-          uint32_t eOpen = wscan_u32((openL ? 1u : 0u) + (openR ? 1u : 0u), tOpen);
-          uint32_t ePos = wscan_u32((openL ? lenL : 0u) + (openR ? lenR : 0u), tPos);
-          uint32_t eL = wscan_u32(sp ? nl : 0u, tL);
+          uint32_t tSp, tOpen, tPos, tL;
+          const uint32_t eSp = wscan_u32(sp ? 1u : 0u, tSp);
+          const uint32_t eOpen = wscan_u32((openL ? 1u : 0u) + (openR ? 1u : 0u), tOpen);
+          const uint32_t ePos = wscan_u32((openL ? lenL : 0u) + (openR ? lenR : 0u), tPos);
+          const uint32_t eL = wscan_u32(sp ? nl : 0u, tL);
           if (sp) {
             const uint32_t childBase = curBase + levelCount + 2 * (carrySplit + eSp);
-            ws.baseL[k] = carryL + eL;
-            ws.baseW[k] = childBase;  // baseW is dead after the search passes
+            ws.baseL[k] = (uint16_t)(carryL + eL);
+            ws.chBase[k] = (uint16_t)childBase;
             uint32_t oi = carryOpen + eOpen;
             uint32_t ps = carryPos + ePos;
             double vL = 0.0, vR = 0.0;
             if (openL) {
-              ws.nxt.start[oi] = (uint8_t)ps; ws.nxt.len[oi] = (uint8_t)lenL;
-              ws.nxt.W[oi] = WLv; ws.nxt.S[oi] = SLv;
-              ws.nxt.heap[oi] = 2ull * ws.cur.heap[k]; ws.nxt.bfs[oi] = childBase;
+              nxt.start[oi] = (uint8_t)ps; nxt.len[oi] = (uint8_t)lenL;
+              nxt.W[oi] = (uint16_t)WLv; nxt.S[oi] = SLv;
+              nxt.heap[oi] = 2ull * cur.heap[k]; nxt.bfs[oi] = (uint16_t)childBase;
               ws.chOpen[2 * k] = (uint8_t)oi;
               ++oi; ps += lenL;
             } else {
@@ -586,9 +650,9 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
               ws.chOpen[2 * k] = kNone;
             }
             if (openR) {
-              ws.nxt.start[oi] = (uint8_t)ps; ws.nxt.len[oi] = (uint8_t)lenR;
-              ws.nxt.W[oi] = WRv; ws.nxt.S[oi] = SRv;
-              ws.nxt.heap[oi] = 2ull * ws.cur.heap[k] + 1ull; ws.nxt.bfs[oi] = childBase + 1;
+              nxt.start[oi] = (uint8_t)ps; nxt.len[oi] = (uint8_t)lenR;
+              nxt.W[oi] = (uint16_t)WRv; nxt.S[oi] = SRv;
+              nxt.heap[oi] = 2ull * cur.heap[k] + 1ull; nxt.bfs[oi] = (uint16_t)(childBase + 1);
               ws.chOpen[2 * k + 1] = (uint8_t)oi;
             } else {
               vR = leaf_value(SRv, WRv, F);
@@ -599,9 +663,11 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             if (kFit) {
               Node16* tn = a.nodes + tree_slot * a.cap;
               uint32_t* ti = a.thr_index + tree_slot * a.cap;
-              const uint32_t me = ws.cur.bfs[k];
+              const uint32_t me = cur.bfs[k];
               Node16 nd;
-              nd.feat = (int32_t)ws.bestF[k]; nd.left = childBase; nd.v = ws.thr[k];
+              nd.feat = (int32_t)((aux >> 8) & 0xFFu);
+              nd.left = childBase;
+              nd.v = __longlong_as_double((long long)ws.bkey[k]);
               tn[me] = nd;
               ti[me] = ws.thrIdx[k];
               if (!openL) { Node16 l; l.feat = -1; l.left = 0; l.v = vL; tn[childBase] = l; ti[childBase] = 0; }
@@ -609,17 +675,15 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             }
           } else if (act) {
             // open node without any candidate split: leaf (R11)
-            double v = leaf_value(ws.cur.S[k], ws.cur.W[k], F);
+            const double v = leaf_value(cur.S[k], cur.W[k], F);
             ws.chVal[2 * k] = v;
             if (kFit) {
               Node16 nd;
               nd.feat = -1; nd.left = 0; nd.v = v;
-              a.nodes[tree_slot * a.cap + ws.cur.bfs[k]] = nd;
-              a.thr_index[tree_slot * a.cap + ws.cur.bfs[k]] = 0;
+              a.nodes[tree_slot * a.cap + cur.bfs[k]] = nd;
+              a.thr_index[tree_slot * a.cap + cur.bfs[k]] = 0;
             }
           }
-          carryW += tW;
-          carryS += tS;
           carrySplit += tSp;
           carryOpen += tOpen;
           carryPos += tPos;
@@ -628,23 +692,27 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         nSplitTotal = (int)carrySplit;
         nOpenNext = (int)carryOpen;
         Nnext = (int)carryPos;
+        NL = (int)carryL;
       }
       __syncwarp();
 
-      // (h) route the task's test rows one level down
+      // ---------------- (f) route the task's test rows one level down
       if (!kFit) {
 #pragma unroll
         for (int s = 0; s < TM; ++s) {
           const int r = lane + 32 * s;
-          uint32_t c = (tcur >> (8 * s)) & 0xFFu;
+          const uint32_t c = (tcur >> (8 * s)) & 0xFFu;
           if (r < nte && c != kNone) {
             const int k = (int)c;
+            const uint32_t aux = ws.baux[k];
             uint32_t nc_;
-            if (!ws.split[k]) {
+            if (!(aux & 0x80000000u)) {
               acc[s] += ws.chVal[2 * k];
               nc_ = kNone;
             } else {
-              const int sd = (cs.xte[(size_t)r * p + ws.bestF[k]] <= ws.thr[k]) ? 0 : 1;
+              const int f = (int)((aux >> 8) & 0xFFu);
+              const double thr = __longlong_as_double((long long)ws.bkey[k]);
+              const int sd = (cs.xte[(size_t)r * p + f] <= thr) ? 0 : 1;
               nc_ = ws.chOpen[2 * k + sd];
               if (nc_ == kNone) acc[s] += ws.chVal[2 * k + sd];
             }
@@ -653,58 +721,57 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         }
       }
 
-      // (i) stable in-place partition of every feature list; leaf rows dropped
-      for (int f = 0; f < p; ++f) {
-        uint32_t rows4[(KM + 3) / 4];
-        uint32_t sides = 0;  // 2 bits per element: 0 drop, 1 left, 2 right
+      // ---------------- (g) stable partition of all p lists (feature-major), ping-pong
+      const bool rows_debug = kFit && a.leaf_of_row != nullptr;
+      if (nOpenNext > 0 || rows_debug) {
+        const int E = p * N;
+        const int Kc = (E + 31) >> 5;
+        const int e0 = min(lane * Kc, E), e1 = min(e0 + Kc, E);
+        // pass 1: left elements in the chunk
         uint32_t lc = 0;
-#pragma unroll
-        for (int i = 0; i < KM; ++i) {
-          const int pos = pbeg + i;
-          if ((i & 3) == 0) rows4[i >> 2] = 0;
-          if (pos < pend) {
-            uint8_t r = ws.list[f * ntr_max + pos];
-            rows4[i >> 2] |= (uint32_t)r << (8 * (i & 3));
-            uint32_t s_ = ws.split[ws.pnode[pos]] ? (ws.side[r] ? 1u : 2u) : 0u;
-            sides |= s_ << (2 * i);
-            lc += (s_ == 1u);
+        {
+          int f = e0 / N, pos = e0 - f * (e0 / N == 0 ? 0 : N);
+          pos = e0 - f * N;
+          for (int e = e0; e < e1; ++e) {
+            const uint8_t r = L[f * ntr_max + pos];
+            lc += (ws.baux[pn[pos]] & 0x80000000u) && ws.side[r];
+            if (++pos == N) { pos = 0; ++f; }
           }
         }
         uint32_t tl_;
         uint32_t run = wscan_u32(lc, tl_);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < KM; ++i) {
-          const int pos = pbeg + i;
-          if (pos < pend) {
-            const int k = ws.pnode[pos];
-            const uint32_t s_ = (sides >> (2 * i)) & 3u;
-            const uint8_t r = (uint8_t)(rows4[i >> 2] >> (8 * (i & 3)));
-            if (s_) {
-              const uint32_t leftBefore = run - ws.baseL[k];
-              const int sideIdx = (s_ == 1u) ? 0 : 1;
+        {
+          int f = e0 / N, pos = e0 - (e0 / N) * N;
+          for (int e = e0; e < e1; ++e) {
+            const uint8_t r = L[f * ntr_max + pos];
+            const int k = pn[pos];
+            const bool sp = (ws.baux[k] & 0x80000000u) != 0;
+            if (sp) {
+              const bool left = ws.side[r] != 0;
+              const uint32_t leftBefore = run - (uint32_t)f * (uint32_t)NL - ws.baseL[k];
+              const int sideIdx = left ? 0 : 1;
               const uint8_t c = ws.chOpen[2 * k + sideIdx];
               if (c != kNone) {
-                uint32_t within = (s_ == 1u) ? leftBefore : (uint32_t)(pos - ws.cur.start[k]) - leftBefore;
-                uint32_t dest = ws.nxt.start[c] + within;
-                ws.list[f * ntr_max + dest] = r;
-                if (f == 0) ws.pnode2[dest] = c;
-              } else if (kFit && f == 0 && a.leaf_of_row) {
-                a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)(ws.baseW[k] + sideIdx);
+                const uint32_t within = left ? leftBefore : (uint32_t)(pos - cur.start[k]) - leftBefore;
+                const uint32_t dest = nxt.start[c] + within;
+                L2[f * ntr_max + dest] = r;
+                if (f == 0) pn2[dest] = c;
+              } else if (rows_debug && f == 0) {
+                a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)(ws.chBase[k] + sideIdx);
               }
-            } else if (kFit && f == 0 && a.leaf_of_row) {
-              a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)ws.cur.bfs[k];
+              run += left;
+            } else if (rows_debug && f == 0) {
+              a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)cur.bfs[k];
             }
-            if (s_ == 1u) ++run;
+            if (++pos == N) { pos = 0; ++f; }
           }
         }
-        __syncwarp();
       }
-
       // advance to the next level
       {
-        NodeSet tmp = ws.cur; ws.cur = ws.nxt; ws.nxt = tmp;
-        uint8_t* tp = ws.pnode; ws.pnode = ws.pnode2; ws.pnode2 = tp;
+        const NodeSet tmp = cur; cur = nxt; nxt = tmp;
+        uint8_t* t8 = L; L = L2; L2 = t8;
+        uint8_t* tp = pn; pn = pn2; pn2 = tp;
       }
       curBase += levelCount;
       levelCount = 2u * (uint32_t)nSplitTotal;
@@ -717,11 +784,16 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     __syncwarp();
   }
 
+  if (a.cand) {
+    unsigned long long c = ncand;
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if (lane == 0) atomicAdd(a.cand, c);
+  }
   if (!kFit) {
     double* out = a.partial + (((size_t)mi * a.ntask + tl) * a.nsub + sub) * a.nte_max;
 #pragma unroll
     for (int s = 0; s < TM; ++s) {
-      int r = lane + 32 * s;
+      const int r = lane + 32 * s;
       if (r < nte) out[r] = acc[s];
     }
   }
@@ -735,41 +807,34 @@ size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   Carve c(nullptr);
   CtaSmem cs;
   carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max);
-  size_t cta = (c.off + 15) / 16 * 16;
+  const size_t cta = (c.off + 15) / 16 * 16;
   Carve w(nullptr);
   WarpSmem ws;
-  carve_warp(w, ws, a.p, a.ntr_max, any_feat);
-  size_t per_warp = (w.off + 15) / 16 * 16;
+  carve_warp(w, ws, a.p, a.ntr_max, any_feat, a.fit_mode != 0);
+  const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
 }
 
-template <bool kFit, int KM, int TM>
+template <bool kFit, int TM>
 static cudaError_t launch_t(const SmallArgs& a, size_t smem, unsigned grid, cudaStream_t s) {
-  auto kern = small_tree_kernel<kFit, KM, TM>;
+  auto kern = small_tree_kernel<kFit, TM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, 32 * a.wpb, smem, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
-template <bool kFit, int TM>
-static cudaError_t launch_k(const SmallArgs& a, size_t smem, unsigned grid, cudaStream_t s) {
-  const int K = (a.ntr_max + 31) / 32;
-  if (K <= 4) return launch_t<kFit, 4, TM>(a, smem, grid, s);
-  if (K <= 6) return launch_t<kFit, 6, TM>(a, smem, grid, s);
-  return launch_t<kFit, 8, TM>(a, smem, grid, s);
-}
-
 cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s) {
-  size_t smem = small_tree_smem_bytes(a, 0);
-  int cta_per_mt = (a.nsub + a.wpb - 1) / a.wpb;
-  long long grid = (long long)a.n_mtry * a.ntask * cta_per_mt;
+  const size_t smem = small_tree_smem_bytes(a, 0);
+  const int cta_per_mt = (a.nsub + a.wpb - 1) / a.wpb;
+  const long long grid = (long long)a.n_mtry * a.ntask * cta_per_mt;
   if (grid <= 0) return cudaSuccess;
-  if (a.fit_mode) return launch_k<true, 1>(a, smem, (unsigned)grid, s);
+  if (a.fit_mode) return launch_t<true, 1>(a, smem, (unsigned)grid, s);
   const int TMn = (a.nte_max + 31) / 32;
-  if (TMn <= 1) return launch_k<false, 1>(a, smem, (unsigned)grid, s);
-  if (TMn <= 2) return launch_k<false, 2>(a, smem, (unsigned)grid, s);
-  return launch_k<false, 8>(a, smem, (unsigned)grid, s);
+  if (TMn <= 1) return launch_t<false, 1>(a, smem, (unsigned)grid, s);
+  if (TMn <= 2) return launch_t<false, 2>(a, smem, (unsigned)grid, s);
+  return launch_t<false, 8>(a, smem, (unsigned)grid, s);
 }
 
 }  // namespace rf

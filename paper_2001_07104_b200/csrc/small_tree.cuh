@@ -49,6 +49,7 @@ struct SmallArgs {
   uint32_t cap;             // node capacity per tree (2 ntr - 1)
   int32_t* leaf_of_row;     // [tree_hi - tree_lo][n] or nullptr
   int* err;                 // device error flag
+  unsigned long long* cand; // evaluated candidate splits (counter) or null
 };
 
 // shared-memory bytes per block for the launch configuration
