@@ -51,7 +51,7 @@ struct CtaSmem {
   uint8_t* ord;    // [p][ntr_max] local rows in x order
   uint8_t* lrank;  // [p][ntr_max] dense rank of x among training rows, by local row
   int64_t* tq;     // [ntr_max]
-  double* rcp;     // [256] RN(1/w)
+  double2* rcp2;   // [256] (w, RN(1/w))
   double* xte;     // [nte_max][p]
 };
 
@@ -77,10 +77,9 @@ struct WarpSmem {
   uint32_t* baux;   // best (feature << 8 | position); bit 31 = split
   uint32_t* bW;     // search: prefix base of W; mark: left W
   uint64_t* bS;     // search: prefix base of S; mark: left S
-  uint32_t* nc;     // bit0 left child non-constant, bit1 right
+  uint8_t* ncb;     // [NM][2] child non-constant flags
   uint8_t* chOpen;  // [NM][2] open index of the children or kNone
   double* chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
-  uint16_t* baseL;  // exclusive prefix of left counts over split nodes
   uint16_t* chBase; // BFS id of the left child
   uint32_t* thrIdx; // fit mode: threshold rank
 };
@@ -93,7 +92,7 @@ __host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_m
   s.ord = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.lrank = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.tq = c.take<int64_t>(ntr_max, 16);
-  s.rcp = c.take<double>(256, 16);
+  s.rcp2 = c.take<double2>(256, 16);
   s.xte = c.take<double>((size_t)nte_max * p, 16);
 }
 
@@ -122,10 +121,9 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.baux = c.take<uint32_t>(NM, 4);
   s.bW = c.take<uint32_t>(NM, 4);
   s.bS = c.take<uint64_t>(NM, 8);
-  s.nc = c.take<uint32_t>(NM, 4);
+  s.ncb = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chOpen = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chVal = c.take<double>((size_t)NM * 2, 8);
-  s.baseL = c.take<uint16_t>(NM, 4);
   s.chBase = c.take<uint16_t>(NM, 4);
   s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : nullptr;
 }
@@ -238,7 +236,8 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       cs.lrank[f * ntr_max + j] = gr[(size_t)f * a.ntr_stride + j];
     }
     for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) cs.rcp[i] = i ? __ddiv_rn(1.0, (double)i) : 0.0;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      cs.rcp2[i] = make_double2((double)i, i ? __ddiv_rn(1.0, (double)i) : 0.0);
     if (!kFit) {
       const uint32_t* te_rows = a.te_rows + (size_t)tl * a.row_stride;
       for (int i = threadIdx.x; i < nte * p; i += blockDim.x) {
@@ -406,18 +405,37 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         const int E = m * N;
         const int Kc = (E + 31) >> 5;
         const int e0 = min(lane * Kc, E), e1 = min(e0 + Kc, E);
-        int k = 0, j = 0, i = 0, st = 0, ln = 1, f = 0;
-        auto locate = [&](int e) {
+        const int cnt = e1 - e0;  // this lane's elements; the loops below run Kc steps in lock-step
+        // cursor over (node k, feature slot j, index i in the segment)
+        int k, j, i, st, ln, f, lbase;
+        uint32_t Wk;
+        int64_t Sk;
+        {
+          const int e = min(e0, E - 1);
           k = pn[min(e / m, N - 1)];
           st = cur.start[k];
           ln = cur.len[k];
+          Wk = cur.W[k];
+          Sk = cur.S[k];
           const int off = e - m * st;
           j = off / ln;
           i = off - j * ln;
-          f = need_feat ? ws.feat[(size_t)k * p + j] : j;
-        };
-        auto advance = [&]() {
-          if (++i == ln) {
+          f = need_feat ? ws.feat[k * p + j] : j;
+          lbase = f * ntr_max;
+        }
+        const int k_init = k, j_init = j, i_init = i, st_init = st, ln_init = ln, f_init = f;
+        const uint32_t W_init = Wk;
+        const int64_t S_init = Sk;
+        // pass 1: lane totals
+        uint32_t lw = 0;
+        uint64_t ls = 0;
+        for (int c = 0; c < Kc; ++c) {
+          const bool act = c < cnt;
+          const uint8_t r = L[lbase + st + i];
+          const uint32_t wv = act ? (uint32_t)ws.w[r] : 0u;
+          lw += wv;
+          ls += (uint64_t)((int64_t)wv * cs.tq[r]);
+          if (++i == ln && c + 1 < cnt) {
             i = 0;
             if (++j == m) {
               j = 0;
@@ -425,120 +443,121 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
               st = cur.start[k];
               ln = cur.len[k];
             }
-            f = need_feat ? ws.feat[(size_t)k * p + j] : j;
-          }
-        };
-        // pass 1: lane totals
-        uint32_t lw = 0;
-        uint64_t ls = 0;
-        if (e0 < e1) {
-          locate(e0);
-          for (int e = e0; e < e1; ++e) {
-            const uint8_t r = L[f * ntr_max + st + i];
-            const uint32_t wv = ws.w[r];
-            lw += wv;
-            ls += (uint64_t)((int64_t)wv * cs.tq[r]);
-            if (e + 1 < e1) advance();
+            f = need_feat ? ws.feat[k * p + j] : j;
+            lbase = f * ntr_max;
           }
         }
         uint32_t tW;
         uint64_t tS;
         uint32_t cW = wscan_u32(lw, tW);
         uint64_t cS = wscan_u64(ls, tS);
-        // pass 2: prefix sums, candidates, best per node run
-        int hk = -1, rk = -1;  // head node, current run node
+        // pass 2: prefix sums, candidates at distinct-value boundaries, best per node run
+        k = k_init; j = j_init; i = i_init; st = st_init; ln = ln_init; f = f_init; lbase = f * ntr_max;
+        Wk = W_init; Sk = S_init;
+        const int hk = cnt > 0 ? k : -1;  // head node
+        int rk = hk;                      // current run node
         unsigned long long hkey = 0ull, rkey = 0ull;
         uint32_t haux = 0x7FFFFFFFu, raux = 0x7FFFFFFFu;
-        if (e0 < e1) {
-          locate(e0);
-          hk = k;
-          rk = k;
-          uint32_t Wk = cur.W[k];
-          int64_t Sk = cur.S[k];
-          uint32_t segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
-          uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
-          uint8_t r = L[f * ntr_max + st + i];
-          for (int e = e0; e < e1; ++e) {
-            const uint32_t wv = ws.w[r];
-            cW += wv;
-            cS += (uint64_t)((int64_t)wv * cs.tq[r]);
-            uint8_t rn = 0;
-            if (i + 1 < ln) {
-              rn = L[f * ntr_max + st + i + 1];
-              if (cs.lrank[f * ntr_max + r] != cs.lrank[f * ntr_max + rn]) {
-                const uint32_t WL = cW - segW;
-                const int64_t SL = (int64_t)(cS - segS);
-                const uint32_t WR = Wk - WL;
-                const int64_t SR = Sk - SL;
-                const double dSL = __ll2double_rn(SL), dSR = __ll2double_rn(SR);
-                const double gl = div_small(__dmul_rn(dSL, dSL), (double)WL, cs.rcp[WL]);
-                const double gr = div_small(__dmul_rn(dSR, dSR), (double)WR, cs.rcp[WR]);
-                const unsigned long long key =
-                    (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull;
-                const uint32_t aux = ((uint32_t)f << 8) | (uint32_t)(st + i);
-                ++ncand;
-                if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
-              }
+        uint32_t hWL = 0, rWL = 0;   // left sums of the best candidate (children sums)
+        int64_t hSL = 0, rSL = 0;
+        uint32_t segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
+        uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
+        uint8_t r = L[lbase + st + i];
+        uint32_t rkr = cs.lrank[lbase + r];
+        for (int c = 0; c < Kc; ++c) {
+          const bool act = c < cnt;
+          const uint32_t wv = act ? (uint32_t)ws.w[r] : 0u;
+          cW += wv;
+          cS += (uint64_t)((int64_t)wv * cs.tq[r]);
+          const bool hasNext = i + 1 < ln;
+          uint8_t rn = L[lbase + st + (hasNext ? i + 1 : i)];
+          uint32_t rkn = cs.lrank[lbase + rn];
+          const uint32_t WL = cW - segW;
+          const int64_t SL = (int64_t)(cS - segS);
+          const uint32_t WR = Wk - WL;
+          const int64_t SR = Sk - SL;
+          const double dSL = __ll2double_rn(SL), dSR = __ll2double_rn(SR);
+          const double2 yl = cs.rcp2[WL & 0xFFu], yr = cs.rcp2[WR & 0xFFu];
+          const double gl = div_small(__dmul_rn(dSL, dSL), yl.x, yl.y);
+          const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
+          const bool cand = act && hasNext && rkr != rkn;
+          const unsigned long long key =
+              cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
+          const uint32_t aux = ((uint32_t)f << 8) | (uint32_t)(st + i);
+          ncand += cand;
+          if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
+          if (!hasNext && c + 1 < cnt) {
+            // end of segment: next feature slot or next node
+            i = 0;
+            if (++j == m) {
+              j = 0;
+              // node k complete inside this lane (no other lane reads its bW/bS any more)
+              if (k == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
+              else { ws.bkey[k] = rkey; ws.baux[k] = raux; ws.bW[k] = rWL; ws.bS[k] = (uint64_t)rSL; }
+              rkey = 0ull; raux = 0x7FFFFFFFu;
+              ++k;
+              rk = k;
+              st = cur.start[k];
+              ln = cur.len[k];
+              Wk = cur.W[k];
+              Sk = cur.S[k];
             }
-            if (e + 1 < e1) {
-              const int pk = k;
-              advance();
-              if (k != pk) {
-                // the run of node pk ended inside this lane: head run or a complete node
-                if (pk == hk) { hkey = rkey; haux = raux; }
-                else { ws.bkey[pk] = rkey; ws.baux[pk] = raux; }
-                rkey = 0ull; raux = 0x7FFFFFFFu;
-                rk = k;
-                Wk = cur.W[k];
-                Sk = cur.S[k];
-              }
-              if (i == 0) {  // new segment (feature slot or node)
-                segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
-                segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
-                r = L[f * ntr_max + st];
-              } else {
-                r = rn;
-              }
-            }
+            f = need_feat ? ws.feat[k * p + j] : j;
+            lbase = f * ntr_max;
+            segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
+            segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
+            rn = L[lbase + st];
+            rkn = cs.lrank[lbase + rn];
+          } else if (act) {
+            ++i;
           }
-          if (rk == hk) { hkey = rkey; haux = raux; }
+          r = rn;
+          rkr = rkn;
         }
+        if (cnt > 0 && rk == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
         // nodes on chunk borders: segmented suffix reduction of the head partials
         unsigned long long vkey = hkey;
-        uint32_t vaux = haux;
+        uint32_t vaux = haux, vWL = hWL;
+        int64_t vSL = hSL;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
           const int ok = __shfl_down_sync(0xffffffffu, hk, d);
           const unsigned long long okey = __shfl_down_sync(0xffffffffu, vkey, d);
           const uint32_t oaux = __shfl_down_sync(0xffffffffu, vaux, d);
-          if (lane + d < 32 && hk >= 0 && ok == hk && better(okey, oaux, vkey, vaux)) { vkey = okey; vaux = oaux; }
+          const uint32_t oWL = __shfl_down_sync(0xffffffffu, vWL, d);
+          const int64_t oSL = __shfl_down_sync(0xffffffffu, vSL, d);
+          if (lane + d < 32 && hk >= 0 && ok == hk && better(okey, oaux, vkey, vaux)) {
+            vkey = okey; vaux = oaux; vWL = oWL; vSL = oSL;
+          }
         }
         const int prev_tail = __shfl_up_sync(0xffffffffu, rk, 1);
         const unsigned long long prev_tkey = __shfl_up_sync(0xffffffffu, rkey, 1);
         const uint32_t prev_taux = __shfl_up_sync(0xffffffffu, raux, 1);
+        const uint32_t prev_tWL = __shfl_up_sync(0xffffffffu, rWL, 1);
+        const int64_t prev_tSL = __shfl_up_sync(0xffffffffu, rSL, 1);
         const int prev_head = __shfl_up_sync(0xffffffffu, hk, 1);
         const int next_head = __shfl_down_sync(0xffffffffu, hk, 1);
         if (hk >= 0) {
           // the first lane whose head is hk writes it, merging the previous lane's tail run
           if (lane == 0 || prev_head != hk) {
             if (lane > 0 && prev_tail == hk && better(prev_tkey, prev_taux, vkey, vaux)) {
-              vkey = prev_tkey; vaux = prev_taux;
+              vkey = prev_tkey; vaux = prev_taux; vWL = prev_tWL; vSL = prev_tSL;
             }
-            ws.bkey[hk] = vkey;
-            ws.baux[hk] = vaux;
+            ws.bkey[hk] = vkey; ws.baux[hk] = vaux; ws.bW[hk] = vWL; ws.bS[hk] = (uint64_t)vSL;
           }
           // a tail run that does not continue into the next lane is a complete node
-          if (rk != hk && !(lane < 31 && next_head == rk)) { ws.bkey[rk] = rkey; ws.baux[rk] = raux; }
+          if (rk != hk && !(lane < 31 && next_head == rk)) {
+            ws.bkey[rk] = rkey; ws.baux[rk] = raux; ws.bW[rk] = rWL; ws.bS[rk] = (uint64_t)rSL;
+          }
         }
       }
       __syncwarp();
 
-      // ---------------- (c) decisions and thresholds
+      // ---------------- (c) decisions and thresholds; first-row targets of the children
       for (int k = lane; k < nOpen; k += 32) {
         const unsigned long long key = ws.bkey[k];
-        ws.nc[k] = 0u;
-        ws.bW[k] = 0u;
-        ws.bS[k] = 0ull;
+        ws.ncb[2 * k] = 0;
+        ws.ncb[2 * k + 1] = 0;
         if (key) {
           const uint32_t aux = ws.baux[k];
           const int f = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
@@ -548,56 +567,25 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
           ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
           ws.baux[k] = aux | 0x80000000u;  // split flag
           if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
+          reinterpret_cast<int64_t*>(ws.chVal)[2 * k] = cs.tq[L[f * ntr_max + cur.start[k]]];
+          reinterpret_cast<int64_t*>(ws.chVal)[2 * k + 1] = cs.tq[rb];
         }
       }
       __syncwarp();
 
-      // ---------------- (d) mark pass: go-left flags, left sums, child constancy
-      {
-        const int Kp = (N + 31) >> 5;
-        const int p0 = min(lane * Kp, N), p1 = min(p0 + Kp, N);
-        int rk = -1;
-        uint32_t rw = 0, rnc = 0;
-        uint64_t rs = 0;
-        int64_t tqL = 0, tqR = 0;
-        int f = 0, bp = 0;
-        bool sp = false;
-        for (int pos = p0; pos < p1; ++pos) {
+      // ---------------- (d) mark pass: go-left flags, child constancy (lock-step, no atomics)
+      for (int base = 0; base < N; base += 32) {
+        const int pos = base + lane;
+        if (pos < N) {
           const int k = pn[pos];
-          if (k != rk) {
-            if (rk >= 0 && sp) {
-              atomicAdd(&ws.bW[rk], rw);
-              atomicAdd(reinterpret_cast<unsigned long long*>(&ws.bS[rk]), (unsigned long long)rs);
-              if (rnc) atomicOr(&ws.nc[rk], rnc);
-            }
-            rk = k; rw = 0; rs = 0; rnc = 0;
-            const uint32_t aux = ws.baux[k];
-            sp = (aux & 0x80000000u) != 0;
-            if (sp) {
-              f = (int)((aux >> 8) & 0xFFu);
-              bp = (int)(aux & 0xFFu);
-              tqL = cs.tq[L[f * ntr_max + cur.start[k]]];
-              tqR = cs.tq[L[f * ntr_max + bp + 1]];
-            }
+          const uint32_t aux = ws.baux[k];
+          if (aux & 0x80000000u) {
+            const int f = (int)((aux >> 8) & 0xFFu);
+            const uint8_t r = L[f * ntr_max + pos];
+            const int sd = pos <= (int)(aux & 0xFFu) ? 0 : 1;
+            ws.side[r] = (uint8_t)(1 - sd);
+            if (cs.tq[r] != reinterpret_cast<const int64_t*>(ws.chVal)[2 * k + sd]) ws.ncb[2 * k + sd] = 1;
           }
-          if (!sp) continue;
-          const uint8_t r = L[f * ntr_max + pos];
-          const bool left = pos <= bp;
-          ws.side[r] = left ? 1 : 0;
-          const int64_t tv = cs.tq[r];
-          if (left) {
-            const uint32_t wv = ws.w[r];
-            rw += wv;
-            rs += (uint64_t)((int64_t)wv * tv);
-            if (tv != tqL) rnc |= 1u;
-          } else if (tv != tqR) {
-            rnc |= 2u;
-          }
-        }
-        if (rk >= 0 && sp) {
-          atomicAdd(&ws.bW[rk], rw);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&ws.bS[rk]), (unsigned long long)rs);
-          if (rnc) atomicOr(&ws.nc[rk], rnc);
         }
       }
       __syncwarp();
@@ -623,9 +611,8 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             lenL = nl;
             lenR = cur.len[k] - nl;
             const bool capd = (a.max_depth >= 0) && (depth + 1 >= a.max_depth);
-            const uint32_t ncb = ws.nc[k];
-            openL = !capd && (int)lenL >= a.min_split && (ncb & 1u);
-            openR = !capd && (int)lenR >= a.min_split && (ncb & 2u);
+            openL = !capd && (int)lenL >= a.min_split && ws.ncb[2 * k];
+            openR = !capd && (int)lenR >= a.min_split && ws.ncb[2 * k + 1];
           }
           uint32_t tSp, tOpen, tPos, tL;
           const uint32_t eSp = wscan_u32(sp ? 1u : 0u, tSp);
@@ -634,7 +621,6 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
           const uint32_t eL = wscan_u32(sp ? nl : 0u, tL);
           if (sp) {
             const uint32_t childBase = curBase + levelCount + 2 * (carrySplit + eSp);
-            ws.baseL[k] = (uint16_t)(carryL + eL);
             ws.chBase[k] = (uint16_t)childBase;
             uint32_t oi = carryOpen + eOpen;
             uint32_t ps = carryPos + ePos;
@@ -660,6 +646,14 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             }
             ws.chVal[2 * k] = vL;
             ws.chVal[2 * k + 1] = vR;
+            {
+              // packed partition record: start | baseL | dstL | dstR | openL | openR | split
+              const uint64_t dL = openL ? nxt.start[ws.chOpen[2 * k]] : kNone;
+              const uint64_t dR = openR ? nxt.start[ws.chOpen[2 * k + 1]] : kNone;
+              ws.bS[k] = (uint64_t)cur.start[k] | ((uint64_t)((carryL + eL) & 0xFFu) << 8) | (dL << 16) |
+                         (dR << 24) | ((uint64_t)ws.chOpen[2 * k] << 32) |
+                         ((uint64_t)ws.chOpen[2 * k + 1] << 40) | (1ull << 48);
+            }
             if (kFit) {
               Node16* tn = a.nodes + tree_slot * a.cap;
               uint32_t* ti = a.thr_index + tree_slot * a.cap;
@@ -677,6 +671,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             // open node without any candidate split: leaf (R11)
             const double v = leaf_value(cur.S[k], cur.W[k], F);
             ws.chVal[2 * k] = v;
+            ws.bS[k] = 0ull;  // partition record: not split
             if (kFit) {
               Node16 nd;
               nd.feat = -1; nd.left = 0; nd.v = v;
@@ -721,50 +716,51 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         }
       }
 
-      // ---------------- (g) stable partition of all p lists (feature-major), ping-pong
+      // ---------------- (g) stable partition of all p lists (feature-major), ping-pong.
+      // One pass in 32-element chunks: a ballot of go-left flags gives every
+      // element its rank among the left rows before it; the node record gives
+      // the child segments (bS[k] holds the packed record, see (e)).
       const bool rows_debug = kFit && a.leaf_of_row != nullptr;
       if (nOpenNext > 0 || rows_debug) {
         const int E = p * N;
-        const int Kc = (E + 31) >> 5;
-        const int e0 = min(lane * Kc, E), e1 = min(e0 + Kc, E);
-        // pass 1: left elements in the chunk
-        uint32_t lc = 0;
-        {
-          int f = e0 / N, pos = e0 - f * (e0 / N == 0 ? 0 : N);
-          pos = e0 - f * N;
-          for (int e = e0; e < e1; ++e) {
-            const uint8_t r = L[f * ntr_max + pos];
-            lc += (ws.baux[pn[pos]] & 0x80000000u) && ws.side[r];
-            if (++pos == N) { pos = 0; ++f; }
+        uint32_t carry = 0;
+        int f = 0, pos = lane;
+        while (pos >= N) { pos -= N; ++f; }
+        for (int base = 0; base < E; base += 32) {
+          const bool valid = base + lane < E;
+          uint64_t info = 0;
+          uint8_t r = 0;
+          int k = 0;
+          bool left = false;
+          if (valid) {
+            k = pn[pos];
+            info = ws.bS[k];
+            r = L[f * ntr_max + pos];
+            left = ((info >> 48) & 1u) && ws.side[r];
           }
-        }
-        uint32_t tl_;
-        uint32_t run = wscan_u32(lc, tl_);
-        {
-          int f = e0 / N, pos = e0 - (e0 / N) * N;
-          for (int e = e0; e < e1; ++e) {
-            const uint8_t r = L[f * ntr_max + pos];
-            const int k = pn[pos];
-            const bool sp = (ws.baux[k] & 0x80000000u) != 0;
-            if (sp) {
-              const bool left = ws.side[r] != 0;
-              const uint32_t leftBefore = run - (uint32_t)f * (uint32_t)NL - ws.baseL[k];
-              const int sideIdx = left ? 0 : 1;
-              const uint8_t c = ws.chOpen[2 * k + sideIdx];
-              if (c != kNone) {
-                const uint32_t within = left ? leftBefore : (uint32_t)(pos - cur.start[k]) - leftBefore;
-                const uint32_t dest = nxt.start[c] + within;
+          const unsigned bal = __ballot_sync(0xffffffffu, left);
+          if (valid) {
+            if ((info >> 48) & 1u) {
+              const uint32_t st = (uint32_t)(info & 0xFFu);
+              const uint32_t leftBefore =
+                  carry + __popc(bal & lanemask_lt()) - (uint32_t)f * (uint32_t)NL - (uint32_t)((info >> 8) & 0xFFu);
+              const uint32_t sh = left ? 0u : 8u;
+              const uint32_t d = (uint32_t)(info >> (16 + sh)) & 0xFFu;   // child segment start
+              if (d != kNone) {
+                const uint32_t within = left ? leftBefore : ((uint32_t)pos - st) - leftBefore;
+                const uint32_t dest = d + within;
                 L2[f * ntr_max + dest] = r;
-                if (f == 0) pn2[dest] = c;
+                if (f == 0) pn2[dest] = (uint8_t)(info >> (32 + sh));
               } else if (rows_debug && f == 0) {
-                a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)(ws.chBase[k] + sideIdx);
+                a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)(ws.chBase[k] + (left ? 0 : 1));
               }
-              run += left;
             } else if (rows_debug && f == 0) {
               a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)cur.bfs[k];
             }
-            if (++pos == N) { pos = 0; ++f; }
           }
+          carry += __popc(bal);
+          pos += 32;
+          while (pos >= N) { pos -= N; ++f; }
         }
       }
       // advance to the next level
