@@ -318,9 +318,9 @@ def measure_e2e(rfg, ds, args):
             "api": "rf_make_folds + rf_cross_validate_grid (host pointers)"}
 
 
-# fp64-pipe operations per evaluated candidate split (from the SASS of
-# split_gain: 2 x DMUL, 2 x DDIV sequence (MUFU.RCP64H + DFMA refinement), 1 x DADD)
-FP64_OPS_PER_CANDIDATE = 21
+# fp64 arithmetic per evaluated candidate split: 2 squares (DMUL),
+# 2 correctly rounded divisions by W <= 255 as DMUL + 2 DFMA each (Markstein), 1 DADD
+FP64_OPS_PER_CANDIDATE = 9
 FP64_PEAK_TOPS = 148 * 64 * 1.965e9 / 1e12
 
 
