@@ -182,6 +182,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2001_07104_b200 as rfg
+    from paper_2001_07104_b200.dist import gather_task_tables
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -206,12 +207,10 @@ def run_ours(args):
             rfg.cross_validate_grid(dX[i], dy[i], K_FOLDS, reps_total, NTREES, MTRYS, fold_ids=folds[i],
                                     target=1 if custom else 0, seed=SEED + i, task_begin=task_lo,
                                     task_end=task_hi, out=out[i])
-        if world > 1:
+        if world > 1:  # a11: fold-MAPE tables of all ranks, in task order (NCCL all_gather)
             for i in range(len(ds)):
-                mine = out[i].reshape(len(MTRYS), len(NTREES), -1)[:, :, task_lo:task_hi].contiguous()
-                gathered = torch.empty((world,) + mine.shape, dtype=mine.dtype, device=dev)
-                dist.all_gather_into_tensor(gathered, mine)
-                out[i].copy_(gathered.permute(1, 2, 0, 3).reshape(out[i].shape))
+                mine = out[i].reshape(len(MTRYS), len(NTREES), -1)[:, :, task_lo:task_hi]
+                out[i].copy_(gather_task_tables(mine, reps_total * K_FOLDS).reshape(out[i].shape))
 
     for _ in range(args.warmup):
         step()
