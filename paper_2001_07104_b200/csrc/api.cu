@@ -237,10 +237,27 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     ntr_max = std::max(ntr_max, hntr[i]);
     nte_max = std::max(nte_max, hnte[i]);
   }
-  if (ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode != RF_SPLIT_EXACT)
-    return rf::cv_large(dX, d, td, dfold, prm, k, reps, ntrees, n_ntree, mtrys, n_mtry, tree_lo,
-                        tree_hi, ntr_max, nte_max, dfold_mape, dpred, dpartial_rows, s, sc, g_err);
-
+  GridPlan gp = plan_mtry(mtrys, n_mtry);
+  const int nmd = (int)gp.mtry_distinct.size();
+  // trees per warp job / chunk: divides every prefix boundary so prefix sums align with jobs
+  int g = 0;
+  for (uint32_t i = 0; i < n_ntree; ++i) g = gcd_i(g, (int)ntrees[i]);
+  if (tree_lo) g = gcd_i(g, tree_lo);
+  if (tree_hi != Tmax) g = gcd_i(g, tree_hi);
+  const int T = tree_hi - tree_lo;
+  const bool large = ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode != RF_SPLIT_EXACT;
+  int Cw = 1, nsub = T;
+  double* partial = nullptr;
+  if (large) {
+    for (int c = 32; c >= 1; --c)
+      if (g % c == 0) { Cw = c; break; }
+    nsub = (T + Cw - 1) / Cw;
+    CK(sc.alloc(&partial, (size_t)nmd * ntask * nsub * nte_max), "alloc partial");
+    ProfScope ps("large_cv", s);
+    rf_status ls = rf::cv_large_partial(d, td, prm, gp.mtry_distinct, tree_lo, tree_hi, Cw, nsub, nte_max,
+                                        partial, s, sc, g_err);
+    if (ls) return ls;
+  } else {
   td.ntr_stride = ntr_max;
   CK(sc.alloc(&td.ord, (size_t)ntask * p * ntr_max), "alloc ord");
   CK(sc.alloc(&td.lrank, (size_t)ntask * p * ntr_max), "alloc lrank");
@@ -248,9 +265,6 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     ProfScope ps("task_orders", s);
     CK(rf::build_task_orders_u8(d.order, d.grank, td, s), "task orders");
   }
-
-  GridPlan gp = plan_mtry(mtrys, n_mtry);
-  const int nmd = (int)gp.mtry_distinct.size();
 
   rf::SmallArgs a;
   memset(&a, 0, sizeof a);
@@ -264,11 +278,6 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
   a.err = d.err;
   a.cand = rf::candidate_counter();
-  // trees per warp job: divides every prefix boundary so prefix sums align with jobs
-  int g = 0;
-  for (uint32_t i = 0; i < n_ntree; ++i) g = gcd_i(g, (int)ntrees[i]);
-  if (tree_lo) g = gcd_i(g, tree_lo);
-  if (tree_hi != Tmax) g = gcd_i(g, tree_hi);
   a.wpb = 4;
   size_t smem = 0;
   for (; a.wpb >= 1; a.wpb >>= 1) {
@@ -276,23 +285,21 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     if (smem <= 227 * 1024) break;
   }
   if (a.wpb == 0) return fail(RF_E_UNSUPPORTED, "small-tree kernel: shared memory budget exceeded");
-  const int T = tree_hi - tree_lo;
   const int resident = resident_warps(smem, a.wpb);
-  int Cw = 1;
   for (int c = 16; c >= 1; --c) {
     if (g % c) continue;
     long long jobs = (long long)nmd * ntask * ((T + c - 1) / c);
     if (jobs >= 2LL * resident || c == 1) { Cw = c; break; }
   }
   a.Cw = Cw;
-  a.nsub = (T + Cw - 1) / Cw;
-  double* partial;
+  a.nsub = nsub = (T + Cw - 1) / Cw;
   CK(sc.alloc(&partial, (size_t)nmd * ntask * a.nsub * nte_max), "alloc partial");
   a.partial = partial;
   {
     ProfScope ps("small_tree", s);
     CK(rf::launch_small_tree(a, s), "small_tree kernel");
   }
+  }  // small path
   // score every distinct mtry, then copy blocks for duplicates
   double* mape_d = nullptr;
   double* pred_d = nullptr;
@@ -306,7 +313,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   if (rows_d) CK(cudaMemsetAsync(rows_d, 0, nmd * blk_rows * 8, s), "memset");
   rf::ScoreArgs sa;
   memset(&sa, 0, sizeof sa);
-  sa.partial = partial; sa.n_mtry = nmd; sa.ntask = ntask; sa.nsub = a.nsub; sa.nte_max = nte_max;
+  sa.partial = partial; sa.n_mtry = nmd; sa.ntask = ntask; sa.nsub = nsub; sa.nte_max = nte_max;
   sa.Cw = Cw; sa.tree_lo = tree_lo; sa.te_rows = td.te_rows; sa.nte = td.nte; sa.n = (int)n;
   sa.k = (int)k; sa.reps = (int)reps; sa.task0 = task_lo; sa.n_ntree = (int)n_ntree;
   for (uint32_t i = 0; i < n_ntree; ++i) sa.ntrees[i] = (int)ntrees[i];

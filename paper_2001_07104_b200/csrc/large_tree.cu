@@ -1,19 +1,1038 @@
-// large_tree.cu -- placeholder until the level-synchronous large-n path lands.
+// large_tree.cu -- level-synchronous exact CART growth in global memory for
+// training sets beyond the CTA-resident kernel (n_tr > 255), SURVEY.md 8(d) C3.
+//
+// Same method and readings as small_tree.cu (sec. 2.2 P:202-215;
+// DESIGN.md R2-R14): identical bootstrap, heap-keyed feature draws, exact int64
+// split sums, canonical fp64 score, tie-break, thresholds, stopping, leaf values
+// and BFS node order.  A batch of B trees grows one level per round; all
+// kernels of a round cover every open node of every tree in the batch:
+//   node_prep   feature draws (Philox keyed by heap index), reset node bests
+//   search      flattened (node, drawn feature, position) elements in node-major
+//               order, tiles of 128 threads x KC elements: pass 1 tile totals,
+//               device-wide exclusive scan, pass 2 exact prefix sums (global
+//               prefix minus segment base, modular uint64) and candidate scores;
+//               per-thread run bests merged into the node best with a 128-bit
+//               compare-and-swap on (G key, feature|position) -- a total order,
+//               so the result does not depend on timing
+//   decide      split flag, threshold, first-row targets for the constancy test
+//   mark        go-left flags per row, child sums (warp-aggregated atomics),
+//               child constancy flags
+//   children    scans over nodes: BFS ids per tree, open children, positions;
+//               next-level node tables; BFS node emission
+//   partition   one CTA per (tree, feature) list: stable partition of every node
+//               segment by the go-left flag (block ballots + running carry)
+// Per-level sizes are read back once per round (one small D2H).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
+
 #include "large_tree.cuh"
+#include "predict.cuh"
 
 namespace rf {
+namespace {
 
-rf_status fit_large(const DevData&, const rf_params*, int, int, int, cudaStream_t, Scratch&, Node16**,
-                    uint32_t**, uint32_t**, uint64_t*, int32_t*, std::string& err) {
-  err = "large-n growth (n > 255 or histogram mode) not built yet";
-  return RF_E_UNSUPPORTED;
+constexpr int kThreads = 128;
+constexpr int kKC = 16;  // elements per thread in the search tiles
+constexpr int kTile = kThreads * kKC;
+
+struct __align__(16) Best {
+  unsigned long long key;  // G bits + 1 (0 = no candidate)
+  unsigned long long aux;  // feature << 32 | position in node (ascending = preferred)
+};
+
+__device__ __forceinline__ bool better(unsigned long long k1, unsigned long long a1, unsigned long long k2,
+                                       unsigned long long a2) {
+  return k1 > k2 || (k1 == k2 && a1 < a2);
 }
 
-rf_status cv_large(const double*, const DevData&, const TaskData&, const int32_t*, const rf_params*,
-                   uint32_t, uint32_t, const uint32_t*, uint32_t, const uint32_t*, uint32_t, int, int,
-                   int, int, double*, double*, double*, cudaStream_t, Scratch&, std::string& err) {
-  err = "large-n CV (n_tr > 255 or histogram mode) not built yet";
-  return RF_E_UNSUPPORTED;
+__device__ __forceinline__ void cas128(Best* addr, unsigned long long key, unsigned long long aux) {
+  unsigned long long clo = addr->key, chi = addr->aux;
+  while (better(key, aux, clo, chi)) {
+    unsigned long long olo, ohi;
+    asm volatile(
+        "{\n .reg .b128 d, c, v;\n mov.b128 c, {%2, %3};\n mov.b128 v, {%4, %5};\n"
+        " atom.global.cas.b128 d, [%6], c, v;\n mov.b128 {%0, %1}, d;\n}\n"
+        : "=l"(olo), "=l"(ohi)
+        : "l"(clo), "l"(chi), "l"(key), "l"(aux), "l"(addr)
+        : "memory");
+    if (olo == clo && ohi == chi) return;
+    clo = olo;
+    chi = ohi;
+  }
+}
+
+struct WS2 {  // (W, S) pair for scans; S in modular uint64
+  unsigned long long w, s;
+};
+struct WS2Sum {
+  __host__ __device__ WS2 operator()(const WS2& a, const WS2& b) const { return WS2{a.w + b.w, a.s + b.s}; }
+};
+struct U4S {  // children scan: split count, open-children count, open positions, left count
+  unsigned int sp, op, pos, nl;
+};
+struct U4Sum {
+  __host__ __device__ U4S operator()(const U4S& a, const U4S& b) const {
+    return U4S{a.sp + b.sp, a.op + b.op, a.pos + b.pos, a.nl + b.nl};
+  }
+};
+
+// node table (structure of arrays), one level
+struct Nodes {
+  uint32_t* tree;
+  uint32_t* start;  // first position in the tree's position space
+  uint32_t* len;    // distinct in-bag rows
+  uint32_t* W;      // sum of multiplicities
+  int64_t* S;       // sum of w * t_q
+  uint64_t* heap;
+  uint32_t* bfs;    // BFS id within the tree
+};
+
+struct Batch {
+  int B, n, p, m, ntr, mss, max_depth;
+  int F;
+  const double* X;
+  const int64_t* tq;
+  const uint32_t* grank;
+  const uint32_t* tr_rows;  // training rows (ascending)
+  uint32_t* keys;           // [B][2]
+  uint8_t* w;               // [B][n] by global row
+  uint8_t* side;            // [B][n]
+  uint32_t* L[2];           // [B][p][ntr]
+  uint32_t* posNode[2];     // [B*ntr] concatenated positions -> node
+  Nodes nd[2];
+  uint8_t* feat;            // [NMAX][m]
+  Best* best;               // [NMAX]
+  uint32_t* accW;           // [NMAX]
+  unsigned long long* accS; // [NMAX]
+  uint8_t* nc;              // [NMAX][2]
+  double* thr;              // [NMAX]
+  uint32_t* thrIdx;         // [NMAX]
+  WS2* nodePref;            // [NMAX] exclusive prefix of (W, S) over nodes
+  U4S* chScan;              // [NMAX] children scan (exclusive)
+  U4S* chVal;               // [NMAX]
+  uint8_t* chFlags;         // [NMAX] bit0 left child open, bit1 right child open
+  WS2* tileTot;             // [tiles]
+  // per tree (device)
+  uint32_t* tNode0;    // first node index of the tree at this level [B+1]
+  uint32_t* tPos0;     // first concatenated position [B+1]
+  uint32_t* tBase;     // BFS id of the first node of this level
+  uint32_t* tCount;    // nodes at this level (incl. leaves created at this depth)
+  // outputs
+  Node16* out;         // [B][cap]
+  uint32_t* outThr;    // [B][cap]
+  uint32_t* outCount;  // [B]
+  uint64_t cap;
+  int32_t* leaf_of_row;  // [B][n] or null
+  int tree0;             // global tree index of batch slot 0
+  int* err;
+};
+
+// ---------------------------------------------------------------- setup ------
+__global__ void k_keys_boot(Batch b, uint64_t seed, int task, int bootstrap) {
+  const int t = blockIdx.y;
+  uint32_t k0, k1;
+  tree_key(seed, (uint32_t)task, (uint32_t)(b.tree0 + t), k0, k1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) { b.keys[2 * t] = k0; b.keys[2 * t + 1] = k1; }
+  uint8_t* w = b.w + (size_t)t * b.n;
+  if (!bootstrap) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) w[b.tr_rows[j]] = 1;
+    return;
+  }
+  const int nblk = (b.ntr + 1) >> 1;
+  for (int blk = blockIdx.x * blockDim.x + threadIdx.x; blk < nblk; blk += gridDim.x * blockDim.x) {
+    uint64_t d0, d1;
+    philox_pair(k0, k1, (uint32_t)blk, 0u, 0u, kTagBoot, d0, d1);
+    const uint32_t r0 = b.tr_rows[mulhi64(d0, (uint64_t)b.ntr)];
+    unsigned int old = atomicAdd(reinterpret_cast<unsigned int*>(w + (r0 & ~3u)), 1u << ((r0 & 3u) * 8));
+    if (((old >> ((r0 & 3u) * 8)) & 0xFFu) == 0xFFu) atomicOr(b.err, kErrOverflow);
+    if (2 * blk + 1 < b.ntr) {
+      const uint32_t r1 = b.tr_rows[mulhi64(d1, (uint64_t)b.ntr)];
+      old = atomicAdd(reinterpret_cast<unsigned int*>(w + (r1 & ~3u)), 1u << ((r1 & 3u) * 8));
+      if (((old >> ((r1 & 3u) * 8)) & 0xFFu) == 0xFFu) atomicOr(b.err, kErrOverflow);
+    }
+  }
+}
+
+// one CTA per (tree, feature): stable compaction of the task order by w > 0
+__global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /*[p][ntr] global rows*/) {
+  const int t = blockIdx.x / b.p, f = blockIdx.x % b.p;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  const uint32_t* src = task_order + (size_t)f * b.ntr;
+  uint32_t* dst = b.L[0] + ((size_t)t * b.p + f) * b.ntr;
+  using BS = cub::BlockScan<uint32_t, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < b.ntr; base += kThreads) {
+    const int j = base + threadIdx.x;
+    uint32_t r = 0, keep = 0;
+    if (j < b.ntr) { r = src[j]; keep = w[r] != 0; }
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(keep, ex, tot);
+    if (keep) dst[carry + ex] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// root node of every tree: W, S, distinct count, constancy
+__global__ void k_root(Batch b, uint32_t* rootInfo /*[B][4]: D, leaf flag*/) {
+  const int t = blockIdx.x;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  long long S = 0;
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  unsigned int D = 0;
+  for (int j = threadIdx.x; j < b.ntr; j += blockDim.x) {
+    const uint32_t r = b.tr_rows[j];
+    const uint32_t wv = w[r];
+    if (wv) {
+      const long long v = b.tq[r];
+      S += (long long)wv * v;
+      mn = min(mn, v);
+      mx = max(mx, v);
+      ++D;
+    }
+  }
+  using BR = cub::BlockReduce<long long, 256>;
+  using BRu = cub::BlockReduce<unsigned int, 256>;
+  __shared__ typename BR::TempStorage t1;
+  __shared__ typename BRu::TempStorage t2;
+  const long long Ssum = BR(t1).Sum(S);
+  __syncthreads();
+  const long long mnr = BR(t1).Reduce(mn, cub::Min());
+  __syncthreads();
+  const long long mxr = BR(t1).Reduce(mx, cub::Max());
+  __syncthreads();
+  const unsigned int Dsum = BRu(t2).Sum(D);
+  if (threadIdx.x == 0) {
+    const bool leaf = (b.max_depth == 0) || ((int)Dsum < b.mss) || (mnr == mxr);
+    rootInfo[4 * t] = Dsum;
+    rootInfo[4 * t + 1] = leaf;
+    Node16 nd;
+    nd.feat = -1; nd.left = 0;
+    nd.v = scalbn(__ddiv_rn(__ll2double_rn(Ssum), __uint2double_rn((unsigned)b.ntr)), -b.F);
+    if (leaf) {
+      b.out[(size_t)t * b.cap] = nd;
+      b.outThr[(size_t)t * b.cap] = 0;
+      b.outCount[t] = 1;
+    }
+    reinterpret_cast<long long*>(rootInfo)[2 * t + 1] = Ssum;  // words 2,3
+  }
+}
+
+// -------------------------------------------------------------- per level ----
+__global__ void k_node_prep(Batch b, int cur, int NO) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Nodes& nd = b.nd[cur];
+  b.best[g] = Best{0ull, ~0ull};
+  b.accW[g] = 0u;
+  b.accS[g] = 0ull;
+  b.nc[2 * g] = 0;
+  b.nc[2 * g + 1] = 0;
+  uint8_t* fp = b.feat + (size_t)g * b.m;
+  if (b.m == b.p) {
+    for (int j = 0; j < b.m; ++j) fp[j] = (uint8_t)j;
+    return;
+  }
+  uint8_t perm[256];
+  for (int f = 0; f < b.p; ++f) perm[f] = (uint8_t)f;
+  const uint32_t t = nd.tree[g];
+  const uint32_t k0 = b.keys[2 * t], k1 = b.keys[2 * t + 1];
+  const uint64_t h = nd.heap[g];
+  for (int j = 0; j < b.m; j += 2) {
+    uint64_t d0, d1;
+    philox_pair(k0, k1, (uint32_t)(j >> 1), (uint32_t)h, (uint32_t)(h >> 32), kTagFeat, d0, d1);
+    int r = j + (int)mulhi64(d0, (uint64_t)(b.p - j));
+    uint8_t tmp = perm[j]; perm[j] = perm[r]; perm[r] = tmp;
+    if (j + 1 < b.m) {
+      r = j + 1 + (int)mulhi64(d1, (uint64_t)(b.p - j - 1));
+      tmp = perm[j + 1]; perm[j + 1] = perm[r]; perm[r] = tmp;
+    }
+  }
+  for (int j = 0; j < b.m; ++j) fp[j] = perm[j];
+}
+
+__global__ void k_node_ws(Batch b, int cur, int NO, WS2* out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  out[g] = WS2{(unsigned long long)b.nd[cur].W[g], (unsigned long long)b.nd[cur].S[g]};
+}
+
+// cursor over the flattened (node g, slot j, index i) space; positions are concatenated
+// over trees (node g's positions [gpos0, gpos0 + len))
+struct Cursor {
+  int g, j, i, len, t, start, f;
+  uint32_t W;
+  int64_t S;
+  long long listBase;  // offset of list (t, f) + start
+};
+
+__device__ __forceinline__ void cursor_load(const Batch& b, const Nodes& nd, Cursor& c) {
+  c.len = (int)nd.len[c.g];
+  c.t = (int)nd.tree[c.g];
+  c.start = (int)nd.start[c.g];
+  c.W = nd.W[c.g];
+  c.S = nd.S[c.g];
+}
+__device__ __forceinline__ void cursor_feat(const Batch& b, Cursor& c) {
+  c.f = b.feat[(size_t)c.g * b.m + c.j];
+  c.listBase = ((long long)c.t * b.p + c.f) * b.ntr + c.start;
+}
+// element e = m * gpos0(g) + j * len + i, gpos0 = concatenated first position of g
+__device__ __forceinline__ void cursor_locate(const Batch& b, const Nodes& nd, const uint32_t* posNode,
+                                              const uint32_t* tPos0, long long e, Cursor& c) {
+  const long long q = e / b.m;
+  c.g = (int)posNode[q];
+  cursor_load(b, nd, c);
+  const long long gpos0 = (long long)tPos0[c.t] + c.start;
+  const long long off = e - (long long)b.m * gpos0;
+  c.j = (int)(off / c.len);
+  c.i = (int)(off - (long long)c.j * c.len);
+  cursor_feat(b, c);
+}
+__device__ __forceinline__ void cursor_next_segment(const Batch& b, const Nodes& nd, Cursor& c) {
+  c.i = 0;
+  if (++c.j == b.m) {
+    c.j = 0;
+    ++c.g;
+    cursor_load(b, nd, c);
+  }
+  cursor_feat(b, c);
+}
+
+__global__ void __launch_bounds__(kThreads) k_search_tot(Batch b, int cur, long long E) {
+  const Nodes& nd = b.nd[cur];
+  const uint32_t* posNode = b.posNode[cur];
+  const long long e0 = (long long)blockIdx.x * kTile + (long long)threadIdx.x * kKC;
+  const long long e1 = min(e0 + kKC, E);
+  unsigned long long lw = 0, ls = 0;
+  if (e0 < e1) {
+    Cursor c;
+    cursor_locate(b, nd, posNode, b.tPos0, e0, c);
+    const uint8_t* w = b.w + (size_t)c.t * b.n;
+    for (long long e = e0; e < e1; ++e) {
+      const uint32_t r = b.L[cur & 1][c.listBase + c.i];
+      const uint32_t wv = b.w[(size_t)c.t * b.n + r];
+      lw += wv;
+      ls += (unsigned long long)((long long)wv * b.tq[r]);
+      if (++c.i == c.len && e + 1 < e1) cursor_next_segment(b, nd, c);
+    }
+    (void)w;
+  }
+  using BR = cub::BlockReduce<WS2, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const WS2 tot = BR(tmp).Reduce(WS2{lw, ls}, WS2Sum());
+  if (threadIdx.x == 0) b.tileTot[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kThreads) k_search_eval(Batch b, int cur, long long E,
+                                                          unsigned long long* ncand) {
+  const Nodes& nd = b.nd[cur];
+  const uint32_t* posNode = b.posNode[cur];
+  const uint32_t* L = b.L[cur & 1];
+  const long long e0 = (long long)blockIdx.x * kTile + (long long)threadIdx.x * kKC;
+  const long long e1 = min(e0 + kKC, E);
+  // pass 1: thread totals, block exclusive scan + tile prefix
+  unsigned long long lw = 0, ls = 0;
+  Cursor c0;
+  if (e0 < e1) {
+    cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
+    Cursor c = c0;
+    for (long long e = e0; e < e1; ++e) {
+      const uint32_t r = L[c.listBase + c.i];
+      const uint32_t wv = b.w[(size_t)c.t * b.n + r];
+      lw += wv;
+      ls += (unsigned long long)((long long)wv * b.tq[r]);
+      if (++c.i == c.len && e + 1 < e1) cursor_next_segment(b, nd, c);
+    }
+  }
+  using BS = cub::BlockScan<WS2, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  WS2 ex;
+  BS(tmp).ExclusiveScan(WS2{lw, ls}, ex, WS2{0ull, 0ull}, WS2Sum());
+  const WS2 tp = b.tileTot[blockIdx.x];  // exclusive prefix of the tile (scanned in place)
+  unsigned long long cW = tp.w + ex.w, cS = tp.s + ex.s;
+  if (e0 >= e1) return;
+  // pass 2
+  Cursor c = c0;
+  unsigned long long segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
+  unsigned long long segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
+  unsigned long long rkey = 0ull, raux = ~0ull;
+  int rg = c.g;
+  unsigned int nc = 0;
+  const uint32_t* grank = b.grank;
+  uint32_t r = L[c.listBase + c.i];
+  uint32_t rk = grank[(size_t)c.f * b.n + r];
+  for (long long e = e0; e < e1; ++e) {
+    const uint32_t wv = b.w[(size_t)c.t * b.n + r];
+    cW += wv;
+    cS += (unsigned long long)((long long)wv * b.tq[r]);
+    const bool hasNext = c.i + 1 < c.len;
+    uint32_t rn = r, rkn = rk;
+    if (hasNext) {
+      rn = L[c.listBase + c.i + 1];
+      rkn = grank[(size_t)c.f * b.n + rn];
+      if (rkn != rk) {
+        const unsigned long long WL = cW - segW;
+        const long long SL = (long long)(cS - segS);
+        const unsigned long long WR = (unsigned long long)c.W - WL;
+        const long long SR = c.S - SL;
+        const double G = split_gain((long long)WL, SL, (long long)WR, SR);
+        const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
+        const unsigned long long aux = ((unsigned long long)c.f << 32) | (unsigned long long)c.i;
+        ++nc;
+        if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
+      }
+    }
+    if (e + 1 < e1) {
+      if (!hasNext) {
+        const int pg = c.g;
+        cursor_next_segment(b, nd, c);
+        if (c.g != pg) {
+          if (rkey) cas128(&b.best[pg], rkey, raux);
+          rkey = 0ull; raux = ~0ull;
+          rg = c.g;
+        }
+        segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
+        segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
+        rn = L[c.listBase];
+        rkn = grank[(size_t)c.f * b.n + rn];
+      } else {
+        ++c.i;
+      }
+    }
+    r = rn;
+    rk = rkn;
+  }
+  if (rkey) cas128(&b.best[rg], rkey, raux);
+  if (ncand) {
+    unsigned long long v = nc;
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(ncand, v);
+  }
+}
+
+__global__ void k_decide(Batch b, int cur, int NO) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Nodes& nd = b.nd[cur];
+  const Best bs = b.best[g];
+  if (!bs.key) return;
+  const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), i = (int)(bs.aux & 0xFFFFFFFFull);
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
+  const uint32_t ra = L[i], rb = L[i + 1];
+  b.thr[g] = midpoint_thr(b.X[(size_t)ra * b.p + f], b.X[(size_t)rb * b.p + f]);
+  b.thrIdx[g] = b.grank[(size_t)f * b.n + ra];
+}
+
+// positions (concatenated): go-left flags, child left sums, child constancy
+__global__ void k_mark(Batch b, int cur, int NP) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const Nodes& nd = b.nd[cur];
+  int g = -1;
+  unsigned int wl = 0;
+  unsigned long long sl = 0;
+  if (q < NP) {
+    g = (int)b.posNode[cur][q];
+    const Best bs = b.best[g];
+    if (bs.key) {
+      const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), bi = (int)(bs.aux & 0xFFFFFFFFull);
+      const int start = (int)nd.start[g];
+      const int i = q - (int)b.tPos0[t] - start;
+      const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + start;
+      const uint32_t r = L[i];
+      const bool left = i <= bi;
+      b.side[(size_t)t * b.n + r] = left ? 1 : 0;
+      const long long tv = b.tq[r];
+      const long long ref = b.tq[left ? L[0] : L[bi + 1]];
+      if (tv != ref) b.nc[2 * g + (left ? 0 : 1)] = 1;
+      if (left) {
+        wl = b.w[(size_t)t * b.n + r];
+        sl = (unsigned long long)((long long)wl * tv);
+      }
+    } else {
+      g = -1;
+    }
+  }
+  // warp-aggregate runs of equal g (positions of a node are contiguous)
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int og = __shfl_down_sync(0xffffffffu, g, d);
+    const unsigned int ow = __shfl_down_sync(0xffffffffu, wl, d);
+    const unsigned long long os = __shfl_down_sync(0xffffffffu, sl, d);
+    if (lane + d < 32 && og == g) { wl += ow; sl += os; }
+  }
+  const int pg = __shfl_up_sync(0xffffffffu, g, 1);
+  if (g >= 0 && (lane == 0 || pg != g)) {
+    // wl/sl now hold the run total only for run heads whose run lies in [lane, lane+31]:
+    // the doubling above sums lanes l..l+2^k-1 with equal g, which covers the whole run
+    if (wl) atomicAdd(&b.accW[g], wl);
+    if (sl) atomicAdd(&b.accS[g], sl);
+  }
+}
+
+__global__ void k_children_count(Batch b, int cur, int NO, int depth) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Nodes& nd = b.nd[cur];
+  const Best bs = b.best[g];
+  U4S v{0u, 0u, 0u, 0u};
+  if (bs.key) {
+    const uint32_t nl = (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
+    const uint32_t lenL = nl, lenR = nd.len[g] - nl;
+    const bool capd = (b.max_depth >= 0) && (depth + 1 >= b.max_depth);
+    const bool oL = !capd && (int)lenL >= b.mss && b.nc[2 * g];
+    const bool oR = !capd && (int)lenR >= b.mss && b.nc[2 * g + 1];
+    v.sp = 1u;
+    v.op = (oL ? 1u : 0u) + (oR ? 1u : 0u);
+    v.pos = (oL ? lenL : 0u) + (oR ? lenR : 0u);
+    v.nl = nl;
+    b.chFlags[g] = (uint8_t)((oL ? 1u : 0u) | (oR ? 2u : 0u));
+  } else {
+    b.chFlags[g] = 0;
+  }
+  b.chVal[g] = v;
+}
+
+// per tree: next-level first node / position, BFS base, level count (from scans at tree borders)
+__global__ void k_tree_update(Batch b, int NO, uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > b.B) return;
+  const uint32_t g0 = b.tNode0[t];
+  const U4S s0 = g0 < (uint32_t)NO ? b.chScan[g0] : U4S{0, 0, 0, 0};
+  U4S send;
+  if (NO > 0) {
+    const U4S last = b.chScan[NO - 1], lv = b.chVal[NO - 1];
+    send = U4S{last.sp + lv.sp, last.op + lv.op, last.pos + lv.pos, last.nl + lv.nl};
+  } else {
+    send = U4S{0, 0, 0, 0};
+  }
+  const U4S a = g0 < (uint32_t)NO ? s0 : send;
+  nextNode0[t] = a.op;
+  nextPos0[t] = a.pos;
+  nlBase[t] = a.nl;
+  if (t < b.B) {
+    const uint32_t g1 = b.tNode0[t + 1];
+    const U4S e = g1 < (uint32_t)NO ? b.chScan[g1] : send;
+    // BFS bookkeeping: next level starts after this level's nodes; it has 2 * splits nodes
+    const uint32_t splits = e.sp - a.sp;
+    b.tBase[t] += b.tCount[t];
+    b.tCount[t] = 2u * splits;
+  }
+}
+
+__global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextNode0, const uint32_t* nextPos0,
+                                 const uint32_t* nlBase, int depth) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Nodes& nd = b.nd[cur];
+  Nodes& nx = b.nd[cur ^ 1];
+  const int t = (int)nd.tree[g];
+  Node16* out = b.out + (size_t)t * b.cap;
+  uint32_t* outThr = b.outThr + (size_t)t * b.cap;
+  const Best bs = b.best[g];
+  const uint32_t me = nd.bfs[g];
+  if (!bs.key) {  // open node without any candidate split: leaf (R11)
+    Node16 l;
+    l.feat = -1; l.left = 0;
+    l.v = scalbn(__ddiv_rn(__ll2double_rn(nd.S[g]), __uint2double_rn(nd.W[g])), -b.F);
+    out[me] = l;
+    outThr[me] = 0;
+    return;
+  }
+  const U4S sc = b.chScan[g], v = b.chVal[g];
+  const uint32_t g0 = b.tNode0[t];
+  const uint32_t splitRank = sc.sp - b.chScan[g0].sp;
+  // tBase/tCount were advanced by k_tree_update: tBase = first BFS id of the next level
+  const uint32_t childBase = b.tBase[t] + 2u * splitRank;
+  const uint32_t WLv = b.accW[g];
+  const int64_t SLv = (int64_t)b.accS[g];
+  const uint32_t WRv = nd.W[g] - WLv;
+  const int64_t SRv = nd.S[g] - SLv;
+  const uint32_t nl = v.nl, lenR = nd.len[g] - nl;
+  const bool oL = b.chFlags[g] & 1u, oR = b.chFlags[g] & 2u;
+  Node16 me_n;
+  me_n.feat = (int32_t)(bs.aux >> 32);
+  me_n.left = childBase;
+  me_n.v = b.thr[g];
+  out[me] = me_n;
+  outThr[me] = b.thrIdx[g];
+  uint32_t oi = sc.op;                             // global open index of the first child
+  uint32_t ps = sc.pos - nextPos0[t];              // tree-local position of the first child
+  if (oL) {
+    nx.tree[oi] = (uint32_t)t; nx.start[oi] = ps; nx.len[oi] = nl; nx.W[oi] = WLv; nx.S[oi] = SLv;
+    nx.heap[oi] = 2ull * nd.heap[g]; nx.bfs[oi] = childBase;
+    ++oi; ps += nl;
+  } else {
+    Node16 l; l.feat = -1; l.left = 0;
+    l.v = scalbn(__ddiv_rn(__ll2double_rn(SLv), __uint2double_rn(WLv)), -b.F);
+    out[childBase] = l; outThr[childBase] = 0;
+  }
+  if (oR) {
+    nx.tree[oi] = (uint32_t)t; nx.start[oi] = ps; nx.len[oi] = lenR; nx.W[oi] = WRv; nx.S[oi] = SRv;
+    nx.heap[oi] = 2ull * nd.heap[g] + 1ull; nx.bfs[oi] = childBase + 1;
+  } else {
+    Node16 l; l.feat = -1; l.left = 0;
+    l.v = scalbn(__ddiv_rn(__ll2double_rn(SRv), __uint2double_rn(WRv)), -b.F);
+    out[childBase + 1] = l; outThr[childBase + 1] = 0;
+  }
+  (void)nlBase;
+  (void)depth;
+}
+
+// one CTA per (tree, feature) list: stable partition of the node segments
+__global__ void __launch_bounds__(256) k_partition(Batch b, int cur, const uint32_t* nextNode0,
+                                                   const uint32_t* nextPos0, const uint32_t* nlBase,
+                                                   int debug_rows) {
+  const int t = blockIdx.x / b.p, f = blockIdx.x % b.p;
+  const Nodes& nd = b.nd[cur];
+  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
+  if (N == 0) return;
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr;
+  uint32_t* L2 = b.L[(cur & 1) ^ 1] + ((size_t)t * b.p + f) * b.ntr;
+  const uint32_t* posNode = b.posNode[cur];
+  uint32_t* posNode2 = b.posNode[cur ^ 1];
+  const uint8_t* side = b.side + (size_t)t * b.n;
+  const uint32_t nlb = nlBase[t];
+  const uint32_t npos0 = nextPos0[t];
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < N; base += 256) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t r = 0, left = 0, g = 0;
+    bool sp = false;
+    Best bs{0ull, 0ull};
+    if (i < N) {
+      g = posNode[pos0 + i];
+      bs = b.best[g];
+      sp = bs.key != 0ull;
+      r = L[i];
+      left = sp && side[r];
+    }
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(left, ex, tot);
+    const uint32_t leftBefore = carry + ex;  // left rows of this list before position i
+    if (i < N) {
+      if (sp) {
+        const U4S sc = b.chScan[g];
+        const uint32_t nodeLeftBase = sc.nl - nlb;      // left rows of earlier split nodes of the tree
+        const uint32_t within = left ? (leftBefore - nodeLeftBase)
+                                     : ((i - nd.start[g]) - (leftBefore - nodeLeftBase));
+        const uint32_t nl = (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
+        const uint32_t fl = b.chFlags[g];
+        const bool openL = fl & 1u, openR = fl & 2u;
+        if (left ? openL : openR) {
+          const uint32_t child = sc.op + ((!left && openL) ? 1u : 0u);
+          const uint32_t cstart = (sc.pos - npos0) + ((!left && openL) ? nl : 0u);
+          const uint32_t dest = cstart + within;
+          L2[dest] = r;
+          if (f == 0) posNode2[nextPos0[t] + dest] = child;
+        } else if (debug_rows && f == 0) {
+          const uint32_t cb = b.out[(size_t)t * b.cap + nd.bfs[g]].left;
+          b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)(cb + (left ? 0 : 1));
+        }
+      } else if (debug_rows && f == 0) {
+        b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void k_init_level0(Batch b, const uint32_t* rootInfo, uint32_t* counters /*[2]: NO, NP*/) {
+  // single thread: root nodes of non-leaf trees, per-tree position spaces
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t no = 0, np = 0;
+  for (int t = 0; t < b.B; ++t) {
+    b.tNode0[t] = no;
+    b.tPos0[t] = np;
+    b.tBase[t] = 0;
+    b.tCount[t] = 1;
+    const uint32_t D = rootInfo[4 * t];
+    const bool leaf = rootInfo[4 * t + 1] != 0;
+    if (!leaf) {
+      Nodes& nd = b.nd[0];
+      nd.tree[no] = (uint32_t)t; nd.start[no] = 0; nd.len[no] = D; nd.W[no] = (uint32_t)b.ntr;
+      nd.S[no] = reinterpret_cast<const long long*>(rootInfo)[2 * t + 1];
+      nd.heap[no] = 1ull; nd.bfs[no] = 0;
+      ++no;
+      np += D;
+    }
+  }
+  b.tNode0[b.B] = no;
+  b.tPos0[b.B] = np;
+  counters[0] = no;
+  counters[1] = np;
+}
+
+__global__ void k_pos_root(Batch b, int NP) {
+  // positions of the root level: tree t's positions [tPos0[t], tPos0[t+1]) -> its root node
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= NP) return;
+  int lo = 0, hi = b.B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if ((int)b.tPos0[mid] <= q) lo = mid; else hi = mid;
+  }
+  b.posNode[0][q] = b.tNode0[lo];
+}
+
+__global__ void k_finish_counts(Batch b) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < b.B) b.outCount[t] = b.tBase[t] + b.tCount[t];
+}
+
+__global__ void k_set_next_tree_tables(Batch b, const uint32_t* nextNode0, const uint32_t* nextPos0,
+                                       uint32_t* counters) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > b.B) return;
+  b.tNode0[t] = nextNode0[t];
+  b.tPos0[t] = nextPos0[t];
+  if (t == b.B) { counters[0] = nextNode0[t]; counters[1] = nextPos0[t]; }
+}
+
+}  // namespace
+
+// ============================================================ host driver ====
+namespace {
+
+__global__ void k_iota(uint32_t* a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = (uint32_t)i;
+}
+
+__global__ void k_root_rows(Batch b, const uint32_t* rootInfo) {
+  // leaf_of_row for trees whose root is a leaf: every in-bag row is in leaf 0
+  const int t = blockIdx.y;
+  if (!rootInfo[4 * t + 1]) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) {
+    const uint32_t r = b.tr_rows[j];
+    if (b.w[(size_t)t * b.n + r]) b.leaf_of_row[(size_t)t * b.n + r] = 0;
+  }
+}
+
+inline unsigned nblk(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
+
+#define LCK(expr)                                       \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) {                            \
+      err = std::string("large path: ") + cudaGetErrorString(_e); \
+      return _e == cudaErrorMemoryAllocation ? RF_E_OOM : RF_E_CUDA; \
+    }                                                   \
+  } while (0)
+
+struct LargePlan {
+  int B;
+  long long nmax, npmax, tiles_max;
+};
+
+// Grows the batch's trees (slots [0, b.B)) to completion.
+rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, uint64_t seed, int task, int bootstrap,
+                     void* cub_tmp, size_t cub_bytes, uint32_t* rootInfo, uint32_t* counters, uint32_t* hcounters,
+                     uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp,
+                     unsigned long long* ncand, cudaStream_t s, std::string& err) {
+  LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
+  LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
+  if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
+  {
+    dim3 g(nblk((b.ntr + 1) / 2, 256) > 64 ? 64 : nblk((b.ntr + 1) / 2, 256), b.B);
+    k_keys_boot<<<g, 256, 0, s>>>(b, seed, task, bootstrap);
+    note_launch();
+  }
+  k_inbag_lists<<<b.B * b.p, kThreads, 0, s>>>(b, task_order);
+  note_launch();
+  k_root<<<b.B, 256, 0, s>>>(b, rootInfo);
+  note_launch();
+  if (b.leaf_of_row) {
+    k_root_rows<<<dim3(32, b.B), 256, 0, s>>>(b, rootInfo);
+    note_launch();
+  }
+  k_init_level0<<<1, 1, 0, s>>>(b, rootInfo, counters);
+  note_launch();
+  LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
+  LCK(cudaStreamSynchronize(s));
+  long long NO = hcounters[0], NP = hcounters[1];
+  if (NP > 0) {
+    k_pos_root<<<nblk(NP, 256), 256, 0, s>>>(b, (int)NP);
+    note_launch();
+  }
+  int cur = 0, depth = 0;
+  while (NO > 0) {
+    k_node_prep<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
+    k_node_ws<<<nblk(NO, 256), 256, 0, s>>>(b, cur, (int)NO, wsTmp);
+    note_launch(2);
+    size_t tb = cub_bytes;
+    LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)NO, s));
+    const long long E = (long long)b.m * NP;
+    const long long tiles = (E + kTile - 1) / kTile;
+    {
+      ProfScope ps("large_search", s);
+      k_search_tot<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E);
+      tb = cub_bytes;
+      LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull}, (int)tiles,
+                                         s));
+      k_search_eval<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand);
+      note_launch(2);
+    }
+    k_decide<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
+    k_mark<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
+    k_children_count<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, depth);
+    note_launch(3);
+    tb = cub_bytes;
+    LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)NO, s));
+    k_tree_update<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, (int)NO, nextNode0, nextPos0, nlBase);
+    k_children_write<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, nextNode0, nextPos0, nlBase, depth);
+    note_launch(2);
+    {
+      ProfScope ps("large_partition", s);
+      k_partition<<<b.B * b.p, 256, 0, s>>>(b, cur, nextNode0, nextPos0, nlBase, b.leaf_of_row ? 1 : 0);
+      note_launch();
+    }
+    k_set_next_tree_tables<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, nextNode0, nextPos0, counters);
+    note_launch();
+    LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
+    LCK(cudaStreamSynchronize(s));
+    NO = hcounters[0];
+    NP = hcounters[1];
+    if (NO > pl.nmax || NP > pl.npmax) {
+      err = "large path: level size exceeds the plan";
+      return RF_E_OVERFLOW;
+    }
+    cur ^= 1;
+    ++depth;
+  }
+  k_finish_counts<<<nblk(b.B, 64), 64, 0, s>>>(b);
+  note_launch();
+  return RF_OK;
+}
+
+}  // namespace
+
+namespace {
+
+// one CTA per feature: the dataset order filtered to a task's training rows (global ids)
+__global__ void k_task_order_u32(const uint32_t* __restrict__ order, const int32_t* __restrict__ loc, int n,
+                                 int ntr, uint32_t* out) {
+  const int f = blockIdx.x;
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 256) {
+    const int j = base + threadIdx.x;
+    uint32_t r = 0, keep = 0;
+    if (j < n) { r = order[(size_t)f * n + j]; keep = loc[r] >= 0; }
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(keep, ex, tot);
+    if (keep) out[(size_t)f * ntr + carry + ex] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// per (test row, tree chunk): sum of the leaf values of the chunk's trees, trees in order
+__global__ void k_chunk_predict(const Node16* __restrict__ nodes, uint64_t cap, int T, int Cw, int nsub,
+                                const double* __restrict__ X, int p, const uint32_t* __restrict__ te_rows, int nte,
+                                int nte_max, double* __restrict__ partial) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nte * nsub) return;
+  const int r = idx % nte, c = idx / nte;
+  const double* x = X + (size_t)te_rows[r] * p;
+  double s = 0.0;
+  for (int t = c * Cw; t < min(T, (c + 1) * Cw); ++t) {
+    const Node16* tn = nodes + (size_t)t * cap;
+    Node16 nd = tn[0];
+    while (nd.feat >= 0) nd = tn[nd.left + ((x[nd.feat] <= nd.v) ? 0u : 1u)];
+    s += nd.v;
+  }
+  partial[(size_t)c * nte_max + r] = s;
+}
+
+}  // namespace
+
+static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
+                             int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
+                             cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
+                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, std::string& err);
+
+rf_status fit_large(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi, cudaStream_t s,
+                    Scratch& sc, Node16** nodes_out, uint32_t** thr_out, uint32_t** nn_out, uint64_t* cap_out,
+                    int32_t* leaf_of_row, std::string& err) {
+  uint32_t* tr_rows;
+  LCK(sc.alloc(&tr_rows, (size_t)d.n));
+  k_iota<<<nblk(d.n, 256) > 1184 ? 1184 : nblk(d.n, 256), 256, 0, s>>>(tr_rows, d.n);
+  note_launch();
+  return grow_forest(d, prm, mtry, tree_lo, tree_hi, 0, tr_rows, d.n, d.order, s, sc, nodes_out, thr_out, nn_out,
+                     cap_out, leaf_of_row, err);
+}
+
+rf_status cv_large_partial(const DevData& d, const TaskData& td, const rf_params* prm,
+                           const std::vector<int>& mtrys, int tree_lo, int tree_hi, int Cw, int nsub,
+                           int nte_max, double* partial, cudaStream_t s, Scratch& sc, std::string& err) {
+  if (prm->split_mode != RF_SPLIT_EXACT) {
+    err = "histogram split mode not built yet";
+    return RF_E_UNSUPPORTED;
+  }
+  const int T = tree_hi - tree_lo;
+  const int ntask = td.ntask;
+  std::vector<int32_t> hntr(ntask), hnte(ntask);
+  LCK(cudaMemcpyAsync(hntr.data(), td.ntr, ntask * 4, cudaMemcpyDeviceToHost, s));
+  LCK(cudaMemcpyAsync(hnte.data(), td.nte, ntask * 4, cudaMemcpyDeviceToHost, s));
+  LCK(cudaStreamSynchronize(s));
+  for (int tl = 0; tl < ntask; ++tl) {
+    const int ntr = hntr[tl], nte = hnte[tl];
+    Scratch ts(s);
+    uint32_t* order;
+    LCK(ts.alloc(&order, (size_t)d.p * ntr));
+    k_task_order_u32<<<d.p, 256, 0, s>>>(d.order, td.loc + (size_t)tl * d.n, d.n, ntr, order);
+    note_launch();
+    for (size_t mi = 0; mi < mtrys.size(); ++mi) {
+      Scratch fs(s);
+      Node16* nodes;
+      uint32_t *thr, *nn;
+      uint64_t cap;
+      rf_status st = grow_forest(d, prm, mtrys[mi], tree_lo, tree_hi, td.task0 + tl,
+                                 td.tr_rows + (size_t)tl * d.n, ntr, order, s, fs, &nodes, &thr, &nn, &cap, nullptr,
+                                 err);
+      if (st) return st;
+      double* part = partial + ((size_t)mi * ntask + tl) * nsub * nte_max;
+      const long long nth = (long long)nte * nsub;
+      k_chunk_predict<<<nblk(nth, 128), 128, 0, s>>>(nodes, cap, T, Cw, nsub, d.X, d.p,
+                                                     td.te_rows + (size_t)tl * d.n, nte, nte_max, part);
+      note_launch();
+    }
+  }
+  return RF_OK;
+}
+
+static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
+                             int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
+                             cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
+                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, std::string& err) {
+  if (prm->split_mode != RF_SPLIT_EXACT) {
+    err = "histogram split mode not built yet";
+    return RF_E_UNSUPPORTED;
+  }
+  if (d.p > 255) {
+    err = "large path: p <= 255";
+    return RF_E_UNSUPPORTED;
+  }
+  const int n = d.n, p = d.p, T = tree_hi - tree_lo;
+  uint64_t cap = 2ull * (uint64_t)ntr - 1ull;
+  if (prm->max_depth >= 0 && prm->max_depth < 40) cap = std::min<uint64_t>(cap, (2ull << prm->max_depth) - 1ull);
+  // batch size: ~lists dominate (2 p ntr 4 B per tree)
+  const size_t per_tree = (size_t)2 * p * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 + (size_t)ntr * 64;
+  int B = (int)std::max<size_t>(1, std::min<size_t>(32, ((size_t)6 << 30) / std::max<size_t>(per_tree, 1)));
+  B = std::min(B, T);
+  LargePlan pl;
+  pl.B = B;
+  pl.nmax = (long long)B * (ntr / 2 + 1);
+  pl.npmax = (long long)B * ntr;
+  pl.tiles_max = ((long long)mtry * pl.npmax + kTile - 1) / kTile;
+
+  Batch b;
+  memset(&b, 0, sizeof b);
+  b.B = B; b.n = n; b.p = p; b.m = mtry; b.ntr = ntr; b.mss = (int)prm->min_samples_split;
+  b.max_depth = prm->max_depth;
+  b.X = d.X; b.tq = d.tq; b.grank = d.grank; b.err = d.err;
+  int32_t hF = 0;
+  LCK(cudaMemcpyAsync(&hF, d.F, 4, cudaMemcpyDeviceToHost, s));
+  LCK(cudaStreamSynchronize(s));
+  b.F = hF;
+  b.tr_rows = tr_rows_in;
+  LCK(sc.alloc(&b.keys, (size_t)2 * B));
+  LCK(sc.alloc(&b.w, (size_t)B * n + 4));
+  LCK(sc.alloc(&b.side, (size_t)B * n));
+  for (int i = 0; i < 2; ++i) {
+    LCK(sc.alloc(&b.L[i], (size_t)B * p * ntr));
+    LCK(sc.alloc(&b.posNode[i], (size_t)pl.npmax));
+    Nodes& nd = b.nd[i];
+    LCK(sc.alloc(&nd.tree, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.start, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.len, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.W, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.S, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.heap, (size_t)pl.nmax));
+    LCK(sc.alloc(&nd.bfs, (size_t)pl.nmax));
+  }
+  LCK(sc.alloc(&b.feat, (size_t)pl.nmax * mtry));
+  LCK(sc.alloc(&b.best, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.accW, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.accS, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.nc, (size_t)pl.nmax * 2));
+  LCK(sc.alloc(&b.thr, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.thrIdx, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.nodePref, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.chScan, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.chVal, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.chFlags, (size_t)pl.nmax));
+  LCK(sc.alloc(&b.tileTot, (size_t)pl.tiles_max + 1));
+  LCK(sc.alloc(&b.tNode0, (size_t)B + 1));
+  LCK(sc.alloc(&b.tPos0, (size_t)B + 1));
+  LCK(sc.alloc(&b.tBase, (size_t)B));
+  LCK(sc.alloc(&b.tCount, (size_t)B));
+  WS2* wsTmp;
+  LCK(sc.alloc(&wsTmp, (size_t)pl.nmax));
+  uint32_t *rootInfo, *counters, *nextNode0, *nextPos0, *nlBase;
+  LCK(sc.alloc(&rootInfo, (size_t)4 * B));
+  LCK(sc.alloc(&counters, 2));
+  LCK(sc.alloc(&nextNode0, (size_t)B + 1));
+  LCK(sc.alloc(&nextPos0, (size_t)B + 1));
+  LCK(sc.alloc(&nlBase, (size_t)B + 1));
+  uint32_t* hcounters = nullptr;
+  LCK(cudaMallocHost(&hcounters, 16));
+  struct HostFree {
+    uint32_t* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hcounters};
+  // CUB temp storage for the largest scan
+  size_t cb1 = 0, cb2 = 0, cb3 = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, cb1, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)pl.nmax, s);
+  cub::DeviceScan::ExclusiveScan(nullptr, cb2, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull},
+                                 (int)pl.tiles_max + 1, s);
+  cub::DeviceScan::ExclusiveScan(nullptr, cb3, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)pl.nmax, s);
+  const size_t cub_bytes = std::max(cb1, std::max(cb2, cb3));
+  char* cub_tmp;
+  LCK(sc.alloc(&cub_tmp, cub_bytes + 16));
+  // outputs
+  Node16* out;
+  uint32_t *outThr, *outCount;
+  LCK(sc.alloc(&out, (size_t)T * cap));
+  LCK(sc.alloc(&outThr, (size_t)T * cap));
+  LCK(sc.alloc(&outCount, (size_t)T));
+  b.cap = cap;
+  for (int t0 = 0; t0 < T; t0 += B) {
+    const int nb = std::min(B, T - t0);
+    b.B = nb;
+    b.tree0 = tree_lo + t0;
+    b.out = out + (size_t)t0 * cap;
+    b.outThr = outThr + (size_t)t0 * cap;
+    b.outCount = outCount + t0;
+    b.leaf_of_row = leaf_of_row ? leaf_of_row + (size_t)t0 * n : nullptr;
+    rf_status st = grow_batch(b, pl, task_order, prm->seed, task, (int)prm->bootstrap, cub_tmp, cub_bytes, rootInfo,
+                              counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, candidate_counter(), s, err);
+    if (st) return st;
+  }
+  *nodes_out = out;
+  *thr_out = outThr;
+  *nn_out = outCount;
+  *cap_out = cap;
+  return RF_OK;
 }
 
 }  // namespace rf

@@ -190,7 +190,7 @@ size_t presort_ws_bytes(int n, int p) {
                                            (unsigned long long*)nullptr, (const uint32_t*)nullptr,
                                            (uint32_t*)nullptr, (int64_t)total, p, (const int64_t*)nullptr,
                                            (const int64_t*)nullptr);
-  return total * (8 + 8 + 4) + temp + 256;
+  return total * (8 + 8 + 4) + (size_t)(p + 1) * 8 + temp + 256;  // keys x2, values, offsets, CUB temp
 }
 
 namespace {

@@ -72,7 +72,7 @@ def _compare_forest(gf, of, X):
     off = e["tree_off"]
     assert e["ntree"] == len(of.trees)
     assert e["F"] == of.F
-    lr = gf.leaf_rows() if gf.n_rows else None
+    lr = gf.leaf_rows() if of.trees and of.trees[0].leaf_of_row is not None else None
     for t, tr in enumerate(of.trees):
         a, b = int(off[t]), int(off[t + 1])
         feat = e["feature"][a:b]
@@ -235,6 +235,43 @@ def test_cv_full_study_config_sampled():
         rep, fold = divmod(task, 10)
         np.testing.assert_allclose(fm_g[[0, 1], :, rep, fold], fm_o[:, :, rep, fold], rtol=RTOL, atol=0)
     assert np.array_equal(fm_g[1], fm_g[2])
+
+
+# ------------------------------------------------- large-n exact path ---
+LARGE_FIT_CASES = [
+    ("n256", lambda: datagen.tiny(256, 4, 21), dict(mtry=2)),
+    ("n300_ties", lambda: datagen.tiny(300, 5, 22, distinct=7), dict(mtry=3)),
+    ("paper1000", lambda: datagen.paper_shaped(1000, "V100", "time"), dict(mtry=4, target=1)),
+    ("paper2000_noboot", lambda: datagen.paper_shaped(2000, "K20", "power"), dict(mtry=12, bootstrap=False)),
+    ("scaled5000_depth", lambda: datagen.scaled(5000, 64), dict(mtry=21, max_depth=8, target=1)),
+    ("mss7", lambda: datagen.tiny(900, 3, 23, distinct=50), dict(mtry=3, min_samples_split=7)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", LARGE_FIT_CASES, ids=[c[0] for c in LARGE_FIT_CASES])
+def test_large_fit_structures_bit_exact(name, data, kw):
+    X, y = data()
+    of = oracle.fit(X, y, ntree=5, seed=31, leaf_rows=True, **kw)
+    gf = rfg.fit(X, y, ntree=5, seed=31, debug=True, **kw)
+    _compare_forest(gf, of, X)
+
+
+def test_large_fit_scaled_100k_sampled():
+    """Config 3 shape (100k x 64, mtry 21, unbounded depth): 2 trees vs the oracle."""
+    X, y = datagen.scaled(100_000, 64)
+    of = oracle.fit(X, y, ntree=2, seed=7, mtry=21, target=1)
+    gf = rfg.fit(X, y, ntree=2, seed=7, mtry=21, target=1)
+    _compare_forest(gf, of, X)
+    Q = datagen.queries(2000, 64)
+    np.testing.assert_allclose(rfg.predict(gf, Q), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
+def test_large_cv_parity():
+    X, y = datagen.paper_shaped(700, "P100", "time")
+    fm_o, pr_o = oracle.cv_grid(X, y, 3, 1, [4, 8], [3, 12], target=1, seed=3, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 3, 1, [4, 8], [3, 12], target=1, seed=3, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
 
 
 # -------------------------------------------------------------- errors ---
