@@ -94,6 +94,13 @@ struct Nodes {
 struct Batch {
   int B, n, p, m, ntr, mss, max_depth;
   int F;
+  int nl;                   // row lists per tree: p (exact, one per feature) or 1 (histogram)
+  int hist;                 // 256-bin histogram split mode (R23)
+  const uint8_t* bins;      // [n][p] bin of every row (histogram mode)
+  const double* cuts;       // [p][256] cut values (histogram mode)
+  const int32_t* ncuts;     // [p]
+  uint32_t* accN;           // [NMAX] rows going left (histogram mode)
+  long long* cmm;           // [NMAX][4] child t_q min/max: minL, maxL, minR, maxR (histogram mode)
   const double* X;
   const int64_t* tq;
   const uint32_t* grank;
@@ -157,12 +164,13 @@ __global__ void k_keys_boot(Batch b, uint64_t seed, int task, int bootstrap) {
   }
 }
 
-// one CTA per (tree, feature): stable compaction of the task order by w > 0
-__global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /*[p][ntr] global rows*/) {
-  const int t = blockIdx.x / b.p, f = blockIdx.x % b.p;
+// one CTA per (tree, list): stable compaction of the task order by w > 0
+// (exact: one list per feature in x order; histogram: one list of training rows)
+__global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /*[nl][ntr] global rows*/) {
+  const int t = blockIdx.x / b.nl, f = blockIdx.x % b.nl;
   const uint8_t* w = b.w + (size_t)t * b.n;
   const uint32_t* src = task_order + (size_t)f * b.ntr;
-  uint32_t* dst = b.L[0] + ((size_t)t * b.p + f) * b.ntr;
+  uint32_t* dst = b.L[0] + ((size_t)t * b.nl + f) * b.ntr;
   using BS = cub::BlockScan<uint32_t, kThreads>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ uint32_t carry;
@@ -479,6 +487,297 @@ __global__ void k_mark(Batch b, int cur, int NP) {
   }
 }
 
+// ------------------------------------------------------- histogram mode ----
+// 256-bin quantile histograms (R23): cuts per
+// (task, feature) from the training rows; bin(x) = #{cuts < x}; per node and
+// drawn feature the (W, S) sums per bin are exact integers (order-free atomics);
+// the candidate after cut c is valid iff WL > 0 and WR > 0; threshold = cut
+// value, threshold index = c; ties -> lowest feature, then lowest c.
+constexpr int kHistThreads = 256;
+constexpr int kHistChunk = 8192;  // rows per histogram work item
+
+// one CTA per feature: cuts from the task's training rows sorted by x_f
+__global__ void k_cuts(const double* __restrict__ X, int p, const uint32_t* __restrict__ order, int ntr,
+                       double* cuts, int32_t* ncuts) {
+  const int f = blockIdx.x;
+  const uint32_t* o = order + (size_t)f * ntr;
+  auto s = [&](int j) { return X[(size_t)o[j] * p + f]; };
+  using BR = cub::BlockReduce<int, 256>;
+  using BS = cub::BlockScan<int, 256>;
+  __shared__ typename BR::TempStorage tr;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ int Dsh, carry;
+  int cnt = 0;
+  for (int j = threadIdx.x; j < ntr; j += blockDim.x) cnt += (j == 0 || s(j) != s(j - 1));
+  const int D = BR(tr).Sum(cnt);
+  if (threadIdx.x == 0) { Dsh = D; carry = 0; }
+  __syncthreads();
+  const double vmax = ntr > 0 ? s(ntr - 1) : 0.0;
+  if (Dsh <= 256) {
+    // all distinct values but the largest, in order
+    for (int base = 0; base < ntr; base += blockDim.x) {
+      const int j = base + threadIdx.x;
+      int keep = 0;
+      double v = 0.0;
+      if (j < ntr) {
+        v = s(j);
+        keep = (j == 0 || v != s(j - 1)) && v != vmax;
+      }
+      int ex, tot;
+      BS(ts).ExclusiveSum(keep, ex, tot);
+      if (keep) cuts[(size_t)f * 256 + carry + ex] = v;
+      __syncthreads();
+      if (threadIdx.x == 0) carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) ncuts[f] = Dsh - 1;
+  } else if (threadIdx.x == 0) {
+    int c = 0;
+    double last = 0.0;
+    for (int jq = 1; jq <= 255; ++jq) {
+      const long long q = ((long long)jq * ntr + 255) / 256 - 1;  // ceil(jq ntr / 256) - 1
+      const double v = s((int)q);
+      if (v == vmax || (c > 0 && v == last)) continue;
+      cuts[(size_t)f * 256 + c++] = v;
+      last = v;
+    }
+    ncuts[f] = c;
+  }
+}
+
+// bin(x) = #{cuts < x} for every row and feature (row-major [n][p] u8)
+__global__ void k_bins(const double* __restrict__ X, int n, int p, const double* __restrict__ cuts,
+                       const int32_t* __restrict__ ncuts, uint8_t* bins) {
+  const size_t total = (size_t)n * p;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int f = (int)(i % p);
+    const double x = X[i];
+    const double* c = cuts + (size_t)f * 256;
+    int lo = 0, hi = ncuts[f];  // first index with c[idx] >= x
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (c[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    bins[i] = (uint8_t)lo;
+  }
+}
+
+__global__ void k_hist_nchunks(Batch b, int cur, int g0, int g1, uint32_t* nch) {
+  const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= g1) return;
+  nch[g - g0] = (b.nd[cur].len[g] + kHistChunk - 1) / kHistChunk;
+}
+
+// multi-chunk nodes accumulate with atomics: zero their histograms first
+__global__ void k_hist_zero(Batch b, int cur, int g0, int g1, uint32_t* hW, unsigned long long* hS) {
+  const int g = g0 + blockIdx.x;
+  if (g >= g1 || b.nd[cur].len[g] <= (uint32_t)kHistChunk) return;
+  const size_t base = (size_t)(g - g0) * b.m * 256;
+  for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) { hW[base + i] = 0u; hS[base + i] = 0ull; }
+}
+
+// work item = (node, chunk of <= kHistChunk rows): shared-memory histograms of the drawn features
+__global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, int g0, int g1,
+                                                             const uint32_t* itemPref, uint32_t* hW,
+                                                             unsigned long long* hS) {
+  extern __shared__ __align__(16) char sm[];
+  unsigned long long* sS = reinterpret_cast<unsigned long long*>(sm);  // [m][256]
+  uint32_t* sW = reinterpret_cast<uint32_t*>(sS + (size_t)b.m * 256);    // [m][256]
+  int* sF = reinterpret_cast<int*>(sW + (size_t)b.m * 256);              // [m]
+  const int item = blockIdx.x;
+  int lo = g0, hi = g1;  // node: last g with itemPref[g - g0] <= item
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)itemPref[mid - g0] <= item) lo = mid; else hi = mid;
+  }
+  const int g = lo;
+  const uint32_t c = (uint32_t)(item - (int)itemPref[g - g0]);
+  const Nodes& nd = b.nd[cur];
+  const int t = (int)nd.tree[g];
+  const uint32_t start = nd.start[g], len = nd.len[g];
+  const uint32_t i0 = c * kHistChunk, i1 = min(len, i0 + (uint32_t)kHistChunk);
+  for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) { sW[i] = 0u; sS[i] = 0ull; }
+  for (int j = threadIdx.x; j < b.m; j += blockDim.x) sF[j] = b.feat[(size_t)g * b.m + j];
+  __syncthreads();
+  const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr + start;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  for (uint32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t r = L[i];
+    const uint32_t wv = w[r];
+    const unsigned long long sv = (unsigned long long)((long long)wv * b.tq[r]);
+    const uint8_t* br = b.bins + (size_t)r * b.p;
+    for (int j = 0; j < b.m; ++j) {
+      const int bin = br[sF[j]];
+      atomicAdd(&sW[j * 256 + bin], wv);
+      atomicAdd(&sS[j * 256 + bin], sv);
+    }
+  }
+  __syncthreads();
+  const size_t base = (size_t)(g - g0) * b.m * 256;
+  const bool single = len <= (uint32_t)kHistChunk;
+  for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) {
+    if (single) {
+      hW[base + i] = sW[i];
+      hS[base + i] = sS[i];
+    } else if (sW[i]) {
+      atomicAdd(&hW[base + i], sW[i]);
+      atomicAdd(&hS[base + i], sS[i]);
+    }
+  }
+}
+
+// one CTA per node: best cut over the drawn features (warp per feature, 8 bins per lane)
+__global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int g1, const uint32_t* hW,
+                                                   const unsigned long long* hS, unsigned long long* ncand) {
+  const int g = g0 + blockIdx.x;
+  if (g >= g1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Nodes& nd = b.nd[cur];
+  const unsigned long long Wt = nd.W[g];
+  const long long St = nd.S[g];
+  unsigned long long bk = 0ull, ba = ~0ull;
+  unsigned int nc = 0;
+  for (int j = warp; j < b.m; j += 8) {
+    const int f = b.feat[(size_t)g * b.m + j];
+    const int ncut = b.ncuts[f];
+    const size_t base = ((size_t)(g - g0) * b.m + j) * 256 + 8 * lane;
+    uint32_t w8[8];
+    unsigned long long s8[8];
+    uint32_t lw = 0;
+    unsigned long long ls = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      w8[k] = hW[base + k];
+      s8[k] = hS[base + k];
+      lw += w8[k];
+      ls += s8[k];
+    }
+    uint32_t xw = lw;
+    unsigned long long xs = ls;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t yw = __shfl_up_sync(0xffffffffu, xw, d);
+      const unsigned long long ys = __shfl_up_sync(0xffffffffu, xs, d);
+      if (lane >= d) { xw += yw; xs += ys; }
+    }
+    unsigned long long cw = xw - lw, cs = xs - ls;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cw += w8[k];
+      cs += s8[k];
+      const int cidx = 8 * lane + k;
+      if (cidx < ncut && cw > 0 && cw < Wt) {
+        const long long SL = (long long)cs;
+        const double G = split_gain((long long)cw, SL, (long long)(Wt - cw), St - SL);
+        const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
+        const unsigned long long aux = ((unsigned long long)f << 32) | (unsigned long long)cidx;
+        ++nc;
+        if (better(key, aux, bk, ba)) { bk = key; ba = aux; }
+      }
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, d);
+    const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ba, d);
+    if (better(ok, oa, bk, ba)) { bk = ok; ba = oa; }
+  }
+  __shared__ unsigned long long sk[8], sa[8];
+  if (lane == 0) { sk[warp] = bk; sa[warp] = ba; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < 8; ++w2)
+      if (better(sk[w2], sa[w2], bk, ba)) { bk = sk[w2]; ba = sa[w2]; }
+    b.best[g] = Best{bk, bk ? ba : ~0ull};
+  }
+  if (ncand) {
+    unsigned long long v = nc;
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0 && v) atomicAdd(ncand, v);
+  }
+}
+
+__global__ void k_decide_hist(Batch b, int NO) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Best bs = b.best[g];
+  if (!bs.key) return;
+  const int f = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
+  b.thr[g] = b.cuts[(size_t)f * 256 + c];
+  b.thrIdx[g] = (uint32_t)c;
+}
+
+// positions: go-left flags (bin <= cut), left count and sums, child t_q min / max
+__global__ void k_mark_hist(Batch b, int cur, int NP) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const Nodes& nd = b.nd[cur];
+  int g = -1;
+  unsigned int cnt = 0, wl = 0;
+  unsigned long long sl = 0;
+  long long mnL = LLONG_MAX, mxL = LLONG_MIN, mnR = LLONG_MAX, mxR = LLONG_MIN;
+  if (q < NP) {
+    g = (int)b.posNode[cur][q];
+    const Best bs = b.best[g];
+    if (bs.key) {
+      const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
+      const int start = (int)nd.start[g];
+      const int i = q - (int)b.tPos0[t] - start;
+      const uint32_t r = b.L[cur & 1][(size_t)t * b.ntr + start + i];
+      const bool left = b.bins[(size_t)r * b.p + f] <= c;
+      b.side[(size_t)t * b.n + r] = left ? 1 : 0;
+      const long long tv = b.tq[r];
+      if (left) {
+        cnt = 1;
+        wl = b.w[(size_t)t * b.n + r];
+        sl = (unsigned long long)((long long)wl * tv);
+        mnL = mxL = tv;
+      } else {
+        mnR = mxR = tv;
+      }
+    } else {
+      g = -1;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int og = __shfl_down_sync(0xffffffffu, g, d);
+    const unsigned int oc = __shfl_down_sync(0xffffffffu, cnt, d);
+    const unsigned int ow = __shfl_down_sync(0xffffffffu, wl, d);
+    const unsigned long long os = __shfl_down_sync(0xffffffffu, sl, d);
+    const long long a0 = __shfl_down_sync(0xffffffffu, mnL, d), a1 = __shfl_down_sync(0xffffffffu, mxL, d);
+    const long long a2 = __shfl_down_sync(0xffffffffu, mnR, d), a3 = __shfl_down_sync(0xffffffffu, mxR, d);
+    if (lane + d < 32 && og == g) {
+      cnt += oc; wl += ow; sl += os;
+      mnL = min(mnL, a0); mxL = max(mxL, a1); mnR = min(mnR, a2); mxR = max(mxR, a3);
+    }
+  }
+  const int pg = __shfl_up_sync(0xffffffffu, g, 1);
+  if (g >= 0 && (lane == 0 || pg != g)) {
+    if (cnt) {
+      atomicAdd(&b.accN[g], cnt);
+      atomicAdd(&b.accW[g], wl);
+      atomicAdd(&b.accS[g], sl);
+      atomicMin(&b.cmm[4 * g], mnL);
+      atomicMax(&b.cmm[4 * g + 1], mxL);
+    }
+    if (mnR != LLONG_MAX) {
+      atomicMin(&b.cmm[4 * g + 2], mnR);
+      atomicMax(&b.cmm[4 * g + 3], mxR);
+    }
+  }
+}
+
+__global__ void k_hist_reset(Batch b, int NO) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  b.accN[g] = 0u;
+  b.cmm[4 * g] = LLONG_MAX;
+  b.cmm[4 * g + 1] = LLONG_MIN;
+  b.cmm[4 * g + 2] = LLONG_MAX;
+  b.cmm[4 * g + 3] = LLONG_MIN;
+}
+
 __global__ void k_children_count(Batch b, int cur, int NO, int depth) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= NO) return;
@@ -486,11 +785,14 @@ __global__ void k_children_count(Batch b, int cur, int NO, int depth) {
   const Best bs = b.best[g];
   U4S v{0u, 0u, 0u, 0u};
   if (bs.key) {
-    const uint32_t nl = (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
+    // left distinct rows: exact mode = position of the boundary + 1; histogram mode = counted
+    const uint32_t nl = b.hist ? b.accN[g] : (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
     const uint32_t lenL = nl, lenR = nd.len[g] - nl;
     const bool capd = (b.max_depth >= 0) && (depth + 1 >= b.max_depth);
-    const bool oL = !capd && (int)lenL >= b.mss && b.nc[2 * g];
-    const bool oR = !capd && (int)lenR >= b.mss && b.nc[2 * g + 1];
+    const bool ncL = b.hist ? (b.cmm[4 * g] != b.cmm[4 * g + 1]) : (b.nc[2 * g] != 0);
+    const bool ncR = b.hist ? (b.cmm[4 * g + 2] != b.cmm[4 * g + 3]) : (b.nc[2 * g + 1] != 0);
+    const bool oL = !capd && (int)lenL >= b.mss && ncL;
+    const bool oR = !capd && (int)lenR >= b.mss && ncR;
     v.sp = 1u;
     v.op = (oL ? 1u : 0u) + (oR ? 1u : 0u);
     v.pos = (oL ? lenL : 0u) + (oR ? lenR : 0u);
@@ -592,12 +894,12 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
 __global__ void __launch_bounds__(256) k_partition(Batch b, int cur, const uint32_t* nextNode0,
                                                    const uint32_t* nextPos0, const uint32_t* nlBase,
                                                    int debug_rows) {
-  const int t = blockIdx.x / b.p, f = blockIdx.x % b.p;
+  const int t = blockIdx.x / b.nl, f = blockIdx.x % b.nl;
   const Nodes& nd = b.nd[cur];
   const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
   if (N == 0) return;
-  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr;
-  uint32_t* L2 = b.L[(cur & 1) ^ 1] + ((size_t)t * b.p + f) * b.ntr;
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr;
+  uint32_t* L2 = b.L[(cur & 1) ^ 1] + ((size_t)t * b.nl + f) * b.ntr;
   const uint32_t* posNode = b.posNode[cur];
   uint32_t* posNode2 = b.posNode[cur ^ 1];
   const uint8_t* side = b.side + (size_t)t * b.n;
@@ -629,7 +931,7 @@ __global__ void __launch_bounds__(256) k_partition(Batch b, int cur, const uint3
         const uint32_t nodeLeftBase = sc.nl - nlb;      // left rows of earlier split nodes of the tree
         const uint32_t within = left ? (leftBefore - nodeLeftBase)
                                      : ((i - nd.start[g]) - (leftBefore - nodeLeftBase));
-        const uint32_t nl = (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
+        const uint32_t nl = b.chVal[g].nl;  // distinct rows going left (both split modes)
         const uint32_t fl = b.chFlags[g];
         const bool openL = fl & 1u, openR = fl & 2u;
         if (left ? openL : openR) {
@@ -739,10 +1041,18 @@ struct LargePlan {
   long long nmax, npmax, tiles_max;
 };
 
+struct HistBufs {  // histogram mode: per-chunk-of-nodes histograms and work-item prefix
+  long long cap = 0;        // nodes per chunk
+  uint32_t* W = nullptr;    // [cap][m][256]
+  unsigned long long* S = nullptr;
+  uint32_t* nch = nullptr;  // [cap + 1]
+  uint32_t* pref = nullptr; // [cap + 1]
+};
+
 // Grows the batch's trees (slots [0, b.B)) to completion.
 rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, uint64_t seed, int task, int bootstrap,
                      void* cub_tmp, size_t cub_bytes, uint32_t* rootInfo, uint32_t* counters, uint32_t* hcounters,
-                     uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp,
+                     uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp, const HistBufs& hb,
                      unsigned long long* ncand, cudaStream_t s, std::string& err) {
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
   LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
@@ -752,7 +1062,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     k_keys_boot<<<g, 256, 0, s>>>(b, seed, task, bootstrap);
     note_launch();
   }
-  k_inbag_lists<<<b.B * b.p, kThreads, 0, s>>>(b, task_order);
+  k_inbag_lists<<<b.B * b.nl, kThreads, 0, s>>>(b, task_order);
   note_launch();
   k_root<<<b.B, 256, 0, s>>>(b, rootInfo);
   note_launch();
@@ -772,25 +1082,52 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   int cur = 0, depth = 0;
   while (NO > 0) {
     k_node_prep<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
-    k_node_ws<<<nblk(NO, 256), 256, 0, s>>>(b, cur, (int)NO, wsTmp);
-    note_launch(2);
+    note_launch();
     size_t tb = cub_bytes;
-    LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)NO, s));
-    const long long E = (long long)b.m * NP;
-    const long long tiles = (E + kTile - 1) / kTile;
-    {
-      ProfScope ps("large_search", s);
-      k_search_tot<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E);
-      tb = cub_bytes;
-      LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull}, (int)tiles,
-                                         s));
-      k_search_eval<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand);
+    if (!b.hist) {
+      k_node_ws<<<nblk(NO, 256), 256, 0, s>>>(b, cur, (int)NO, wsTmp);
+      note_launch();
+      LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)NO, s));
+      const long long E = (long long)b.m * NP;
+      const long long tiles = (E + kTile - 1) / kTile;
+      {
+        ProfScope ps("large_search", s);
+        k_search_tot<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E);
+        tb = cub_bytes;
+        LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull},
+                                           (int)tiles, s));
+        k_search_eval<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand);
+        note_launch(2);
+      }
+      k_decide<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
+      k_mark<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
+      note_launch(2);
+    } else {
+      k_hist_reset<<<nblk(NO, 256), 256, 0, s>>>(b, (int)NO);
+      note_launch();
+      const size_t hsm = (size_t)b.m * 256 * 12 + (size_t)b.m * 4 + 16;
+      ProfScope ps("hist_search", s);
+      for (long long g0 = 0; g0 < NO; g0 += hb.cap) {
+        const long long g1 = std::min<long long>(NO, g0 + hb.cap);
+        const int cnt = (int)(g1 - g0);
+        k_hist_nchunks<<<nblk(cnt, 256), 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.nch);
+        note_launch();
+        tb = cub_bytes;
+        LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, hb.nch, hb.pref, cnt + 1, s));
+        uint32_t items = 0;
+        LCK(cudaMemcpyAsync(&items, hb.pref + cnt, 4, cudaMemcpyDeviceToHost, s));
+        LCK(cudaStreamSynchronize(s));
+        k_hist_zero<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S);
+        k_hist_build<<<items, kHistThreads, hsm, s>>>(b, cur, (int)g0, (int)g1, hb.pref, hb.W, hb.S);
+        k_hist_best<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S, ncand);
+        note_launch(3);
+      }
+      k_decide_hist<<<nblk(NO, 128), 128, 0, s>>>(b, (int)NO);
+      k_mark_hist<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
       note_launch(2);
     }
-    k_decide<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
-    k_mark<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
     k_children_count<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, depth);
-    note_launch(3);
+    note_launch();
     tb = cub_bytes;
     LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)NO, s));
     k_tree_update<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, (int)NO, nextNode0, nextPos0, nlBase);
@@ -798,7 +1135,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     note_launch(2);
     {
       ProfScope ps("large_partition", s);
-      k_partition<<<b.B * b.p, 256, 0, s>>>(b, cur, nextNode0, nextPos0, nlBase, b.leaf_of_row ? 1 : 0);
+      k_partition<<<b.B * b.nl, 256, 0, s>>>(b, cur, nextNode0, nextPos0, nlBase, b.leaf_of_row ? 1 : 0);
       note_launch();
     }
     k_set_next_tree_tables<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, nextNode0, nextPos0, counters);
@@ -884,10 +1221,6 @@ rf_status fit_large(const DevData& d, const rf_params* prm, int mtry, int tree_l
 rf_status cv_large_partial(const DevData& d, const TaskData& td, const rf_params* prm,
                            const std::vector<int>& mtrys, int tree_lo, int tree_hi, int Cw, int nsub,
                            int nte_max, double* partial, cudaStream_t s, Scratch& sc, std::string& err) {
-  if (prm->split_mode != RF_SPLIT_EXACT) {
-    err = "histogram split mode not built yet";
-    return RF_E_UNSUPPORTED;
-  }
   const int T = tree_hi - tree_lo;
   const int ntask = td.ntask;
   std::vector<int32_t> hntr(ntask), hnte(ntask);
@@ -924,32 +1257,70 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
                              int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
                              cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
                              uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, std::string& err) {
-  if (prm->split_mode != RF_SPLIT_EXACT) {
-    err = "histogram split mode not built yet";
-    return RF_E_UNSUPPORTED;
-  }
   if (d.p > 255) {
     err = "large path: p <= 255";
     return RF_E_UNSUPPORTED;
   }
+  const bool hist = prm->split_mode == RF_SPLIT_HIST256;
   const int n = d.n, p = d.p, T = tree_hi - tree_lo;
+  const int nlists = hist ? 1 : p;
   uint64_t cap = 2ull * (uint64_t)ntr - 1ull;
   if (prm->max_depth >= 0 && prm->max_depth < 40) cap = std::min<uint64_t>(cap, (2ull << prm->max_depth) - 1ull);
-  // batch size: ~lists dominate (2 p ntr 4 B per tree)
-  const size_t per_tree = (size_t)2 * p * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 + (size_t)ntr * 64;
+  // open nodes per level per tree <= min(ntr / 2, 2^(max_depth - 1))
+  long long open_max = ntr / 2 + 1;
+  if (prm->max_depth >= 1 && prm->max_depth < 31) open_max = std::min<long long>(open_max, 1ll << (prm->max_depth - 1));
+  // batch size: the row lists dominate (2 lists-per-tree x ntr x 4 B per tree)
+  const size_t per_tree = (size_t)2 * nlists * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 + (size_t)open_max * 128;
   int B = (int)std::max<size_t>(1, std::min<size_t>(32, ((size_t)6 << 30) / std::max<size_t>(per_tree, 1)));
   B = std::min(B, T);
   LargePlan pl;
   pl.B = B;
-  pl.nmax = (long long)B * (ntr / 2 + 1);
+  pl.nmax = (long long)B * open_max;
   pl.npmax = (long long)B * ntr;
-  pl.tiles_max = ((long long)mtry * pl.npmax + kTile - 1) / kTile;
+  pl.tiles_max = hist ? 1 : ((long long)mtry * pl.npmax + kTile - 1) / kTile;
 
   Batch b;
   memset(&b, 0, sizeof b);
   b.B = B; b.n = n; b.p = p; b.m = mtry; b.ntr = ntr; b.mss = (int)prm->min_samples_split;
   b.max_depth = prm->max_depth;
   b.X = d.X; b.tq = d.tq; b.grank = d.grank; b.err = d.err;
+  b.nl = nlists;
+  b.hist = hist ? 1 : 0;
+  HistBufs hb;
+  const uint32_t* list_src = task_order;
+  if (hist) {
+    // cuts of this task's training rows (R23) and the bins of every row
+    double* cuts;
+    int32_t* ncuts;
+    uint8_t* bins;
+    LCK(sc.alloc(&cuts, (size_t)p * 256));
+    LCK(sc.alloc(&ncuts, (size_t)p));
+    LCK(sc.alloc(&bins, (size_t)n * p));
+    {
+      ProfScope ps("hist_binning", s);
+      k_cuts<<<p, 256, 0, s>>>(d.X, p, task_order, ntr, cuts, ncuts);
+      k_bins<<<std::min<unsigned>(nblk((long long)n * p, 256), 148 * 32), 256, 0, s>>>(d.X, n, p, cuts, ncuts, bins);
+      note_launch(2);
+    }
+    b.cuts = cuts;
+    b.ncuts = ncuts;
+    b.bins = bins;
+    LCK(sc.alloc(&b.accN, (size_t)pl.nmax));
+    LCK(sc.alloc(&b.cmm, (size_t)pl.nmax * 4));
+    hb.cap = std::max<long long>(1, std::min<long long>(pl.nmax, ((long long)2 << 30) / ((long long)mtry * 256 * 12)));
+    LCK(sc.alloc(&hb.W, (size_t)hb.cap * mtry * 256));
+    LCK(sc.alloc(&hb.S, (size_t)hb.cap * mtry * 256));
+    LCK(sc.alloc(&hb.nch, (size_t)hb.cap + 1));
+    LCK(sc.alloc(&hb.pref, (size_t)hb.cap + 1));
+    LCK(cudaMemsetAsync(hb.nch, 0, ((size_t)hb.cap + 1) * 4, s));
+    const size_t hsm = (size_t)mtry * 256 * 12 + (size_t)mtry * 4 + 16;
+    if (hsm > 227 * 1024) {
+      err = "histogram mode: mtry too large for the shared-memory histograms (mtry <= 73)";
+      return RF_E_UNSUPPORTED;
+    }
+    LCK(cudaFuncSetAttribute(k_hist_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    list_src = tr_rows_in;  // one node-grouped list of training rows
+  }
   int32_t hF = 0;
   LCK(cudaMemcpyAsync(&hF, d.F, 4, cudaMemcpyDeviceToHost, s));
   LCK(cudaStreamSynchronize(s));
@@ -959,7 +1330,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(sc.alloc(&b.w, (size_t)B * n + 4));
   LCK(sc.alloc(&b.side, (size_t)B * n));
   for (int i = 0; i < 2; ++i) {
-    LCK(sc.alloc(&b.L[i], (size_t)B * p * ntr));
+    LCK(sc.alloc(&b.L[i], (size_t)B * nlists * ntr));
     LCK(sc.alloc(&b.posNode[i], (size_t)pl.npmax));
     Nodes& nd = b.nd[i];
     LCK(sc.alloc(&nd.tree, (size_t)pl.nmax));
@@ -1006,7 +1377,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   cub::DeviceScan::ExclusiveScan(nullptr, cb2, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull},
                                  (int)pl.tiles_max + 1, s);
   cub::DeviceScan::ExclusiveScan(nullptr, cb3, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)pl.nmax, s);
-  const size_t cub_bytes = std::max(cb1, std::max(cb2, cb3));
+  size_t cb4 = 0;
+  if (hist) cub::DeviceScan::ExclusiveSum(nullptr, cb4, hb.nch, hb.pref, (int)hb.cap + 1, s);
+  const size_t cub_bytes = std::max(std::max(cb1, cb4), std::max(cb2, cb3));
   char* cub_tmp;
   LCK(sc.alloc(&cub_tmp, cub_bytes + 16));
   // outputs
@@ -1024,8 +1397,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     b.outThr = outThr + (size_t)t0 * cap;
     b.outCount = outCount + t0;
     b.leaf_of_row = leaf_of_row ? leaf_of_row + (size_t)t0 * n : nullptr;
-    rf_status st = grow_batch(b, pl, task_order, prm->seed, task, (int)prm->bootstrap, cub_tmp, cub_bytes, rootInfo,
-                              counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, candidate_counter(), s, err);
+    rf_status st = grow_batch(b, pl, list_src, prm->seed, task, (int)prm->bootstrap, cub_tmp, cub_bytes, rootInfo,
+                              counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, hb, candidate_counter(), s,
+                              err);
     if (st) return st;
   }
   *nodes_out = out;

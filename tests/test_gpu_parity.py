@@ -274,6 +274,44 @@ def test_large_cv_parity():
     np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
 
 
+# ------------------------------------------------ histogram split mode ---
+HIST_CASES = [
+    ("few_distinct", lambda: datagen.tiny(300, 5, 41, distinct=40), dict(mtry=3)),
+    ("paper600", lambda: datagen.paper_shaped(600, "K20", "time"), dict(mtry=4, target=1)),
+    ("scaled3000", lambda: datagen.scaled(3000, 64), dict(mtry=21, max_depth=6, target=1)),
+    ("small_n", lambda: datagen.tiny(120, 3, 42), dict(mtry=2)),
+    ("noboot_mss", lambda: datagen.tiny(800, 4, 43, distinct=300), dict(mtry=4, bootstrap=False, min_samples_split=5)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", HIST_CASES, ids=[c[0] for c in HIST_CASES])
+def test_hist_fit_structures_bit_exact(name, data, kw):
+    X, y = data()
+    of = oracle.fit(X, y, ntree=4, seed=17, leaf_rows=True, split_mode=1, **kw)
+    gf = rfg.fit(X, y, ntree=4, seed=17, debug=True, split_mode=1, **kw)
+    _compare_forest(gf, of, X)
+
+
+def test_hist_equals_exact_structure_when_few_distinct():
+    """Cross-mode pin: with <= 256 distinct values per feature the histogram
+    mode grows the same partitions as the exact mode."""
+    X, y = datagen.tiny(2000, 6, 44, distinct=100)
+    ge = rfg.fit(X, y, ntree=6, seed=2, mtry=3, debug=True).export()
+    gh = rfg.fit(X, y, ntree=6, seed=2, mtry=3, debug=True, split_mode=1).export()
+    for key in ("feature", "left", "thr_index"):
+        assert np.array_equal(ge[key], gh[key]), key
+    leaves = ge["feature"] < 0
+    assert np.array_equal(ge["value"][leaves].view(np.int64), gh["value"][leaves].view(np.int64))
+
+
+def test_hist_cv_parity():
+    X, y = datagen.paper_shaped(500, "V100", "power")
+    fm_o, pr_o = oracle.cv_grid(X, y, 4, 1, [3, 6], [4], seed=5, split_mode=1, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 4, 1, [3, 6], [4], seed=5, split_mode=1, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+
+
 # -------------------------------------------------------------- errors ---
 def test_errors():
     X, y = datagen.tiny(20, 3, 1)
