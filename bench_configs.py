@@ -54,6 +54,8 @@ def c1(rfg, torch):
 def c3(rfg, torch, ntrees):
     X, y = datagen.scaled(100_000, 64)
     Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
+    rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7)  # warm-up (allocator pool, modules)
+    torch.cuda.synchronize()
     rfg.set_profiling(True)
     t0 = time.perf_counter()
     f = rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7)
@@ -63,6 +65,25 @@ def c3(rfg, torch, ntrees):
     rfg.set_profiling(False)
     info = f.info()
     return {"config": f"C3 rf_fit 100k x 64 exact, mtry 21, unbounded depth ({ntrees} of 500 trees)",
+            "trees": ntrees, "seconds": sec, "trees_per_s": ntrees / sec,
+            "nodes_per_tree": info["total_nodes"] / ntrees, "kernels_ms": {k: v[0] for k, v in prof.items()}}
+
+
+def c4(rfg, torch, ntrees, nrows):
+    X, y = datagen.scaled(nrows, 64)
+    Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
+    del X
+    rfg.fit(Xd, yd, ntree=2, mtry=21, target=1, seed=7, max_depth=12, split_mode=1)  # warm-up
+    torch.cuda.synchronize()
+    rfg.set_profiling(True)
+    t0 = time.perf_counter()
+    f = rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7, max_depth=12, split_mode=1)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    prof = rfg.last_profile()
+    rfg.set_profiling(False)
+    info = f.info()
+    return {"config": f"C4 rf_fit {nrows} x 64 histogram-256, mtry 21, max_depth 12 ({ntrees} of 1000 trees, 1 GPU)",
             "trees": ntrees, "seconds": sec, "trees_per_s": ntrees / sec,
             "nodes_per_tree": info["total_nodes"] / ntrees, "kernels_ms": {k: v[0] for k, v in prof.items()}}
 
@@ -104,6 +125,8 @@ def main():
     ap.add_argument("--configs", default="c1,c3,c5")
     ap.add_argument("--c3-trees", type=int, default=16)
     ap.add_argument("--c5-rows", type=int, default=1_000_000)
+    ap.add_argument("--c4-trees", type=int, default=32)
+    ap.add_argument("--c4-rows", type=int, default=10_000_000)
     a = ap.parse_args()
     import torch
     import paper_2001_07104_b200 as rfg
@@ -113,6 +136,8 @@ def main():
             r = c1(rfg, torch)
         elif c == "c3":
             r = c3(rfg, torch, a.c3_trees)
+        elif c == "c4":
+            r = c4(rfg, torch, a.c4_trees, a.c4_rows)
         elif c == "c5":
             r = c5(rfg, torch, a.c5_rows)
         else:

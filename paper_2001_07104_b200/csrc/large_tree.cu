@@ -890,14 +890,53 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
   (void)depth;
 }
 
-// one CTA per (tree, feature) list: stable partition of the node segments
-__global__ void __launch_bounds__(256) k_partition(Batch b, int cur, const uint32_t* nextNode0,
-                                                   const uint32_t* nextPos0, const uint32_t* nlBase,
-                                                   int debug_rows) {
-  const int t = blockIdx.x / b.nl, f = blockIdx.x % b.nl;
+// Stable partition of every (tree, list) in tiles of kPartTile positions: tile
+// counts of go-left rows -> device-wide exclusive scan -> scatter (block scan +
+// tile prefix - list's first tile prefix = left rows of this list before the
+// element).  tileTab[2t] = first tile of tree t, tileTab[2t+1] = tiles per list.
+constexpr int kPartThreads = 256, kPartItems = 8, kPartTile = kPartThreads * kPartItems;
+
+__device__ __forceinline__ void part_locate(const Batch& b, const uint32_t* tileTab, int tile, int& t, int& f,
+                                            int& k) {
+  int lo = 0, hi = b.B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)tileTab[2 * mid] <= tile) lo = mid; else hi = mid;
+  }
+  t = lo;
+  const int rel = tile - (int)tileTab[2 * t], per = (int)tileTab[2 * t + 1];
+  f = rel / per;
+  k = rel - f * per;
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_count(Batch b, int cur, const uint32_t* tileTab,
+                                                             uint32_t* tileCnt) {
+  int t, f, k;
+  part_locate(b, tileTab, blockIdx.x, t, f, k);
+  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr;
+  const uint32_t* posNode = b.posNode[cur];
+  const uint8_t* side = b.side + (size_t)t * b.n;
+  const uint32_t i0 = (uint32_t)k * kPartTile + threadIdx.x * kPartItems;
+  uint32_t c = 0;
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    const uint32_t i = i0 + it;
+    if (i < N && b.best[posNode[pos0 + i]].key) c += side[L[i]];
+  }
+  using BR = cub::BlockReduce<uint32_t, kPartThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint32_t tot = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) tileCnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur, const uint32_t* tileTab,
+                                                               const uint32_t* tilePref, const uint32_t* nextPos0,
+                                                               const uint32_t* nlBase, int debug_rows) {
+  int t, f, k;
+  part_locate(b, tileTab, blockIdx.x, t, f, k);
   const Nodes& nd = b.nd[cur];
   const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
-  if (N == 0) return;
   const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr;
   uint32_t* L2 = b.L[(cur & 1) ^ 1] + ((size_t)t * b.nl + f) * b.ntr;
   const uint32_t* posNode = b.posNode[cur];
@@ -905,52 +944,59 @@ __global__ void __launch_bounds__(256) k_partition(Batch b, int cur, const uint3
   const uint8_t* side = b.side + (size_t)t * b.n;
   const uint32_t nlb = nlBase[t];
   const uint32_t npos0 = nextPos0[t];
-  using BS = cub::BlockScan<uint32_t, 256>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < N; base += 256) {
-    const uint32_t i = base + threadIdx.x;
-    uint32_t r = 0, left = 0, g = 0;
-    bool sp = false;
-    Best bs{0ull, 0ull};
+  const int firstTile = (int)tileTab[2 * t] + f * (int)tileTab[2 * t + 1];
+  const uint32_t i0 = (uint32_t)k * kPartTile + threadIdx.x * kPartItems;
+  uint32_t rr[kPartItems], gg[kPartItems];
+  uint32_t flags = 0, c = 0;  // bit 2it: split node, bit 2it+1: left
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    const uint32_t i = i0 + it;
+    rr[it] = 0;
+    gg[it] = 0;
     if (i < N) {
-      g = posNode[pos0 + i];
-      bs = b.best[g];
-      sp = bs.key != 0ull;
-      r = L[i];
-      left = sp && side[r];
-    }
-    uint32_t ex, tot;
-    BS(tmp).ExclusiveSum(left, ex, tot);
-    const uint32_t leftBefore = carry + ex;  // left rows of this list before position i
-    if (i < N) {
-      if (sp) {
-        const U4S sc = b.chScan[g];
-        const uint32_t nodeLeftBase = sc.nl - nlb;      // left rows of earlier split nodes of the tree
-        const uint32_t within = left ? (leftBefore - nodeLeftBase)
-                                     : ((i - nd.start[g]) - (leftBefore - nodeLeftBase));
-        const uint32_t nl = b.chVal[g].nl;  // distinct rows going left (both split modes)
-        const uint32_t fl = b.chFlags[g];
-        const bool openL = fl & 1u, openR = fl & 2u;
-        if (left ? openL : openR) {
-          const uint32_t child = sc.op + ((!left && openL) ? 1u : 0u);
-          const uint32_t cstart = (sc.pos - npos0) + ((!left && openL) ? nl : 0u);
-          const uint32_t dest = cstart + within;
-          L2[dest] = r;
-          if (f == 0) posNode2[nextPos0[t] + dest] = child;
-        } else if (debug_rows && f == 0) {
-          const uint32_t cb = b.out[(size_t)t * b.cap + nd.bfs[g]].left;
-          b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)(cb + (left ? 0 : 1));
-        }
-      } else if (debug_rows && f == 0) {
-        b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
+      const uint32_t g = posNode[pos0 + i];
+      const uint32_t r = L[i];
+      gg[it] = g;
+      rr[it] = r;
+      if (b.best[g].key) {
+        const uint32_t lf = side[r];
+        flags |= (1u | (lf << 1)) << (2 * it);
+        c += lf;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
+  }
+  using BS = cub::BlockScan<uint32_t, kPartThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  uint32_t ex;
+  BS(tmp).ExclusiveSum(c, ex);
+  uint32_t leftBefore = (tilePref[blockIdx.x] - tilePref[firstTile]) + ex;  // left rows of this list before i0
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    const uint32_t i = i0 + it;
+    if (i >= N) break;
+    const uint32_t g = gg[it], r = rr[it];
+    const bool sp = (flags >> (2 * it)) & 1u, left = (flags >> (2 * it + 1)) & 1u;
+    if (sp) {
+      const U4S sc = b.chScan[g];
+      const uint32_t nodeLeftBase = sc.nl - nlb;  // left rows of earlier split nodes of the tree
+      const uint32_t within = left ? (leftBefore - nodeLeftBase) : ((i - nd.start[g]) - (leftBefore - nodeLeftBase));
+      const uint32_t nl = b.chVal[g].nl;  // distinct rows going left (both split modes)
+      const uint32_t fl = b.chFlags[g];
+      const bool openL = fl & 1u, openR = fl & 2u;
+      if (left ? openL : openR) {
+        const uint32_t child = sc.op + ((!left && openL) ? 1u : 0u);
+        const uint32_t cstart = (sc.pos - npos0) + ((!left && openL) ? nl : 0u);
+        const uint32_t dest = cstart + within;
+        L2[dest] = r;
+        if (f == 0) posNode2[npos0 + dest] = child;
+      } else if (debug_rows && f == 0) {
+        const uint32_t cb = b.out[(size_t)t * b.cap + nd.bfs[g]].left;
+        b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)(cb + (left ? 0 : 1));
+      }
+      leftBefore += left;
+    } else if (debug_rows && f == 0) {
+      b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
+    }
   }
 }
 
@@ -1049,11 +1095,18 @@ struct HistBufs {  // histogram mode: per-chunk-of-nodes histograms and work-ite
   uint32_t* pref = nullptr; // [cap + 1]
 };
 
-// Grows the batch's trees (slots [0, b.B)) to completion.
+struct PartBufs {  // partition tiles
+  uint32_t* tab = nullptr;   // [2 B]
+  uint32_t* cnt = nullptr;   // [max tiles]
+  uint32_t* pref = nullptr;  // [max tiles]
+};
+
+// Grows the batch's trees (slots [0, b.B)) to completion.  hcounters: pinned host
+// buffer of >= 4 + 3 (B + 1) words.
 rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, uint64_t seed, int task, int bootstrap,
                      void* cub_tmp, size_t cub_bytes, uint32_t* rootInfo, uint32_t* counters, uint32_t* hcounters,
                      uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp, const HistBufs& hb,
-                     unsigned long long* ncand, cudaStream_t s, std::string& err) {
+                     const PartBufs& pb, unsigned long long* ncand, cudaStream_t s, std::string& err) {
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
   LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
   if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
@@ -1073,6 +1126,9 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   k_init_level0<<<1, 1, 0, s>>>(b, rootInfo, counters);
   note_launch();
   LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
+  uint32_t* htPos0 = hcounters + 4;            // [B + 1] per-tree first positions (host)
+  uint32_t* htab = htPos0 + (b.B + 1);         // [2 B] partition tile table (host)
+  LCK(cudaMemcpyAsync(htPos0, b.tPos0, (size_t)(b.B + 1) * 4, cudaMemcpyDeviceToHost, s));
   LCK(cudaStreamSynchronize(s));
   long long NO = hcounters[0], NP = hcounters[1];
   if (NP > 0) {
@@ -1135,12 +1191,29 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     note_launch(2);
     {
       ProfScope ps("large_partition", s);
-      k_partition<<<b.B * b.nl, 256, 0, s>>>(b, cur, nextNode0, nextPos0, nlBase, b.leaf_of_row ? 1 : 0);
-      note_launch();
+      // tile table of the current level (per-tree position counts read back at the level start)
+      uint32_t tiles = 0;
+      for (int t = 0; t < b.B; ++t) {
+        const uint32_t Nt = htPos0[t + 1] - htPos0[t];
+        const uint32_t per = (Nt + kPartTile - 1) / kPartTile;
+        htab[2 * t] = tiles;
+        htab[2 * t + 1] = per ? per : 1u;
+        tiles += per * (uint32_t)b.nl;
+      }
+      if (tiles > 0) {
+        LCK(cudaMemcpyAsync(pb.tab, htab, (size_t)2 * b.B * 4, cudaMemcpyHostToDevice, s));
+        k_part_count<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.cnt);
+        tb = cub_bytes;
+        LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, pb.cnt, pb.pref, (int)tiles, s));
+        k_part_scatter<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.pref, nextPos0, nlBase,
+                                                       b.leaf_of_row ? 1 : 0);
+        note_launch(2);
+      }
     }
     k_set_next_tree_tables<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, nextNode0, nextPos0, counters);
     note_launch();
     LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
+    LCK(cudaMemcpyAsync(htPos0, b.tPos0, (size_t)(b.B + 1) * 4, cudaMemcpyDeviceToHost, s));
     LCK(cudaStreamSynchronize(s));
     NO = hcounters[0];
     NP = hcounters[1];
@@ -1366,7 +1439,12 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(sc.alloc(&nextPos0, (size_t)B + 1));
   LCK(sc.alloc(&nlBase, (size_t)B + 1));
   uint32_t* hcounters = nullptr;
-  LCK(cudaMallocHost(&hcounters, 16));
+  LCK(cudaMallocHost(&hcounters, (size_t)(4 + 3 * (B + 1)) * 4));
+  PartBufs pbufs;
+  const long long max_tiles = (long long)nlists * (B + pl.npmax / kPartTile + 1) + 1;
+  LCK(sc.alloc(&pbufs.tab, (size_t)2 * B));
+  LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
+  LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
   struct HostFree {
     uint32_t* p;
     ~HostFree() { cudaFreeHost(p); }
@@ -1377,9 +1455,10 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   cub::DeviceScan::ExclusiveScan(nullptr, cb2, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull},
                                  (int)pl.tiles_max + 1, s);
   cub::DeviceScan::ExclusiveScan(nullptr, cb3, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)pl.nmax, s);
-  size_t cb4 = 0;
+  size_t cb4 = 0, cb5 = 0;
   if (hist) cub::DeviceScan::ExclusiveSum(nullptr, cb4, hb.nch, hb.pref, (int)hb.cap + 1, s);
-  const size_t cub_bytes = std::max(std::max(cb1, cb4), std::max(cb2, cb3));
+  cub::DeviceScan::ExclusiveSum(nullptr, cb5, pbufs.cnt, pbufs.pref, (int)max_tiles, s);
+  const size_t cub_bytes = std::max(std::max(std::max(cb1, cb4), std::max(cb2, cb3)), cb5);
   char* cub_tmp;
   LCK(sc.alloc(&cub_tmp, cub_bytes + 16));
   // outputs
@@ -1398,8 +1477,8 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     b.outCount = outCount + t0;
     b.leaf_of_row = leaf_of_row ? leaf_of_row + (size_t)t0 * n : nullptr;
     rf_status st = grow_batch(b, pl, list_src, prm->seed, task, (int)prm->bootstrap, cub_tmp, cub_bytes, rootInfo,
-                              counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, hb, candidate_counter(), s,
-                              err);
+                              counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, hb, pbufs, candidate_counter(),
+                              s, err);
     if (st) return st;
   }
   *nodes_out = out;

@@ -304,6 +304,17 @@ def test_hist_equals_exact_structure_when_few_distinct():
     assert np.array_equal(ge["value"][leaves].view(np.int64), gh["value"][leaves].view(np.int64))
 
 
+def test_hist_config4_shape_sampled():
+    """Config 4 shape (x 64 features, mtry 21, max_depth 12, histogram mode) at 200k rows,
+    2 trees vs the oracle; predictions on held-out rows."""
+    X, y = datagen.scaled(200_000, 64)
+    of = oracle.fit(X, y, ntree=2, seed=11, mtry=21, max_depth=12, split_mode=1, target=1)
+    gf = rfg.fit(X, y, ntree=2, seed=11, mtry=21, max_depth=12, split_mode=1, target=1)
+    _compare_forest(gf, of, X)
+    Q = datagen.queries(5000, 64)
+    np.testing.assert_allclose(rfg.predict(gf, Q), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
 def test_hist_cv_parity():
     X, y = datagen.paper_shaped(500, "V100", "power")
     fm_o, pr_o = oracle.cv_grid(X, y, 4, 1, [3, 6], [4], seed=5, split_mode=1, want_pred=True)
