@@ -562,7 +562,7 @@ rf_status rf_fit_debug(const double* X, uint64_t n, uint32_t p, const double* y,
 }
 
 static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, uint32_t p, double* dout,
-                              int mode, cudaStream_t s) {
+                              int mode, cudaStream_t s, double* host_out = nullptr) {
   if (!f) return fail(RF_E_ARG, "forest is NULL");
   if (p != f->p) return fail(RF_E_ARITY, "p differs from the forest's");
   if (n == 0) return RF_OK;
@@ -570,11 +570,21 @@ static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, 
   int* err;
   CK(sc.alloc(&err, 1), "alloc");
   CK(cudaMemsetAsync(err, 0, 4, s), "memset");
-  CK(rf::check_finite(dX, n * p, err, s), "check");
+  const bool few = (long long)n <= rf::kFewRows;
+  if (!few) CK(rf::check_finite(dX, n * p, err, s), "check");
   {
     ProfScope ps("predict", s);
-    CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s),
+    CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s,
+                          few ? err : nullptr),
        "predict");
+  }
+  if (host_out) {  // one synchronisation for result and error flag
+    int h = 0;
+    CK(cudaMemcpyAsync(host_out, dout, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "sync");
+    if (h) return fail(RF_E_NONFINITE, "non-finite value in X");
+    return RF_OK;
   }
   return read_err(err, s);
 }
@@ -614,11 +624,7 @@ rf_status rf_predict(const rf_forest* f, const double* X, uint64_t n, uint32_t p
   CK(sc.alloc(&dX, n * p), "alloc");
   CK(sc.alloc(&dy, n), "alloc");
   CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
-  rf_status st = predict_core(f, dX, n, p, dy, f->target == RF_TARGET_LOG ? 2 : 1, s);
-  if (st) return st;
-  CK(cudaMemcpyAsync(yhat, dy, n * 8, cudaMemcpyDeviceToHost, s), "d2h");
-  CK(cudaStreamSynchronize(s), "sync");
-  return RF_OK;
+  return predict_core(f, dX, n, p, dy, f->target == RF_TARGET_LOG ? 2 : 1, s, yhat);
 }
 
 rf_status rf_make_folds_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,

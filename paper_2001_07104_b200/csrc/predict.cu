@@ -37,6 +37,42 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
   }
 }
 
+// Few rows (single-query latency, T4/T5 of the paper): one CTA per row, threads
+// over trees (tree t -> thread t mod 256, each thread in tree order), a fixed-shape
+// block reduction (deterministic), finiteness check of the row in the same kernel.
+constexpr int kFewThreads = 256;
+
+__global__ void __launch_bounds__(kFewThreads) k_predict_few(const Node16* __restrict__ nodes,
+                                                             const uint64_t* __restrict__ tree_off, int T,
+                                                             const double* __restrict__ X, int p, int mode,
+                                                             double* __restrict__ out, int* err) {
+  const long long r = blockIdx.x;
+  const double* x = X + r * p;
+  bool bad = false;
+  for (int j = threadIdx.x; j < p; j += kFewThreads) bad |= !isfinite(x[j]);
+  if (bad) atomicOr(err, 1);
+  double s = 0.0;
+  for (int t = threadIdx.x; t < T; t += kFewThreads) {
+    const Node16* tn = nodes + tree_off[t];
+    Node16 nd = tn[0];
+    while (nd.feat >= 0) nd = tn[nd.left + ((x[nd.feat] <= nd.v) ? 0u : 1u)];
+    s += nd.v;
+  }
+  // fixed-order block reduction: warps by shuffles, then warp sums in warp order
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
+  __shared__ double ws[kFewThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < kFewThreads / 32; ++w) tot += ws[w];
+    if (mode == 1) tot = tot / (double)T;
+    if (mode == 2) tot = exp(tot / (double)T);
+    out[r] = tot;
+  }
+}
+
 __global__ void k_pred_finalize(const double* partial, long long n, int T, int target, double* out) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
        r += (long long)gridDim.x * blockDim.x) {
@@ -56,8 +92,13 @@ __global__ void k_check_finite(const double* X, size_t total, int* err) {
 }  // namespace
 
 cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
-                           long long n, int p, int mode, double* out, cudaStream_t s) {
+                           long long n, int p, int mode, double* out, cudaStream_t s, int* err_few) {
   if (n <= 0) return cudaSuccess;
+  if (err_few && n <= kFewRows) {  // latency path: rows checked for finiteness in-kernel
+    k_predict_few<<<(unsigned)n, kFewThreads, 0, s>>>(nodes, tree_off, T, X, p, mode, out, err_few);
+    note_launch();
+    return cudaGetLastError();
+  }
   long long blocks = (n + 255) / 256;
   if (blocks > 148LL * 64) blocks = 148LL * 64;
   k_predict<<<(unsigned)blocks, 256, 0, s>>>(nodes, tree_off, T, X, n, p, mode, out);

@@ -158,6 +158,20 @@ def test_predict_parity(target):
     np.testing.assert_allclose(fin, want, rtol=RTOL, atol=0)
 
 
+@pytest.mark.parametrize("nq", [1, 7, 256, 257])
+def test_predict_few_rows_latency_path(nq):
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    of = oracle.fit(X, y, ntree=512, seed=3, mtry=12, target=1)
+    gf = rfg.fit(X, y, ntree=512, seed=3, mtry=12, target=1)
+    Q = datagen.paper_shaped(300, "K20", "time", seed=77)[0][:nq]
+    np.testing.assert_allclose(rfg.predict(gf, Q), oracle.predict(of, Q), rtol=RTOL, atol=0)
+    Qn = Q.copy()
+    Qn[-1, 3] = np.inf
+    with pytest.raises(rfg.RFError) as e:
+        rfg.predict(gf, Qn)
+    assert e.value.code == rfg.E_NONFINITE
+
+
 def test_predict_fits_exactly():
     X, y = datagen.paper_shaped(189, "K20", "time")
     _, idx = np.unique(X, axis=0, return_index=True)
