@@ -1344,7 +1344,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   if (prm->max_depth >= 1 && prm->max_depth < 31) open_max = std::min<long long>(open_max, 1ll << (prm->max_depth - 1));
   // batch size: the row lists dominate (2 lists-per-tree x ntr x 4 B per tree)
   const size_t per_tree = (size_t)2 * nlists * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 + (size_t)open_max * 128;
-  int B = (int)std::max<size_t>(1, std::min<size_t>(32, ((size_t)6 << 30) / std::max<size_t>(per_tree, 1)));
+  // trees per batch: per-level launch and sync costs are shared by the batch, so batches are
+  // as large as a 16 GB working-set budget allows (of the 180 GB HBM), up to 128 trees
+  int B = (int)std::max<size_t>(1, std::min<size_t>(128, ((size_t)16 << 30) / std::max<size_t>(per_tree, 1)));
   B = std::min(B, T);
   LargePlan pl;
   pl.B = B;
