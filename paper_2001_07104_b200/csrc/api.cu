@@ -278,14 +278,18 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
   a.err = d.err;
   a.cand = rf::candidate_counter();
-  a.wpb = 4;
+  // warps per CTA: the most resident warps per SM (registers and shared memory both bound it)
+  int best_wpb = 0, best_warps = 0;
   size_t smem = 0;
-  for (; a.wpb >= 1; a.wpb >>= 1) {
-    smem = rf::small_tree_smem_bytes(a, 0);
-    if (smem <= 227 * 1024) break;
+  for (int w = 1; w <= rf::kSmallMaxWpb; ++w) {
+    a.wpb = w;
+    const int warps = w * rf::small_tree_ctas_per_sm(a);
+    if (warps > best_warps) { best_warps = warps; best_wpb = w; }
   }
-  if (a.wpb == 0) return fail(RF_E_UNSUPPORTED, "small-tree kernel: shared memory budget exceeded");
-  const int resident = resident_warps(smem, a.wpb);
+  if (best_wpb == 0) return fail(RF_E_UNSUPPORTED, "small-tree kernel: shared memory budget exceeded");
+  a.wpb = best_wpb;
+  smem = rf::small_tree_smem_bytes(a, 0);
+  const int resident = 148 * best_warps;
   for (int c = 16; c >= 1; --c) {
     if (g % c) continue;
     long long jobs = (long long)nmd * ntask * ((T + c - 1) / c);

@@ -34,54 +34,71 @@
 namespace rf {
 namespace {
 
+// All shared-memory arrays are 32-bit offsets into one extern __shared__ symbol:
+// the compiler then addresses them as shared memory directly (LDS/STS with a
+// register offset) instead of converting generic pointers, and each handle costs
+// one register instead of two.
+extern __shared__ __align__(16) char g_smem[];
+
+template <typename T>
+struct SA {
+  uint32_t off;
+  template <typename I>
+  __device__ __forceinline__ T& operator[](I i) const {
+    return reinterpret_cast<T*>(g_smem + off)[i];
+  }
+  __device__ __forceinline__ SA operator+(int i) const { return SA{off + (uint32_t)i * (uint32_t)sizeof(T)}; }
+  __device__ __forceinline__ T* ptr() const { return reinterpret_cast<T*>(g_smem + off); }
+};
+
 struct Carve {
-  char* base;
   size_t off;
-  __host__ __device__ Carve(char* b) : base(b), off(0) {}
+  __host__ __device__ explicit Carve(size_t start = 0) : off(start) {}
   template <typename T>
-  __host__ __device__ T* take(size_t count, size_t align = 8) {
+  __host__ __device__ SA<T> take(size_t count, size_t align = 8) {
     off = (off + align - 1) / align * align;
-    T* p = reinterpret_cast<T*>(base + off);
+    SA<T> p{(uint32_t)off};
     off += count * sizeof(T);
     return p;
   }
 };
 
 struct CtaSmem {
-  uint8_t* ord;    // [p][ntr_max] local rows in x order
-  uint8_t* lrank;  // [p][ntr_max] dense rank of x among training rows, by local row
-  int64_t* tq;     // [ntr_max]
-  double2* rcp2;   // [256] (w, RN(1/w))
-  double* xte;     // [nte_max][p]
+  SA<uint8_t> ord;    // [p][ntr_max] local rows in x order
+  SA<uint8_t> lrank;  // [p][ntr_max] dense rank of x among training rows, by local row
+  SA<int64_t> tq;     // [ntr_max]
+  SA<double2> rcp2;   // [256] (w, RN(1/w))
+  SA<double> xte;     // [nte_max][p]
 };
 
 struct NodeSet {  // open nodes of one level
-  uint8_t* start;
-  uint8_t* len;
-  uint16_t* W;
-  int64_t* S;
-  uint64_t* heap;
-  uint16_t* bfs;
+  SA<uint8_t> start;
+  SA<uint8_t> len;
+  SA<uint16_t> W;
+  SA<int64_t> S;
+  SA<uint64_t> heap;
+  SA<uint16_t> bfs;
 };
 
 struct WarpSmem {
-  uint8_t* w;       // [ntr_max] bootstrap multiplicities
-  uint8_t* listA;   // [p][ntr_max]
-  uint8_t* listB;   // [p][ntr_max]
-  uint8_t* pnA;     // [ntr_max] position -> open node
-  uint8_t* pnB;
-  uint8_t* side;    // [ntr_max] by local row: 1 = goes left
+  SA<uint8_t> w;       // [ntr_max] bootstrap multiplicities
+  SA<uint8_t> listA;   // [p][ntr_max]
+  SA<uint8_t> listB;   // [p][ntr_max]
+  SA<uint8_t> pnA;     // [ntr_max] position -> open node
+  SA<uint8_t> pnB;
+  SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
-  uint8_t* feat;    // [NM][p] drawn features (partial Fisher-Yates)
-  unsigned long long* bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
-  uint32_t* baux;   // best (feature << 8 | position); bit 31 = split
-  uint32_t* bW;     // search: prefix base of W; mark: left W
-  uint64_t* bS;     // search: prefix base of S; mark: left S
-  uint8_t* ncb;     // [NM][2] child non-constant flags
-  uint8_t* chOpen;  // [NM][2] open index of the children or kNone
-  double* chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
-  uint16_t* chBase; // BFS id of the left child
-  uint32_t* thrIdx; // fit mode: threshold rank
+  SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates)
+  SA<unsigned long long> bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
+  SA<uint32_t> baux;   // best (feature << 8 | position); bit 31 = split
+  SA<uint32_t> bW;     // search: prefix base of W; then the best's left W
+  SA<uint64_t> bS;     // search: prefix base of S; then the best's left S; then the partition record
+  SA<uint8_t> ncb;     // [NM][2] child non-constant flags
+  SA<uint8_t> chOpen;  // [NM][2] open index of the children or kNone
+  SA<double> chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
+  SA<uint16_t> chBase; // BFS id of the left child
+  SA<uint32_t> thrIdx; // fit mode: threshold rank
+  SA<uint32_t> desc;   // [ntr_max] partition descriptor per position (shared by all lists)
 };
 
 constexpr uint8_t kNone = 0xFF;
@@ -116,7 +133,7 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.side = c.take<uint8_t>(ntr_max, 4);
   carve_nodeset(c, s.cur, NM);
   carve_nodeset(c, s.nxt, NM);
-  s.feat = need_feat ? c.take<uint8_t>((size_t)NM * p, 4) : nullptr;
+  s.feat = need_feat ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
   s.bkey = c.take<unsigned long long>(NM, 8);
   s.baux = c.take<uint32_t>(NM, 4);
   s.bW = c.take<uint32_t>(NM, 4);
@@ -125,11 +142,17 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.chOpen = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chVal = c.take<double>((size_t)NM * 2, 8);
   s.chBase = c.take<uint16_t>(NM, 4);
-  s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : nullptr;
+  s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
+  s.desc = c.take<uint32_t>(ntr_max, 4);
 }
 
 // ---------------------------------------------------------------- warp ops --
-__device__ __forceinline__ uint32_t wscan_u32(uint32_t v, uint32_t& total) {
+// Out of line (one copy each): every inlined shuffle carries divergence-handling
+// code, and the kernel's per-level code must fit the instruction caches.
+struct Scan32 { uint32_t ex, tot; };
+struct Scan64 { uint64_t ex, tot; };
+
+__device__ __noinline__ Scan32 wscan32(uint32_t v) {
   const int lane = threadIdx.x & 31;
   uint32_t x = v;
 #pragma unroll
@@ -137,11 +160,10 @@ __device__ __forceinline__ uint32_t wscan_u32(uint32_t v, uint32_t& total) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
     if (lane >= d) x += y;
   }
-  total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
+  return Scan32{x - v, __shfl_sync(0xffffffffu, x, 31)};
 }
 
-__device__ __forceinline__ uint64_t wscan_u64(uint64_t v, uint64_t& total) {
+__device__ __noinline__ Scan64 wscan64(uint64_t v) {
   const int lane = threadIdx.x & 31;
   uint64_t x = v;
 #pragma unroll
@@ -149,28 +171,45 @@ __device__ __forceinline__ uint64_t wscan_u64(uint64_t v, uint64_t& total) {
     const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
     if (lane >= d) x += y;
   }
-  total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
+  return Scan64{x - v, __shfl_sync(0xffffffffu, x, 31)};
 }
 
-__device__ __forceinline__ int64_t wsum_i64(int64_t v) {
+__device__ __forceinline__ uint32_t wscan_u32(uint32_t v, uint32_t& total) {
+  const Scan32 s = wscan32(v);
+  total = s.tot;
+  return s.ex;
+}
+__device__ __forceinline__ uint64_t wscan_u64(uint64_t v, uint64_t& total) {
+  const Scan64 s = wscan64(v);
+  total = s.tot;
+  return s.ex;
+}
+
+__device__ __noinline__ int64_t wsum_i64(int64_t v) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
   return v;
 }
-__device__ __forceinline__ int64_t wmin_i64(int64_t v) {
+__device__ __noinline__ int64_t wmin_i64(int64_t v) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) { int64_t o = __shfl_xor_sync(0xffffffffu, v, d); v = o < v ? o : v; }
   return v;
 }
-__device__ __forceinline__ int64_t wmax_i64(int64_t v) {
+__device__ __noinline__ int64_t wmax_i64(int64_t v) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) { int64_t o = __shfl_xor_sync(0xffffffffu, v, d); v = o > v ? o : v; }
   return v;
 }
 
-__device__ __forceinline__ double leaf_value(int64_t S, uint32_t W, int F) {
+// Rarely executed helpers are out of line: the kernel's hot per-level code must fit
+// the instruction caches (ncu showed no_instruction stalls with everything inlined).
+__device__ __noinline__ double leaf_value(int64_t S, uint32_t W, int F) {
   return scalbn(__ddiv_rn(__ll2double_rn(S), __uint2double_rn(W)), -F);
+}
+
+__device__ __noinline__ void philox_pair_ool(uint32_t k0, uint32_t k1, uint32_t b, uint32_t c1, uint32_t c2,
+                                             uint32_t c3, uint64_t& d0, uint64_t& d1) {
+  philox_pair(k0, k1, b, c1, c2, c3, d0, d1);
 }
 
 // RN(a / w) for an integer 1 <= w <= 255 with y = RN(1/w): one Markstein correction
@@ -188,8 +227,7 @@ __device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsig
 // -------------------------------------------------------------- the kernel --
 // TM: max test rows per lane.
 template <bool kFit, int TM>
-__global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
-  extern __shared__ __align__(16) char smem[];
+__global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int p = a.p;
@@ -207,17 +245,17 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   bool any_feat = false;
   for (int i = 0; i < a.n_mtry; ++i) any_feat |= (a.mtrys[i] < p);
 
-  Carve cv(smem);
+  Carve cv;
   CtaSmem cs;
   carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max);
   WarpSmem ws;
   {
     const size_t cta_bytes = (cv.off + 15) / 16 * 16;
-    Carve cw(nullptr);
+    Carve cw;
     WarpSmem dummy;
     carve_warp(cw, dummy, p, ntr_max, any_feat, kFit);
     const size_t per_warp = (cw.off + 15) / 16 * 16;
-    Carve mine(smem + cta_bytes + per_warp * warp);
+    Carve mine(cta_bytes + per_warp * warp);
     carve_warp(mine, ws, p, ntr_max, any_feat, kFit);
   }
 
@@ -230,16 +268,20 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
   {
     const uint8_t* go = a.ord + (size_t)tl * p * a.ntr_stride;
     const uint8_t* gr = a.lrank + (size_t)tl * p * a.ntr_stride;
+    #pragma unroll 1
     for (int i = threadIdx.x; i < p * ntr; i += blockDim.x) {
       const int f = i / ntr, j = i - f * ntr;
       cs.ord[f * ntr_max + j] = go[(size_t)f * a.ntr_stride + j];
       cs.lrank[f * ntr_max + j] = gr[(size_t)f * a.ntr_stride + j];
     }
+    #pragma unroll 1
     for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
+    #pragma unroll 1
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
       cs.rcp2[i] = make_double2((double)i, i ? __ddiv_rn(1.0, (double)i) : 0.0);
     if (!kFit) {
       const uint32_t* te_rows = a.te_rows + (size_t)tl * a.row_stride;
+      #pragma unroll 1
       for (int i = threadIdx.x; i < nte * p; i += blockDim.x) {
         const int r = i / p, f = i - r * p;
         cs.xte[i] = a.X[(size_t)te_rows[r] * p + f];
@@ -265,32 +307,38 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     const size_t tree_slot = (size_t)(t - a.tree_lo);
 
     // ---- bootstrap (R2): n_tr draws with replacement -> u8 counts (n_tr <= 255)
-    for (int i = lane; i < (ntr + 3) / 4; i += 32) reinterpret_cast<uint32_t*>(ws.w)[i] = 0u;
+    const SA<uint32_t> w32{ws.w.off};
+    #pragma unroll 1
+    for (int i = lane; i < (ntr + 3) / 4; i += 32) w32[i] = 0u;
     __syncwarp();
     if (a.bootstrap) {
       const int nblk = (ntr + 1) >> 1;
+      #pragma unroll 1
       for (int b = lane; b < nblk; b += 32) {
         uint64_t d0, d1;
-        philox_pair(k0, k1, (uint32_t)b, 0u, 0u, kTagBoot, d0, d1);
+        philox_pair_ool(k0, k1, (uint32_t)b, 0u, 0u, kTagBoot, d0, d1);
         const uint32_t i0 = (uint32_t)mulhi64(d0, (uint64_t)ntr);
-        atomicAdd(reinterpret_cast<uint32_t*>(ws.w) + (i0 >> 2), 1u << ((i0 & 3) * 8));
+        atomicAdd(&w32[i0 >> 2], 1u << ((i0 & 3) * 8));
         if (2 * b + 1 < ntr) {
           const uint32_t i1 = (uint32_t)mulhi64(d1, (uint64_t)ntr);
-          atomicAdd(reinterpret_cast<uint32_t*>(ws.w) + (i1 >> 2), 1u << ((i1 & 3) * 8));
+          atomicAdd(&w32[i1 >> 2], 1u << ((i1 & 3) * 8));
         }
       }
     } else {
+      #pragma unroll 1
       for (int i = lane; i < ntr; i += 32) ws.w[i] = 1;
     }
     __syncwarp();
 
     if (kFit && a.leaf_of_row)
+      #pragma unroll 1
       for (int i = lane; i < ntr; i += 32)
         if (!ws.w[i]) a.leaf_of_row[tree_slot * a.n + tr_rows[i]] = -1;
 
     // ---- root statistics
     int64_t S = 0, mn = INT64_MAX, mx = INT64_MIN;
     uint32_t D = 0;
+    #pragma unroll 1
     for (int i = lane; i < ntr; i += 32) {
       const uint32_t wv = ws.w[i];
       if (wv) {
@@ -322,6 +370,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         a.tree_nnodes[tree_slot] = 1;
       }
       if (kFit && a.leaf_of_row)
+        #pragma unroll 1
         for (int i = lane; i < ntr; i += 32)
           if (ws.w[i]) a.leaf_of_row[tree_slot * a.n + tr_rows[i]] = 0;
       __syncwarp();
@@ -329,13 +378,15 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
     }
 
     // ---- in-bag lists: stable compaction of the presorted orders by w > 0
-    uint8_t* L = ws.listA;
-    uint8_t* L2 = ws.listB;
-    uint8_t* pn = ws.pnA;
-    uint8_t* pn2 = ws.pnB;
+    SA<uint8_t> L = ws.listA;
+    SA<uint8_t> L2 = ws.listB;
+    SA<uint8_t> pn = ws.pnA;
+    SA<uint8_t> pn2 = ws.pnB;
     NodeSet cur = ws.cur, nxt = ws.nxt;
+    #pragma unroll 1
     for (int f = 0; f < p; ++f) {
       uint32_t off = 0;
+      #pragma unroll 1
       for (int c = 0; c < ntr; c += 32) {
         const int j = c + lane;
         uint8_t r = 0;
@@ -346,6 +397,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         off += __popc(bal);
       }
     }
+    #pragma unroll 1
     for (int i = lane; i < (int)D; i += 32) pn[i] = 0;
     if (lane == 0) {
       cur.start[0] = 0; cur.len[0] = (uint8_t)D; cur.W[0] = (uint16_t)Wroot; cur.S[0] = S;
@@ -363,6 +415,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       {
         uint32_t carryW = 0;
         uint64_t carryS = 0;
+        #pragma unroll 1
         for (int b0 = 0; b0 < nOpen; b0 += 32) {
           const int k = b0 + lane;
           const bool act = k < nOpen;
@@ -378,13 +431,15 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             ws.bkey[k] = 0ull;
             ws.baux[k] = 0x7FFFFFFFu;
             if (need_feat) {
-              uint8_t* fp = ws.feat + (size_t)k * p;
+              const SA<uint8_t> fp = ws.feat + k * p;
+              #pragma unroll 1
               for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
               const uint64_t h = cur.heap[k];
               const uint32_t hlo = (uint32_t)h, hhi = (uint32_t)(h >> 32);
+              #pragma unroll 1
               for (int j = 0; j < m; j += 2) {
                 uint64_t d0, d1;
-                philox_pair(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
+                philox_pair_ool(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
                 int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
                 uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
                 if (j + 1 < m) {
@@ -429,6 +484,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         // pass 1: lane totals
         uint32_t lw = 0;
         uint64_t ls = 0;
+        #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
           const uint8_t r = L[lbase + st + i];
@@ -464,6 +520,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
         uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
         uint8_t r = L[lbase + st + i];
         uint32_t rkr = cs.lrank[lbase + r];
+        #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
           const uint32_t wv = act ? (uint32_t)ws.w[r] : 0u;
@@ -554,6 +611,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       __syncwarp();
 
       // ---------------- (c) decisions and thresholds; first-row targets of the children
+      #pragma unroll 1
       for (int k = lane; k < nOpen; k += 32) {
         const unsigned long long key = ws.bkey[k];
         ws.ncb[2 * k] = 0;
@@ -567,13 +625,15 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
           ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
           ws.baux[k] = aux | 0x80000000u;  // split flag
           if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
-          reinterpret_cast<int64_t*>(ws.chVal)[2 * k] = cs.tq[L[f * ntr_max + cur.start[k]]];
-          reinterpret_cast<int64_t*>(ws.chVal)[2 * k + 1] = cs.tq[rb];
+          const SA<int64_t> tqf{ws.chVal.off};  // child first-row targets (chVal is free here)
+          tqf[2 * k] = cs.tq[L[f * ntr_max + cur.start[k]]];
+          tqf[2 * k + 1] = cs.tq[rb];
         }
       }
       __syncwarp();
 
       // ---------------- (d) mark pass: go-left flags, child constancy (lock-step, no atomics)
+      #pragma unroll 1
       for (int base = 0; base < N; base += 32) {
         const int pos = base + lane;
         if (pos < N) {
@@ -584,7 +644,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
             const uint8_t r = L[f * ntr_max + pos];
             const int sd = pos <= (int)(aux & 0xFFu) ? 0 : 1;
             ws.side[r] = (uint8_t)(1 - sd);
-            if (cs.tq[r] != reinterpret_cast<const int64_t*>(ws.chVal)[2 * k + sd]) ws.ncb[2 * k + sd] = 1;
+            if (cs.tq[r] != SA<int64_t>{ws.chVal.off}[2 * k + sd]) ws.ncb[2 * k + sd] = 1;
           }
         }
       }
@@ -594,6 +654,7 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       int nSplitTotal = 0, nOpenNext = 0, Nnext = 0, NL = 0;
       {
         uint32_t carrySplit = 0, carryOpen = 0, carryPos = 0, carryL = 0;
+        #pragma unroll 1
         for (int b0 = 0; b0 < nOpen; b0 += 32) {
           const int k = b0 + lane;
           const bool act = k < nOpen;
@@ -722,12 +783,15 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
       // the child segments (bS[k] holds the packed record, see (e)).
       const bool rows_debug = kFit && a.leaf_of_row != nullptr;
       if (nOpenNext > 0 || rows_debug) {
-        const int E = p * N;
+        const unsigned lt = lanemask_lt();
+        // list 0: also writes the next level's position -> node map (and debug leaf rows);
+        // builds the per-position descriptor shared by the other lists:
+        //   dL | dR << 8 | leftBase << 16 | start << 24, or ~0 for positions of unsplit nodes
         uint32_t carry = 0;
-        int f = 0, pos = lane;
-        while (pos >= N) { pos -= N; ++f; }
-        for (int base = 0; base < E; base += 32) {
-          const bool valid = base + lane < E;
+        #pragma unroll 1
+        for (int base = 0; base < N; base += 32) {
+          const int pos = base + lane;
+          const bool valid = pos < N;
           uint64_t info = 0;
           uint8_t r = 0;
           int k = 0;
@@ -735,39 +799,70 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
           if (valid) {
             k = pn[pos];
             info = ws.bS[k];
-            r = L[f * ntr_max + pos];
+            r = L[pos];
             left = ((info >> 48) & 1u) && ws.side[r];
+            ws.desc[pos] = ((info >> 48) & 1u) ? (uint32_t)((info >> 16) & 0xFFFFu) |
+                                                     ((uint32_t)((info >> 8) & 0xFFu) << 16) |
+                                                     ((uint32_t)(info & 0xFFu) << 24)
+                                               : 0xFFFFFFFFu;
           }
           const unsigned bal = __ballot_sync(0xffffffffu, left);
           if (valid) {
             if ((info >> 48) & 1u) {
               const uint32_t st = (uint32_t)(info & 0xFFu);
-              const uint32_t leftBefore =
-                  carry + __popc(bal & lanemask_lt()) - (uint32_t)f * (uint32_t)NL - (uint32_t)((info >> 8) & 0xFFu);
+              const uint32_t leftBefore = carry + __popc(bal & lt) - (uint32_t)((info >> 8) & 0xFFu);
               const uint32_t sh = left ? 0u : 8u;
-              const uint32_t d = (uint32_t)(info >> (16 + sh)) & 0xFFu;   // child segment start
+              const uint32_t d = (uint32_t)(info >> (16 + sh)) & 0xFFu;  // child segment start
               if (d != kNone) {
-                const uint32_t within = left ? leftBefore : ((uint32_t)pos - st) - leftBefore;
-                const uint32_t dest = d + within;
-                L2[f * ntr_max + dest] = r;
-                if (f == 0) pn2[dest] = (uint8_t)(info >> (32 + sh));
-              } else if (rows_debug && f == 0) {
+                const uint32_t dest = d + (left ? leftBefore : ((uint32_t)pos - st) - leftBefore);
+                L2[dest] = r;
+                pn2[dest] = (uint8_t)(info >> (32 + sh));
+              } else if (rows_debug) {
                 a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)(ws.chBase[k] + (left ? 0 : 1));
               }
-            } else if (rows_debug && f == 0) {
+            } else if (rows_debug) {
               a.leaf_of_row[tree_slot * a.n + tr_rows[r]] = (int32_t)cur.bfs[k];
             }
           }
           carry += __popc(bal);
-          pos += 32;
-          while (pos >= N) { pos -= N; ++f; }
+        }
+        __syncwarp();
+        // lists 1..p-1, flattened feature-major: element e -> list 1 + e / N, position e % N
+        // (e / N exactly via a float reciprocal: e < 2^16)
+        const int E = (p - 1) * N;
+        const float invN = 1.0f / (float)N;
+        carry = 0;
+        #pragma unroll 1
+        for (int base = 0; base < E; base += 32) {
+          const int e = base + lane;
+          const bool valid = e < E;
+          int fi = (int)((float)e * invN);
+          fi += (e - fi * N >= N) ? 1 : 0;
+          fi -= (e - fi * N < 0) ? 1 : 0;
+          const int pos = e - fi * N;
+          const int f = fi + 1;
+          uint32_t dsc = 0xFFFFFFFFu;
+          uint8_t r = 0;
+          if (valid) {
+            dsc = ws.desc[pos];
+            r = L[f * ntr_max + pos];
+          }
+          const bool left = dsc != 0xFFFFFFFFu && ws.side[r];
+          const unsigned bal = __ballot_sync(0xffffffffu, left);
+          const uint32_t d = left ? (dsc & 0xFFu) : ((dsc >> 8) & 0xFFu);
+          if (valid && d != kNone) {
+            const uint32_t leftBefore = carry + __popc(bal & lt) - (uint32_t)fi * (uint32_t)NL - ((dsc >> 16) & 0xFFu);
+            const uint32_t dest = d + (left ? leftBefore : ((uint32_t)pos - (dsc >> 24)) - leftBefore);
+            L2[f * ntr_max + dest] = r;
+          }
+          carry += __popc(bal);
         }
       }
       // advance to the next level
       {
         const NodeSet tmp = cur; cur = nxt; nxt = tmp;
-        uint8_t* t8 = L; L = L2; L2 = t8;
-        uint8_t* tp = pn; pn = pn2; pn2 = tp;
+        const SA<uint8_t> t8 = L; L = L2; L2 = t8;
+        const SA<uint8_t> tp = pn; pn = pn2; pn2 = tp;
       }
       curBase += levelCount;
       levelCount = 2u * (uint32_t)nSplitTotal;
@@ -800,15 +895,34 @@ __global__ void __launch_bounds__(128) small_tree_kernel(SmallArgs a) {
 size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   bool any_feat = false;
   for (int i = 0; i < a.n_mtry; ++i) any_feat |= (a.mtrys[i] < a.p);
-  Carve c(nullptr);
+  Carve c;
   CtaSmem cs;
   carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max);
   const size_t cta = (c.off + 15) / 16 * 16;
-  Carve w(nullptr);
+  Carve w;
   WarpSmem ws;
   carve_warp(w, ws, a.p, a.ntr_max, any_feat, a.fit_mode != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
+}
+
+template <bool kFit, int TM>
+static int ctas_t(const SmallArgs& a) {
+  const size_t smem = small_tree_smem_bytes(a, 0);
+  if (smem > 227 * 1024) return 0;
+  auto kern = small_tree_kernel<kFit, TM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * a.wpb, smem) != cudaSuccess) return 0;
+  return nb;
+}
+
+int small_tree_ctas_per_sm(const SmallArgs& a) {
+  if (a.fit_mode) return ctas_t<true, 1>(a);
+  const int TMn = (a.nte_max + 31) / 32;
+  if (TMn <= 1) return ctas_t<false, 1>(a);
+  if (TMn <= 2) return ctas_t<false, 2>(a);
+  return ctas_t<false, 8>(a);
 }
 
 template <bool kFit, int TM>

@@ -10,6 +10,7 @@ constexpr int kSmallMaxRows = 255;  // n_tr <= 255: u8 local indices, u8 bootstr
 constexpr int kSmallMaxP = 64;
 constexpr int kSmallKMax = 8;       // ceil(255 / 32)
 constexpr int kMaxMtry = 16;        // grid points per launch
+constexpr int kSmallMaxWpb = 7;     // warps per CTA (launch bound 224 threads x 2 CTAs/SM)
 
 struct SmallArgs {
   // dataset (device)
@@ -54,6 +55,8 @@ struct SmallArgs {
 
 // shared-memory bytes per block for the launch configuration
 size_t small_tree_smem_bytes(const SmallArgs& a, int mmax);
+// resident CTAs per SM for a.wpb warps per CTA (0 if it does not fit)
+int small_tree_ctas_per_sm(const SmallArgs& a);
 cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s);
 
 }  // namespace rf
