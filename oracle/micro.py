@@ -22,6 +22,7 @@ import math
 M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
 MASK32 = 0xFFFFFFFF
 TAG_FOLD, TAG_STRATUM, TAG_KEYDERIV, TAG_BOOT, TAG_FEAT = 0xD0, 0xD1, 0x4B, 0xB0, 0xF0
+TAG_THR = 0xE7
 
 
 def philox(ctr, key):
@@ -138,7 +139,16 @@ class Node:
                  "gain_exact_best", "gain_exact_chosen", "W", "S")
 
 
-def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None):
+def extra_threshold(key, heap, j, lo, hi):
+    """ExtraTrees threshold of drawn slot j (R29):
+    uniform in [lo, hi) as scikit-learn's rand_uniform(lo, hi) = (hi - lo) u + lo,
+    u = 53 random bits / 2^53 from stream (key; heap, TAG_THR)."""
+    u = math.ldexp(draw(key, heap & MASK32, (heap >> 32) & MASK32, TAG_THR, j) >> 11, -53)
+    thr = (hi - lo) * u + lo  # Python floats: IEEE binary64, round to nearest, no FMA
+    return thr if thr < hi else lo
+
+
+def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None, extra=False):
     """Depth-first recursive growth; returns the root Node."""
     n, p = len(X), len(X[0])
     gvals = [sorted(set(X[i][f] for i in range(n))) for f in range(p)]
@@ -155,8 +165,22 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
         cands = []
         if not leaf:
             parent_sse = sse(rows, w, tq)
-            for f in draw_features(key, heap, p, mtry):
-                if hist_cuts_per_f is None:
+            for j, f in enumerate(draw_features(key, heap, p, mtry)):
+                if extra:
+                    vals = [X[r][f] for r in rows]
+                    lo, hi = min(vals), max(vals)
+                    if lo == hi:
+                        continue
+                    thr = extra_threshold(key, heap, j, lo, hi)
+                    L = [r for r in rows if X[r][f] <= thr]
+                    R = [r for r in rows if X[r][f] > thr]
+                    WL = sum(w[r] for r in L)
+                    SL = sum(w[r] * tq[r] for r in L)
+                    a = max(X[r][f] for r in L)
+                    red = parent_sse - sse(L, w, tq) - sse(R, w, tq)
+                    cands.append((canonical_gain(WL, SL, nd.W - WL, nd.S - SL), f,
+                                  gvals[f].index(a), thr, red, set(L), j))
+                elif hist_cuts_per_f is None:
                     srt = sorted(rows, key=lambda r: (X[r][f], r))
                     for i in range(len(srt) - 1):
                         a, b = X[srt[i]][f], X[srt[i + 1]][f]
@@ -170,10 +194,10 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
                         if thr == b:
                             thr = a
                         cands.append((canonical_gain(WL, SL, nd.W - WL, nd.S - SL), f,
-                                      gvals[f].index(a), thr, red, set(L)))
+                                      gvals[f].index(a), thr, red, set(L), j))
                 else:
                     cuts = hist_cuts_per_f[f]
-                    for j, c in enumerate(cuts):
+                    for ci, c in enumerate(cuts):
                         L = [r for r in rows if X[r][f] <= c]
                         R = [r for r in rows if X[r][f] > c]
                         WL = sum(w[r] for r in L)
@@ -182,7 +206,7 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
                             continue
                         SL = sum(w[r] * tq[r] for r in L)
                         red = parent_sse - sse(L, w, tq) - sse(R, w, tq)
-                        cands.append((canonical_gain(WL, SL, WR, nd.S - SL), f, j, c, red, set(L)))
+                        cands.append((canonical_gain(WL, SL, WR, nd.S - SL), f, ci, c, red, set(L), j))
             if not cands:
                 leaf = True
         if leaf:
@@ -191,7 +215,8 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
             nd.value = float(Fraction(nd.S, nd.W) * Fraction(2) ** (-F)) if F >= 0 else \
                 float(Fraction(nd.S, nd.W) / Fraction(2) ** F)
             return nd
-        best = min(cands, key=lambda c: (-c[0], c[1], c[2]))
+        # tie-break (R9): first drawn feature (slot j), then lowest threshold rank
+        best = min(cands, key=lambda c: (-c[0], c[6], c[2]))
         nd.feature, nd.thr_index, nd.thr_value = best[1], best[2], best[3]
         nd.gain_exact_best = max(c[4] for c in cands)
         nd.gain_exact_chosen = best[4]
@@ -227,8 +252,9 @@ def to_bfs(root):
 
 
 def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=-1, hist=False,
-             task=0, train_rows=None):
-    """Tree t of `task` over train_rows (default all rows)."""
+             task=0, train_rows=None, extra=False):
+    """Tree t of `task` over train_rows (default all rows).  extra=True grows an
+    Extremely Randomized tree (split_mode 2)."""
     X = [[(0.0 if v == 0.0 else float(v)) for v in row] for row in X]
     _, tq, F = quantize(list(y), target)
     n = len(X)
@@ -238,7 +264,7 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     cuts = None
     if hist:
         cuts = [hist_cuts([X[r][f] for r in tr]) for f in range(len(X[0]))]
-    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts)
+    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra)
     return to_bfs(root), F
 
 

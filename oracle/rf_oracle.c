@@ -26,6 +26,8 @@
  *     custom split for time.
  *   - everything the paper leaves open (bootstrap, RNG addressing, exact
  *     sums, tie-break, thresholds, histogram cuts) follows DESIGN.md R1-R28.
+ *   - split_mode 2: Extremely Randomized Trees, one uniform random
+ *     threshold per drawn feature (R29).
  *
  * Parity status of each exported function is listed in DESIGN.md section 3.
  */
@@ -44,7 +46,7 @@
 #define OR_W1 0xBB67AE85u
 
 enum { TAG_FOLD = 0xD0, TAG_STRATUM = 0xD1, TAG_KEYDERIV = 0x4B,
-       TAG_BOOT = 0xB0, TAG_FEAT = 0xF0 };
+       TAG_BOOT = 0xB0, TAG_FEAT = 0xF0, TAG_THR = 0xE7 };
 
 void or_philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
 {
@@ -359,6 +361,8 @@ typedef struct {
     uint64_t *gnd;
     /* hist mode: cuts per feature for this task, bins per row (n x p) */
     int hist;
+    /* ExtraTrees mode (split_mode 2): one random threshold per drawn feature (R29) */
+    int extra;
     double **cuts;
     uint32_t *ncuts;
     uint16_t *bins; /* [row*p + f] */
@@ -425,6 +429,10 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
         int found = 0;
         double bestG = 0.0;
         uint32_t bestF = 0;
+        /* tie-break (R9): among bitwise-equal G the feature drawn first (lowest
+           draw slot), then the lowest threshold rank -- scikit-learn's splitter
+           visits features in the random draw order and keeps the first best. */
+        uint32_t bestSlot = 0;
         uint64_t bestRank = 0; /* exact: rank_f(a) ; hist: cut index j */
         double bestA = 0.0, bestB = 0.0;
         if (!is_leaf) {
@@ -438,7 +446,46 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
             }
             for (uint32_t jj = 0; jj < c->mtry; ++jj) {
                 uint32_t f = perm[jj];
-                if (!c->hist) {
+                if (c->extra) {
+                    /* Extremely Randomized Trees (R29):
+                       thr uniform in [lo, hi) of the node's values of f,
+                       thr = fl(fl(fl(hi - lo) * u) + lo), u = (draw >> 11) 2^-53,
+                       replaced by lo if it does not fall below hi. */
+                    double lo = c->X[nd.rows[0] * p + f], hi = lo;
+                    for (uint64_t i = 1; i < nd.nrows; ++i) {
+                        double x = c->X[nd.rows[i] * p + f];
+                        if (x < lo) lo = x;
+                        if (x > hi) hi = x;
+                    }
+                    if (lo == hi) continue; /* constant feature in this node */
+                    uint64_t ud = or_draw(k0, k1, hlo, hhi, TAG_THR, jj);
+                    double u = (double)(ud >> 11) * 0x1p-53;
+                    double span = hi - lo;
+                    double thr = span * u;
+                    thr = thr + lo;
+                    if (!(thr < hi)) thr = lo;
+                    int64_t WL = 0, SL = 0;
+                    double a = lo; /* largest node value <= thr */
+                    for (uint64_t i = 0; i < nd.nrows; ++i) {
+                        uint64_t r = nd.rows[i];
+                        double x = c->X[r * p + f];
+                        if (x <= thr) {
+                            WL += (int64_t)w[r];
+                            SL += (int64_t)w[r] * c->tq[r];
+                            if (x > a) a = x;
+                        }
+                    }
+                    double G = gain(WL, SL, nd.W - WL, nd.S - SL);
+                    int better = 0;
+                    if (!found) better = 1;
+                    else if (G > bestG) better = 1;
+                    else if (G == bestG && jj < bestSlot) better = 1;
+                    if (better) {
+                        found = 1; bestG = G; bestF = f; bestSlot = jj;
+                        bestRank = find_index(c->gdist[f], c->gnd[f], a);
+                        bestA = thr; bestB = 0.0;
+                    }
+                } else if (!c->hist) {
                     for (uint64_t i = 0; i < nd.nrows; ++i) {
                         xr[i].row = nd.rows[i];
                         xr[i].x = c->X[nd.rows[i] * p + f];
@@ -456,11 +503,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                         if (!found) better = 1;
                         else if (G > bestG) better = 1;
                         else if (G == bestG) {
-                            if (f < bestF) better = 1;
-                            else if (f == bestF && rk < bestRank) better = 1;
+                            if (jj < bestSlot) better = 1;
+                            else if (jj == bestSlot && rk < bestRank) better = 1;
                         }
                         if (better) {
-                            found = 1; bestG = G; bestF = f; bestRank = rk;
+                            found = 1; bestG = G; bestF = f; bestSlot = jj; bestRank = rk;
                             bestA = xr[i].x; bestB = xr[i + 1].x;
                         }
                     }
@@ -484,11 +531,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                         if (!found) better = 1;
                         else if (G > bestG) better = 1;
                         else if (G == bestG) {
-                            if (f < bestF) better = 1;
-                            else if (f == bestF && j < bestRank) better = 1;
+                            if (jj < bestSlot) better = 1;
+                            else if (jj == bestSlot && j < bestRank) better = 1;
                         }
                         if (better) {
-                            found = 1; bestG = G; bestF = f; bestRank = j;
+                            found = 1; bestG = G; bestF = f; bestSlot = jj; bestRank = j;
                             bestA = c->cuts[f][j]; bestB = 0.0;
                         }
                     }
@@ -506,7 +553,9 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
             continue;
         }
         double thr;
-        if (!c->hist) {
+        if (c->extra) {
+            thr = bestA; /* the drawn threshold (R29) */
+        } else if (!c->hist) {
             thr = bestA / 2.0 + bestB / 2.0; /* R8 */
             if (thr == bestB) thr = bestA;
         } else {
@@ -642,7 +691,7 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
            uint32_t *left, double *leaf_value, int32_t *leaf_of_row, int32_t *F_out)
 {
     if (n == 0) return 2;
-    if (p == 0 || mtry == 0 || mtry > p || min_split < 2) return 1;
+    if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || split_mode > 2) return 1;
     double *Xc = (double *)malloc(sizeof(double) * n * p);
     int st = validate_X(X, n, p, Xc);
     if (st) { free(Xc); return st; }
@@ -659,6 +708,7 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
     g.X = Xc; g.n = n; g.p = p; g.tq = tq; g.F = F;
     g.mtry = mtry; g.min_split = min_split; g.max_depth = max_depth;
     g.hist = (split_mode == 1);
+    g.extra = (split_mode == 2);
     if (g.hist) setup_hist(&g, Xc, n, p, tr, n); else setup_exact(&g, Xc, n, p);
     uint32_t *w = (uint32_t *)malloc(sizeof(uint32_t) * n);
     or_tree tree = { NULL, 0, 0 };
@@ -733,7 +783,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
 {
     if (n == 0) return 2;
     if (k < 2 || (uint64_t)k > n) return 6;
-    if (p == 0 || min_split < 2 || n_ntree == 0 || n_mtry == 0) return 1;
+    if (p == 0 || min_split < 2 || n_ntree == 0 || n_mtry == 0 || split_mode > 2) return 1;
     for (uint32_t i = 0; i < n_mtry; ++i) if (mtrys[i] == 0 || mtrys[i] > p) return 1;
     for (uint32_t i = 0; i < n_ntree; ++i) if (ntrees[i] == 0) return 1;
     for (uint64_t i = 0; i < n; ++i) {
@@ -774,6 +824,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     g.X = Xc; g.n = n; g.p = p; g.tq = tq; g.F = F;
     g.min_split = min_split; g.max_depth = max_depth;
     g.hist = (split_mode == 1);
+    g.extra = (split_mode == 2);
     if (!g.hist) setup_exact(&g, Xc, n, p);
     uint64_t *tr = (uint64_t *)malloc(sizeof(uint64_t) * n);
     uint64_t *te = (uint64_t *)malloc(sizeof(uint64_t) * n);
