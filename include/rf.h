@@ -63,7 +63,12 @@ typedef enum {
   RF_E_UNSUPPORTED = 10    /* valid request outside what this build implements    */
 } rf_status;
 
-typedef enum { RF_SPLIT_EXACT = 0, RF_SPLIT_HIST256 = 1 } rf_split_mode;
+/* Split rule.  EXACT: every boundary between consecutive distinct in-node
+   values (R8).  HIST256: 256 quantile bins per (task, feature) (R23).
+   EXTRA: Extremely Randomized Trees, the paper's learner: per
+   drawn feature one threshold uniform in [min, max) of its in-node values
+   (R29).  All three share the criterion, tie-break, stopping and leaves. */
+typedef enum { RF_SPLIT_EXACT = 0, RF_SPLIT_HIST256 = 1, RF_SPLIT_EXTRA = 2 } rf_split_mode;
 typedef enum { RF_TARGET_IDENTITY = 0, RF_TARGET_LOG = 1 } rf_target;
 
 /* Hyper-parameters and sharding. */
@@ -74,7 +79,7 @@ typedef struct {
   uint32_t min_samples_split; /* >= 2: nodes with fewer distinct in-bag rows are leaves   */
   int32_t max_depth;          /* -1 = unbounded (default, R11)                    */
   uint32_t bootstrap;         /* 1: n_tr draws with replacement (R2); 0: all weights 1   */
-  uint32_t split_mode;        /* rf_split_mode: exact presorted (R8) or 256-bin (R23)    */
+  uint32_t split_mode;        /* rf_split_mode: exact (R8), 256-bin (R23), extra (R29)   */
   uint32_t target;            /* rf_target: LOG fits ln y, predicts exp      */
   uint64_t seed;              /* Philox key of every random draw (R14-R16)               */
   int32_t device;             /* CUDA ordinal for host-pointer calls                     */

@@ -24,7 +24,7 @@ OK, E_ARG, E_EMPTY, E_NONFINITE, E_NONPOSITIVE_Y, E_ARITY, E_TOO_FEW, E_CUDA, E_
     E_UNSUPPORTED = range(11)
 STATUS_NAMES = ["OK", "ARG", "EMPTY", "NONFINITE", "NONPOSITIVE_Y", "ARITY", "TOO_FEW", "CUDA", "OOM",
                 "OVERFLOW", "UNSUPPORTED"]
-SPLIT_EXACT, SPLIT_HIST256 = 0, 1
+SPLIT_EXACT, SPLIT_HIST256, SPLIT_EXTRA = 0, 1, 2
 TARGET_IDENTITY, TARGET_LOG = 0, 1
 
 # every entry point declared in include/rf.h and include/rf_debug.h

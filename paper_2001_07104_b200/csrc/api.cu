@@ -83,7 +83,7 @@ rf_status check_params(const rf_params* prm, uint32_t p, uint32_t* mtry_out) {
   if (p > (uint32_t)rf::kSmallMaxP && p > 4096) return fail(RF_E_ARG, "p too large");
   if (prm->min_samples_split < 2) return fail(RF_E_ARG, "min_samples_split must be >= 2");
   if (prm->max_depth < -1) return fail(RF_E_ARG, "max_depth must be >= -1");
-  if (prm->split_mode > 1 || prm->target > 1) return fail(RF_E_ARG, "bad split_mode/target");
+  if (prm->split_mode > RF_SPLIT_EXTRA || prm->target > 1) return fail(RF_E_ARG, "bad split_mode/target");
   uint32_t m = prm->mtry ? prm->mtry : std::max<uint32_t>(1, p / 3);
   if (m > p) return fail(RF_E_ARG, "mtry must be <= p");
   if (mtry_out) *mtry_out = m;
@@ -245,7 +245,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   if (tree_lo) g = gcd_i(g, tree_lo);
   if (tree_hi != Tmax) g = gcd_i(g, tree_hi);
   const int T = tree_hi - tree_lo;
-  const bool large = ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode != RF_SPLIT_EXACT;
+  const bool large = ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode == RF_SPLIT_HIST256;
   int Cw = 1, nsub = T;
   double* partial = nullptr;
   if (large) {
@@ -273,6 +273,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
   a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = ntr_max; a.nte_max = nte_max;
   a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
+  a.extra = prm->split_mode == RF_SPLIT_EXTRA;
   a.max_depth = prm->max_depth; a.n_mtry = nmd;
   for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
@@ -388,7 +389,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   cudaGetDevice(&dev);
 
   const bool small = n <= (uint64_t)rf::kSmallMaxRows && p <= (uint32_t)rf::kSmallMaxP &&
-                     prm->split_mode == RF_SPLIT_EXACT;
+                     prm->split_mode != RF_SPLIT_HIST256;
   rf::Node16* nodes_w = nullptr;
   uint32_t* tidx_w = nullptr;
   uint32_t* nn_d = nullptr;
@@ -418,6 +419,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
     a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = (int)n; a.nte_max = 0;
     a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
+    a.extra = prm->split_mode == RF_SPLIT_EXTRA;
     a.max_depth = prm->max_depth; a.n_mtry = 1; a.mtrys[0] = (int)mtry;
     a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
     a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;

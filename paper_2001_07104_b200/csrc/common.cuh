@@ -22,6 +22,7 @@ constexpr uint32_t kTagStratum = 0xD1u;
 constexpr uint32_t kTagKeyDeriv = 0x4Bu;
 constexpr uint32_t kTagBoot = 0xB0u;
 constexpr uint32_t kTagFeat = 0xF0u;
+constexpr uint32_t kTagThr = 0xE7u;  // ExtraTrees thresholds (R29)
 
 struct U4 { uint32_t x, y, z, w; };
 
@@ -97,6 +98,18 @@ __device__ __forceinline__ double split_gain(int64_t WL, int64_t SL, int64_t WR,
 __device__ __forceinline__ double midpoint_thr(double a, double b) {
   double t = __dadd_rn(__dmul_rn(a, 0.5), __dmul_rn(b, 0.5));
   return (t == b) ? a : t;
+}
+
+// ExtraTrees threshold of draw slot j at heap node h (R29):
+// u = (draw(j) of stream (k_t; h_lo, h_hi, 0xE7) >> 11) 2^-53 (exact),
+// thr = fl(fl(fl(hi - lo) u) + lo), replaced by lo unless thr < hi.
+__device__ __forceinline__ double extra_thr(uint32_t k0, uint32_t k1, uint64_t h, int j, double lo, double hi) {
+  uint64_t d0, d1;
+  philox_pair(k0, k1, (uint32_t)(j >> 1), (uint32_t)h, (uint32_t)(h >> 32), kTagThr, d0, d1);
+  const uint64_t d = (j & 1) ? d1 : d0;
+  const double u = __dmul_rn(__ull2double_rn(d >> 11), 0x1p-53);
+  const double t = __dadd_rn(__dmul_rn(__dsub_rn(hi, lo), u), lo);
+  return t < hi ? t : lo;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

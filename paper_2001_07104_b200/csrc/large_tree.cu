@@ -12,8 +12,10 @@
 //               device-wide exclusive scan, pass 2 exact prefix sums (global
 //               prefix minus segment base, modular uint64) and candidate scores;
 //               per-thread run bests merged into the node best with a 128-bit
-//               compare-and-swap on (G key, feature|position) -- a total order,
+//               compare-and-swap on (G key, draw slot|position) -- a total order,
 //               so the result does not depend on timing
+//   (ExtraTrees, R29: extra_bounds locates each (node, slot) segment's random
+//   threshold first; the search then scores only that boundary)
 //   decide      split flag, threshold, first-row targets for the constancy test
 //   mark        go-left flags per row, child sums (warp-aggregated atomics),
 //               child constancy flags
@@ -96,6 +98,8 @@ struct Batch {
   int F;
   int nl;                   // row lists per tree: p (exact, one per feature) or 1 (histogram)
   int hist;                 // 256-bin histogram split mode (R23)
+  int extra;                // ExtraTrees split mode (R29)
+  uint32_t* xb;             // [NMAX][m] ExtraTrees: boundary index in the (node, slot) segment or ~0
   const uint8_t* bins;      // [n][p] bin of every row (histogram mode)
   const double* cuts;       // [p][256] cut values (histogram mode)
   const int32_t* ncuts;     // [p]
@@ -244,11 +248,8 @@ __global__ void k_node_prep(Batch b, int cur, int NO) {
   b.accS[g] = 0ull;
   b.nc[2 * g] = 0;
   b.nc[2 * g + 1] = 0;
+  // the draw order matters even for m = p: ties go to the first drawn feature (R9)
   uint8_t* fp = b.feat + (size_t)g * b.m;
-  if (b.m == b.p) {
-    for (int j = 0; j < b.m; ++j) fp[j] = (uint8_t)j;
-    return;
-  }
   uint8_t perm[256];
   for (int f = 0; f < b.p; ++f) perm[f] = (uint8_t)f;
   const uint32_t t = nd.tree[g];
@@ -267,6 +268,31 @@ __global__ void k_node_prep(Batch b, int cur, int NO) {
   for (int j = 0; j < b.m; ++j) fp[j] = perm[j];
 }
 
+// ExtraTrees (R29): thread per (node, slot): the slot's random threshold in [lo, hi) of the
+// segment (sorted by x_f) and its boundary = last segment index with x <= thr (~0 if lo = hi)
+__global__ void k_extra_bounds(Batch b, int cur, long long NQ) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= NQ) return;
+  const int g = (int)(q / b.m), j = (int)(q - (long long)g * b.m);
+  const Nodes& nd = b.nd[cur];
+  const int t = (int)nd.tree[g], f = b.feat[q];
+  const uint32_t len = nd.len[g];
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
+  const double* Xf = b.X + f;
+  const double lo = Xf[(size_t)L[0] * b.p], hi = Xf[(size_t)L[len - 1] * b.p];
+  uint32_t bnd = ~0u;
+  if (lo < hi) {
+    const double thr = extra_thr(b.keys[2 * t], b.keys[2 * t + 1], nd.heap[g], j, lo, hi);
+    uint32_t l = 0, u = len - 1;  // x[l] <= thr < x[u]
+    while (u - l > 1) {
+      const uint32_t mid = (l + u) >> 1;
+      if (Xf[(size_t)L[mid] * b.p] <= thr) l = mid; else u = mid;
+    }
+    bnd = l;
+  }
+  b.xb[q] = bnd;
+}
+
 __global__ void k_node_ws(Batch b, int cur, int NO, WS2* out) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= NO) return;
@@ -277,6 +303,7 @@ __global__ void k_node_ws(Batch b, int cur, int NO, WS2* out) {
 // over trees (node g's positions [gpos0, gpos0 + len))
 struct Cursor {
   int g, j, i, len, t, start, f;
+  uint32_t xb;  // ExtraTrees boundary of the segment
   uint32_t W;
   int64_t S;
   long long listBase;  // offset of list (t, f) + start
@@ -292,6 +319,7 @@ __device__ __forceinline__ void cursor_load(const Batch& b, const Nodes& nd, Cur
 __device__ __forceinline__ void cursor_feat(const Batch& b, Cursor& c) {
   c.f = b.feat[(size_t)c.g * b.m + c.j];
   c.listBase = ((long long)c.t * b.p + c.f) * b.ntr + c.start;
+  if (b.extra) c.xb = b.xb[(size_t)c.g * b.m + c.j];
 }
 // element e = m * gpos0(g) + j * len + i, gpos0 = concatenated first position of g
 __device__ __forceinline__ void cursor_locate(const Batch& b, const Nodes& nd, const uint32_t* posNode,
@@ -386,15 +414,21 @@ __global__ void __launch_bounds__(kThreads) k_search_eval(Batch b, int cur, long
     uint32_t rn = r, rkn = rk;
     if (hasNext) {
       rn = L[c.listBase + c.i + 1];
-      rkn = grank[(size_t)c.f * b.n + rn];
-      if (rkn != rk) {
+      bool cand;
+      if (b.extra) {
+        cand = (uint32_t)c.i == c.xb;  // the segment's one candidate (R29)
+      } else {
+        rkn = grank[(size_t)c.f * b.n + rn];
+        cand = rkn != rk;
+      }
+      if (cand) {
         const unsigned long long WL = cW - segW;
         const long long SL = (long long)(cS - segS);
         const unsigned long long WR = (unsigned long long)c.W - WL;
         const long long SR = c.S - SL;
         const double G = split_gain((long long)WL, SL, (long long)WR, SR);
         const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
-        const unsigned long long aux = ((unsigned long long)c.f << 32) | (unsigned long long)c.i;
+        const unsigned long long aux = ((unsigned long long)c.j << 32) | (unsigned long long)c.i;  // R9
         ++nc;
         if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
       }
@@ -433,11 +467,18 @@ __global__ void k_decide(Batch b, int cur, int NO) {
   const Nodes& nd = b.nd[cur];
   const Best bs = b.best[g];
   if (!bs.key) return;
-  const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), i = (int)(bs.aux & 0xFFFFFFFFull);
+  const int j = (int)(bs.aux >> 32), i = (int)(bs.aux & 0xFFFFFFFFull);
+  const int t = (int)nd.tree[g], f = b.feat[(size_t)g * b.m + j];
   const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
   const uint32_t ra = L[i], rb = L[i + 1];
-  b.thr[g] = midpoint_thr(b.X[(size_t)ra * b.p + f], b.X[(size_t)rb * b.p + f]);
+  if (b.extra) {  // the drawn threshold of slot j (R29)
+    const double lo = b.X[(size_t)L[0] * b.p + f], hi = b.X[(size_t)L[nd.len[g] - 1] * b.p + f];
+    b.thr[g] = extra_thr(b.keys[2 * t], b.keys[2 * t + 1], nd.heap[g], j, lo, hi);
+  } else {
+    b.thr[g] = midpoint_thr(b.X[(size_t)ra * b.p + f], b.X[(size_t)rb * b.p + f]);
+  }
   b.thrIdx[g] = b.grank[(size_t)f * b.n + ra];
+  b.best[g].aux = ((unsigned long long)f << 32) | (unsigned long long)i;  // slot -> feature for the later kernels
 }
 
 // positions (concatenated): go-left flags, child left sums, child constancy
@@ -492,7 +533,7 @@ __global__ void k_mark(Batch b, int cur, int NP) {
 // (task, feature) from the training rows; bin(x) = #{cuts < x}; per node and
 // drawn feature the (W, S) sums per bin are exact integers (order-free atomics);
 // the candidate after cut c is valid iff WL > 0 and WR > 0; threshold = cut
-// value, threshold index = c; ties -> lowest feature, then lowest c.
+// value, threshold index = c; ties -> first drawn feature (R9), then lowest c.
 constexpr int kHistThreads = 256;
 constexpr int kHistChunk = 8192;  // rows per histogram work item
 
@@ -670,7 +711,7 @@ __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int
         const long long SL = (long long)cs;
         const double G = split_gain((long long)cw, SL, (long long)(Wt - cw), St - SL);
         const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
-        const unsigned long long aux = ((unsigned long long)f << 32) | (unsigned long long)cidx;
+        const unsigned long long aux = ((unsigned long long)j << 32) | (unsigned long long)cidx;  // R9
         ++nc;
         if (better(key, aux, bk, ba)) { bk = key; ba = aux; }
       }
@@ -702,9 +743,11 @@ __global__ void k_decide_hist(Batch b, int NO) {
   if (g >= NO) return;
   const Best bs = b.best[g];
   if (!bs.key) return;
-  const int f = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
+  const int j = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
+  const int f = b.feat[(size_t)g * b.m + j];
   b.thr[g] = b.cuts[(size_t)f * 256 + c];
   b.thrIdx[g] = (uint32_t)c;
+  b.best[g].aux = ((unsigned long long)f << 32) | (unsigned long long)c;  // slot -> feature
 }
 
 // positions: go-left flags (bin <= cut), left count and sums, child t_q min / max
@@ -1139,6 +1182,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   while (NO > 0) {
     k_node_prep<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
     note_launch();
+    if (b.extra) {
+      k_extra_bounds<<<nblk(NO * b.m, 128), 128, 0, s>>>(b, cur, NO * b.m);
+      note_launch();
+    }
     size_t tb = cub_bytes;
     if (!b.hist) {
       k_node_ws<<<nblk(NO, 256), 256, 0, s>>>(b, cur, (int)NO, wsTmp);
@@ -1335,6 +1382,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     return RF_E_UNSUPPORTED;
   }
   const bool hist = prm->split_mode == RF_SPLIT_HIST256;
+  const bool extra = prm->split_mode == RF_SPLIT_EXTRA;
   const int n = d.n, p = d.p, T = tree_hi - tree_lo;
   const int nlists = hist ? 1 : p;
   uint64_t cap = 2ull * (uint64_t)ntr - 1ull;
@@ -1343,7 +1391,8 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   long long open_max = ntr / 2 + 1;
   if (prm->max_depth >= 1 && prm->max_depth < 31) open_max = std::min<long long>(open_max, 1ll << (prm->max_depth - 1));
   // batch size: the row lists dominate (2 lists-per-tree x ntr x 4 B per tree)
-  const size_t per_tree = (size_t)2 * nlists * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 + (size_t)open_max * 128;
+  const size_t per_tree = (size_t)2 * nlists * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 +
+                          (size_t)open_max * (128 + (extra ? 4 * (size_t)mtry : 0));
   // trees per batch: per-level launch and sync costs are shared by the batch, so batches are
   // as large as a 16 GB working-set budget allows (of the 180 GB HBM), up to 128 trees
   int B = (int)std::max<size_t>(1, std::min<size_t>(128, ((size_t)16 << 30) / std::max<size_t>(per_tree, 1)));
@@ -1361,6 +1410,8 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.X = d.X; b.tq = d.tq; b.grank = d.grank; b.err = d.err;
   b.nl = nlists;
   b.hist = hist ? 1 : 0;
+  b.extra = extra ? 1 : 0;
+  if (extra) LCK(sc.alloc(&b.xb, (size_t)pl.nmax * mtry));
   HistBufs hb;
   const uint32_t* list_src = task_order;
   if (hist) {

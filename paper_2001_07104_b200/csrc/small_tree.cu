@@ -10,9 +10,12 @@
 //   drawn feature scan the node's rows in x order, exact int64 prefix sums
 //   WL = sum w, SL = sum w t_q (R7), score G = SL^2/WL + SR^2/WR in canonical
 //   fp64 (R6, R28) at every boundary between distinct values (R8); best by
-//   (G desc, feature asc, threshold rank asc) (R9); threshold midway (R8);
+//   (G desc, draw slot asc, threshold rank asc) (R9); threshold midway (R8);
 //   leaf if depth cap, < min_split distinct rows, constant t_q or no
 //   candidate (R11); leaf value fl(S/W) 2^-F (R13).
+//   ExtraTrees (split_mode 2, R29): the only candidate of a
+//   (node, slot) segment is the boundary of its random threshold, located by
+//   a binary search before the search pass; everything else is shared.
 //
 // Per level the warp runs three lane-serial passes (each lane owns a
 // contiguous chunk; lane totals are combined by one warp scan):
@@ -88,7 +91,8 @@ struct WarpSmem {
   SA<uint8_t> pnB;
   SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
-  SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates)
+  SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates), in draw order
+  SA<uint8_t> xb;      // ExtraTrees: [NM][p] boundary position in the segment per draw slot, or kNone
   SA<unsigned long long> bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
   SA<uint32_t> baux;   // best (feature << 8 | position); bit 31 = split
   SA<uint32_t> bW;     // search: prefix base of W; then the best's left W
@@ -122,7 +126,7 @@ __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
   s.bfs = c.take<uint16_t>(NM, 4);
 }
 
-__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool need_feat,
+__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool extra,
                                            bool fit) {
   const int NM = nmax_of(ntr_max);
   s.w = c.take<uint8_t>((ntr_max + 3) / 4 * 4, 16);
@@ -133,7 +137,8 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.side = c.take<uint8_t>(ntr_max, 4);
   carve_nodeset(c, s.cur, NM);
   carve_nodeset(c, s.nxt, NM);
-  s.feat = need_feat ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
+  s.feat = c.take<uint8_t>((size_t)NM * p, 4);
+  s.xb = extra ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
   s.bkey = c.take<unsigned long long>(NM, 8);
   s.baux = c.take<uint32_t>(NM, 4);
   s.bW = c.take<uint32_t>(NM, 4);
@@ -219,14 +224,14 @@ __device__ __forceinline__ double div_small(double a, double dw, double y) {
   return __fma_rn(r, y, q);
 }
 
-// total order of candidates: key (G bits + 1) descending, aux (feature, position) ascending
+// total order of candidates: key (G bits + 1) descending, aux (draw slot, position) ascending (R9)
 __device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsigned long long k2, uint32_t a2) {
   return k1 > k2 || (k1 == k2 && a1 < a2);
 }
 
 // -------------------------------------------------------------- the kernel --
-// TM: max test rows per lane.
-template <bool kFit, int TM>
+// TM: max test rows per lane.  kExtra: ExtraTrees split mode (R29).
+template <bool kFit, int TM, bool kExtra>
 __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -241,9 +246,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
   const int tl = bid % a.ntask;
   const int mi = bid / a.ntask;
   const int m = a.mtrys[mi];
-  const bool need_feat = m < p;
-  bool any_feat = false;
-  for (int i = 0; i < a.n_mtry; ++i) any_feat |= (a.mtrys[i] < p);
+  constexpr bool extra = kExtra;
 
   Carve cv;
   CtaSmem cs;
@@ -253,10 +256,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     const size_t cta_bytes = (cv.off + 15) / 16 * 16;
     Carve cw;
     WarpSmem dummy;
-    carve_warp(cw, dummy, p, ntr_max, any_feat, kFit);
+    carve_warp(cw, dummy, p, ntr_max, extra, kFit);
     const size_t per_warp = (cw.off + 15) / 16 * 16;
     Carve mine(cta_bytes + per_warp * warp);
-    carve_warp(mine, ws, p, ntr_max, any_feat, kFit);
+    carve_warp(mine, ws, p, ntr_max, extra, kFit);
   }
 
   const int ntr = a.ntr[tl];
@@ -430,22 +433,21 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
             ws.bS[k] = carryS + eS;
             ws.bkey[k] = 0ull;
             ws.baux[k] = 0x7FFFFFFFu;
-            if (need_feat) {
-              const SA<uint8_t> fp = ws.feat + k * p;
-              #pragma unroll 1
-              for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
-              const uint64_t h = cur.heap[k];
-              const uint32_t hlo = (uint32_t)h, hhi = (uint32_t)(h >> 32);
-              #pragma unroll 1
-              for (int j = 0; j < m; j += 2) {
-                uint64_t d0, d1;
-                philox_pair_ool(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
-                int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
-                uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
-                if (j + 1 < m) {
-                  r = j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1));
-                  tmp = fp[j + 1]; fp[j + 1] = fp[r]; fp[r] = tmp;
-                }
+            // draw order matters even for m = p: ties go to the first drawn feature (R9)
+            const SA<uint8_t> fp = ws.feat + k * p;
+            #pragma unroll 1
+            for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
+            const uint64_t h = cur.heap[k];
+            const uint32_t hlo = (uint32_t)h, hhi = (uint32_t)(h >> 32);
+            #pragma unroll 1
+            for (int j = 0; j < m; j += 2) {
+              uint64_t d0, d1;
+              philox_pair_ool(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
+              int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
+              uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
+              if (j + 1 < m) {
+                r = j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1));
+                tmp = fp[j + 1]; fp[j + 1] = fp[r]; fp[r] = tmp;
               }
             }
           }
@@ -454,6 +456,31 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
       }
       __syncwarp();
+      if (extra) {
+        // ExtraTrees (R29): per (node, draw slot) the random threshold in [lo, hi) of the
+        // segment and its boundary = last segment position with x <= thr (kNone if lo = hi)
+        #pragma unroll 1
+        for (int q = lane; q < nOpen * m; q += 32) {
+          const int k = q / m, j = q - k * m;
+          const int f = ws.feat[k * p + j];
+          const int st = cur.start[k], ln = cur.len[k];
+          const SA<uint8_t> seg = L + (f * ntr_max + st);
+          const double* Xf = a.X + f;
+          const double lo = Xf[(size_t)tr_rows[seg[0]] * p], hi = Xf[(size_t)tr_rows[seg[ln - 1]] * p];
+          uint8_t bnd = kNone;
+          if (lo < hi) {
+            const double thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
+            int l = 0, u = ln - 1;  // x[l] <= thr < x[u]
+            while (u - l > 1) {
+              const int mid = (l + u) >> 1;
+              if (Xf[(size_t)tr_rows[seg[mid]] * p] <= thr) l = mid; else u = mid;
+            }
+            bnd = (uint8_t)l;
+          }
+          ws.xb[k * p + j] = bnd;
+        }
+        __syncwarp();
+      }
 
       // ---------------- (b) search pass over (node, feature slot, position), node-major
       {
@@ -475,7 +502,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const int off = e - m * st;
           j = off / ln;
           i = off - j * ln;
-          f = need_feat ? ws.feat[k * p + j] : j;
+          f = ws.feat[k * p + j];
           lbase = f * ntr_max;
         }
         const int k_init = k, j_init = j, i_init = i, st_init = st, ln_init = ln, f_init = f;
@@ -499,7 +526,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               st = cur.start[k];
               ln = cur.len[k];
             }
-            f = need_feat ? ws.feat[k * p + j] : j;
+            f = ws.feat[k * p + j];
             lbase = f * ntr_max;
           }
         }
@@ -520,6 +547,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
         uint8_t r = L[lbase + st + i];
         uint32_t rkr = cs.lrank[lbase + r];
+        int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
         #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
@@ -537,10 +565,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const double2 yl = cs.rcp2[WL & 0xFFu], yr = cs.rcp2[WR & 0xFFu];
           const double gl = div_small(__dmul_rn(dSL, dSL), yl.x, yl.y);
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
-          const bool cand = act && hasNext && rkr != rkn;
+          const bool cand = act && hasNext && (extra ? i == xbj : rkr != rkn);
           const unsigned long long key =
               cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
-          const uint32_t aux = ((uint32_t)f << 8) | (uint32_t)(st + i);
+          const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
@@ -559,7 +587,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               Wk = cur.W[k];
               Sk = cur.S[k];
             }
-            f = need_feat ? ws.feat[k * p + j] : j;
+            f = ws.feat[k * p + j];
+            if (extra) xbj = ws.xb[k * p + j];
             lbase = f * ntr_max;
             segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
             segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
@@ -618,12 +647,21 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         ws.ncb[2 * k + 1] = 0;
         if (key) {
           const uint32_t aux = ws.baux[k];
-          const int f = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
+          const int j = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
+          const int f = ws.feat[k * p + j];
           const uint8_t ra = L[f * ntr_max + bp], rb = L[f * ntr_max + bp + 1];
           const uint32_t ga = tr_rows[ra], gb = tr_rows[rb];
-          const double thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
+          double thr;
+          if (extra) {  // the drawn threshold of slot j (R29), recomputed from the segment's range
+            const int st = cur.start[k];
+            const double lo = a.X[(size_t)tr_rows[L[f * ntr_max + st]] * p + f];
+            const double hi = a.X[(size_t)tr_rows[L[f * ntr_max + st + cur.len[k] - 1]] * p + f];
+            thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
+          } else {
+            thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
+          }
           ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
-          ws.baux[k] = aux | 0x80000000u;  // split flag
+          ws.baux[k] = ((uint32_t)f << 8) | (uint32_t)bp | 0x80000000u;  // feature, boundary, split flag
           if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
           const SA<int64_t> tqf{ws.chVal.off};  // child first-row targets (chVal is free here)
           tqf[2 * k] = cs.tq[L[f * ntr_max + cur.start[k]]];
@@ -893,46 +931,40 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 }  // namespace
 
 size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
-  bool any_feat = false;
-  for (int i = 0; i < a.n_mtry; ++i) any_feat |= (a.mtrys[i] < a.p);
   Carve c;
   CtaSmem cs;
   carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max);
   const size_t cta = (c.off + 15) / 16 * 16;
   Carve w;
   WarpSmem ws;
-  carve_warp(w, ws, a.p, a.ntr_max, any_feat, a.fit_mode != 0);
+  carve_warp(w, ws, a.p, a.ntr_max, a.extra != 0, a.fit_mode != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
 }
 
-template <bool kFit, int TM>
-static int ctas_t(const SmallArgs& a) {
-  const size_t smem = small_tree_smem_bytes(a, 0);
-  if (smem > 227 * 1024) return 0;
-  auto kern = small_tree_kernel<kFit, TM>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * a.wpb, smem) != cudaSuccess) return 0;
-  return nb;
+// calls fn(kernel) with the variant for (fit mode, test rows per lane, split mode)
+template <bool kFit, int TM, typename Fn>
+static auto with_split(const SmallArgs& a, Fn&& fn) {
+  return a.extra ? fn(small_tree_kernel<kFit, TM, true>) : fn(small_tree_kernel<kFit, TM, false>);
+}
+template <typename Fn>
+static auto with_variant(const SmallArgs& a, Fn&& fn) {
+  if (a.fit_mode) return with_split<true, 1>(a, fn);
+  const int TMn = (a.nte_max + 31) / 32;
+  if (TMn <= 1) return with_split<false, 1>(a, fn);
+  if (TMn <= 2) return with_split<false, 2>(a, fn);
+  return with_split<false, 8>(a, fn);
 }
 
 int small_tree_ctas_per_sm(const SmallArgs& a) {
-  if (a.fit_mode) return ctas_t<true, 1>(a);
-  const int TMn = (a.nte_max + 31) / 32;
-  if (TMn <= 1) return ctas_t<false, 1>(a);
-  if (TMn <= 2) return ctas_t<false, 2>(a);
-  return ctas_t<false, 8>(a);
-}
-
-template <bool kFit, int TM>
-static cudaError_t launch_t(const SmallArgs& a, size_t smem, unsigned grid, cudaStream_t s) {
-  auto kern = small_tree_kernel<kFit, TM>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, 32 * a.wpb, smem, s>>>(a);
-  note_launch();
-  return cudaGetLastError();
+  const size_t smem = small_tree_smem_bytes(a, 0);
+  if (smem > 227 * 1024) return 0;
+  return with_variant(a, [&](void (*kern)(SmallArgs)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * a.wpb, smem) != cudaSuccess) return 0;
+    return nb;
+  });
 }
 
 cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s) {
@@ -940,11 +972,13 @@ cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s) {
   const int cta_per_mt = (a.nsub + a.wpb - 1) / a.wpb;
   const long long grid = (long long)a.n_mtry * a.ntask * cta_per_mt;
   if (grid <= 0) return cudaSuccess;
-  if (a.fit_mode) return launch_t<true, 1>(a, smem, (unsigned)grid, s);
-  const int TMn = (a.nte_max + 31) / 32;
-  if (TMn <= 1) return launch_t<false, 1>(a, smem, (unsigned)grid, s);
-  if (TMn <= 2) return launch_t<false, 2>(a, smem, (unsigned)grid, s);
-  return launch_t<false, 8>(a, smem, (unsigned)grid, s);
+  return with_variant(a, [&](void (*kern)(SmallArgs)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, 32 * a.wpb, smem, s>>>(a);
+    note_launch();
+    return cudaGetLastError();
+  });
 }
 
 }  // namespace rf

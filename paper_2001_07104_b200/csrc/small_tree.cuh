@@ -34,6 +34,7 @@ struct SmallArgs {
   // forest parameters
   uint64_t seed;
   int bootstrap, min_split, max_depth;
+  int extra;                // ExtraTrees split mode (R29): one random threshold per drawn feature
   int n_mtry;
   int mtrys[kMaxMtry];
   int tree_lo, tree_hi;     // trees [tree_lo, tree_hi)

@@ -337,6 +337,54 @@ def test_hist_cv_parity():
     np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
 
 
+# ------------------------------------- ExtraTrees split mode (R29, NEXT-1) ---
+EXTRA_CASES = [
+    ("paper_time_m12_noboot", lambda: datagen.paper_shaped(189, "K20", "time"), dict(mtry=12, target=1, bootstrap=False)),
+    ("paper_time_m3", lambda: datagen.paper_shaped(189, "V100", "time"), dict(mtry=3, target=1)),
+    ("paper_power", lambda: datagen.paper_shaped(168, "P100", "power"), dict(mtry=4, bootstrap=False)),
+    ("ties", lambda: datagen.tiny(200, 5, 3, distinct=6), dict(mtry=2)),
+    ("depth3", lambda: datagen.paper_shaped(189, "TitanXp", "time"), dict(mtry=5, max_depth=3, target=1)),
+    ("mss5", lambda: datagen.tiny(150, 6, 8, distinct=20), dict(mtry=3, min_samples_split=5, bootstrap=False)),
+    ("n255", lambda: datagen.tiny(255, 3, 9), dict(mtry=1)),
+    ("n2", lambda: (np.array([[0.0], [1.0]]), np.array([1.0, 3.0])), dict(mtry=1)),
+    ("negzero", lambda: (np.array([[-0.0, 1], [0.0, 2], [1, 3], [2, 1]]), np.array([1.0, 2, 3, 4])), dict(mtry=2)),
+    # large path (n_tr > 255)
+    ("large_n256", lambda: datagen.tiny(256, 4, 21), dict(mtry=2)),
+    ("large_paper1000", lambda: datagen.paper_shaped(1000, "V100", "time"), dict(mtry=12, target=1, bootstrap=False)),
+    ("large_ties", lambda: datagen.tiny(900, 3, 23, distinct=50), dict(mtry=3, min_samples_split=7)),
+    ("large_scaled5000_depth", lambda: datagen.scaled(5000, 64), dict(mtry=21, max_depth=8, target=1)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", EXTRA_CASES, ids=[c[0] for c in EXTRA_CASES])
+def test_extra_fit_structures_bit_exact(name, data, kw):
+    X, y = data()
+    of = oracle.fit(X, y, ntree=12, seed=13, leaf_rows=True, split_mode=2, **kw)
+    gf = rfg.fit(X, y, ntree=12, seed=13, debug=True, split_mode=rfg.SPLIT_EXTRA, **kw)
+    _compare_forest(gf, of, X)
+
+
+def test_extra_large_scaled_50k_sampled():
+    X, y = datagen.scaled(50_000, 64)
+    of = oracle.fit(X, y, ntree=2, seed=5, mtry=64, bootstrap=False, target=1, split_mode=2)
+    gf = rfg.fit(X, y, ntree=2, seed=5, mtry=64, bootstrap=False, target=1, split_mode=rfg.SPLIT_EXTRA)
+    _compare_forest(gf, of, X)
+    Q = datagen.queries(2000, 64)
+    np.testing.assert_allclose(rfg.predict(gf, Q), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("n,boot", [(189, False), (189, True), (600, False)])
+def test_extra_cv_parity(n, boot):
+    X, y = datagen.paper_shaped(n, "GTX1650", "time")
+    f = oracle.make_folds(y, 10, 2, seed=8, custom=True)
+    fm_o, pr_o = oracle.cv_grid(X, y, 10, 2, [8, 16], [12, 3], fold_ids=f, target=1, seed=8, bootstrap=boot,
+                                split_mode=2, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 10, 2, [8, 16], [12, 3], fold_ids=f, target=1, seed=8,
+                                         bootstrap=boot, split_mode=rfg.SPLIT_EXTRA, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+
+
 # -------------------------------------------------------------- errors ---
 def test_errors():
     X, y = datagen.tiny(20, 3, 1)
