@@ -51,7 +51,16 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--split", default="exact", choices=["exact", "extra"],
+                    help="exact: bootstrap + exhaustive CART (north_star, default); extra: the paper's "
+                         "ExtraTrees learner without bootstrap (P:468-469, R29)")
     return ap.parse_args()
+
+
+def split_kw(args):
+    if args.split == "extra":
+        return {"split_mode": 2, "bootstrap": False}
+    return {}
 
 
 def dist_env():
@@ -138,7 +147,7 @@ def run_reference(args):
     def step():
         t0 = time.perf_counter()
         oracle.cv_grid(ds["X"], ds["y"], K_FOLDS, 1, NTREES, [12, 3], fold_ids=folds, target=1, seed=SEED,
-                       task_begin=0, task_end=sample_tasks)
+                       task_begin=0, task_end=sample_tasks, **split_kw(args))
         return time.perf_counter() - t0
 
     for _ in range(args.warmup):
@@ -160,7 +169,7 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def cpu_baseline_sample():
+def cpu_baseline_sample(skw):
     import oracle
     oracle.build()
     ds = study_inputs()[0]
@@ -168,7 +177,7 @@ def cpu_baseline_sample():
     tasks = 2
     t0 = time.perf_counter()
     oracle.cv_grid(ds["X"], ds["y"], K_FOLDS, 1, NTREES, [12, 3], fold_ids=folds, target=1, seed=SEED,
-                   task_begin=0, task_end=tasks)
+                   task_begin=0, task_end=tasks, **skw)
     dt = time.perf_counter() - t0
     trees = tasks * DISTINCT_MTRY * max(NTREES)
     return {"value": trees / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -199,6 +208,7 @@ def run_ours(args):
     folds = [torch.empty((reps_total, d["X"].shape[0]), dtype=torch.int32, device=dev) for d in ds]
     out = [torch.empty((len(MTRYS), len(NTREES), reps_total, K_FOLDS), dtype=torch.float64, device=dev) for _ in ds]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
+    skw = split_kw(args)
 
     def step():
         for i, d in enumerate(ds):
@@ -206,7 +216,7 @@ def run_ours(args):
             rfg.make_folds(dy[i], K_FOLDS, reps_total, seed=SEED + i, custom=custom, out=folds[i])
             rfg.cross_validate_grid(dX[i], dy[i], K_FOLDS, reps_total, NTREES, MTRYS, fold_ids=folds[i],
                                     target=1 if custom else 0, seed=SEED + i, task_begin=task_lo,
-                                    task_end=task_hi, out=out[i])
+                                    task_end=task_hi, out=out[i], **skw)
         if world > 1:  # a11: fold-MAPE tables of all ranks, in task order (NCCL all_gather)
             for i in range(len(ds)):
                 mine = out[i].reshape(len(MTRYS), len(NTREES), -1)[:, :, task_lo:task_hi]
@@ -263,7 +273,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and rank == 0 and world == 1:
-        e2e = measure_e2e(rfg, ds, args)
+        e2e = measure_e2e(rfg, ds, args, skw)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -274,6 +284,8 @@ def run_ours(args):
                        "trees_per_step": trees_per_step_rank * world,
                        "nominal_grid_trees_per_step": len(ds) * REPS * K_FOLDS * len(MTRYS) * sum(NTREES) * world,
                        "l2": "flushed between timed steps (256 MB write)",
+                       "split": ("ExtraTrees, no bootstrap (P:468-469)" if args.split == "extra"
+                                 else "bootstrap + exact CART (north_star)"),
                        "parallelism": f"task-sharded x{world}"},
             "roofline": roofline,
             "gpu_launches": launches,
@@ -284,13 +296,13 @@ def run_ours(args):
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline_sample()
+            line["cpu_baseline"] = cpu_baseline_sample(skw)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def measure_e2e(rfg, ds, args):
+def measure_e2e(rfg, ds, args, skw):
     """Same study through the host-pointer C ABI (rf_make_folds + rf_cross_validate_grid):
     H2D of X, y and D2H of fold MAPE inside the timed region."""
     h2d = sum(d["X"].nbytes + d["y"].nbytes for d in ds)
@@ -303,7 +315,7 @@ def measure_e2e(rfg, ds, args):
             custom = d["target"] == "time"
             f = rfg.make_folds(d["y"], K_FOLDS, REPS, seed=SEED + i, custom=custom)
             fm = rfg.cross_validate_grid(d["X"], d["y"], K_FOLDS, REPS, NTREES, MTRYS, fold_ids=f,
-                                         target=1 if custom else 0, seed=SEED + i)
+                                         target=1 if custom else 0, seed=SEED + i, **skw)
             d2h += fm.nbytes + f.nbytes
     step()
     t0 = time.perf_counter()

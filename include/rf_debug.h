@@ -19,6 +19,12 @@ RF_API rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, u
    (host count) and candidate splits evaluated by the split-search kernels on
    the current device (device counter; this call synchronises the device). */
 RF_API rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates);
+/* Per-phase SM cycles of the warp-per-tree kernel, summed over warps (lane 0
+   of each warp adds clock64 deltas; out[16], phase names in DESIGN.md sec. 6).
+   Only a library built with RF_PHASE_TIMING=1 (a profiling build) records
+   them; the normal build returns RF_E_UNSUPPORTED.  reset != 0 zeroes the
+   counters after reading.  Synchronises the current device. */
+RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librfgpu.so")
+# RFGPU_LIB selects another in-tree build of the same library (the profiling build
+# librfgpu_pt.so, see build.py); the default is the product build.
+LIB_PATH = os.environ.get("RFGPU_LIB") or os.path.join(_HERE, "librfgpu.so")
 
 OK, E_ARG, E_EMPTY, E_NONFINITE, E_NONPOSITIVE_Y, E_ARITY, E_TOO_FEW, E_CUDA, E_OOM, E_OVERFLOW, \
     E_UNSUPPORTED = range(11)
@@ -34,7 +36,7 @@ ABI_SYMBOLS = [
     "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
     "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_last_profile", "rf_set_profiling",
-    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters",
+    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles",
 ]
 
 
@@ -93,6 +95,7 @@ def lib():
             "rf_debug_ln_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_philox_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_counters": ([P, P], C.c_int),
+            "rf_debug_phase_cycles": ([P, C.c_int], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -354,6 +357,21 @@ def counters():
 
 def launch_count():
     return counters()[0]
+
+
+PHASE_NAMES = ["tree setup (bootstrap, root, in-bag lists)", "(a) node prefixes", "(a) feature draws",
+               "(a) ExtraTrees bounds", "(b) search pass 1 + scan", "(b) search pass 2 + node bests",
+               "(c) decide", "(d) mark", "(e) children / emission", "(f) test-row routing",
+               "(g) partition list 0", "(g) partition lists 1..p-1", "level advance", "tree end",
+               "CTA prologue", "unused"]
+
+
+def phase_cycles(reset=True):
+    """Per-phase SM cycles of the tree kernel summed over warps (profiling build only:
+    RF_PHASE_TIMING=1 python -m paper_2001_07104_b200.build, then RFGPU_LIB=.../librfgpu_pt.so)."""
+    out = np.zeros(16, np.uint64)
+    _check(lib().rf_debug_phase_cycles(_ptr(out), 1 if reset else 0))
+    return dict(zip(PHASE_NAMES, out.tolist()))
 
 
 def candidate_count():

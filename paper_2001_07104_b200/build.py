@@ -18,12 +18,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(os.path.dirname(HERE), "include")
-BUILD = os.path.join(os.path.dirname(HERE), "build")
-LIB = os.path.join(HERE, "librfgpu.so")
+# RF_PHASE_TIMING=1: profiling build (per-phase clock64 counters in the tree kernel,
+# rf_debug_phase_cycles) into build_pt/ and librfgpu_pt.so; load it with RFGPU_LIB.
+PHASE_TIMING = os.environ.get("RF_PHASE_TIMING", "0") == "1"
+BUILD = os.path.join(os.path.dirname(HERE), "build_pt" if PHASE_TIMING else "build")
+LIB = os.path.join(HERE, "librfgpu_pt.so" if PHASE_TIMING else "librfgpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-I" + INC, "--expt-relaxed-constexpr"]
+         "-I" + INC, "--expt-relaxed-constexpr"] + (["-DRF_PHASE_TIMING"] if PHASE_TIMING else [])
 
 
 def _deps_mtime():

@@ -245,9 +245,33 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   if (tree_lo) g = gcd_i(g, tree_lo);
   if (tree_hi != Tmax) g = gcd_i(g, tree_hi);
   const int T = tree_hi - tree_lo;
-  const bool large = ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode == RF_SPLIT_HIST256;
+  bool large = ntr_max > rf::kSmallMaxRows || (int)p > rf::kSmallMaxP || prm->split_mode == RF_SPLIT_HIST256;
   int Cw = 1, nsub = T;
   double* partial = nullptr;
+  rf::SmallArgs a;
+  memset(&a, 0, sizeof a);
+  a.X = d.X; a.n = (int)n; a.p = (int)p; a.tq = d.tq; a.dF = d.F; a.grank = d.grank;
+  a.ntask = ntask; a.task0 = task_lo; a.row_stride = (int)n; a.ntr_stride = ntr_max;
+  a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
+  a.ntr_max = ntr_max; a.nte_max = nte_max;
+  a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
+  a.extra = prm->split_mode == RF_SPLIT_EXTRA;
+  a.max_depth = prm->max_depth; a.n_mtry = nmd;
+  for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
+  a.tree_lo = tree_lo; a.tree_hi = tree_hi;
+  a.err = d.err;
+  a.cand = rf::candidate_counter();
+  // warps per CTA: the most resident warps per SM (registers and shared memory both bound it);
+  // a task shape whose CTA-resident data does not fit shared memory takes the large path
+  int best_wpb = 0, best_warps = 0;
+  if (!large) {
+    for (int w = 1; w <= rf::kSmallMaxWpb; ++w) {
+      a.wpb = w;
+      const int warps = w * rf::small_tree_ctas_per_sm(a);
+      if (warps > best_warps) { best_warps = warps; best_wpb = w; }
+    }
+    if (best_wpb == 0) large = true;
+  }
   if (large) {
     for (int c = 32; c >= 1; --c)
       if (g % c == 0) { Cw = c; break; }
@@ -265,31 +289,8 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     ProfScope ps("task_orders", s);
     CK(rf::build_task_orders_u8(d.order, d.grank, td, s), "task orders");
   }
-
-  rf::SmallArgs a;
-  memset(&a, 0, sizeof a);
-  a.X = d.X; a.n = (int)n; a.p = (int)p; a.tq = d.tq; a.dF = d.F; a.grank = d.grank;
-  a.ntask = ntask; a.task0 = task_lo; a.row_stride = (int)n; a.ntr_stride = ntr_max;
-  a.ntr = td.ntr; a.nte = td.nte; a.tr_rows = td.tr_rows; a.te_rows = td.te_rows;
-  a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = ntr_max; a.nte_max = nte_max;
-  a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
-  a.extra = prm->split_mode == RF_SPLIT_EXTRA;
-  a.max_depth = prm->max_depth; a.n_mtry = nmd;
-  for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
-  a.tree_lo = tree_lo; a.tree_hi = tree_hi;
-  a.err = d.err;
-  a.cand = rf::candidate_counter();
-  // warps per CTA: the most resident warps per SM (registers and shared memory both bound it)
-  int best_wpb = 0, best_warps = 0;
-  size_t smem = 0;
-  for (int w = 1; w <= rf::kSmallMaxWpb; ++w) {
-    a.wpb = w;
-    const int warps = w * rf::small_tree_ctas_per_sm(a);
-    if (warps > best_warps) { best_warps = warps; best_wpb = w; }
-  }
-  if (best_wpb == 0) return fail(RF_E_UNSUPPORTED, "small-tree kernel: shared memory budget exceeded");
+  a.ord = td.ord; a.lrank = td.lrank;
   a.wpb = best_wpb;
-  smem = rf::small_tree_smem_bytes(a, 0);
   const int resident = 148 * best_warps;
   for (int c = 16; c >= 1; --c) {
     if (g % c) continue;
@@ -388,8 +389,8 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   int dev = 0;
   cudaGetDevice(&dev);
 
-  const bool small = n <= (uint64_t)rf::kSmallMaxRows && p <= (uint32_t)rf::kSmallMaxP &&
-                     prm->split_mode != RF_SPLIT_HIST256;
+  bool small = n <= (uint64_t)rf::kSmallMaxRows && p <= (uint32_t)rf::kSmallMaxP &&
+               prm->split_mode != RF_SPLIT_HIST256;
   rf::Node16* nodes_w = nullptr;
   uint32_t* tidx_w = nullptr;
   uint32_t* nn_d = nullptr;
@@ -430,11 +431,15 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
       smem = rf::small_tree_smem_bytes(a, 0);
       if (smem <= 227 * 1024) break;
     }
-    if (a.wpb == 0) { cudaFree(lor); return fail(RF_E_UNSUPPORTED, "shared memory budget"); }
-    ProfScope ps("small_tree_fit", s);
-    cudaError_t e = rf::launch_small_tree(a, s);
-    if (e != cudaSuccess) { cudaFree(lor); return cuda_fail(e, "small_tree fit"); }
-  } else {
+    if (a.wpb == 0) {
+      small = false;  // CTA-resident data does not fit shared memory: large path
+    } else {
+      ProfScope ps("small_tree_fit", s);
+      cudaError_t e = rf::launch_small_tree(a, s);
+      if (e != cudaSuccess) { cudaFree(lor); return cuda_fail(e, "small_tree fit"); }
+    }
+  }
+  if (!small) {
     rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,
                                  &cap, lor, g_err);
     if (ls) { cudaFree(lor); return ls; }
@@ -857,6 +862,15 @@ rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates) {
     unsigned long long* c = rf::candidate_counter();
     if (c) CK(cudaMemcpy(candidates, c, 8, cudaMemcpyDeviceToHost), "counter");
   }
+  return RF_OK;
+}
+
+rf_status rf_debug_phase_cycles(uint64_t* out16, int reset) {
+  if (!out16) return fail(RF_E_ARG, "out is NULL");
+  if (!rf::small_tree_phase_timing_enabled())
+    return fail(RF_E_UNSUPPORTED, "phase timing needs a library built with RF_PHASE_TIMING=1");
+  if (rf_status st = check_device()) return st;
+  CK(rf::small_tree_phase_cycles(out16, reset != 0), "phase cycles");
   return RF_OK;
 }
 

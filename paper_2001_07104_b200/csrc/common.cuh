@@ -103,13 +103,15 @@ __device__ __forceinline__ double midpoint_thr(double a, double b) {
 // ExtraTrees threshold of draw slot j at heap node h (R29):
 // u = (draw(j) of stream (k_t; h_lo, h_hi, 0xE7) >> 11) 2^-53 (exact),
 // thr = fl(fl(fl(hi - lo) u) + lo), replaced by lo unless thr < hi.
-__device__ __forceinline__ double extra_thr(uint32_t k0, uint32_t k1, uint64_t h, int j, double lo, double hi) {
-  uint64_t d0, d1;
-  philox_pair(k0, k1, (uint32_t)(j >> 1), (uint32_t)h, (uint32_t)(h >> 32), kTagThr, d0, d1);
-  const uint64_t d = (j & 1) ? d1 : d0;
+__device__ __forceinline__ double extra_thr_draw(uint64_t d, double lo, double hi) {
   const double u = __dmul_rn(__ull2double_rn(d >> 11), 0x1p-53);
   const double t = __dadd_rn(__dmul_rn(__dsub_rn(hi, lo), u), lo);
   return t < hi ? t : lo;
+}
+__device__ __forceinline__ double extra_thr(uint32_t k0, uint32_t k1, uint64_t h, int j, double lo, double hi) {
+  uint64_t d0, d1;
+  philox_pair(k0, k1, (uint32_t)(j >> 1), (uint32_t)h, (uint32_t)(h >> 32), kTagThr, d0, d1);
+  return extra_thr_draw((j & 1) ? d1 : d0, lo, hi);
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -14,8 +14,9 @@
 //   leaf if depth cap, < min_split distinct rows, constant t_q or no
 //   candidate (R11); leaf value fl(S/W) 2^-F (R13).
 //   ExtraTrees (split_mode 2, R29): the only candidate of a
-//   (node, slot) segment is the boundary of its random threshold, located by
-//   a binary search before the search pass; everything else is shared.
+//   (node, slot) segment is the boundary of its random threshold, given as a
+//   dense-rank threshold found by a binary search in a shared-memory table of
+//   the task's distinct values; everything else is shared.
 //
 // Per level the warp runs three lane-serial passes (each lane owns a
 // contiguous chunk; lane totals are combined by one warp scan):
@@ -72,6 +73,7 @@ struct CtaSmem {
   SA<int64_t> tq;     // [ntr_max]
   SA<double2> rcp2;   // [256] (w, RN(1/w))
   SA<double> xte;     // [nte_max][p]
+  SA<double> xs;      // ExtraTrees: [p][ntr_max] distinct training values of x_f by dense rank
 };
 
 struct NodeSet {  // open nodes of one level
@@ -92,7 +94,8 @@ struct WarpSmem {
   SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
   SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates), in draw order
-  SA<uint8_t> xb;      // ExtraTrees: [NM][p] boundary position in the segment per draw slot, or kNone
+  SA<uint8_t> swp;     // [NM][p] Fisher-Yates swap index of each draw slot
+  SA<uint8_t> xb;      // ExtraTrees: [NM][p] rank threshold per draw slot (last rank with x <= thr) or kNone
   SA<unsigned long long> bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
   SA<uint32_t> baux;   // best (feature << 8 | position); bit 31 = split
   SA<uint32_t> bW;     // search: prefix base of W; then the best's left W
@@ -109,12 +112,13 @@ constexpr uint8_t kNone = 0xFF;
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
 
-__host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_max, int nte_max) {
+__host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_max, int nte_max, bool extra) {
   s.ord = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.lrank = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.tq = c.take<int64_t>(ntr_max, 16);
   s.rcp2 = c.take<double2>(256, 16);
   s.xte = c.take<double>((size_t)nte_max * p, 16);
+  s.xs = extra ? c.take<double>((size_t)p * ntr_max, 16) : SA<double>{0u};
 }
 
 __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
@@ -138,6 +142,7 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   carve_nodeset(c, s.cur, NM);
   carve_nodeset(c, s.nxt, NM);
   s.feat = c.take<uint8_t>((size_t)NM * p, 4);
+  s.swp = c.take<uint8_t>((size_t)NM * p, 4);
   s.xb = extra ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
   s.bkey = c.take<unsigned long long>(NM, 8);
   s.baux = c.take<uint32_t>(NM, 4);
@@ -229,6 +234,23 @@ __device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsig
   return k1 > k2 || (k1 == k2 && a1 < a2);
 }
 
+// ------------------------------------------------- profiling build only --
+// RF_PHASE_TIMING: lane 0 of every warp adds the clock64 delta since the previous
+// mark to g_phase_cyc[i] (phase names: DESIGN.md sec. 6).  Compiled out otherwise.
+__device__ unsigned long long g_phase_cyc[kPhases];
+#ifdef RF_PHASE_TIMING
+#define PT_MARK(i)                                                              \
+  do {                                                                          \
+    const long long _t = clock64();                                             \
+    if (lane == 0) atomicAdd(&g_phase_cyc[i], (unsigned long long)(_t - pt0)); \
+    pt0 = _t;                                                                   \
+  } while (0)
+#else
+#define PT_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 // -------------------------------------------------------------- the kernel --
 // TM: max test rows per lane.  kExtra: ExtraTrees split mode (R29).
 template <bool kFit, int TM, bool kExtra>
@@ -237,6 +259,9 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
   const int warp = threadIdx.x >> 5;
   const int p = a.p;
   const int ntr_max = a.ntr_max;
+#ifdef RF_PHASE_TIMING
+  long long pt0 = clock64();
+#endif
 
   // work item of this CTA: (mtry index, task, chunk of warp jobs)
   const int cta_per_mt = (a.nsub + a.wpb - 1) / a.wpb;
@@ -250,7 +275,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 
   Carve cv;
   CtaSmem cs;
-  carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max);
+  carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max, extra);
   WarpSmem ws;
   {
     const size_t cta_bytes = (cv.off + 15) / 16 * 16;
@@ -276,6 +301,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
       const int f = i / ntr, j = i - f * ntr;
       cs.ord[f * ntr_max + j] = go[(size_t)f * a.ntr_stride + j];
       cs.lrank[f * ntr_max + j] = gr[(size_t)f * a.ntr_stride + j];
+      // ExtraTrees: value table by dense rank (rows of equal value write the same value)
+      if (extra) cs.xs[f * ntr_max + gr[(size_t)f * a.ntr_stride + j]] = a.X[(size_t)tr_rows[j] * p + f];
     }
     #pragma unroll 1
     for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
@@ -292,6 +319,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     }
   }
   __syncthreads();
+  PT_MARK(14);
 
   const int sub = cchunk * a.wpb + warp;
   if (sub >= a.nsub) return;
@@ -412,6 +440,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     int N = (int)D;
     uint32_t curBase = 0, levelCount = 1;
     int depth = 0;
+    PT_MARK(0);
 
     while (nOpen > 0) {
       // ---------------- (a) per node: prefix bases, reset best, feature draws
@@ -433,53 +462,85 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
             ws.bS[k] = carryS + eS;
             ws.bkey[k] = 0ull;
             ws.baux[k] = 0x7FFFFFFFu;
-            // draw order matters even for m = p: ties go to the first drawn feature (R9)
-            const SA<uint8_t> fp = ws.feat + k * p;
-            #pragma unroll 1
-            for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
-            const uint64_t h = cur.heap[k];
-            const uint32_t hlo = (uint32_t)h, hhi = (uint32_t)(h >> 32);
-            #pragma unroll 1
-            for (int j = 0; j < m; j += 2) {
-              uint64_t d0, d1;
-              philox_pair_ool(k0, k1, (uint32_t)(j >> 1), hlo, hhi, kTagFeat, d0, d1);
-              int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
-              uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
-              if (j + 1 < m) {
-                r = j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1));
-                tmp = fp[j + 1]; fp[j + 1] = fp[r]; fp[r] = tmp;
-              }
-            }
           }
           carryW += tW;
           carryS += tS;
         }
       }
+      PT_MARK(1);
+      // feature draws (R4), flattened over (node, Philox block) so every lane works: the
+      // Fisher-Yates swap index of each slot; the draw order matters even for m = p
+      // (ties go to the first drawn feature, R9)
+      const int nblk = (m + 1) >> 1;
+      #pragma unroll 1
+      for (int q = lane; q < nOpen * nblk; q += 32) {
+        const int k = q / nblk, b = q - k * nblk;
+        const uint64_t h = cur.heap[k];
+        uint64_t d0, d1;
+        philox_pair_ool(k0, k1, (uint32_t)b, (uint32_t)h, (uint32_t)(h >> 32), kTagFeat, d0, d1);
+        const int j = 2 * b;
+        ws.swp[k * p + j] = (uint8_t)(j + (int)mulhi64(d0, (uint64_t)(p - j)));
+        if (j + 1 < m) ws.swp[k * p + j + 1] = (uint8_t)(j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1)));
+      }
       __syncwarp();
+      // apply the swaps, one lane per node (p <= 16: nibble-packed in a register)
+      #pragma unroll 1
+      for (int k = lane; k < nOpen; k += 32) {
+        const SA<uint8_t> fp = ws.feat + k * p;
+        const SA<uint8_t> sp = ws.swp + k * p;
+        if (p <= 16) {
+          uint64_t perm = 0xFEDCBA9876543210ull;
+          #pragma unroll 1
+          for (int j = 0; j < m; ++j) {
+            const int r = sp[j];
+            const uint64_t x = ((perm >> (4 * j)) ^ (perm >> (4 * r))) & 0xFull;
+            perm ^= (x << (4 * j)) | (x << (4 * r));
+            fp[j] = (uint8_t)((perm >> (4 * j)) & 0xFull);
+          }
+        } else {
+          #pragma unroll 1
+          for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
+          #pragma unroll 1
+          for (int j = 0; j < m; ++j) {
+            const int r = sp[j];
+            const uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
+          }
+        }
+      }
+      __syncwarp();
+      PT_MARK(2);
       if (extra) {
         // ExtraTrees (R29): per (node, draw slot) the random threshold in [lo, hi) of the
-        // segment and its boundary = last segment position with x <= thr (kNone if lo = hi)
+        // segment's values and its rank threshold = last dense rank with x <= thr
+        // (kNone if lo = hi); one Philox block serves two slots
         #pragma unroll 1
-        for (int q = lane; q < nOpen * m; q += 32) {
-          const int k = q / m, j = q - k * m;
-          const int f = ws.feat[k * p + j];
+        for (int q = lane; q < nOpen * nblk; q += 32) {
+          const int k = q / nblk, b = q - k * nblk;
+          const uint64_t h = cur.heap[k];
+          uint64_t d0, d1;
+          philox_pair_ool(k0, k1, (uint32_t)b, (uint32_t)h, (uint32_t)(h >> 32), kTagThr, d0, d1);
           const int st = cur.start[k], ln = cur.len[k];
-          const SA<uint8_t> seg = L + (f * ntr_max + st);
-          const double* Xf = a.X + f;
-          const double lo = Xf[(size_t)tr_rows[seg[0]] * p], hi = Xf[(size_t)tr_rows[seg[ln - 1]] * p];
-          uint8_t bnd = kNone;
-          if (lo < hi) {
-            const double thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
-            int l = 0, u = ln - 1;  // x[l] <= thr < x[u]
-            while (u - l > 1) {
-              const int mid = (l + u) >> 1;
-              if (Xf[(size_t)tr_rows[seg[mid]] * p] <= thr) l = mid; else u = mid;
+          #pragma unroll 1
+          for (int s = 0; s < 2 && 2 * b + s < m; ++s) {
+            const int j = 2 * b + s;
+            const int f = ws.feat[k * p + j];
+            const int fb = f * ntr_max;
+            const int rlo = cs.lrank[fb + L[fb + st]], rhi = cs.lrank[fb + L[fb + st + ln - 1]];
+            uint8_t bnd = kNone;
+            if (rlo < rhi) {
+              const double thr = extra_thr_draw(s ? d1 : d0, cs.xs[fb + rlo], cs.xs[fb + rhi]);
+              int l = rlo, u = rhi;  // xs[l] <= thr < xs[u]
+              while (u - l > 1) {
+                const int mid = (l + u) >> 1;
+                if (cs.xs[fb + mid] <= thr) l = mid; else u = mid;
+              }
+              bnd = (uint8_t)l;
             }
-            bnd = (uint8_t)l;
+            ws.xb[k * p + j] = bnd;
           }
-          ws.xb[k * p + j] = bnd;
         }
         __syncwarp();
+        PT_MARK(3);
       }
 
       // ---------------- (b) search pass over (node, feature slot, position), node-major
@@ -534,6 +595,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         uint64_t tS;
         uint32_t cW = wscan_u32(lw, tW);
         uint64_t cS = wscan_u64(ls, tS);
+        PT_MARK(4);
         // pass 2: prefix sums, candidates at distinct-value boundaries, best per node run
         k = k_init; j = j_init; i = i_init; st = st_init; ln = ln_init; f = f_init; lbase = f * ntr_max;
         Wk = W_init; Sk = S_init;
@@ -565,7 +627,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const double2 yl = cs.rcp2[WL & 0xFFu], yr = cs.rcp2[WR & 0xFFu];
           const double gl = div_small(__dmul_rn(dSL, dSL), yl.x, yl.y);
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
-          const bool cand = act && hasNext && (extra ? i == xbj : rkr != rkn);
+          const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
           const unsigned long long key =
               cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
           const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);
@@ -638,6 +700,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
       }
       __syncwarp();
+      PT_MARK(5);
 
       // ---------------- (c) decisions and thresholds; first-row targets of the children
       #pragma unroll 1
@@ -653,9 +716,9 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const uint32_t ga = tr_rows[ra], gb = tr_rows[rb];
           double thr;
           if (extra) {  // the drawn threshold of slot j (R29), recomputed from the segment's range
-            const int st = cur.start[k];
-            const double lo = a.X[(size_t)tr_rows[L[f * ntr_max + st]] * p + f];
-            const double hi = a.X[(size_t)tr_rows[L[f * ntr_max + st + cur.len[k] - 1]] * p + f];
+            const int st = cur.start[k], fb = f * ntr_max;
+            const double lo = cs.xs[fb + cs.lrank[fb + L[fb + st]]];
+            const double hi = cs.xs[fb + cs.lrank[fb + L[fb + st + cur.len[k] - 1]]];
             thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
           } else {
             thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
@@ -669,6 +732,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
       }
       __syncwarp();
+      PT_MARK(6);
 
       // ---------------- (d) mark pass: go-left flags, child constancy (lock-step, no atomics)
       #pragma unroll 1
@@ -687,6 +751,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
       }
       __syncwarp();
+      PT_MARK(7);
 
       // ---------------- (e) children, node emission, next-level tables
       int nSplitTotal = 0, nOpenNext = 0, Nnext = 0, NL = 0;
@@ -789,6 +854,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         NL = (int)carryL;
       }
       __syncwarp();
+      PT_MARK(8);
 
       // ---------------- (f) route the task's test rows one level down
       if (!kFit) {
@@ -814,6 +880,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           }
         }
       }
+      PT_MARK(9);
 
       // ---------------- (g) stable partition of all p lists (feature-major), ping-pong.
       // One pass in 32-element chunks: a ballot of go-left flags gives every
@@ -865,6 +932,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           carry += __popc(bal);
         }
         __syncwarp();
+        PT_MARK(10);
         // lists 1..p-1, flattened feature-major: element e -> list 1 + e / N, position e % N
         // (e / N exactly via a float reciprocal: e < 2^16)
         const int E = (p - 1) * N;
@@ -896,6 +964,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           carry += __popc(bal);
         }
       }
+      PT_MARK(11);
       // advance to the next level
       {
         const NodeSet tmp = cur; cur = nxt; nxt = tmp;
@@ -908,9 +977,11 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
       N = Nnext;
       ++depth;
       __syncwarp();
+      PT_MARK(12);
     }
     if (kFit && lane == 0) a.tree_nnodes[tree_slot] = curBase + levelCount;
     __syncwarp();
+    PT_MARK(13);
   }
 
   if (a.cand) {
@@ -933,7 +1004,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   Carve c;
   CtaSmem cs;
-  carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max);
+  carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max, a.extra != 0);
   const size_t cta = (c.off + 15) / 16 * 16;
   Carve w;
   WarpSmem ws;
@@ -965,6 +1036,24 @@ int small_tree_ctas_per_sm(const SmallArgs& a) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * a.wpb, smem) != cudaSuccess) return 0;
     return nb;
   });
+}
+
+bool small_tree_phase_timing_enabled() {
+#ifdef RF_PHASE_TIMING
+  return true;
+#else
+  return false;
+#endif
+}
+
+cudaError_t small_tree_phase_cycles(uint64_t* out, bool reset) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out, g_phase_cyc, sizeof(unsigned long long) * kPhases);
+  if (e == cudaSuccess && reset) {
+    static const unsigned long long zeros[kPhases] = {};
+    e = cudaMemcpyToSymbol(g_phase_cyc, zeros, sizeof zeros);
+  }
+  return e;
 }
 
 cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s) {

@@ -60,4 +60,9 @@ size_t small_tree_smem_bytes(const SmallArgs& a, int mmax);
 int small_tree_ctas_per_sm(const SmallArgs& a);
 cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s);
 
+// profiling build (RF_PHASE_TIMING): per-phase clock64 sums of the kernel's warps
+constexpr int kPhases = 16;
+bool small_tree_phase_timing_enabled();
+cudaError_t small_tree_phase_cycles(uint64_t* out, bool reset);
+
 }  // namespace rf
