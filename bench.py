@@ -233,7 +233,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = rfg.launch_count()
+    launches0, cands0 = rfg.counters()  # cumulative since process start (incl. warm-up)
     with ClockSampler(local) as clk:
         wall0 = time.perf_counter()
         for s in range(args.steps):
@@ -243,7 +243,8 @@ def run_ours(args):
             stop[s].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
-    launches = rfg.launch_count() - launches0
+    launches1, cands1 = rfg.counters()
+    launches, cands = launches1 - launches0, cands1 - cands0
     if world > 1:
         dist.barrier()
     dev_ms = sum(a.elapsed_time(b) for a, b in zip(start, stop))
@@ -258,7 +259,6 @@ def run_ours(args):
 
     # dominant kernel roofline: the small-tree kernel is ALU (fp64 + integer/SMEM issue) bound
     kern_ms, kern_n = prof.get("small_tree", (0.0, 0))
-    cands = rfg.candidate_count()
     roofline = None
     if kern_n:
         ops_per_cand = FP64_OPS_PER_CANDIDATE

@@ -21,12 +21,16 @@ INC = os.path.join(os.path.dirname(HERE), "include")
 # RF_PHASE_TIMING=1: profiling build (per-phase clock64 counters in the tree kernel,
 # rf_debug_phase_cycles) into build_pt/ and librfgpu_pt.so; load it with RFGPU_LIB.
 PHASE_TIMING = os.environ.get("RF_PHASE_TIMING", "0") == "1"
-BUILD = os.path.join(os.path.dirname(HERE), "build_pt" if PHASE_TIMING else "build")
-LIB = os.path.join(HERE, "librfgpu_pt.so" if PHASE_TIMING else "librfgpu.so")
+# RF_VARIANT=<tag> with RF_DEFS="-DX ...": an experimental variant (A/B timing) in
+# build_<tag>/ and librfgpu_<tag>.so; never the product library.
+VARIANT = os.environ.get("RF_VARIANT", "pt" if PHASE_TIMING else "")
+BUILD = os.path.join(os.path.dirname(HERE), f"build_{VARIANT}" if VARIANT else "build")
+LIB = os.path.join(HERE, f"librfgpu_{VARIANT}.so" if VARIANT else "librfgpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-I" + INC, "--expt-relaxed-constexpr"] + (["-DRF_PHASE_TIMING"] if PHASE_TIMING else [])
+         "-I" + INC, "--expt-relaxed-constexpr"] + (["-DRF_PHASE_TIMING"] if PHASE_TIMING else []) + \
+    (os.environ.get("RF_DEFS", "").split() if VARIANT else [])
 
 
 def _deps_mtime():

@@ -94,7 +94,6 @@ struct WarpSmem {
   SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
   SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates), in draw order
-  SA<uint8_t> swp;     // [NM][p] Fisher-Yates swap index of each draw slot
   SA<uint8_t> xb;      // ExtraTrees: [NM][p] rank threshold per draw slot (last rank with x <= thr) or kNone
   SA<unsigned long long> bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
   SA<uint32_t> baux;   // best (feature << 8 | position); bit 31 = split
@@ -105,12 +104,15 @@ struct WarpSmem {
   SA<double> chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
   SA<uint16_t> chBase; // BFS id of the left child
   SA<uint32_t> thrIdx; // fit mode: threshold rank
-  SA<uint32_t> desc;   // [ntr_max] partition descriptor per position (shared by all lists)
+  SA<uint32_t> desc;   // [ntr_max] partition descriptor per position (shared by all lists);
+                       // aliases bkey (free once the level's thresholds are used, (g))
 };
 
 constexpr uint8_t kNone = 0xFF;
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
+// per-feature stride of the row lists: a multiple of 4 (32-bit list words in (g))
+__host__ __device__ inline int stride_of(int ntr_max) { return (ntr_max + 3) & ~3; }
 
 __host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_max, int nte_max, bool extra) {
   s.ord = c.take<uint8_t>((size_t)p * ntr_max, 16);
@@ -142,9 +144,8 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   carve_nodeset(c, s.cur, NM);
   carve_nodeset(c, s.nxt, NM);
   s.feat = c.take<uint8_t>((size_t)NM * p, 4);
-  s.swp = c.take<uint8_t>((size_t)NM * p, 4);
   s.xb = extra ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
-  s.bkey = c.take<unsigned long long>(NM, 8);
+  s.bkey = c.take<unsigned long long>(NM, 16);  // 16-aligned: desc aliases it (uint4 loads)
   s.baux = c.take<uint32_t>(NM, 4);
   s.bW = c.take<uint32_t>(NM, 4);
   s.bS = c.take<uint64_t>(NM, 8);
@@ -153,7 +154,7 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.chVal = c.take<double>((size_t)NM * 2, 8);
   s.chBase = c.take<uint16_t>(NM, 4);
   s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
-  s.desc = c.take<uint32_t>(ntr_max, 4);
+  s.desc = SA<uint32_t>{s.bkey.off};  // ntr_max * 4 <= NM * 8 bytes
 }
 
 // ---------------------------------------------------------------- warp ops --
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int p = a.p;
-  const int ntr_max = a.ntr_max;
+  const int ntr_max = stride_of(a.ntr_max);  // list stride: 4-byte aligned words (g)
 #ifdef RF_PHASE_TIMING
   long long pt0 = clock64();
 #endif
@@ -468,44 +469,66 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
       }
       PT_MARK(1);
-      // feature draws (R4), flattened over (node, Philox block) so every lane works: the
-      // Fisher-Yates swap index of each slot; the draw order matters even for m = p
-      // (ties go to the first drawn feature, R9)
+      // feature draws (R4): partial Fisher-Yates; the draw order matters even for m = p
+      // (ties go to the first drawn feature, R9).
       const int nblk = (m + 1) >> 1;
-      #pragma unroll 1
-      for (int q = lane; q < nOpen * nblk; q += 32) {
-        const int k = q / nblk, b = q - k * nblk;
-        const uint64_t h = cur.heap[k];
-        uint64_t d0, d1;
-        philox_pair_ool(k0, k1, (uint32_t)b, (uint32_t)h, (uint32_t)(h >> 32), kTagFeat, d0, d1);
-        const int j = 2 * b;
-        ws.swp[k * p + j] = (uint8_t)(j + (int)mulhi64(d0, (uint64_t)(p - j)));
-        if (j + 1 < m) ws.swp[k * p + j + 1] = (uint8_t)(j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1)));
-      }
-      __syncwarp();
-      // apply the swaps, one lane per node (p <= 16: nibble-packed in a register)
+      if (p <= 16) {
+        // L lanes per node share its Philox blocks; the swap indices (4 bits per slot) are
+        // OR-combined across the group, then one lane applies the swaps to a nibble-packed
+        // permutation in a register
+        int Lg = 1;
+        while (Lg * 2 * nOpen <= 32 && Lg < nblk) Lg *= 2;
+        #pragma unroll 1
+        for (int base = 0; base < nOpen * Lg; base += 32) {
+          const int q = base + lane;
+          const int k = q / Lg, sub = q & (Lg - 1);
+          uint64_t sw = 0;
+          if (k < nOpen) {
+            const uint64_t h = cur.heap[k];
+            #pragma unroll 1
+            for (int b = sub; b < nblk; b += Lg) {
+              uint64_t d0, d1;
+              philox_pair_ool(k0, k1, (uint32_t)b, (uint32_t)h, (uint32_t)(h >> 32), kTagFeat, d0, d1);
+              const int j = 2 * b;
+              sw |= (uint64_t)(j + (int)mulhi64(d0, (uint64_t)(p - j))) << (4 * j);
+              if (j + 1 < m) sw |= (uint64_t)(j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1))) << (4 * j + 4);
+            }
+          }
+          #pragma unroll 1
+          for (int d = 1; d < Lg; d <<= 1) sw |= __shfl_xor_sync(0xffffffffu, sw, d);
+          if (k < nOpen && sub == 0) {
+            const SA<uint8_t> fp = ws.feat + k * p;
+            uint64_t perm = 0xFEDCBA9876543210ull;
+            #pragma unroll 1
+            for (int j = 0; j < m; ++j) {
+              const int r = (int)((sw >> (4 * j)) & 0xFull);
+              const uint64_t x = ((perm >> (4 * j)) ^ (perm >> (4 * r))) & 0xFull;
+              perm ^= (x << (4 * j)) | (x << (4 * r));
+              fp[j] = (uint8_t)((perm >> (4 * j)) & 0xFull);
+            }
+          }
+        }
+      } else {
       #pragma unroll 1
       for (int k = lane; k < nOpen; k += 32) {
         const SA<uint8_t> fp = ws.feat + k * p;
-        const SA<uint8_t> sp = ws.swp + k * p;
-        if (p <= 16) {
-          uint64_t perm = 0xFEDCBA9876543210ull;
-          #pragma unroll 1
-          for (int j = 0; j < m; ++j) {
-            const int r = sp[j];
-            const uint64_t x = ((perm >> (4 * j)) ^ (perm >> (4 * r))) & 0xFull;
-            perm ^= (x << (4 * j)) | (x << (4 * r));
-            fp[j] = (uint8_t)((perm >> (4 * j)) & 0xFull);
-          }
-        } else {
+        const uint64_t h = cur.heap[k];
+        {
           #pragma unroll 1
           for (int f = 0; f < p; ++f) fp[f] = (uint8_t)f;
           #pragma unroll 1
-          for (int j = 0; j < m; ++j) {
-            const int r = sp[j];
-            const uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
+          for (int j = 0; j < m; j += 2) {
+            uint64_t d0, d1;
+            philox_pair_ool(k0, k1, (uint32_t)(j >> 1), (uint32_t)h, (uint32_t)(h >> 32), kTagFeat, d0, d1);
+            int r = j + (int)mulhi64(d0, (uint64_t)(p - j));
+            uint8_t tmp = fp[j]; fp[j] = fp[r]; fp[r] = tmp;
+            if (j + 1 < m) {
+              r = j + 1 + (int)mulhi64(d1, (uint64_t)(p - j - 1));
+              tmp = fp[j + 1]; fp[j + 1] = fp[r]; fp[r] = tmp;
+            }
           }
         }
+      }
       }
       __syncwarp();
       PT_MARK(2);
@@ -630,7 +653,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
           const unsigned long long key =
               cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
-          const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);
+          const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);  // draw slot, position (R9)
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
@@ -933,35 +956,52 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         }
         __syncwarp();
         PT_MARK(10);
-        // lists 1..p-1, flattened feature-major: element e -> list 1 + e / N, position e % N
-        // (e / N exactly via a float reciprocal: e < 2^16)
-        const int E = (p - 1) * N;
-        const float invN = 1.0f / (float)N;
+        // lists 1..p-1, flattened feature-major in chunks of 4 positions (one 32-bit word of
+        // a list, one 16-byte load of descriptors): chunk c -> list 1 + c / nc4, positions
+        // 4 (c % nc4) .. +3 (c / nc4 exactly via a float reciprocal: c < 2^16).  Four
+        // ballots give each element its rank among the left rows before it.
+        const int nc4 = (N + 3) >> 2;
+        const int C = (p - 1) * nc4;
+        const float inv4 = 1.0f / (float)nc4;
         carry = 0;
         #pragma unroll 1
-        for (int base = 0; base < E; base += 32) {
-          const int e = base + lane;
-          const bool valid = e < E;
-          int fi = (int)((float)e * invN);
-          fi += (e - fi * N >= N) ? 1 : 0;
-          fi -= (e - fi * N < 0) ? 1 : 0;
-          const int pos = e - fi * N;
+        for (int base = 0; base < C; base += 32) {
+          const int c = base + lane;
+          const bool valid = c < C;
+          int fi = (int)((float)c * inv4);
+          fi += (c - fi * nc4 >= nc4) ? 1 : 0;
+          fi -= (c - fi * nc4 < 0) ? 1 : 0;
+          const int q4 = (c - fi * nc4) * 4;
           const int f = fi + 1;
-          uint32_t dsc = 0xFFFFFFFFu;
-          uint8_t r = 0;
+          uint32_t rows4 = 0;
+          uint4 d4 = make_uint4(~0u, ~0u, ~0u, ~0u);
           if (valid) {
-            dsc = ws.desc[pos];
-            r = L[f * ntr_max + pos];
+            rows4 = *reinterpret_cast<const uint32_t*>(L.ptr() + f * ntr_max + q4);
+            d4 = *reinterpret_cast<const uint4*>(ws.desc.ptr() + q4);
           }
-          const bool left = dsc != 0xFFFFFFFFu && ws.side[r];
-          const unsigned bal = __ballot_sync(0xffffffffu, left);
-          const uint32_t d = left ? (dsc & 0xFFu) : ((dsc >> 8) & 0xFFu);
-          if (valid && d != kNone) {
-            const uint32_t leftBefore = carry + __popc(bal & lt) - (uint32_t)fi * (uint32_t)NL - ((dsc >> 16) & 0xFFu);
-            const uint32_t dest = d + (left ? leftBefore : ((uint32_t)pos - (dsc >> 24)) - leftBefore);
-            L2[f * ntr_max + dest] = r;
+          uint32_t dsc[4] = {d4.x, d4.y, d4.z, d4.w};
+          bool left[4];
+          unsigned bal[4];
+          uint32_t before = carry;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (q4 + i >= N) dsc[i] = 0xFFFFFFFFu;  // padding positions (stale descriptors)
+            left[i] = dsc[i] != 0xFFFFFFFFu && ws.side[(rows4 >> (8 * i)) & 0xFFu];
+            bal[i] = __ballot_sync(0xffffffffu, left[i]);
+            before += __popc(bal[i] & lt);
           }
-          carry += __popc(bal);
+          before -= (uint32_t)fi * (uint32_t)NL;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t d = left[i] ? (dsc[i] & 0xFFu) : ((dsc[i] >> 8) & 0xFFu);
+            if (d != kNone) {  // also false for padding and unsplit positions
+              const uint32_t leftBefore = before - ((dsc[i] >> 16) & 0xFFu);
+              const uint32_t dest = d + (left[i] ? leftBefore : ((uint32_t)(q4 + i) - (dsc[i] >> 24)) - leftBefore);
+              L2[f * ntr_max + dest] = (uint8_t)(rows4 >> (8 * i));
+            }
+            before += left[i] ? 1u : 0u;
+          }
+          carry += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
         }
       }
       PT_MARK(11);
@@ -1004,11 +1044,11 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   Carve c;
   CtaSmem cs;
-  carve_cta(c, cs, a.p, a.ntr_max, a.fit_mode ? 0 : a.nte_max, a.extra != 0);
+  carve_cta(c, cs, a.p, stride_of(a.ntr_max), a.fit_mode ? 0 : a.nte_max, a.extra != 0);
   const size_t cta = (c.off + 15) / 16 * 16;
   Carve w;
   WarpSmem ws;
-  carve_warp(w, ws, a.p, a.ntr_max, a.extra != 0, a.fit_mode != 0);
+  carve_warp(w, ws, a.p, stride_of(a.ntr_max), a.extra != 0, a.fit_mode != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
 }
