@@ -194,6 +194,21 @@ RF_API rf_status rf_forest_export_leaf_rows(const rf_forest* f, int32_t* leaf_of
 /* rf_fit that also records leaf_of_row (parity tests). */
 RF_API rf_status rf_fit_debug(const double* X, uint64_t n, uint32_t p, const double* y,
                        const rf_params* prm, rf_forest** out);
+/* Feature importance (mean decrease in impurity; SURVEY 8(f) NEXT-3, P:218-219,
+   Table 6).  Each split adds W imp(node) - WL imp(L) - WR imp(R)
+   (imp = in-bag weighted MSE of the quantised target, R30) to its
+   feature; importance[p] (host) = the per-tree sums divided by their tree's
+   total, summed over trees, divided by the grand total (scikit-learn's rule;
+   all zeros if no tree has a positive decrease).  raw (host [ntree][p] or
+   NULL) receives the per-tree sums in target units.  Only forests grown by
+   rf_fit / rf_fit_dev carry them: RF_E_UNSUPPORTED for imported forests
+   (combine shards' raw arrays with rf_importance_dev). */
+RF_API rf_status rf_forest_importance(const rf_forest* f, double* importance, double* raw);
+/* Device: importance[p] from per-tree sums draw [ntree][p] (e.g. all-gathered
+   from tree shards), same rule.  Synchronises nothing; stream-ordered. */
+RF_API rf_status rf_importance_dev(const double* draw, uint32_t ntree, uint32_t p, double* dimportance,
+                                   void* stream);
+
 /* Build a forest from flattened arrays on the host (multi-GPU assembly). */
 RF_API rf_status rf_forest_import(const int32_t* feature, const uint32_t* left, const double* value,
                            const uint32_t* thr_index, const uint64_t* tree_off, uint32_t ntree,

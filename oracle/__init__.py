@@ -64,7 +64,7 @@ def lib():
         _lib.or_quantize.argtypes = [P, u64, C.c_int, P, P, P]
         _lib.or_make_folds.argtypes = [P, u64, u32, u32, u64, u32, P]
         _lib.or_fit.argtypes = [P, u64, u32, P, u32, u32, i32, u32, u32, u32, u64,
-                                u32, u32, u64, P, P, P, P, P, P, P, P]
+                                u32, u32, u64, P, P, P, P, P, P, P, P, P]
         _lib.or_predict.argtypes = [P, P, P, P, P, u32, u32, P, u64, u32, P]
         _lib.or_mape.argtypes = [P, P, u64]
         _lib.or_mape.restype = dbl
@@ -137,6 +137,7 @@ class Tree:
     left: np.ndarray        # uint32, right = left + 1
     leaf_value: np.ndarray  # float64
     leaf_of_row: np.ndarray | None = None  # int32 [n], -1 out of bag
+    imp_raw: np.ndarray | None = None      # float64 [p]: sum of the MDI decreases per feature
 
     @property
     def n_nodes(self):
@@ -170,6 +171,32 @@ class Forest:
         cat = lambda name: np.ascontiguousarray(np.concatenate([getattr(t, name) for t in self.trees]))
         return (cat("feature"), cat("thr_value"), cat("left"), cat("leaf_value"), off)
 
+    def importance(self):
+        """Feature importance (mean decrease in impurity), see ``importance``."""
+        return importance(np.stack([t.imp_raw for t in self.trees]))
+
+
+def importance(raw):
+    """MDI feature importance of a forest (Table 6
+    P:926-948) from per-tree sums of split decreases raw [T][p], following the
+    library the paper uses (scikit-learn): each tree's vector is divided by its
+    sum (trees without any decrease contribute zeros), the vectors are summed
+    over trees and the result is divided by its sum."""
+    raw = np.asarray(raw, dtype=np.float64)
+    T, p = raw.shape
+    acc = np.zeros(p)
+    for t in range(T):
+        s = 0.0
+        for f in range(p):
+            s += raw[t, f]
+        if s > 0.0:
+            for f in range(p):
+                acc[f] += raw[t, f] / s
+    tot = 0.0
+    for f in range(p):
+        tot += acc[f]
+    return acc / tot if tot > 0.0 else acc
+
 
 def fit(X, y, ntree=1, mtry=None, min_samples_split=2, max_depth=-1, bootstrap=True,
         split_mode=0, target=0, seed=0, tree_begin=0, tree_end=None, leaf_rows=False):
@@ -190,17 +217,18 @@ def fit(X, y, ntree=1, mtry=None, min_samples_split=2, max_depth=-1, bootstrap=T
     lf = np.zeros((T, cap), dtype=np.uint32)
     lv = np.zeros((T, cap), dtype=np.float64)
     lor = np.zeros((T, n), dtype=np.int32) if leaf_rows else None
+    imp = np.zeros((T, p), dtype=np.float64)
     F = np.zeros(1, dtype=np.int32)
     st = lib().or_fit(_p(X), n, p, _p(y), mtry, min_samples_split, max_depth, int(bootstrap),
                       split_mode, target, seed, tree_begin, tree_end, cap,
-                      _p(nn), _p(feat), _p(ti), _p(tv), _p(lf), _p(lv), _p(lor), _p(F))
+                      _p(nn), _p(feat), _p(ti), _p(tv), _p(lf), _p(lv), _p(lor), _p(F), _p(imp))
     if st:
         raise OracleError(st)
     trees = []
     for t in range(T):
         m = int(nn[t])
         trees.append(Tree(feat[t, :m].copy(), ti[t, :m].copy(), tv[t, :m].copy(), lf[t, :m].copy(),
-                          lv[t, :m].copy(), None if lor is None else lor[t].copy()))
+                          lv[t, :m].copy(), None if lor is None else lor[t].copy(), imp[t].copy()))
     return Forest(trees, int(F[0]), target)
 
 

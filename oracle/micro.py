@@ -265,7 +265,15 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     if hist:
         cuts = [hist_cuts([X[r][f] for r in tr]) for f in range(len(X[0]))]
     root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra)
-    return to_bfs(root), F
+    out = to_bfs(root)
+    # MDI (NEXT-3): per feature, the exact SSE reductions of its splits (the definition
+    # W imp(node) - WL imp(L) - WR imp(R), two-pass sums) in target units (x 2^-2F)
+    raw = [Fraction(0)] * len(X[0])
+    for nd in out["nodes"]:
+        if nd.children is not None:
+            raw[nd.feature] += nd.gain_exact_chosen
+    out["imp_raw"] = [float(v * Fraction(2) ** (-2 * F)) for v in raw]
+    return out, F
 
 
 def mape_exact(y, yhat):

@@ -381,9 +381,23 @@ static double gain(int64_t WL, int64_t SL, int64_t WR, int64_t SR)
     return a + b;
 }
 
-/* grows one tree; w[] = multiplicities per row (0 = out of bag) */
+/* Mean-decrease-in-impurity of one split (feature importance, SURVEY 8(f)
+   NEXT-3; Table 6): W imp(node) - WL imp(L) - WR imp(R)
+   with imp = weighted MSE; the sum-of-squares terms cancel, leaving
+   SL^2/WL + SR^2/WR - S^2/W = (SL WR - SR WL)^2 / (W WL WR), in target units
+   (x 2^-2F).  Evaluated exactly in __int128, then once in binary128. */
+static double mdi_decrease(int64_t WL, int64_t SL, int64_t WR, int64_t SR, int32_t F)
+{
+    __int128 num = (__int128)SL * WR - (__int128)SR * WL;
+    __float128 q = (__float128)num;
+    q = q * q / ((__float128)(WL + WR) * (__float128)WL * (__float128)WR);
+    return (double)ldexpq(q, -2 * F);
+}
+
+/* grows one tree; w[] = multiplicities per row (0 = out of bag);
+   imp (or NULL): per-feature sums of split decreases, BFS order */
 static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_t k1,
-                      or_tree *out, int32_t *leaf_of_row)
+                      or_tree *out, int32_t *leaf_of_row, double *imp)
 {
     const uint32_t p = c->p;
     /* root */
@@ -579,6 +593,7 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                 R.rows[R.nrows++] = r; R.W += (int64_t)w[r]; R.S += (int64_t)w[r] * c->tq[r];
             }
         }
+        if (imp) imp[bestF] += mdi_decrease(L.W, L.S, R.W, R.S, c->F);
         L.depth = R.depth = nd.depth + 1;
         L.heap = 2 * nd.heap;       /* uint64 wrap-around (R14) */
         R.heap = 2 * nd.heap + 1;
@@ -682,13 +697,16 @@ static double tree_predict(const or_tree *t, const double *x)
 /* Fit trees [tree_begin, tree_end) of task 0 (all rows train).
    Outputs per tree (index t - tree_begin) with capacity cap nodes:
    n_nodes[T], feature/thr_index/thr_value/left/leaf_value [T][cap],
-   leaf_of_row [T][n] (or NULL; -1 = out of bag). Returns status. */
+   leaf_of_row [T][n] (or NULL; -1 = out of bag), imp_raw [T][p] (or NULL):
+   per tree and feature the sum of the MDI decreases of its splits (target
+   units, see mdi_decrease). Returns status. */
 int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
            uint32_t mtry, uint32_t min_split, int32_t max_depth, uint32_t boot,
            uint32_t split_mode, uint32_t target, uint64_t seed,
            uint32_t tree_begin, uint32_t tree_end, uint64_t cap,
            uint64_t *n_nodes, int32_t *feature, uint32_t *thr_index, double *thr_value,
-           uint32_t *left, double *leaf_value, int32_t *leaf_of_row, int32_t *F_out)
+           uint32_t *left, double *leaf_value, int32_t *leaf_of_row, int32_t *F_out,
+           double *imp_raw)
 {
     if (n == 0) return 2;
     if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || split_mode > 2) return 1;
@@ -719,7 +737,9 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
         uint64_t o = tt - tree_begin;
         int32_t *lor = leaf_of_row ? leaf_of_row + o * n : NULL;
         if (lor) for (uint64_t i = 0; i < n; ++i) lor[i] = -1;
-        grow_tree(&g, w, k0, k1, &tree, lor);
+        double *imp = imp_raw ? imp_raw + o * p : NULL;
+        if (imp) for (uint32_t f = 0; f < p; ++f) imp[f] = 0.0;
+        grow_tree(&g, w, k0, k1, &tree, lor, imp);
         n_nodes[o] = tree.n;
         if (tree.n > cap) { st = 9; break; }
         for (uint64_t i = 0; i < tree.n; ++i) {
@@ -849,7 +869,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
                 uint32_t k0, k1;
                 tree_key(seed, task, tt, &k0, &k1);
                 bootstrap(k0, k1, tr, ntr, n, (int)boot, w);
-                grow_tree(&g, w, k0, k1, &tree, NULL);
+                grow_tree(&g, w, k0, k1, &tree, NULL, NULL);
                 for (uint64_t i = 0; i < nte; ++i) sum[i] += tree_predict(&tree, Xc + te[i] * p);
                 for (uint32_t ni = 0; ni < n_ntree; ++ni) {
                     if (ntrees[ni] != tt + 1) continue;

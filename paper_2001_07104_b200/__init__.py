@@ -35,7 +35,8 @@ ABI_SYMBOLS = [
     "rf_predict_partial_dev", "rf_predict_finalize_dev", "rf_make_folds", "rf_make_folds_dev",
     "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
     "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
-    "rf_forest_export_leaf_rows", "rf_forest_import", "rf_last_profile", "rf_set_profiling",
+    "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
+    "rf_last_profile", "rf_set_profiling",
     "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles",
 ]
 
@@ -89,6 +90,8 @@ def lib():
             "rf_forest_info": ([P, P, P, P, P, P], C.c_int),
             "rf_forest_export": ([P, P, P, P, P, P], C.c_int),
             "rf_forest_export_leaf_rows": ([P, P], C.c_int),
+            "rf_forest_importance": ([P, P, P], C.c_int),
+            "rf_importance_dev": ([P, u32, u32, P, P], C.c_int),
             "rf_forest_import": ([P, P, P, P, P, u32, u32, i32, u32, i32, P], C.c_int),
             "rf_last_profile": ([P, P, P, u32], u32),
             "rf_set_profiling": ([C.c_int], None),
@@ -185,6 +188,15 @@ class Forest:
         off = np.zeros(T + 1, np.uint64)
         _check(lib().rf_forest_export(self.handle, _ptr(feat), _ptr(left), _ptr(val), _ptr(ti), _ptr(off)))
         return dict(feature=feat, left=left, value=val, thr_index=ti, tree_off=off, **inf)
+
+    def importance(self, raw=False):
+        """Feature importance [p] (MDI, rf_forest_importance); raw=True also returns the
+        per-tree split-decrease sums [ntree][p]."""
+        inf = self.info()
+        imp = np.zeros(inf["p"], np.float64)
+        r = np.zeros((inf["ntree"], inf["p"]), np.float64) if raw else None
+        _check(lib().rf_forest_importance(self.handle, _ptr(imp), _ptr(r)))
+        return (imp, r) if raw else imp
 
     def leaf_rows(self):
         inf = self.info()
@@ -393,3 +405,14 @@ def debug_philox(ctr_key):
     out = torch.empty((m, 4), dtype=torch.int32, device=ctr_key.device)
     _check(lib().rf_debug_philox_dev(_ptr(inp), _ptr(out), m, _stream()))
     return out.to(torch.int64) & 0xFFFFFFFF
+
+
+def importance_dev(raw, out=None):
+    """Device: importance [p] from per-tree split-decrease sums raw [ntree][p]
+    (torch float64 CUDA tensor; e.g. all-gathered tree shards), rf_importance_dev."""
+    import torch
+    T, p = raw.shape
+    if out is None:
+        out = torch.empty(p, dtype=torch.float64, device=raw.device)
+    _check(lib().rf_importance_dev(_ptr(raw), T, p, _ptr(out), _stream()))
+    return out

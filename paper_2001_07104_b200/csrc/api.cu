@@ -19,6 +19,7 @@
 #include "prep.cuh"
 #include "small_tree.cuh"
 #include "host_util.cuh"
+#include "importance.cuh"
 
 struct rf_forest {
   int device = 0;
@@ -30,6 +31,7 @@ struct rf_forest {
   uint64_t* tree_off = nullptr;  // device [ntree + 1]
   std::vector<uint64_t> h_tree_off;
   int32_t* leaf_of_row = nullptr;  // device [ntree][n_rows] (debug fits)
+  double* imp = nullptr;           // device [ntree][p] MDI decreases (rf_fit), null if imported
   uint64_t n_rows = 0;
 };
 
@@ -397,6 +399,14 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   int32_t* lor = nullptr;
   uint64_t cap = 0;
   if (debug) CK(cudaMalloc(&lor, (size_t)T * n * sizeof(int32_t)), "alloc leaf_of_row");
+  // per-tree MDI decreases [T][p] (feature importance, NEXT-3), owned by the forest
+  double* imp = nullptr;
+  {
+    cudaError_t e = cudaMalloc(&imp, (size_t)T * p * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(imp, 0, (size_t)T * p * sizeof(double), s);
+    if (e != cudaSuccess) { cudaFree(lor); cudaFree(imp); return cuda_fail(e, "alloc importance"); }
+  }
+  auto drop = [&]() { cudaFree(lor); cudaFree(imp); };
   if (small) {
     rf::TaskData td;
     td.ntask = 1; td.task0 = 0; td.n = (int)n; td.p = (int)p; td.ntr_stride = (int)n;
@@ -424,7 +434,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     a.max_depth = prm->max_depth; a.n_mtry = 1; a.mtrys[0] = (int)mtry;
     a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
     a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;
-    a.cap = (uint32_t)cap; a.leaf_of_row = lor; a.err = d.err;
+    a.cap = (uint32_t)cap; a.leaf_of_row = lor; a.imp = imp; a.err = d.err;
     a.cand = rf::candidate_counter();
     size_t smem = 0;
     for (; a.wpb >= 1; a.wpb >>= 1) {
@@ -436,21 +446,22 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     } else {
       ProfScope ps("small_tree_fit", s);
       cudaError_t e = rf::launch_small_tree(a, s);
-      if (e != cudaSuccess) { cudaFree(lor); return cuda_fail(e, "small_tree fit"); }
+      if (e != cudaSuccess) { drop(); return cuda_fail(e, "small_tree fit"); }
     }
   }
   if (!small) {
     rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,
-                                 &cap, lor, g_err);
-    if (ls) { cudaFree(lor); return ls; }
+                                 &cap, lor, imp, g_err);
+    if (ls) { drop(); return ls; }
   }
   std::vector<uint32_t> hnn(T);
   CK(cudaMemcpyAsync(hnn.data(), nn_d, T * 4, cudaMemcpyDeviceToHost, s), "d2h");
   int32_t hF = 0;
   CK(cudaMemcpyAsync(&hF, d.F, 4, cudaMemcpyDeviceToHost, s), "d2h");
   st = read_err(d.err, s);
-  if (st) { cudaFree(lor); return st; }
+  if (st) { drop(); return st; }
   rf_forest* f = new rf_forest();
+  f->imp = imp;
   f->device = dev; f->ntree = (uint32_t)T; f->p = p; f->target = prm->target; f->F = hF;
   f->h_tree_off.resize(T + 1);
   f->h_tree_off[0] = 0;
@@ -524,6 +535,7 @@ void rf_forest_free(rf_forest* f) {
   cudaFree(f->thr_index);
   cudaFree(f->tree_off);
   cudaFree(f->leaf_of_row);
+  cudaFree(f->imp);
   delete f;
 }
 
@@ -790,6 +802,33 @@ rf_status rf_forest_export_leaf_rows(const rf_forest* f, int32_t* leaf_of_row) {
   if (!f->leaf_of_row) return fail(RF_E_ARG, "forest was not grown with rf_fit_debug");
   CK(cudaSetDevice(f->device), "set device");
   CK(cudaMemcpy(leaf_of_row, f->leaf_of_row, (size_t)f->ntree * f->n_rows * 4, cudaMemcpyDeviceToHost), "d2h");
+  return RF_OK;
+}
+
+rf_status rf_forest_importance(const rf_forest* f, double* importance, double* raw) {
+  if (!f || !importance) return fail(RF_E_ARG, "forest or output is NULL");
+  if (!f->imp) return fail(RF_E_UNSUPPORTED, "forest has no split statistics (imported): use rf_importance_dev");
+  CK(cudaSetDevice(f->device), "set device");
+  cudaStream_t s = host_stream(f->device);
+  Scratch sc(s);
+  double *ws, *out;
+  CK(sc.alloc(&ws, (size_t)f->ntree + f->p), "alloc");
+  CK(sc.alloc(&out, (size_t)f->p), "alloc");
+  CK(rf::importance_combine(f->imp, (int)f->ntree, (int)f->p, out, ws, s), "importance");
+  CK(cudaMemcpyAsync(importance, out, (size_t)f->p * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  if (raw) CK(cudaMemcpyAsync(raw, f->imp, (size_t)f->ntree * f->p * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
+rf_status rf_importance_dev(const double* draw, uint32_t ntree, uint32_t p, double* dimportance, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!draw || !dimportance || ntree == 0 || p == 0) return fail(RF_E_ARG, "bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Scratch sc(s);
+  double* ws;
+  CK(sc.alloc(&ws, (size_t)ntree + p), "alloc");
+  CK(rf::importance_combine(draw, (int)ntree, (int)p, dimportance, ws, s), "importance");
   return RF_OK;
 }
 

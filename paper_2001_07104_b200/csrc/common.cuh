@@ -114,6 +114,22 @@ __device__ __forceinline__ double extra_thr(uint32_t k0, uint32_t k1, uint64_t h
   return extra_thr_draw((j & 1) ? d1 : d0, lo, hi);
 }
 
+// Mean decrease in impurity of one split (feature importance, SURVEY 8(f) NEXT-3;
+// P:218-219): W imp(node) - WL imp(L) - WR imp(R) = (SL WR - SR WL)^2 / (W WL WR),
+// scaled by 2^-2F to target units.  The numerator is exact in __int128 and rounded
+// once (plus the split into two 64-bit halves); the rest is fp64 (relative error
+// a few ulp; the sums over splits run in atomics, so importances carry a ~1e-15
+// order dependence -- the parity bar is 1e-9).
+__device__ __forceinline__ double mdi_decrease(int64_t WL, int64_t SL, int64_t WR, int64_t SR, int F) {
+  const __int128 num = (__int128)SL * WR - (__int128)SR * WL;
+  const bool neg = num < 0;
+  const unsigned __int128 u = neg ? (unsigned __int128)(-num) : (unsigned __int128)num;
+  const double dn = __dadd_rn(__dmul_rn(__ull2double_rn((unsigned long long)(u >> 64)), 0x1p64),
+                              __ull2double_rn((unsigned long long)u));
+  const double den = __dmul_rn(__dmul_rn(__ll2double_rn(WL + WR), __ll2double_rn(WL)), __ll2double_rn(WR));
+  return scalbn(__ddiv_rn(__dmul_rn(dn, dn), den), -2 * F);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -138,6 +138,7 @@ struct Batch {
   uint32_t* outCount;  // [B]
   uint64_t cap;
   int32_t* leaf_of_row;  // [B][n] or null
+  double* imp;           // [B][p] MDI decreases per tree and feature (fit), or null
   int tree0;             // global tree index of batch slot 0
   int* err;
 };
@@ -910,6 +911,8 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
   me_n.v = b.thr[g];
   out[me] = me_n;
   outThr[me] = b.thrIdx[g];
+  if (b.imp)  // feature importance (MDI, NEXT-3)
+    atomicAdd(&b.imp[(size_t)t * b.p + me_n.feat], mdi_decrease(WLv, SLv, WRv, SRv, b.F));
   uint32_t oi = sc.op;                             // global open index of the first child
   uint32_t ps = sc.pos - nextPos0[t];              // tree-local position of the first child
   if (oL) {
@@ -1325,17 +1328,17 @@ __global__ void k_chunk_predict(const Node16* __restrict__ nodes, uint64_t cap, 
 static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
                              int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
                              cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
-                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, std::string& err);
+                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, double* imp, std::string& err);
 
 rf_status fit_large(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi, cudaStream_t s,
                     Scratch& sc, Node16** nodes_out, uint32_t** thr_out, uint32_t** nn_out, uint64_t* cap_out,
-                    int32_t* leaf_of_row, std::string& err) {
+                    int32_t* leaf_of_row, double* imp, std::string& err) {
   uint32_t* tr_rows;
   LCK(sc.alloc(&tr_rows, (size_t)d.n));
   k_iota<<<nblk(d.n, 256) > 1184 ? 1184 : nblk(d.n, 256), 256, 0, s>>>(tr_rows, d.n);
   note_launch();
   return grow_forest(d, prm, mtry, tree_lo, tree_hi, 0, tr_rows, d.n, d.order, s, sc, nodes_out, thr_out, nn_out,
-                     cap_out, leaf_of_row, err);
+                     cap_out, leaf_of_row, imp, err);
 }
 
 rf_status cv_large_partial(const DevData& d, const TaskData& td, const rf_params* prm,
@@ -1361,7 +1364,7 @@ rf_status cv_large_partial(const DevData& d, const TaskData& td, const rf_params
       uint64_t cap;
       rf_status st = grow_forest(d, prm, mtrys[mi], tree_lo, tree_hi, td.task0 + tl,
                                  td.tr_rows + (size_t)tl * d.n, ntr, order, s, fs, &nodes, &thr, &nn, &cap, nullptr,
-                                 err);
+                                 nullptr, err);
       if (st) return st;
       double* part = partial + ((size_t)mi * ntask + tl) * nsub * nte_max;
       const long long nth = (long long)nte * nsub;
@@ -1376,7 +1379,7 @@ rf_status cv_large_partial(const DevData& d, const TaskData& td, const rf_params
 static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
                              int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
                              cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
-                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, std::string& err) {
+                             uint32_t** nn_out, uint64_t* cap_out, int32_t* leaf_of_row, double* imp, std::string& err) {
   if (d.p > 255) {
     err = "large path: p <= 255";
     return RF_E_UNSUPPORTED;
@@ -1529,6 +1532,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     b.outThr = outThr + (size_t)t0 * cap;
     b.outCount = outCount + t0;
     b.leaf_of_row = leaf_of_row ? leaf_of_row + (size_t)t0 * n : nullptr;
+    b.imp = imp ? imp + (size_t)t0 * p : nullptr;
     rf_status st = grow_batch(b, pl, list_src, prm->seed, task, (int)prm->bootstrap, cub_tmp, cub_bytes, rootInfo,
                               counters, hcounters, nextNode0, nextPos0, nlBase, wsTmp, hb, pbufs, candidate_counter(),
                               s, err);

@@ -15,7 +15,8 @@ namespace rf {
 // owned by `sc`): per-tree BFS node blocks of capacity *cap, node counts.
 rf_status fit_large(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
                     cudaStream_t s, Scratch& sc, Node16** nodes, uint32_t** thr_index,
-                    uint32_t** nnodes, uint64_t* cap, int32_t* leaf_of_row, std::string& err);
+                    uint32_t** nnodes, uint64_t* cap, int32_t* leaf_of_row, double* imp,
+                    std::string& err);
 
 // CV tasks whose training sets exceed the small-tree kernel: for every task and
 // every distinct mtry, grow trees [tree_lo, tree_hi) and write the per-chunk

@@ -853,6 +853,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               ti[me] = ws.thrIdx[k];
               if (!openL) { Node16 l; l.feat = -1; l.left = 0; l.v = vL; tn[childBase] = l; ti[childBase] = 0; }
               if (!openR) { Node16 r; r.feat = -1; r.left = 0; r.v = vR; tn[childBase + 1] = r; ti[childBase + 1] = 0; }
+              if (a.imp)  // feature importance (MDI, NEXT-3)
+                atomicAdd(&a.imp[tree_slot * p + nd.feat], mdi_decrease(WLv, SLv, WRv, SRv, F));
             }
           } else if (act) {
             // open node without any candidate split: leaf (R11)

@@ -50,6 +50,7 @@ struct SmallArgs {
   uint32_t* tree_nnodes;    // [tree_hi - tree_lo]
   uint32_t cap;             // node capacity per tree (2 ntr - 1)
   int32_t* leaf_of_row;     // [tree_hi - tree_lo][n] or nullptr
+  double* imp;              // [tree_hi - tree_lo][p] MDI decreases per tree and feature, or nullptr
   int* err;                 // device error flag
   unsigned long long* cand; // evaluated candidate splits (counter) or null
 };

@@ -385,6 +385,48 @@ def test_extra_cv_parity(n, boot):
     np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
 
 
+# ------------------------------------- feature importance (MDI, NEXT-3) ---
+IMP_CASES = [
+    ("small_exact", lambda: datagen.paper_shaped(189, "K20", "time"), dict(mtry=4, target=1)),
+    ("small_exact_m12", lambda: datagen.paper_shaped(168, "P100", "power"), dict(mtry=12)),
+    ("small_extra", lambda: datagen.paper_shaped(189, "V100", "time"), dict(mtry=12, target=1, bootstrap=False,
+                                                                          split_mode=2)),
+    ("large_exact", lambda: datagen.paper_shaped(1000, "TitanXp", "time"), dict(mtry=4, target=1)),
+    ("large_extra", lambda: datagen.paper_shaped(800, "K20", "power"), dict(mtry=6, split_mode=2)),
+    ("hist", lambda: datagen.paper_shaped(600, "GTX1650", "time"), dict(mtry=4, target=1, split_mode=1)),
+    ("scaled_depth", lambda: datagen.scaled(5000, 64), dict(mtry=21, max_depth=8, target=1)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", IMP_CASES, ids=[c[0] for c in IMP_CASES])
+def test_importance_parity(name, data, kw):
+    """Per-tree split-decrease sums within 1e-12 relative (order of the atomic sums and
+    one rounding of the int128 numerator differ), importance vector within 1e-12."""
+    X, y = data()
+    of = oracle.fit(X, y, ntree=8, seed=21, **kw)
+    gf = rfg.fit(X, y, ntree=8, seed=21, **kw)
+    _compare_forest(gf, of, X)
+    imp, raw = gf.importance(raw=True)
+    want_raw = np.stack([t.imp_raw for t in of.trees])
+    np.testing.assert_allclose(raw, want_raw, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(imp, of.importance(), rtol=0, atol=1e-12)
+    assert abs(imp.sum() - 1.0) < 1e-12
+    # tree shards: the combined raw arrays give the same vector (multi-GPU assembly)
+    a = rfg.fit(X, y, ntree=8, seed=21, tree_begin=0, tree_end=3, **kw).importance(raw=True)[1]
+    b = rfg.fit(X, y, ntree=8, seed=21, tree_begin=3, tree_end=8, **kw).importance(raw=True)[1]
+    comb = rfg.importance_dev(_cuda(np.concatenate([a, b]))).cpu().numpy()
+    np.testing.assert_allclose(comb, imp, rtol=0, atol=1e-14)
+
+
+def test_importance_imported_forest_unsupported():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    e = rfg.fit(X, y, ntree=2, seed=1, mtry=3).export()
+    f = rfg.forest_import(e["feature"], e["left"], e["value"], e["thr_index"], e["tree_off"], 12, e["F"], 0)
+    with pytest.raises(rfg.RFError) as err:
+        f.importance()
+    assert err.value.code == rfg.E_UNSUPPORTED
+
+
 # -------------------------------------------------------------- errors ---
 def test_errors():
     X, y = datagen.tiny(20, 3, 1)

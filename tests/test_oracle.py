@@ -541,6 +541,54 @@ def test_rf_vs_sklearn_advisory():
     assert abs(a - b) <= 0.10 * b, (a, b)
 
 
+# -------------------------------------- feature importance (MDI, NEXT-3) ---
+@pytest.mark.parametrize("case", CASES[:4] + XCASES[:2])
+@pytest.mark.parametrize("seed", range(4))
+def test_importance_raw_equals_micro(case, seed):
+    # per-tree decreases: C oracle closed form (int128 / binary128) vs the micro
+    # oracle's exact two-pass SSE reductions (the definition)
+    n, p, m, dist, boot, md, target = case[:7]
+    mode = 2 if case in XCASES else (1 if case[7] else 0)
+    X, y = datagen.tiny(n, p, seed, distinct=dist)
+    fo = oracle.fit(X, y, ntree=3, mtry=m, seed=seed, bootstrap=boot, max_depth=md, target=target,
+                    split_mode=mode)
+    for t in range(3):
+        mt, _ = micro.fit_tree(X, y, t, m, seed=seed, boot=boot, target=target, max_depth=md,
+                               hist=mode == 1, extra=mode == 2)
+        np.testing.assert_allclose(fo.trees[t].imp_raw, mt["imp_raw"], rtol=1e-15, atol=0)
+
+
+def test_importance_stump_and_normalisation():
+    X, y = datagen.paper_shaped(189, "V100", "time", seed=3)
+    f = oracle.fit(X, y, ntree=40, mtry=4, seed=2, max_depth=1, target=1)
+    imp = f.importance()
+    # a depth-1 tree credits everything to its root feature: importance = share of roots
+    roots = np.bincount([t.feature[0] for t in f.trees if t.feature[0] >= 0], minlength=12)
+    np.testing.assert_allclose(imp, roots / roots.sum(), rtol=1e-15, atol=1e-16)
+    f = oracle.fit(X, y, ntree=10, mtry=3, seed=2, target=1)
+    imp = f.importance()
+    assert (imp >= 0).all() and abs(imp.sum() - 1) < 1e-15
+    # constant target: no split anywhere -> zeros (scikit-learn's convention)
+    g = oracle.fit(X, np.full(189, 2.0), ntree=3, mtry=3)
+    assert (g.importance() == 0).all()
+
+
+def test_importance_vs_sklearn_tree():
+    # one unbootstrapped tree with m = p on tie-free fp32-exact data is scikit-learn's
+    # tree (test_sklearn_structure_advisory) as long as no two features tie on a node
+    # (depth-capped so every node keeps many rows); feature_importances_ must agree
+    sk = pytest.importorskip("sklearn.tree")
+    rnd = np.random.default_rng(5)
+    n = 400
+    X = np.stack([rnd.permutation(n) for _ in range(4)], 1).astype(np.float64)
+    y = X[:, 0] * 0.5 + np.sin(X[:, 2] / 7) * 20 + rnd.normal(size=n)
+    f = oracle.fit(X, y, ntree=1, mtry=4, bootstrap=False, max_depth=4)
+    reg = sk.DecisionTreeRegressor(max_features=None, random_state=0, max_depth=4).fit(X, y)
+    assert sorted(f.trees[0].feature[f.trees[0].feature >= 0].tolist()) == \
+        sorted(reg.tree_.feature[reg.tree_.feature >= 0].tolist())
+    np.testing.assert_allclose(f.importance(), reg.feature_importances_, rtol=1e-9, atol=1e-12)
+
+
 def test_sklearn_structure_advisory():
     sk = pytest.importorskip("sklearn.tree")
     rnd = np.random.default_rng(4)
