@@ -96,7 +96,39 @@ def allgather_forest_arrays(feature, left, value, thr_index, tree_off, group=Non
     return (torch.cat(feats), torch.cat(lefts), torch.cat(vals).view(torch.float64), torch.cat(tis), off)
 
 
+def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
+    """Concatenate per-rank row blocks [n_r, ...] of different lengths in rank order
+    (e.g. per-tree importance sums of tree shards) on every rank."""
+    rank, world = _world(group)
+    if world == 1:
+        return local
+    dev = local.device
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
+    alln = torch.empty((world,), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(alln, n, group=group)
+    sizes = alln.tolist()
+    m = max(sizes)
+    pad = torch.zeros((m,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+    pad[: local.shape[0]] = local
+    out = torch.empty((world * m,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    out = out.view((world, m) + tuple(local.shape[1:]))
+    return torch.cat([out[r, : sizes[r]] for r in range(world)])
+
+
 # -------------------------------------------------------------- drivers ----
+def importance_sharded(local_forest, group=None, device=None):
+    """Feature importance of a tree-sharded forest: all_gather of the per-tree split
+    decrease sums of every rank's shard, combined by rf_importance_dev (same vector as
+    a single-GPU fit of all trees, up to the order of fp64 sums)."""
+    from . import importance_dev
+    _, raw = local_forest.importance(raw=True)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    full = gather_rows(torch.as_tensor(raw, device=dev), group)
+    return importance_dev(full.contiguous())
+
+
+
 def fit_sharded(X, y, *, ntree, group=None, **kw):
     """Tree-sharded rf_fit: rank r grows trees shard(ntree, r, world); the forest is
     assembled on every rank (identical to a single-GPU fit of ntree trees, R15)."""

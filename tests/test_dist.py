@@ -108,3 +108,21 @@ def _assemble(rank, world):
 
 def test_allgather_forest_matches_full_forest():
     run_world(_assemble)
+
+
+def _gather_rows(rank, world):
+    # importance of a tree-sharded forest: per-tree raw rows of uneven shards, rank order
+    from paper_2001_07104_b200.dist import gather_rows, shard
+    X, y = datagen.paper_shaped(189, "V100", "time")
+    T = 7
+    full = oracle.fit(X, y, ntree=T, mtry=4, seed=3, target=1)
+    lo, hi = shard(T, rank, world)
+    part = oracle.fit(X, y, ntree=T, mtry=4, seed=3, target=1, tree_begin=lo, tree_end=hi)
+    got = gather_rows(torch.as_tensor(np.stack([t.imp_raw for t in part.trees])))
+    want = np.stack([t.imp_raw for t in full.trees])
+    assert np.array_equal(got.numpy(), want)
+    assert np.array_equal(oracle.importance(got.numpy()), full.importance())
+
+
+def test_gather_rows_importance_shards():
+    run_world(_gather_rows)
