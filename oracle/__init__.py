@@ -63,6 +63,7 @@ def lib():
         _lib.or_ln.restype = dbl
         _lib.or_quantize.argtypes = [P, u64, C.c_int, P, P, P]
         _lib.or_make_folds.argtypes = [P, u64, u32, u32, u64, u32, P]
+        _lib.or_make_folds_masked.argtypes = [P, u64, u32, u32, u64, u32, P, P]
         _lib.or_fit.argtypes = [P, u64, u32, P, u32, u32, i32, u32, u32, u32, u64,
                                 u32, u32, u64, P, P, P, P, P, P, P, P, P]
         _lib.or_predict.argtypes = [P, P, P, P, P, u32, u32, P, u64, u32, P]
@@ -270,3 +271,83 @@ def cv_grid(X, y, k, reps, ntrees, mtrys, fold_ids=None, min_samples_split=2, ma
     if st:
         raise OracleError(st)
     return (fm, pr) if want_pred else fm
+
+
+# ------------------------------------------------- nested CV / LOO (NEXT-2) ---
+NESTED_SEED_TAG = 0x4E45535445440000  # "NESTED\0\0": inner folds use seed ^ tag (R31)
+APE_EDGES = (10.0, 25.0, 50.0, 100.0)  # error buckets of the LOO analysis, percent
+
+
+def make_folds_masked(y, k, mask, seed, custom=False):
+    """Folds of a row subset per rep (mask [reps][n] != 0): the subset is split like
+    make_folds splits a dataset of those rows; other rows get -2 (R31)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    mk = np.ascontiguousarray(mask, dtype=np.uint8)
+    reps, n = mk.shape
+    out = np.zeros((reps, n), dtype=np.int32)
+    st = lib().or_make_folds_masked(_p(y), n, k, reps, seed, int(custom), _p(mk), _p(out))
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def nested_cv(X, y, k_outer, k_inner, iterations, ntrees, mtrys, custom=False, seed=0, **kw):
+    """Nested cross-validation (R31), followed step by step:
+    1. outer folds: make_folds(y, k_outer, iterations, seed, custom);
+    2. for every (iteration it, outer fold o) -- combo c = it*k_outer + o -- the inner
+       folds split the outer-training rows (outer fold id != o) with make_folds_masked
+       (rep c, seed ^ NESTED_SEED_TAG); the rest is excluded (-2);
+    3. inner grid CV on those fold sets (one cv_grid call, reps = combos);
+    4. per combo: score of grid point g = (sum of its inner fold MAPEs in fold order) / k_inner;
+       best = the lowest score, ties to the first grid point (mtry-major, then ntree);
+    5. outer grid CV on the outer folds; the combo's outer score = its fold MAPE at best.
+    Returns (best [it][k_outer] grid index, outer_mape [it][k_outer],
+             inner_score [it][k_outer][n_mtry][n_ntree])."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = y.shape[0]
+    nm, nt = len(mtrys), len(ntrees)
+    outer = make_folds(y, k_outer, iterations, seed, custom)
+    C = iterations * k_outer
+    mask = np.zeros((C, n), dtype=np.uint8)
+    for it in range(iterations):
+        for o in range(k_outer):
+            mask[it * k_outer + o] = outer[it] != o
+    inner = make_folds_masked(y, k_inner, mask, seed ^ NESTED_SEED_TAG, custom)
+    fm_in = cv_grid(X, y, k_inner, C, ntrees, mtrys, fold_ids=inner, seed=seed ^ NESTED_SEED_TAG, **kw)
+    score = np.zeros((C, nm, nt))
+    best = np.zeros(C, dtype=np.int32)
+    for c in range(C):
+        bs, bg = None, 0
+        for mi in range(nm):
+            for ti in range(nt):
+                s = 0.0
+                for f in range(k_inner):
+                    s += fm_in[mi, ti, c, f]
+                s = s / k_inner
+                score[c, mi, ti] = s
+                if bs is None or s < bs:
+                    bs, bg = s, mi * nt + ti
+        best[c] = bg
+    fm_out = cv_grid(X, y, k_outer, iterations, ntrees, mtrys, fold_ids=outer, seed=seed, **kw)
+    outer_mape = np.zeros(C)
+    for c in range(C):
+        it, o = divmod(c, k_outer)
+        mi, ti = divmod(int(best[c]), nt)
+        outer_mape[c] = fm_out[mi, ti, it, o]
+    return (best.reshape(iterations, k_outer), outer_mape.reshape(iterations, k_outer),
+            score.reshape(iterations, k_outer, nm, nt))
+
+
+def error_buckets(y, yhat):
+    """Counts of absolute percentage errors 100 |y - yhat| / y in [0,10), [10,25), [25,50),
+    [50,100), [100, inf) (the LOO analysis of P:741-754); NaN predictions are skipped."""
+    counts = [0, 0, 0, 0, 0]
+    for a, b in zip(np.asarray(y, dtype=np.float64), np.asarray(yhat, dtype=np.float64)):
+        if b != b:
+            continue
+        e = 100.0 * abs(a - b) / a
+        j = 0
+        while j < 4 and e >= APE_EDGES[j]:
+            j += 1
+        counts[j] += 1
+    return np.array(counts, dtype=np.int64)

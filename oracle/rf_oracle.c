@@ -238,6 +238,77 @@ int or_make_folds(const double *y, uint64_t n, uint32_t k, uint32_t reps, uint64
     return 0;
 }
 
+/* Folds of a row subset (nested CV, R31): for each rep, the rows
+   with mask[rep*n + i] != 0 are split exactly like or_make_folds splits a
+   dataset of those rows (Philox keys still indexed by the original row i,
+   stream (seed; rep, ...)); rows outside the subset get -2 (excluded).
+   Returns 0, 6 (a subset too small for k folds). */
+int or_make_folds_masked(const double *y, uint64_t n, uint32_t k, uint32_t reps, uint64_t seed,
+                         uint32_t custom, const uint8_t *mask, int32_t *fold_ids)
+{
+    uint32_t s0 = (uint32_t)seed, s1 = (uint32_t)(seed >> 32);
+    if (k < 2) return 6;
+    keyidx *ki = (keyidx *)malloc(sizeof(keyidx) * (n ? n : 1));
+    yidx *yi = (yidx *)malloc(sizeof(yidx) * (n ? n : 1));
+    int st = 0;
+    for (uint32_t rep = 0; rep < reps && !st; ++rep) {
+        int32_t *fid = fold_ids + (uint64_t)rep * n;
+        const uint8_t *mk = mask + (uint64_t)rep * n;
+        uint64_t na = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            fid[i] = -2;
+            if (mk[i]) ++na;
+        }
+        if ((!custom && (uint64_t)k > na) || (custom && (na < 5 || na - 5 < (uint64_t)k))) { st = 6; break; }
+        if (!custom) {
+            uint64_t m = 0;
+            for (uint64_t i = 0; i < n; ++i) {
+                if (!mk[i]) continue;
+                ki[m].key = or_draw(s0, s1, rep, 0u, TAG_FOLD, i);
+                ki[m].idx = i;
+                ++m;
+            }
+            qsort(ki, m, sizeof(keyidx), cmp_keyidx);
+            uint64_t pos = 0;
+            for (uint32_t f = 0; f < k; ++f) {
+                uint64_t size = na / k + ((uint64_t)f < na % k ? 1 : 0);
+                for (uint64_t j = 0; j < size; ++j) fid[ki[pos + j].idx] = (int32_t)f;
+                pos += size;
+            }
+        } else {
+            uint64_t m = 0;
+            for (uint64_t i = 0; i < n; ++i)
+                if (mk[i]) { yi[m].y = y[i]; yi[m].idx = i; ++m; }
+            qsort(yi, m, sizeof(yidx), cmp_ydesc);
+            int32_t *pin = (int32_t *)calloc(n ? n : 1, sizeof(int32_t));
+            for (int j = 0; j < 5; ++j) pin[yi[j].idx] = 1;
+            uint64_t deal = 0;
+            for (uint32_t s = 0; s < 3; ++s) {
+                uint64_t q = 0;
+                for (uint64_t i = 0; i < n; ++i) {
+                    if (!mk[i] || pin[i]) continue;
+                    double v = y[i];
+                    uint32_t sv = (v < 1000.0) ? 0u : (v < 100000.0 ? 1u : 2u);
+                    if (sv != s) continue;
+                    ki[q].key = or_draw(s0, s1, rep, s, TAG_STRATUM, i);
+                    ki[q].idx = i;
+                    ++q;
+                }
+                qsort(ki, q, sizeof(keyidx), cmp_keyidx);
+                for (uint64_t j = 0; j < q; ++j) {
+                    fid[ki[j].idx] = (int32_t)(deal % k);
+                    ++deal;
+                }
+            }
+            for (uint64_t i = 0; i < n; ++i) if (pin[i]) fid[i] = -1;
+            free(pin);
+        }
+    }
+    free(ki);
+    free(yi);
+    return st;
+}
+
 /* ------------------------------------------------------------------ */
 /* Dense ranks and histogram cuts (R10, R23)                 */
 /* ------------------------------------------------------------------ */
@@ -788,7 +859,8 @@ double or_mape(const double *y, const double *yhat, uint64_t m)
 }
 
 /* Grid cross-validation (R16-R19).
-   fold_ids: [reps][n] or NULL (plain folds from seed).
+   fold_ids: [reps][n] or NULL (plain folds from seed); -1 = always train,
+   -2 = excluded from the task (neither trains nor tests; nested CV, R31).
    ntrees evaluated as prefixes of max(ntrees).  Outputs:
    fold_mape [n_mtry][n_ntree][reps][k];  pred (optional) [n_mtry][n_ntree][reps][n]
    = prediction of each row by the forest of its test fold (raw units; rows with
@@ -859,7 +931,8 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
         const int32_t *fr = fid + (uint64_t)rep * n;
         uint64_t ntr = 0, nte = 0;
         for (uint64_t i = 0; i < n; ++i) {
-            if (fr[i] == (int32_t)fold) te[nte++] = i; else tr[ntr++] = i;
+            if (fr[i] == (int32_t)fold) te[nte++] = i;
+            else if (fr[i] != -2) tr[ntr++] = i; /* -2: excluded row (nested CV, R31) */
         }
         if (g.hist) setup_hist(&g, Xc, n, p, tr, ntr);
         for (uint32_t mi = 0; mi < n_mtry; ++mi) {

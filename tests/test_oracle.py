@@ -603,3 +603,95 @@ def test_sklearn_structure_advisory():
     pairs = set(zip(a.tolist(), b.tolist()))
     assert len(pairs) == len(set(a.tolist())) == len(set(b.tolist()))
     np.testing.assert_allclose([tr.predict_row(x) for x in X], reg.predict(X), rtol=1e-12)
+
+
+# ------------------------------------------- nested CV, LOO, buckets (NEXT-2) ---
+@pytest.mark.parametrize("custom", [False, True])
+def test_masked_folds_all_active_equals_plain(custom):
+    y = datagen.paper_shaped(189, "K20", "time")[1]
+    a = oracle.make_folds(y, 10, 4, seed=11, custom=custom)
+    b = oracle.make_folds_masked(y, 10, np.ones((4, 189), np.uint8), seed=11, custom=custom)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("custom", [False, True])
+def test_masked_folds_subset(custom):
+    y = datagen.paper_shaped(189, "P100", "time")[1]
+    rnd = np.random.default_rng(2)
+    mask = (rnd.random((6, 189)) < 0.7).astype(np.uint8)
+    f = oracle.make_folds_masked(y, 7, mask, seed=5, custom=custom)
+    for r in range(6):
+        act = mask[r] != 0
+        assert (f[r][~act] == -2).all() and (f[r][act] >= -1).all()
+        if custom:
+            top5 = np.argsort(-y[act], kind="stable")[:5]
+            assert set(np.nonzero(f[r] == -1)[0]) == set(np.nonzero(act)[0][top5])
+            sizes = np.bincount(f[r][f[r] >= 0], minlength=7)
+            assert sizes.max() - sizes.min() <= 1
+        else:
+            sizes = np.bincount(f[r][act], minlength=7)
+            na = act.sum()
+            assert sorted(sizes.tolist(), reverse=True) == [na // 7 + (i < na % 7) for i in range(7)]
+            assert np.array_equal(sizes, sorted(sizes, reverse=True))  # first n mod k folds larger
+
+
+def test_excluded_rows_equal_removed_rows():
+    # fold id -2 removes a row from the task: same fold MAPE as CV on the dataset without
+    # it (integer targets keep the quantisation grid exact across the two datasets)
+    X, y = datagen.tiny(60, 3, 7, distinct=12)
+    y = np.round(y * 10) + 3.0
+    f = oracle.make_folds(y, 5, 2, seed=4)
+    drop = np.zeros(60, bool)
+    drop[[3, 17, 40, 41]] = True
+    g = f.copy()
+    g[:, drop] = -2
+    a = oracle.cv_grid(X, y, 5, 2, [4, 9], [2, 3], fold_ids=g, seed=8)
+    b = oracle.cv_grid(X[~drop], y[~drop], 5, 2, [4, 9], [2, 3], fold_ids=f[:, ~drop], seed=8)
+    np.testing.assert_allclose(a, b, rtol=1e-15, atol=0)
+
+
+def test_nested_cv_single_point_is_plain_cv():
+    # one grid point: the inner loop selects it everywhere and the outer scores are the
+    # plain repeated k-fold CV of that point (SPEC S:379 example)
+    X, y = datagen.paper_shaped(189, "V100", "time")
+    best, outer, score = oracle.nested_cv(X, y, 5, 4, 2, [6], [3], custom=True, seed=9, target=1)
+    assert (best == 0).all() and score.shape == (2, 5, 1, 1)
+    f = oracle.make_folds(y, 5, 2, seed=9, custom=True)
+    plain = oracle.cv_grid(X, y, 5, 2, [6], [3], fold_ids=f, seed=9, target=1)
+    assert np.array_equal(outer, plain[0, 0])
+
+
+def test_nested_cv_selection_uses_only_outer_training_rows():
+    X, y = datagen.paper_shaped(168, "K20", "power")
+    best, outer, score = oracle.nested_cv(X, y, 4, 3, 1, [4, 8], [12, 3], seed=2)
+    assert outer.shape == (1, 4) and np.isfinite(outer).all()
+    for o in range(4):
+        s = score[0, o].reshape(-1)
+        assert best[0, o] == int(np.argmin(s))  # first minimum in grid order
+    # inner fold sets exclude the outer test fold
+    of = oracle.make_folds(y, 4, 1, seed=2)
+    mask = np.stack([of[0] != o for o in range(4)]).astype(np.uint8)
+    inner = oracle.make_folds_masked(y, 3, mask, seed=2 ^ oracle.NESTED_SEED_TAG)
+    for o in range(4):
+        assert (inner[o][of[0] == o] == -2).all() and (inner[o][of[0] != o] >= 0).all()
+
+
+def test_error_buckets():
+    assert oracle.error_buckets([2.0, 2.0], [2.0, 2.0]).tolist() == [2, 0, 0, 0, 0]
+    rnd = np.random.default_rng(4)
+    y = 10 ** rnd.uniform(0, 5, 500)
+    yh = y * np.exp(rnd.normal(0, 0.4, 500))
+    yh[7] = np.nan
+    ape = np.abs(y - yh) / y * 100
+    ape = ape[~np.isnan(ape)]
+    want = np.histogram(ape, bins=[0, 10, 25, 50, 100, np.inf])[0]
+    assert oracle.error_buckets(y, yh).tolist() == want.tolist()
+
+
+def test_loo_is_k_equals_n():
+    X, y = datagen.paper_shaped(40, "K20", "time")
+    fm, pred = oracle.cv_grid(X, y, 40, 1, [8], [4], target=1, seed=3, want_pred=True)
+    assert np.isfinite(pred).all() and fm.shape == (1, 1, 1, 40)
+    # one test row per fold: its fold MAPE is its own APE
+    f = oracle.make_folds(y, 40, 1, seed=3)
+    np.testing.assert_allclose(fm[0, 0, 0, f[0]], 100 * np.abs(y - pred[0, 0, 0]) / y, rtol=1e-14)
