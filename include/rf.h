@@ -136,6 +136,15 @@ RF_API rf_status rf_make_folds(const double* y, uint64_t n, uint32_t k, uint32_t
 RF_API rf_status rf_make_folds_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats,
                             uint64_t seed, uint32_t custom, int32_t* dfold_ids, void* stream);
 
+/* Folds of a row subset per repeat (nested CV, R31): rows with
+   dmask[rep*n + i] != 0 are split exactly as rf_make_folds splits a dataset
+   of those rows (Philox keys indexed by the original row); the others get
+   -2 (excluded: neither train nor test in the CV calls).  n <= 4096
+   (RF_E_UNSUPPORTED beyond).  Stream-ordered, no synchronisation. */
+RF_API rf_status rf_make_folds_masked_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats,
+                                          uint64_t seed, uint32_t custom, const uint8_t* dmask,
+                                          int32_t* dfold_ids, void* stream);
+
 /* rf_cross_validate_grid: repeated k-fold CV of every (mtry,
    ntree) grid point.  For each task (rep, fold) and each mtry,
    max(ntrees) trees are grown on the training rows (fold id != fold) and
@@ -162,6 +171,41 @@ RF_API rf_status rf_cross_validate_grid_dev(const double* dX, uint64_t n, uint32
 RF_API rf_status rf_cross_validate(const double* X, uint64_t n, uint32_t p, const double* y,
                             const rf_params* prm, uint32_t k, uint32_t repeats,
                             const int32_t* fold_ids, double* fold_mape);
+
+/* Nested cross-validation ("First the scores of each hyperparameter
+   combination are computed on all splits, then the best parameter combination
+   is used to compute scores on all splits again"; R31), as two
+   batched grid-CV launches:
+     outer folds  = rf_make_folds(y, k_outer, iterations, prm->seed, custom);
+     combo c = it*k_outer + o: inner folds split the rows outside outer fold o
+       (rf_make_folds_masked, rep c, seed prm->seed ^ 0x4E45535445440000);
+     inner grid CV over all combos (one call, tree keys from the inner seed);
+     best[c] = first grid point g = mi*n_ntree + ti with the lowest
+       (sum of its inner fold MAPEs in fold order) / k_inner;
+     outer grid CV on the outer folds; outer_mape[c] = its fold MAPE at best[c].
+   Outputs (host or device per twin): best int32 [iterations][k_outer],
+   outer_mape fp64 [iterations][k_outer], inner_score fp64
+   [iterations][k_outer][n_mtry][n_ntree] (or NULL).  prm->ntree/mtry are
+   ignored (the grid decides); tree/task ranges must be 0.  n <= 4096.
+   Errors: as rf_cross_validate_grid; RF_E_TOO_FEW if an outer-training set
+   cannot hold k_inner folds. */
+RF_API rf_status rf_nested_cv(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                              uint32_t k_outer, uint32_t k_inner, uint32_t iterations, uint32_t custom,
+                              const uint32_t* ntrees, uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry,
+                              int32_t* best, double* outer_mape, double* inner_score);
+RF_API rf_status rf_nested_cv_dev(const double* dX, uint64_t n, uint32_t p, const double* dy,
+                                  const rf_params* prm, uint32_t k_outer, uint32_t k_inner,
+                                  uint32_t iterations, uint32_t custom, const uint32_t* ntrees,
+                                  uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry, int32_t* dbest,
+                                  double* douter_mape, double* dinner_score, void* stream);
+
+/* LOO error buckets: counts[5] of the absolute percentage error
+   100 * (|y - yhat| / y) in [0,10), [10,25), [25,50), [50,100), [100,inf);
+   NaN predictions (rows without a prediction) are skipped.  Leave-one-out
+   itself is rf_cross_validate_grid with k = n. */
+RF_API rf_status rf_error_buckets(const double* y, const double* yhat, uint64_t n, uint64_t* counts);
+RF_API rf_status rf_error_buckets_dev(const double* dy, const double* dyhat, uint64_t n, uint64_t* dcounts,
+                                      void* stream);
 
 /* Tree-sharded CV (multi-GPU): per-row partial sums of
    leaf values over this rank's trees [tree_begin, tree_end) for each grid

@@ -345,7 +345,7 @@ def error_buckets(y, yhat):
     for a, b in zip(np.asarray(y, dtype=np.float64), np.asarray(yhat, dtype=np.float64)):
         if b != b:
             continue
-        e = 100.0 * abs(a - b) / a
+        e = 100.0 * (abs(a - b) / a)  # relative error first, as in Eq. 1
         j = 0
         while j < 4 and e >= APE_EDGES[j]:
             j += 1

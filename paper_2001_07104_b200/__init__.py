@@ -33,6 +33,7 @@ TARGET_IDENTITY, TARGET_LOG = 0, 1
 ABI_SYMBOLS = [
     "rf_params_default", "rf_fit", "rf_fit_dev", "rf_fit_debug", "rf_predict", "rf_predict_dev",
     "rf_predict_partial_dev", "rf_predict_finalize_dev", "rf_make_folds", "rf_make_folds_dev",
+    "rf_make_folds_masked_dev", "rf_nested_cv", "rf_nested_cv_dev", "rf_error_buckets", "rf_error_buckets_dev",
     "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
     "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
@@ -79,6 +80,11 @@ def lib():
             "rf_predict_finalize_dev": ([P, u64, u32, u32, P, P], C.c_int),
             "rf_make_folds": ([P, u64, u32, u32, u64, u32, P], C.c_int),
             "rf_make_folds_dev": ([P, u64, u32, u32, u64, u32, P, P], C.c_int),
+            "rf_make_folds_masked_dev": ([P, u64, u32, u32, u64, u32, P, P, P], C.c_int),
+            "rf_nested_cv": ([P, u64, u32, P, pp, u32, u32, u32, u32, P, u32, P, u32, P, P, P], C.c_int),
+            "rf_nested_cv_dev": ([P, u64, u32, P, pp, u32, u32, u32, u32, P, u32, P, u32, P, P, P, P], C.c_int),
+            "rf_error_buckets": ([P, P, u64, P], C.c_int),
+            "rf_error_buckets_dev": ([P, P, u64, P, P], C.c_int),
             "rf_cross_validate_grid": ([P, u64, u32, P, pp, u32, u32, P, P, u32, P, u32, P, P], C.c_int),
             "rf_cross_validate_grid_dev": ([P, u64, u32, P, pp, u32, u32, P, P, u32, P, u32, P, P, P],
                                            C.c_int),
@@ -283,6 +289,56 @@ def make_folds(y, k, repeats=1, seed=0, custom=False, out=None):
     out = np.zeros((repeats, y.shape[0]), np.int32)
     _check(lib().rf_make_folds(_ptr(y), y.shape[0], k, repeats, seed, int(custom), _ptr(out)))
     return out
+
+
+def make_folds_masked(y, k, mask, seed=0, custom=False, out=None):
+    """Device fold ids [reps, n] of the row subsets mask [reps, n] != 0 (others -2), R31."""
+    torch = _torch()
+    reps, n = mask.shape
+    out = torch.empty((reps, n), dtype=torch.int32, device=y.device) if out is None else out
+    _check(lib().rf_make_folds_masked_dev(_ptr(y), n, k, reps, seed, int(custom), _ptr(mask.to(torch.uint8)),
+                                          _ptr(out), _stream()))
+    return out
+
+
+def nested_cv(X, y, k_outer, k_inner, iterations, ntrees, mtrys, *, custom=False, min_samples_split=2,
+              max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0):
+    """Nested CV (rf_nested_cv, R31): (best [it, k_outer] grid index mi*n_ntree+ti,
+    outer_mape [it, k_outer], inner_score [it, k_outer, n_mtry, n_ntree])."""
+    prm = params(ntree=max(ntrees), mtry=0, min_samples_split=min_samples_split, max_depth=max_depth,
+                 bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device)
+    nt, mt = _u32(ntrees), _u32(mtrys)
+    if _is_torch(X):
+        torch = _torch()
+        n, p = X.shape
+        best = torch.empty((iterations, k_outer), dtype=torch.int32, device=X.device)
+        om = torch.empty((iterations, k_outer), dtype=torch.float64, device=X.device)
+        sc = torch.empty((iterations, k_outer, len(mt), len(nt)), dtype=torch.float64, device=X.device)
+        _check(lib().rf_nested_cv_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), k_outer, k_inner, iterations,
+                                      int(custom), _ptr(nt), len(nt), _ptr(mt), len(mt), _ptr(best), _ptr(om),
+                                      _ptr(sc), _stream()))
+        return best, om, sc
+    X, y = _host(X, np.float64), _host(y, np.float64)
+    n, p = X.shape
+    best = np.zeros((iterations, k_outer), np.int32)
+    om = np.zeros((iterations, k_outer), np.float64)
+    sc = np.zeros((iterations, k_outer, len(mt), len(nt)), np.float64)
+    _check(lib().rf_nested_cv(_ptr(X), n, p, _ptr(y), C.byref(prm), k_outer, k_inner, iterations, int(custom),
+                              _ptr(nt), len(nt), _ptr(mt), len(mt), _ptr(best), _ptr(om), _ptr(sc)))
+    return best, om, sc
+
+
+def error_buckets(y, yhat):
+    """LOO error buckets (rf_error_buckets): counts of APE in [0,10) [10,25) [25,50) [50,100) [100,inf) %."""
+    if _is_torch(y):
+        torch = _torch()
+        out = torch.zeros(5, dtype=torch.int64, device=y.device)
+        _check(lib().rf_error_buckets_dev(_ptr(y), _ptr(yhat), y.shape[0], _ptr(out), _stream()))
+        return out
+    y, yhat = _host(y, np.float64), _host(yhat, np.float64)
+    out = np.zeros(5, np.uint64)
+    _check(lib().rf_error_buckets(_ptr(y), _ptr(yhat), y.shape[0], _ptr(out)))
+    return out.astype(np.int64)
 
 
 def cross_validate_grid(X, y, k, repeats, ntrees, mtrys, fold_ids=None, *, want_pred=False,

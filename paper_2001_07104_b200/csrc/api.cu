@@ -667,6 +667,140 @@ rf_status rf_make_folds_dev(const double* dy, uint64_t n, uint32_t k, uint32_t r
   return RF_OK;
 }
 
+rf_status rf_make_folds_masked_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
+                                   uint32_t custom, const uint8_t* dmask, int32_t* dfold_ids, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (!dmask || !dfold_ids) return fail(RF_E_ARG, "NULL mask or output");
+  if (k < 2) return fail(RF_E_TOO_FEW, "k < 2");
+  if (n > 4096) return fail(RF_E_UNSUPPORTED, "masked folds limited to n <= 4096");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(rf::make_folds(dy, (int)n, (int)k, (int)repeats, seed, (int)custom, dfold_ids, nullptr, 0, s, dmask),
+     "masked folds");
+  return RF_OK;
+}
+
+namespace {
+rf_status nested_core(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                      uint32_t k_outer, uint32_t k_inner, uint32_t iterations, uint32_t custom,
+                      const uint32_t* ntrees, uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry,
+                      int32_t* dbest, double* douter, double* dscore, cudaStream_t s) {
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  if (iterations == 0) return fail(RF_E_ARG, "iterations must be >= 1");
+  if (n > 4096) return fail(RF_E_UNSUPPORTED, "nested CV limited to n <= 4096 (masked folds)");
+  if (prm->tree_begin || prm->tree_end || prm->task_begin || prm->task_end)
+    return fail(RF_E_ARG, "nested CV runs whole forests and all tasks");
+  const uint64_t pin = custom ? 5 : 0;
+  if (k_outer < 2 || k_inner < 2 || n < pin + k_outer) return fail(RF_E_TOO_FEW, "too few rows for the folds");
+  // the smallest outer-training set: n - (largest outer fold)
+  const uint64_t big = (n - pin + k_outer - 1) / k_outer;
+  if (n - big < pin + k_inner) return fail(RF_E_TOO_FEW, "too few outer-training rows for k_inner folds");
+  const int C = (int)(iterations * k_outer);
+  const uint64_t seed_in = prm->seed ^ 0x4E45535445440000ull;  // R31
+  Scratch sc(s);
+  int32_t *outer, *inner;
+  uint8_t* mask;
+  double *fm_in, *fm_out;
+  CK(sc.alloc(&outer, (size_t)iterations * n), "alloc");
+  CK(sc.alloc(&mask, (size_t)C * n), "alloc");
+  CK(sc.alloc(&inner, (size_t)C * n), "alloc");
+  CK(sc.alloc(&fm_in, (size_t)n_mtry * n_ntree * C * k_inner), "alloc");
+  CK(sc.alloc(&fm_out, (size_t)n_mtry * n_ntree * iterations * k_outer), "alloc");
+  CK(rf::make_folds(dy, (int)n, (int)k_outer, (int)iterations, prm->seed, (int)custom, outer, nullptr, 0, s),
+     "outer folds");
+  CK(rf::nested_mask(outer, (int)n, (int)k_outer, C, mask, s), "mask");
+  CK(rf::make_folds(dy, (int)n, (int)k_inner, C, seed_in, (int)custom, inner, nullptr, 0, s, mask),
+     "inner folds");
+  rf_params pin_prm = *prm;
+  pin_prm.seed = seed_in;
+  rf_status st = cv_core(dX, n, p, dy, &pin_prm, k_inner, (uint32_t)C, inner, ntrees, n_ntree, mtrys, n_mtry,
+                         fm_in, nullptr, nullptr, s);
+  if (st) return st;
+  CK(rf::nested_select(fm_in, (int)n_mtry, (int)n_ntree, C, (int)k_inner, dbest, dscore, s), "select");
+  st = cv_core(dX, n, p, dy, prm, k_outer, iterations, outer, ntrees, n_ntree, mtrys, n_mtry, fm_out, nullptr,
+               nullptr, s);
+  if (st) return st;
+  CK(rf::nested_pick(fm_out, dbest, (int)n_ntree, C, (int)k_outer, (int)iterations, douter, s), "pick");
+  return RF_OK;
+}
+}  // namespace
+
+rf_status rf_nested_cv_dev(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                           uint32_t k_outer, uint32_t k_inner, uint32_t iterations, uint32_t custom,
+                           const uint32_t* ntrees, uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry,
+                           int32_t* dbest, double* douter_mape, double* dinner_score, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!dbest || !douter_mape) return fail(RF_E_ARG, "NULL output");
+  try {
+    return nested_core(dX, n, p, dy, prm, k_outer, k_inner, iterations, custom, ntrees, n_ntree, mtrys, n_mtry,
+                       dbest, douter_mape, dinner_score, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+rf_status rf_nested_cv(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                       uint32_t k_outer, uint32_t k_inner, uint32_t iterations, uint32_t custom,
+                       const uint32_t* ntrees, uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry,
+                       int32_t* best, double* outer_mape, double* inner_score) {
+  if (rf_status st = check_device()) return st;
+  if (!prm || !X || !y || !best || !outer_mape) return fail(RF_E_ARG, "NULL argument");
+  CK(cudaSetDevice(prm->device), "set device");
+  cudaStream_t s = host_stream(prm->device);
+  try {
+    Scratch sc(s);
+    double *dX, *dy, *dout, *dsc = nullptr;
+    int32_t* db;
+    const size_t C = (size_t)iterations * k_outer;
+    CK(sc.alloc(&dX, n * p), "alloc");
+    CK(sc.alloc(&dy, n), "alloc");
+    CK(sc.alloc(&db, C), "alloc");
+    CK(sc.alloc(&dout, C), "alloc");
+    if (inner_score) CK(sc.alloc(&dsc, C * n_mtry * n_ntree), "alloc");
+    CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+    CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+    rf_status st = nested_core(dX, n, p, dy, prm, k_outer, k_inner, iterations, custom, ntrees, n_ntree, mtrys,
+                               n_mtry, db, dout, dsc, s);
+    if (st) return st;
+    CK(cudaMemcpyAsync(best, db, C * 4, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaMemcpyAsync(outer_mape, dout, C * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    if (inner_score) CK(cudaMemcpyAsync(inner_score, dsc, C * n_mtry * n_ntree * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "sync");
+    return RF_OK;
+  } catch (...) {
+    return fail(RF_E_CUDA, "internal exception");
+  }
+}
+
+rf_status rf_error_buckets_dev(const double* dy, const double* dyhat, uint64_t n, uint64_t* dcounts, void* stream) {
+  if (rf_status st = check_device()) return st;
+  if (!dcounts || (n && (!dy || !dyhat))) return fail(RF_E_ARG, "NULL argument");
+  CK(rf::ape_buckets(dy, dyhat, (int64_t)n, reinterpret_cast<unsigned long long*>(dcounts),
+                     static_cast<cudaStream_t>(stream)), "buckets");
+  return RF_OK;
+}
+
+rf_status rf_error_buckets(const double* y, const double* yhat, uint64_t n, uint64_t* counts) {
+  if (rf_status st = check_device()) return st;
+  if (!counts || (n && (!y || !yhat))) return fail(RF_E_ARG, "NULL argument");
+  cudaStream_t s = host_stream(0);
+  Scratch sc(s);
+  double *dy, *dh;
+  unsigned long long* dc;
+  CK(sc.alloc(&dy, std::max<uint64_t>(n, 1)), "alloc");
+  CK(sc.alloc(&dh, std::max<uint64_t>(n, 1)), "alloc");
+  CK(sc.alloc(&dc, 5), "alloc");
+  if (n) {
+    CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+    CK(cudaMemcpyAsync(dh, yhat, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+  }
+  CK(rf::ape_buckets(dy, dh, (int64_t)n, dc, s), "buckets");
+  CK(cudaMemcpyAsync(counts, dc, 5 * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
 rf_status rf_make_folds(const double* y, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
                         uint32_t custom, int32_t* fold_ids) {
   if (rf_status st = check_device()) return st;

@@ -6,6 +6,7 @@
 // The paper's custom split pins the 5 largest targets to training and deals
 // the short / medium / long strata round-robin in Philox order.
 // Scoring: MAPE, Eq. 1, in percent, on raw targets.
+#include <algorithm>
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include "common.cuh"
 #include "host_util.cuh"
@@ -22,21 +23,34 @@ __device__ __forceinline__ int fold_of_pos(int pos, int n, int k) {
   return pos < big ? pos / (q + 1) : r + (pos - big) / q;
 }
 
-__global__ void k_folds_plain_small(int n, int k, uint64_t seed, int32_t* fold) {
+// mask (nullable) [reps][n]: only rows with mask != 0 are split (nested CV, R31); the
+// others get -2.  Keys stay indexed by the original row.
+__global__ void k_folds_plain_small(int n, int k, uint64_t seed, const uint8_t* __restrict__ mask,
+                                    int32_t* fold) {
   extern __shared__ unsigned long long key[];
+  uint8_t* act = reinterpret_cast<uint8_t*>(key + n);
+  __shared__ int nact;
   const int rep = blockIdx.x;
   const uint32_t s0 = (uint32_t)seed, s1 = (uint32_t)(seed >> 32);
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    key[i] = draw64(s0, s1, (uint32_t)rep, 0u, kTagFold, (uint64_t)i);
+  if (threadIdx.x == 0) nact = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint8_t a = mask ? (mask[(size_t)rep * n + i] != 0) : 1;
+    act[i] = a;
+    key[i] = draw64(s0, s1, (uint32_t)rep, 0u, kTagFold, (uint64_t)i);
+    if (a) atomicAdd(&nact, 1);
+  }
+  __syncthreads();
+  const int na = nact;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (!act[i]) { fold[(size_t)rep * n + i] = -2; continue; }
     const unsigned long long ki = key[i];
     int pos = 0;
     for (int j = 0; j < n; ++j) {
       const unsigned long long kj = key[j];
-      pos += (kj < ki) | ((kj == ki) & (j < i));
+      pos += act[j] & ((kj < ki) | ((kj == ki) & (j < i)));
     }
-    fold[(size_t)rep * n + i] = fold_of_pos(pos, n, k);
+    fold[(size_t)rep * n + i] = fold_of_pos(pos, na, k);
   }
 }
 
@@ -45,20 +59,25 @@ __device__ __forceinline__ int stratum_of(double y) {
 }
 
 __global__ void k_folds_custom_small(const double* __restrict__ y, int n, int k, uint64_t seed,
-                                     int32_t* fold) {
+                                     const uint8_t* __restrict__ mask, int32_t* fold) {
   extern __shared__ unsigned long long key[];
   double* ys = reinterpret_cast<double*>(key + n);
-  uint8_t* st = reinterpret_cast<uint8_t*>(ys + n);  // stratum, 3 = pinned
+  uint8_t* st = reinterpret_cast<uint8_t*>(ys + n);  // stratum, 3 = pinned, 4 = excluded
+  uint8_t* act = st + n;
   __shared__ int cnt[3];
   const int rep = blockIdx.x;
   const uint32_t s0 = (uint32_t)seed, s1 = (uint32_t)(seed >> 32);
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ys[i] = y[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    ys[i] = y[i];
+    act[i] = mask ? (mask[(size_t)rep * n + i] != 0) : 1;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (!act[i]) { st[i] = 4; continue; }
     const double yi = ys[i];
     int r = 0;
-    for (int j = 0; j < n; ++j) r += (ys[j] > yi) | ((ys[j] == yi) & (j < i));
+    for (int j = 0; j < n; ++j) r += act[j] & ((ys[j] > yi) | ((ys[j] == yi) & (j < i)));
     int s = (r < 5) ? 3 : stratum_of(yi);
     st[i] = (uint8_t)s;
     if (s < 3) {
@@ -69,6 +88,7 @@ __global__ void k_folds_custom_small(const double* __restrict__ y, int n, int k,
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int s = st[i];
+    if (s == 4) { fold[(size_t)rep * n + i] = -2; continue; }
     if (s == 3) { fold[(size_t)rep * n + i] = -1; continue; }
     const unsigned long long ki = key[i];
     int q = 0;
@@ -125,7 +145,8 @@ __global__ void k_tasks(const int32_t* __restrict__ fold, int n, int k, int task
     const int i = base + threadIdx.x;
     const bool valid = i < n;
     const bool test = valid && fr && fr[i] == fd;
-    const bool train = valid && !test;
+    const bool train = valid && !test && !(fr && fr[i] == -2);  // -2: excluded row (nested CV, R31)
+    if (valid && !train && !test) L[i] = -1;
     const unsigned btr = __ballot_sync(0xffffffffu, train), bte = __ballot_sync(0xffffffffu, test);
     if (lane == 0) { wtr[warp] = __popc(btr); wte[warp] = __popc(bte); }
     __syncthreads();
@@ -299,23 +320,24 @@ size_t make_folds_ws_bytes(int n, int reps, int custom) {
 }
 
 cudaError_t make_folds(const double* dy, int n, int k, int reps, uint64_t seed, int custom,
-                       int32_t* dfold, void* ws, size_t ws_bytes, cudaStream_t s) {
+                       int32_t* dfold, void* ws, size_t ws_bytes, cudaStream_t s, const uint8_t* dmask) {
   if (reps <= 0) return cudaSuccess;
   if (custom) {
     if (n > kFoldSmallMax) return cudaErrorNotSupported;
-    size_t smem = (size_t)n * 17;
+    size_t smem = (size_t)n * 18;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_folds_custom_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_folds_custom_small<<<reps, 256, smem, s>>>(dy, n, k, seed, dfold);
+    k_folds_custom_small<<<reps, 256, smem, s>>>(dy, n, k, seed, dmask, dfold);
     note_launch();
     return cudaGetLastError();
   }
   if (n <= kFoldSmallMax) {
-    size_t smem = (size_t)n * 8;
-    k_folds_plain_small<<<reps, 256, smem, s>>>(n, k, seed, dfold);
+    size_t smem = (size_t)n * 9;
+    k_folds_plain_small<<<reps, 256, smem, s>>>(n, k, seed, dmask, dfold);
     note_launch();
     return cudaGetLastError();
   }
+  if (dmask) return cudaErrorNotSupported;  // masked folds: n <= 4096 (nested CV)
   const size_t total = (size_t)n * reps;
   char* w = static_cast<char*>(ws);
   unsigned long long* kin = reinterpret_cast<unsigned long long*>(w);
@@ -370,6 +392,100 @@ cudaError_t finalize_cv(const double* reduced, const double* y, const int32_t* f
   a.fold_mape = fold_mape; a.pred = pred;
   const int warps = n_mtry * n_ntree * reps * k;
   k_finalize<<<(warps * 32 + 127) / 128, 128, 0, s>>>(a);
+  note_launch();
+  return cudaGetLastError();
+}
+
+
+
+// ----------------------------------------------------- nested CV (R31) ----
+namespace {
+
+// mask[c][i] = (outer fold of row i in iteration it) != o, c = it * k_outer + o
+__global__ void k_nested_mask(const int32_t* __restrict__ outer, int n, int k_outer, int C, uint8_t* mask) {
+  const size_t total = (size_t)C * n;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(q / n), i = (int)(q - (size_t)c * n);
+    const int it = c / k_outer, o = c - it * k_outer;
+    mask[q] = outer[(size_t)it * n + i] != o;
+  }
+}
+
+// thread per combo: score of every grid point = (sum of its inner fold MAPEs in fold
+// order) / k_inner; best = first minimum in grid order (mtry-major, then ntree)
+__global__ void k_nested_select(const double* __restrict__ fm_in, int nm, int nt, int C, int k_in,
+                                int32_t* best, double* score) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double bs = 0.0;
+  int bg = -1;
+  for (int mi = 0; mi < nm; ++mi)
+    for (int ti = 0; ti < nt; ++ti) {
+      const double* f = fm_in + (((size_t)mi * nt + ti) * C + c) * k_in;
+      double s = 0.0;
+      for (int j = 0; j < k_in; ++j) s = __dadd_rn(s, f[j]);
+      s = __ddiv_rn(s, (double)k_in);
+      if (score) score[((size_t)c * nm + mi) * nt + ti] = s;
+      if (bg < 0 || s < bs) { bs = s; bg = mi * nt + ti; }
+    }
+  best[c] = bg;
+}
+
+// thread per combo: the outer fold's MAPE at the selected grid point
+__global__ void k_nested_pick(const double* __restrict__ fm_out, const int32_t* __restrict__ best, int nt,
+                              int C, int k_out, int iters, double* outer_mape) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int g = best[c], mi = g / nt, ti = g - mi * nt;
+  const int it = c / k_out, o = c - it * k_out;
+  outer_mape[c] = fm_out[(((size_t)mi * nt + ti) * iters + it) * k_out + o];
+}
+
+// APE buckets [0,10) [10,25) [25,50) [50,100) [100,inf) percent; NaN skipped
+__global__ void k_ape_buckets(const double* __restrict__ y, const double* __restrict__ yhat, int64_t n,
+                              unsigned long long* counts) {
+  __shared__ unsigned int c[5];
+  if (threadIdx.x < 5) c[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double b = yhat[i];
+    if (b != b) continue;
+    const double e = __dmul_rn(100.0, __ddiv_rn(fabs(__dsub_rn(y[i], b)), y[i]));
+    const int j = (e < 10.0) ? 0 : (e < 25.0) ? 1 : (e < 50.0) ? 2 : (e < 100.0) ? 3 : 4;
+    atomicAdd(&c[j], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 && c[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)c[threadIdx.x]);
+}
+
+}  // namespace
+
+cudaError_t nested_mask(const int32_t* outer, int n, int k_outer, int C, uint8_t* mask, cudaStream_t s) {
+  const size_t total = (size_t)C * n;
+  k_nested_mask<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(outer, n, k_outer, C, mask);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t nested_select(const double* fm_in, int nm, int nt, int C, int k_in, int32_t* best, double* score,
+                          cudaStream_t s) {
+  k_nested_select<<<(C + 127) / 128, 128, 0, s>>>(fm_in, nm, nt, C, k_in, best, score);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t nested_pick(const double* fm_out, const int32_t* best, int nt, int C, int k_out, int iters,
+                        double* outer_mape, cudaStream_t s) {
+  k_nested_pick<<<(C + 127) / 128, 128, 0, s>>>(fm_out, best, nt, C, k_out, iters, outer_mape);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t ape_buckets(const double* y, const double* yhat, int64_t n, unsigned long long* counts, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, 5 * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  if (n <= 0) return cudaSuccess;
+  k_ape_buckets<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, s>>>(y, yhat, n, counts);
   note_launch();
   return cudaGetLastError();
 }

@@ -6,9 +6,11 @@
 
 namespace rf {
 
-// fold ids [reps][n]; custom = paper's time split (R17)
+// fold ids [reps][n]; custom = paper's time split (R17); dmask (nullable,
+// [reps][n], n <= 4096): split only the rows with mask != 0, the others get -2 (R31)
 cudaError_t make_folds(const double* dy, int n, int k, int reps, uint64_t seed, int custom,
-                       int32_t* dfold, void* ws, size_t ws_bytes, cudaStream_t s);
+                       int32_t* dfold, void* ws, size_t ws_bytes, cudaStream_t s,
+                       const uint8_t* dmask = nullptr);
 size_t make_folds_ws_bytes(int n, int reps, int custom);
 
 struct TaskData {
@@ -50,5 +52,15 @@ cudaError_t score_cv(const ScoreArgs& a, cudaStream_t s);
 cudaError_t finalize_cv(const double* reduced, const double* y, const int32_t* fold, int n, int k,
                         int reps, int n_mtry, int n_ntree, const int* ntrees, int target,
                         double* fold_mape, double* pred, cudaStream_t s);
+
+// nested CV (R31): mask[c][i] = outer[it][i] != o (c = it*k_outer + o); per combo the
+// first grid point with the lowest mean inner MAPE; the outer MAPE at that point
+cudaError_t nested_mask(const int32_t* outer, int n, int k_outer, int C, uint8_t* mask, cudaStream_t s);
+cudaError_t nested_select(const double* fm_in, int nm, int nt, int C, int k_in, int32_t* best, double* score,
+                          cudaStream_t s);
+cudaError_t nested_pick(const double* fm_out, const int32_t* best, int nt, int C, int k_out, int iters,
+                        double* outer_mape, cudaStream_t s);
+// LOO error buckets: counts[5] of APE in [0,10) [10,25) [25,50) [50,100) [100,inf) %
+cudaError_t ape_buckets(const double* y, const double* yhat, int64_t n, unsigned long long* counts, cudaStream_t s);
 
 }  // namespace rf

@@ -427,6 +427,74 @@ def test_importance_imported_forest_unsupported():
     assert err.value.code == rfg.E_UNSUPPORTED
 
 
+# ----------------------------------------- nested CV, LOO, buckets (NEXT-2) ---
+@pytest.mark.parametrize("custom", [False, True])
+def test_masked_folds_bit_exact(custom):
+    y = datagen.paper_shaped(189, "K20", "time")[1]
+    rnd = np.random.default_rng(8)
+    mask = (rnd.random((12, 189)) < 0.8).astype(np.uint8)
+    want = oracle.make_folds_masked(y, 6, mask, seed=13, custom=custom)
+    got = rfg.make_folds_masked(_cuda(y), 6, _cuda(mask, torch.uint8), seed=13, custom=custom).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_cv_excluded_rows_parity():
+    X, y = datagen.paper_shaped(189, "P100", "time")
+    f = oracle.make_folds(y, 5, 3, seed=6, custom=True)
+    f[:, ::7] = -2
+    fm_o, pr_o = oracle.cv_grid(X, y, 5, 3, [8, 16], [12, 3], fold_ids=f, target=1, seed=6, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 5, 3, [8, 16], [12, 3], fold_ids=f, target=1, seed=6, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+    assert np.isnan(pr_g[:, :, :, ::7]).all()
+
+
+@pytest.mark.parametrize("custom,split_mode", [(True, 0), (False, 0), (True, 2)])
+def test_nested_cv_parity(custom, split_mode):
+    """Inner scores and outer fold MAPEs <= 1e-9 relative; the selected grid point equal
+    wherever the oracle's best beats the runner-up by more than 1e-8 relative (else both
+    tied candidates are valid and the outer MAPE must be that candidate's)."""
+    X, y = datagen.paper_shaped(189, "GTX1650", "time")
+    kw = dict(custom=custom, seed=17, target=1, split_mode=split_mode,
+              bootstrap=split_mode != 2)
+    b_o, om_o, sc_o = oracle.nested_cv(X, y, 5, 4, 3, [8, 24], [12, 3], **kw)
+    b_g, om_g, sc_g = rfg.nested_cv(X, y, 5, 4, 3, [8, 24], [12, 3], **kw)
+    np.testing.assert_allclose(sc_g, sc_o, rtol=RTOL, atol=0)
+    flat = sc_o.reshape(3, 5, -1)
+    for it in range(3):
+        for o in range(5):
+            s = np.sort(flat[it, o])
+            if s[1] - s[0] > 1e-8 * s[0]:
+                assert b_g[it, o] == b_o[it, o]
+            else:
+                assert abs(flat[it, o, b_g[it, o]] - s[0]) <= 1e-8 * s[0]
+    f = oracle.make_folds(y, 5, 3, seed=17, custom=custom)
+    fm = oracle.cv_grid(X, y, 5, 3, [8, 24], [12, 3], fold_ids=f, seed=17, target=1, split_mode=split_mode,
+                        bootstrap=split_mode != 2)
+    for it in range(3):
+        for o in range(5):
+            mi, ti = divmod(int(b_g[it, o]), 2)
+            np.testing.assert_allclose(om_g[it, o], fm[mi, ti, it, o], rtol=RTOL)
+    # device twin
+    bd, omd, _ = rfg.nested_cv(_cuda(X), _cuda(y), 5, 4, 3, [8, 24], [12, 3], **kw)
+    assert np.array_equal(bd.cpu().numpy(), b_g) and np.array_equal(omd.cpu().numpy(), om_g)
+
+
+def test_loo_and_error_buckets_parity():
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    fm_o, pr_o = oracle.cv_grid(X, y, 189, 1, [64], [12], target=1, seed=2, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 189, 1, [64], [12], target=1, seed=2, want_pred=True)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    want = oracle.error_buckets(y, pr_o[0, 0, 0])
+    assert rfg.error_buckets(y, pr_g[0, 0, 0]).tolist() == want.tolist()
+    assert rfg.error_buckets(_cuda(y), _cuda(pr_g[0, 0, 0])).cpu().numpy().tolist() == want.tolist()
+    # with ties at the bucket edges: y = 100, yhat on the edges
+    ye = np.full(6, 100.0)
+    yh = np.array([90.0, 110.0, 75.0, 150.0, 200.0, np.nan])
+    assert rfg.error_buckets(ye, yh).tolist() == oracle.error_buckets(ye, yh).tolist() == [0, 2, 1, 1, 1]
+
+
 # -------------------------------------------------------------- errors ---
 def test_errors():
     X, y = datagen.tiny(20, 3, 1)
