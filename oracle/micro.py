@@ -148,8 +148,32 @@ def extra_threshold(key, heap, j, lo, hi):
     return thr if thr < hi else lo
 
 
-def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None, extra=False):
-    """Depth-first recursive growth; returns the root Node."""
+def wmedian(rows, w, tq):
+    """Weighted median (scikit-learn's rule, R32): values ascending, k = first
+    with cumulative weight >= W/2; exactly W/2 -> mean of t_k and the next value."""
+    srt = sorted(rows, key=lambda r: (tq[r], r))
+    W = sum(w[r] for r in srt)
+    cum = 0
+    for i, r in enumerate(srt):
+        cum += w[r]
+        if 2 * cum >= W:
+            if 2 * cum == W and i + 1 < len(srt):
+                return Fraction(tq[r] + tq[srt[i + 1]], 2)
+            return Fraction(tq[r])
+    return Fraction(0)
+
+
+def sad(rows, w, tq):
+    """Sum of weighted absolute deviations from the weighted median (MAE impurity x W)."""
+    if not rows:
+        return Fraction(0)
+    m = wmedian(rows, w, tq)
+    return sum(w[r] * abs(tq[r] - m) for r in rows)
+
+
+def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None, extra=False, mae=False):
+    """Depth-first recursive growth; returns the root Node.  mae: MAE criterion (R32) --
+    cost = SAD_L + SAD_R minimised (candidates as for MSE), leaves = weighted medians."""
     n, p = len(X), len(X[0])
     gvals = [sorted(set(X[i][f] for i in range(n))) for f in range(p)]
 
@@ -164,7 +188,9 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
             len(set(tq[r] for r in rows)) == 1
         cands = []
         if not leaf:
-            parent_sse = sse(rows, w, tq)
+            parent_sse = sse(rows, w, tq) if not mae else sad(rows, w, tq)
+            imp_of = (lambda L, R: sse(L, w, tq) + sse(R, w, tq)) if not mae else \
+                (lambda L, R: sad(L, w, tq) + sad(R, w, tq))
             for j, f in enumerate(draw_features(key, heap, p, mtry)):
                 if extra:
                     vals = [X[r][f] for r in rows]
@@ -177,9 +203,9 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
                     WL = sum(w[r] for r in L)
                     SL = sum(w[r] * tq[r] for r in L)
                     a = max(X[r][f] for r in L)
-                    red = parent_sse - sse(L, w, tq) - sse(R, w, tq)
-                    cands.append((canonical_gain(WL, SL, nd.W - WL, nd.S - SL), f,
-                                  gvals[f].index(a), thr, red, set(L), j))
+                    red = parent_sse - imp_of(L, R)
+                    score = canonical_gain(WL, SL, nd.W - WL, nd.S - SL) if not mae else -imp_of(L, R)
+                    cands.append((score, f, gvals[f].index(a), thr, red, set(L), j))
                 elif hist_cuts_per_f is None:
                     srt = sorted(rows, key=lambda r: (X[r][f], r))
                     for i in range(len(srt) - 1):
@@ -189,12 +215,12 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
                         L, R = srt[:i + 1], srt[i + 1:]
                         WL = sum(w[r] for r in L)
                         SL = sum(w[r] * tq[r] for r in L)
-                        red = parent_sse - sse(L, w, tq) - sse(R, w, tq)
+                        red = parent_sse - imp_of(L, R)
                         thr = a / 2.0 + b / 2.0
                         if thr == b:
                             thr = a
-                        cands.append((canonical_gain(WL, SL, nd.W - WL, nd.S - SL), f,
-                                      gvals[f].index(a), thr, red, set(L), j))
+                        score = canonical_gain(WL, SL, nd.W - WL, nd.S - SL) if not mae else -imp_of(L, R)
+                        cands.append((score, f, gvals[f].index(a), thr, red, set(L), j))
                 else:
                     cuts = hist_cuts_per_f[f]
                     for ci, c in enumerate(cuts):
@@ -212,8 +238,8 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
         if leaf:
             nd.feature = -1
             nd.thr_index, nd.thr_value = 0, 0.0
-            nd.value = float(Fraction(nd.S, nd.W) * Fraction(2) ** (-F)) if F >= 0 else \
-                float(Fraction(nd.S, nd.W) / Fraction(2) ** F)
+            v = wmedian(rows, w, tq) if mae else Fraction(nd.S, nd.W)  # R32 / R13
+            nd.value = float(v * Fraction(2) ** (-F)) if F >= 0 else float(v / Fraction(2) ** F)
             return nd
         # tie-break (R9): first drawn feature (slot j), then lowest threshold rank
         best = min(cands, key=lambda c: (-c[0], c[6], c[2]))
@@ -252,7 +278,7 @@ def to_bfs(root):
 
 
 def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=-1, hist=False,
-             task=0, train_rows=None, extra=False):
+             task=0, train_rows=None, extra=False, mae=False):
     """Tree t of `task` over train_rows (default all rows).  extra=True grows an
     Extremely Randomized tree (split_mode 2)."""
     X = [[(0.0 if v == 0.0 else float(v)) for v in row] for row in X]
@@ -264,7 +290,7 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     cuts = None
     if hist:
         cuts = [hist_cuts([X[r][f] for r in tr]) for f in range(len(X[0]))]
-    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra)
+    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra, mae)
     out = to_bfs(root)
     # MDI (NEXT-3): per feature, the exact SSE reductions of its splits (the definition
     # W imp(node) - WL imp(L) - WR imp(R), two-pass sums) in target units (x 2^-2F)
@@ -272,7 +298,8 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     for nd in out["nodes"]:
         if nd.children is not None:
             raw[nd.feature] += nd.gain_exact_chosen
-    out["imp_raw"] = [float(v * Fraction(2) ** (-2 * F)) for v in raw]
+    scale = Fraction(2) ** (-F if mae else -2 * F)  # SAD is linear in t, SSE quadratic
+    out["imp_raw"] = [float(v * scale) for v in raw]
     return out, F
 
 

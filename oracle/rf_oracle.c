@@ -434,6 +434,9 @@ typedef struct {
     int hist;
     /* ExtraTrees mode (split_mode 2): one random threshold per drawn feature (R29) */
     int extra;
+    /* MAE criterion (R32): splits minimise the summed absolute deviations from the
+       children's weighted medians; leaves hold the weighted median */
+    int mae;
     double **cuts;
     uint32_t *ncuts;
     uint16_t *bins; /* [row*p + f] */
@@ -450,6 +453,61 @@ static double gain(int64_t WL, int64_t SL, int64_t WR, int64_t SR)
     double b = dSR * dSR;
     b = b / dWR;
     return a + b;
+}
+
+/* ---- MAE criterion (T4/T5 P:858-861; R32) ---- */
+typedef struct { int64_t t; uint64_t row; } trow;
+
+static int cmp_trow(const void *a, const void *b)
+{
+    const trow *u = (const trow *)a, *v = (const trow *)b;
+    if (u->t < v->t) return -1;
+    if (u->t > v->t) return 1;
+    if (u->row < v->row) return -1;
+    if (u->row > v->row) return 1;
+    return 0;
+}
+
+/* 2 x the weighted median of t_q over rows (scikit-learn's rule): values in
+   ascending order, k = the first with 2 cum_k >= W; if 2 cum_k == W the median
+   is (t_k + t_k+1) / 2, else t_k.  Doubling keeps it an exact integer. */
+static int64_t median2(const uint64_t *rows, uint64_t m, const uint32_t *w, const int64_t *tq, trow *buf)
+{
+    int64_t W = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        buf[i].t = tq[rows[i]];
+        buf[i].row = rows[i];
+        W += (int64_t)w[rows[i]];
+    }
+    qsort(buf, m, sizeof(trow), cmp_trow);
+    int64_t cum = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        cum += (int64_t)w[buf[i].row];
+        if (2 * cum >= W) {
+            if (2 * cum == W && i + 1 < m) return buf[i].t + buf[i + 1].t;
+            return 2 * buf[i].t;
+        }
+    }
+    return 0;
+}
+
+/* 2 x the sum of weighted absolute deviations from the median: sum w |2 t - m2| (exact) */
+static unsigned __int128 sad2(const uint64_t *rows, uint64_t m, const uint32_t *w, const int64_t *tq,
+                              int64_t m2)
+{
+    unsigned __int128 s = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        __int128 d = (__int128)2 * tq[rows[i]] - m2;
+        if (d < 0) d = -d;
+        s += (unsigned __int128)w[rows[i]] * (unsigned __int128)d;
+    }
+    return s;
+}
+
+static unsigned __int128 mae_cost(const uint64_t *rows, uint64_t m, const uint32_t *w, const int64_t *tq,
+                                  trow *buf)
+{
+    return sad2(rows, m, w, tq, median2(rows, m, w, tq, buf));
 }
 
 /* Mean-decrease-in-impurity of one split (feature importance, SURVEY 8(f)
@@ -491,6 +549,10 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
     out->n = 0;
     uint32_t *perm = (uint32_t *)malloc(sizeof(uint32_t) * p);
     xrow *xr = (xrow *)malloc(sizeof(xrow) * (nr ? nr : 1));
+    uint64_t *lr = (uint64_t *)malloc(sizeof(uint64_t) * (nr ? nr : 1)); /* MAE: child row sets */
+    uint64_t *rr = (uint64_t *)malloc(sizeof(uint64_t) * (nr ? nr : 1));
+    trow *tb = (trow *)malloc(sizeof(trow) * (nr ? nr : 1));
+    unsigned __int128 bestD = 0;
     int64_t *hW = (int64_t *)malloc(sizeof(int64_t) * 257);
     int64_t *hS = (int64_t *)malloc(sizeof(int64_t) * 257);
 
@@ -529,7 +591,53 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                 uint32_t r = j + (uint32_t)or_mulhi64(u, (uint64_t)(p - j));
                 uint32_t tmp = perm[j]; perm[j] = perm[r]; perm[r] = tmp;
             }
-            for (uint32_t jj = 0; jj < c->mtry; ++jj) {
+            for (uint32_t jj = 0; jj < c->mtry && c->mae; ++jj) {
+                /* MAE criterion (R32): candidates as in R8 (exact) or R29 (ExtraTrees);
+                   cost D = 2 (SAD_L + SAD_R), exact integers; best = lowest D, ties by
+                   draw slot, then threshold rank (R9) */
+                uint32_t f = perm[jj];
+                for (uint64_t i = 0; i < nd.nrows; ++i) {
+                    xr[i].row = nd.rows[i];
+                    xr[i].x = c->X[nd.rows[i] * p + f];
+                }
+                qsort(xr, nd.nrows, sizeof(xrow), cmp_xrow);
+                uint64_t i0 = 0, i1 = nd.nrows - 1; /* candidate boundaries i in [i0, i1) */
+                double ethr = 0.0;
+                if (c->extra) {
+                    double lo = xr[0].x, hi = xr[nd.nrows - 1].x;
+                    if (lo == hi) continue;
+                    uint64_t ud = or_draw(k0, k1, hlo, hhi, TAG_THR, jj);
+                    double u = (double)(ud >> 11) * 0x1p-53;
+                    double span = hi - lo;
+                    ethr = span * u;
+                    ethr = ethr + lo;
+                    if (!(ethr < hi)) ethr = lo;
+                    uint64_t b = 0;
+                    while (b + 1 < nd.nrows && xr[b + 1].x <= ethr) ++b;
+                    i0 = b; i1 = b + 1;
+                }
+                for (uint64_t i = i0; i < i1; ++i) {
+                    if (!(xr[i].x < xr[i + 1].x)) continue;
+                    for (uint64_t a = 0; a <= i; ++a) lr[a] = xr[a].row;
+                    for (uint64_t a = i + 1; a < nd.nrows; ++a) rr[a - i - 1] = xr[a].row;
+                    unsigned __int128 D = mae_cost(lr, i + 1, w, c->tq, tb) +
+                                          mae_cost(rr, nd.nrows - i - 1, w, c->tq, tb);
+                    uint64_t rk = find_index(c->gdist[f], c->gnd[f], xr[i].x);
+                    int better = 0;
+                    if (!found) better = 1;
+                    else if (D < bestD) better = 1;
+                    else if (D == bestD) {
+                        if (jj < bestSlot) better = 1;
+                        else if (jj == bestSlot && rk < bestRank) better = 1;
+                    }
+                    if (better) {
+                        found = 1; bestD = D; bestF = f; bestSlot = jj; bestRank = rk;
+                        bestA = c->extra ? ethr : xr[i].x;
+                        bestB = c->extra ? 0.0 : xr[i + 1].x;
+                    }
+                }
+            }
+            for (uint32_t jj = 0; jj < c->mtry && !c->mae; ++jj) {
                 uint32_t f = perm[jj];
                 if (c->extra) {
                     /* Extremely Randomized Trees (R29):
@@ -630,7 +738,10 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
         }
         if (is_leaf) {
             rec.feature = -1;
-            rec.leaf_value = ldexp((double)nd.S / (double)nd.W, -c->F);
+            if (c->mae) /* weighted median (R32) */
+                rec.leaf_value = ldexp((double)median2(nd.rows, nd.nrows, w, c->tq, tb), -c->F - 1);
+            else
+                rec.leaf_value = ldexp((double)nd.S / (double)nd.W, -c->F);
             if (leaf_of_row)
                 for (uint64_t i = 0; i < nd.nrows; ++i) leaf_of_row[nd.rows[i]] = (int32_t)out->n;
             tree_push(out, rec);
@@ -664,7 +775,9 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                 R.rows[R.nrows++] = r; R.W += (int64_t)w[r]; R.S += (int64_t)w[r] * c->tq[r];
             }
         }
-        if (imp) imp[bestF] += mdi_decrease(L.W, L.S, R.W, R.S, c->F);
+        if (imp && c->mae) /* (SAD_node - SAD_L - SAD_R) in target units (R30, R32) */
+            imp[bestF] += ldexp((double)(mae_cost(nd.rows, nd.nrows, w, c->tq, tb) - bestD), -c->F - 1);
+        else if (imp) imp[bestF] += mdi_decrease(L.W, L.S, R.W, R.S, c->F);
         L.depth = R.depth = nd.depth + 1;
         L.heap = 2 * nd.heap;       /* uint64 wrap-around (R14) */
         R.heap = 2 * nd.heap + 1;
@@ -677,7 +790,7 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
         tree_push(out, rec);
         free(nd.rows);
     }
-    free(q); free(perm); free(xr); free(hW); free(hS);
+    free(q); free(perm); free(xr); free(hW); free(hS); free(lr); free(rr); free(tb);
 }
 
 /* ------------------------------------------------------------------ */
@@ -780,7 +893,10 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
            double *imp_raw)
 {
     if (n == 0) return 2;
-    if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || split_mode > 2) return 1;
+    /* split_mode: bits 0-7 the split rule (0 exact, 1 hist, 2 ExtraTrees), bit 8 the MAE
+       criterion (R32; exact and ExtraTrees only) */
+    if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || (split_mode & 0xFFu) > 2 || (split_mode >> 8) > 1 ||
+        split_mode == 0x101u) return 1;
     double *Xc = (double *)malloc(sizeof(double) * n * p);
     int st = validate_X(X, n, p, Xc);
     if (st) { free(Xc); return st; }
@@ -796,8 +912,9 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
     memset(&g, 0, sizeof g);
     g.X = Xc; g.n = n; g.p = p; g.tq = tq; g.F = F;
     g.mtry = mtry; g.min_split = min_split; g.max_depth = max_depth;
-    g.hist = (split_mode == 1);
-    g.extra = (split_mode == 2);
+    g.hist = ((split_mode & 0xFFu) == 1);
+    g.extra = ((split_mode & 0xFFu) == 2);
+    g.mae = (int)(split_mode >> 8);
     if (g.hist) setup_hist(&g, Xc, n, p, tr, n); else setup_exact(&g, Xc, n, p);
     uint32_t *w = (uint32_t *)malloc(sizeof(uint32_t) * n);
     or_tree tree = { NULL, 0, 0 };
@@ -875,7 +992,8 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
 {
     if (n == 0) return 2;
     if (k < 2 || (uint64_t)k > n) return 6;
-    if (p == 0 || min_split < 2 || n_ntree == 0 || n_mtry == 0 || split_mode > 2) return 1;
+    if (p == 0 || min_split < 2 || n_ntree == 0 || n_mtry == 0 || (split_mode & 0xFFu) > 2 ||
+        (split_mode >> 8) > 1 || split_mode == 0x101u) return 1;
     for (uint32_t i = 0; i < n_mtry; ++i) if (mtrys[i] == 0 || mtrys[i] > p) return 1;
     for (uint32_t i = 0; i < n_ntree; ++i) if (ntrees[i] == 0) return 1;
     for (uint64_t i = 0; i < n; ++i) {
@@ -915,8 +1033,9 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     memset(&g, 0, sizeof g);
     g.X = Xc; g.n = n; g.p = p; g.tq = tq; g.F = F;
     g.min_split = min_split; g.max_depth = max_depth;
-    g.hist = (split_mode == 1);
-    g.extra = (split_mode == 2);
+    g.hist = ((split_mode & 0xFFu) == 1);
+    g.extra = ((split_mode & 0xFFu) == 2);
+    g.mae = (int)(split_mode >> 8);
     if (!g.hist) setup_exact(&g, Xc, n, p);
     uint64_t *tr = (uint64_t *)malloc(sizeof(uint64_t) * n);
     uint64_t *te = (uint64_t *)malloc(sizeof(uint64_t) * n);
