@@ -58,7 +58,7 @@ def ln_cr(y: float) -> float:
         return float(decimal.Decimal(y).ln())
 
 
-def quantize(y, target):
+def quantize(y, target, guard=0):
     t = [ln_cr(v) if target == 1 else float(v) for v in y]
     n = len(t)
     M = max(abs(v) for v in t)
@@ -72,7 +72,7 @@ def quantize(y, target):
             e -= 1
         while Fraction(M) > Fraction(2) ** e:
             e += 1
-        F = 62 - (n - 1).bit_length() - e
+        F = 62 - (n - 1).bit_length() - e - guard  # guard = 2 under MAE (R32)
     tq = []
     for v in t:
         q = Fraction(v) * Fraction(2) ** F
@@ -282,7 +282,7 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     """Tree t of `task` over train_rows (default all rows).  extra=True grows an
     Extremely Randomized tree (split_mode 2)."""
     X = [[(0.0 if v == 0.0 else float(v)) for v in row] for row in X]
-    _, tq, F = quantize(list(y), target)
+    _, tq, F = quantize(list(y), target, 2 if mae else 0)
     n = len(X)
     tr = list(range(n)) if train_rows is None else list(train_rows)
     key = tree_key(seed, task, t)

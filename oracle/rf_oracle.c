@@ -128,8 +128,19 @@ static int exp_ceil(double M)
     return ex;
 }
 
-/* Returns 0 on success, 3 non-finite, 4 non-positive y with LOG. */
+/* Returns 0 on success, 3 non-finite, 4 non-positive y with LOG.  guard: extra
+   headroom bits (2 under the MAE criterion, R32: doubled medians and absolute-
+   deviation costs stay below 2^63). */
+static int quantize_g(const double *y, uint64_t n, int target, int guard, double *t_out, int64_t *tq,
+                      int32_t *F_out);
+
 int or_quantize(const double *y, uint64_t n, int target, double *t_out, int64_t *tq, int32_t *F_out)
+{
+    return quantize_g(y, n, target, 0, t_out, tq, F_out);
+}
+
+static int quantize_g(const double *y, uint64_t n, int target, int guard, double *t_out, int64_t *tq,
+                      int32_t *F_out)
 {
     double *t = t_out;
     double M = 0.0;
@@ -141,7 +152,7 @@ int or_quantize(const double *y, uint64_t n, int target, double *t_out, int64_t 
         if (a > M) M = a;
     }
     int F = 0;
-    if (M > 0.0) F = 62 - ceil_log2_u64(n) - exp_ceil(M);
+    if (M > 0.0) F = 62 - ceil_log2_u64(n) - exp_ceil(M) - guard;
     for (uint64_t i = 0; i < n; ++i) {
         double s = ldexp(t[i], F);
         double r = nearbyint(s); /* default rounding mode: half-to-even */
@@ -903,7 +914,7 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
     double *t = (double *)malloc(sizeof(double) * n);
     int64_t *tq = (int64_t *)malloc(sizeof(int64_t) * n);
     int32_t F;
-    st = or_quantize(y, n, (int)target, t, tq, &F);
+    st = quantize_g(y, n, (int)target, (split_mode >> 8) ? 2 : 0, t, tq, &F);
     if (st) { free(Xc); free(t); free(tq); return st; }
     if (F_out) *F_out = F;
     uint64_t *tr = (uint64_t *)malloc(sizeof(uint64_t) * n);
@@ -1006,7 +1017,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     double *t = (double *)malloc(sizeof(double) * n);
     int64_t *tq = (int64_t *)malloc(sizeof(int64_t) * n);
     int32_t F;
-    st = or_quantize(y, n, (int)target, t, tq, &F);
+    st = quantize_g(y, n, (int)target, (split_mode >> 8) ? 2 : 0, t, tq, &F);
     if (st) { free(Xc); free(t); free(tq); return st; }
     int32_t *fid = (int32_t *)malloc(sizeof(int32_t) * n * reps);
     if (fold_ids_in) memcpy(fid, fold_ids_in, sizeof(int32_t) * n * reps);
