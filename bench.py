@@ -127,6 +127,19 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- data -------
+def study_config(args, world):
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": "full study (configs[1]): 5 GPUs x {time n=189, power n=168} x 12 features, "
+                        "30x10-fold CV per rank, ntree {128,256,512,1024} x mtry {12,3,3}",
+            "trees_per_step": len(datagen.GPU_NAMES) * 2 * REPS * K_FOLDS * DISTINCT_MTRY * max(NTREES) * world,
+            "nominal_grid_trees_per_step": len(datagen.GPU_NAMES) * 2 * REPS * K_FOLDS * len(MTRYS) * sum(NTREES)
+            * world,
+            "l2": "flushed between timed steps (256 MB write)",
+            "split": ("ExtraTrees, no bootstrap (P:468-469)" if args.split == "extra"
+                      else "bootstrap + exact CART (north_star)"),
+            "parallelism": f"task-sharded x{world}"}
+
+
 def study_inputs():
     return datagen.study(datagen.SEED)
 
@@ -141,8 +154,8 @@ def run_reference(args):
     oracle.build()
     ds = study_inputs()[0]  # K20 / time
     folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
-    # bounded sample: repeat 0, tasks (folds) 0..1 of one dataset, full grid
-    sample_tasks = 2
+    # bounded sample: repeat 0, tasks (folds) 0..3 of one dataset, full grid (~3 s per step)
+    sample_tasks = 4
 
     def step():
         t0 = time.perf_counter()
@@ -160,10 +173,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "full study (configs[1]) sample: K20/time, repeat 0, folds 0-1, "
-                               "ntree {128..1024} x mtry {12,3}", "trees_per_step": trees},
+        "config": dict(study_config(args, 1), reference_sample=f"per step: K20/time, repeat 0, folds "
+                       f"0-{sample_tasks - 1}, ntree {{128..1024}} x mtry {{12,3}} = {trees} trees"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{trees} trees (2 CV tasks x 2 mtry x 1024) of the K20 time dataset"},
+                         "sample": f"{trees} trees ({sample_tasks} CV tasks x 2 mtry x 1024) of the K20 time dataset per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -174,14 +187,14 @@ def cpu_baseline_sample(skw):
     oracle.build()
     ds = study_inputs()[0]
     folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
-    tasks = 2
+    tasks = 10  # one whole repeat of 10-fold CV: ~8 s on one host core
     t0 = time.perf_counter()
     oracle.cv_grid(ds["X"], ds["y"], K_FOLDS, 1, NTREES, [12, 3], fold_ids=folds, target=1, seed=SEED,
                    task_begin=0, task_end=tasks, **skw)
     dt = time.perf_counter() - t0
     trees = tasks * DISTINCT_MTRY * max(NTREES)
     return {"value": trees / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{trees} trees: K20/time dataset, repeat 0 folds 0-1, ntree<=1024 x mtry {{12,3}} "
+            "sample": f"{trees} trees: K20/time dataset, repeat 0 (folds 0-{tasks - 1}), ntree<=1024 x mtry {{12,3}} "
                       f"({dt:.1f} s on 1 host core)"}
 
 
@@ -279,14 +292,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "full study (configs[1]): 5 GPUs x {time n=189, power n=168} x 12 features, "
-                                   "30x10-fold CV per rank, ntree {128,256,512,1024} x mtry {12,3,3}",
-                       "trees_per_step": trees_per_step_rank * world,
-                       "nominal_grid_trees_per_step": len(ds) * REPS * K_FOLDS * len(MTRYS) * sum(NTREES) * world,
-                       "l2": "flushed between timed steps (256 MB write)",
-                       "split": ("ExtraTrees, no bootstrap (P:468-469)" if args.split == "extra"
-                                 else "bootstrap + exact CART (north_star)"),
-                       "parallelism": f"task-sharded x{world}"},
+            "config": study_config(args, world),
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk.summary(),
