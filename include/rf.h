@@ -70,6 +70,17 @@ typedef enum {
    (R29).  All three share the criterion, tie-break, stopping and leaves. */
 typedef enum { RF_SPLIT_EXACT = 0, RF_SPLIT_HIST256 = 1, RF_SPLIT_EXTRA = 2 } rf_split_mode;
 typedef enum { RF_TARGET_IDENTITY = 0, RF_TARGET_LOG = 1 } rf_target;
+/* Split criterion.  MSE: variance reduction, leaves hold the
+   weighted in-bag mean (R6, R13).  MAE (the paper's best models
+   in Tables 4/5): a split minimises the summed weighted absolute
+   deviations of the children from their weighted medians, leaves hold the
+   weighted median (R32).  MAE is implemented for the exact and ExtraTrees
+   split modes on the CTA-resident path (training sets of <= 255 rows, p <= 64;
+   the paper's datasets have 189 / 168 rows); other shapes return
+   RF_E_UNSUPPORTED.  Under MAE the targets are quantised with 2 guard bits
+   (F = 62 - ceil(log2 n) - e - 2) so doubled medians and doubled absolute-
+   deviation sums are exact integers below 2^63. */
+typedef enum { RF_CRITERION_MSE = 0, RF_CRITERION_MAE = 1 } rf_criterion;
 
 /* Hyper-parameters and sharding. */
 typedef struct {
@@ -87,10 +98,11 @@ typedef struct {
   uint32_t tree_end;
   uint32_t task_begin;        /* CV tasks (task = rep*k + fold) [task_begin, task_end);  */
   uint32_t task_end;          /*   0,0 = all; outputs of other tasks are NaN             */
+  uint32_t criterion;         /* rf_criterion: MSE (default) or MAE (R32)                */
 } rf_params;
 
 /* Fills the defaults: ntree 100, mtry 0, min_samples_split 2, max_depth -1,
-   bootstrap 1, exact, IDENTITY, seed 0, device 0, no sharding. */
+   bootstrap 1, exact, IDENTITY, seed 0, device 0, no sharding, MSE. */
 RF_API void rf_params_default(rf_params* prm);
 
 /* Opaque device-resident forest: flattened BFS nodes (16 B each:

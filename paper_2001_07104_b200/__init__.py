@@ -28,6 +28,7 @@ STATUS_NAMES = ["OK", "ARG", "EMPTY", "NONFINITE", "NONPOSITIVE_Y", "ARITY", "TO
                 "OVERFLOW", "UNSUPPORTED"]
 SPLIT_EXACT, SPLIT_HIST256, SPLIT_EXTRA = 0, 1, 2
 TARGET_IDENTITY, TARGET_LOG = 0, 1
+CRITERION_MSE, CRITERION_MAE = 0, 1
 
 # every entry point declared in include/rf.h and include/rf_debug.h
 ABI_SYMBOLS = [
@@ -53,7 +54,7 @@ class Params(C.Structure):
                 ("min_samples_split", C.c_uint32), ("max_depth", C.c_int32), ("bootstrap", C.c_uint32),
                 ("split_mode", C.c_uint32), ("target", C.c_uint32), ("seed", C.c_uint64),
                 ("device", C.c_int32), ("tree_begin", C.c_uint32), ("tree_end", C.c_uint32),
-                ("task_begin", C.c_uint32), ("task_end", C.c_uint32)]
+                ("task_begin", C.c_uint32), ("task_end", C.c_uint32), ("criterion", C.c_uint32)]
 
 
 _lib = None
@@ -227,11 +228,12 @@ def forest_import(feature, left, value, thr_index, tree_off, p, F, target, devic
 # ------------------------------------------------------------------- API --
 def fit(X, y, *, ntree=100, mtry=0, min_samples_split=2, max_depth=-1, bootstrap=True,
         split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0, tree_begin=0, tree_end=0,
-        debug=False) -> Forest:
-    """Grow a forest (rf_fit).  X: [n, p] fp64, y: [n] fp64 (numpy or CUDA tensors)."""
+        debug=False, criterion=CRITERION_MSE) -> Forest:
+    """Grow a forest (rf_fit).  X: [n, p] fp64, y: [n] fp64 (numpy or CUDA tensors).
+    criterion: CRITERION_MSE (P:215) or CRITERION_MAE (P:489, R32)."""
     prm = params(ntree=ntree, mtry=mtry, min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
-                 tree_begin=tree_begin, tree_end=tree_end)
+                 tree_begin=tree_begin, tree_end=tree_end, criterion=criterion)
     h = C.c_void_p()
     if _is_torch(X):
         if debug:
@@ -302,11 +304,13 @@ def make_folds_masked(y, k, mask, seed=0, custom=False, out=None):
 
 
 def nested_cv(X, y, k_outer, k_inner, iterations, ntrees, mtrys, *, custom=False, min_samples_split=2,
-              max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0):
+              max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0,
+              criterion=CRITERION_MSE):
     """Nested CV (rf_nested_cv, R31): (best [it, k_outer] grid index mi*n_ntree+ti,
     outer_mape [it, k_outer], inner_score [it, k_outer, n_mtry, n_ntree])."""
     prm = params(ntree=max(ntrees), mtry=0, min_samples_split=min_samples_split, max_depth=max_depth,
-                 bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device)
+                 bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
+                 criterion=criterion)
     nt, mt = _u32(ntrees), _u32(mtrys)
     if _is_torch(X):
         torch = _torch()
@@ -343,11 +347,12 @@ def error_buckets(y, yhat):
 
 def cross_validate_grid(X, y, k, repeats, ntrees, mtrys, fold_ids=None, *, want_pred=False,
                         min_samples_split=2, max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT,
-                        target=TARGET_IDENTITY, seed=0, device=0, task_begin=0, task_end=0, out=None):
+                        target=TARGET_IDENTITY, seed=0, device=0, task_begin=0, task_end=0, out=None,
+                        criterion=CRITERION_MSE):
     """fold_mape [n_mtry, n_ntree, repeats, k] (+ pred [n_mtry, n_ntree, repeats, n])."""
     prm = params(ntree=max(ntrees), mtry=0, min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
-                 task_begin=task_begin, task_end=task_end)
+                 task_begin=task_begin, task_end=task_end, criterion=criterion)
     nt, mt = _u32(ntrees), _u32(mtrys)
     shape = (len(mt), len(nt), repeats, k)
     if _is_torch(X):
@@ -378,11 +383,13 @@ def cross_validate(X, y, k, repeats=1, fold_ids=None, *, ntree=100, mtry=0, **kw
 
 
 def cv_partial(X, y, k, repeats, fold_ids, ntrees, mtrys, *, tree_begin, tree_end, min_samples_split=2,
-               max_depth=-1, bootstrap=True, target=TARGET_IDENTITY, seed=0, out=None):
+               max_depth=-1, bootstrap=True, target=TARGET_IDENTITY, seed=0, out=None, split_mode=SPLIT_EXACT,
+               criterion=CRITERION_MSE):
     """Tree-sharded CV partial sums [n_mtry, n_ntree, repeats, n] (device tensors)."""
     torch = _torch()
     prm = params(ntree=max(ntrees), min_samples_split=min_samples_split, max_depth=max_depth,
-                 bootstrap=int(bootstrap), target=target, seed=seed, tree_begin=tree_begin, tree_end=tree_end)
+                 bootstrap=int(bootstrap), target=target, seed=seed, tree_begin=tree_begin, tree_end=tree_end,
+                 split_mode=split_mode, criterion=criterion)
     nt, mt = _u32(ntrees), _u32(mtrys)
     n, p = X.shape
     out = torch.empty((len(mt), len(nt), repeats, n), dtype=torch.float64, device=X.device) if out is None else out

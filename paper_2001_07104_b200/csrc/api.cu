@@ -86,6 +86,9 @@ rf_status check_params(const rf_params* prm, uint32_t p, uint32_t* mtry_out) {
   if (prm->min_samples_split < 2) return fail(RF_E_ARG, "min_samples_split must be >= 2");
   if (prm->max_depth < -1) return fail(RF_E_ARG, "max_depth must be >= -1");
   if (prm->split_mode > RF_SPLIT_EXTRA || prm->target > 1) return fail(RF_E_ARG, "bad split_mode/target");
+  if (prm->criterion > RF_CRITERION_MAE) return fail(RF_E_ARG, "bad criterion");
+  if (prm->criterion == RF_CRITERION_MAE && prm->split_mode == RF_SPLIT_HIST256)
+    return fail(RF_E_UNSUPPORTED, "MAE criterion: exact and ExtraTrees split modes only (R32)");
   uint32_t m = prm->mtry ? prm->mtry : std::max<uint32_t>(1, p / 3);
   if (m > p) return fail(RF_E_ARG, "mtry must be <= p");
   if (mtry_out) *mtry_out = m;
@@ -104,7 +107,7 @@ rf_status read_err(const int* derr, cudaStream_t s) {
 
 // dataset on device: canonical X, t_q, F, presort
 rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, int target,
-                  int require_pos, bool need_sort, rf::DevData& d, Scratch& sc, cudaStream_t s) {
+                  int require_pos, bool need_sort, rf::DevData& d, Scratch& sc, cudaStream_t s, int guard = 0) {
   d.n = (int)n;
   d.p = (int)p;
   CK(sc.alloc(&d.X, n * p), "alloc X");
@@ -116,7 +119,7 @@ rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, in
   CK(sc.alloc(&t, n + 2), "alloc t");
   {
     ProfScope ps("prep", s);
-    CK(rf::prep_targets(dX, dy, (int)n, (int)p, target, require_pos, d, t, s), "prep");
+    CK(rf::prep_targets(dX, dy, (int)n, (int)p, target, require_pos, guard, d, t, s), "prep");
   }
   if (need_sort) {
     CK(sc.alloc(&d.order, n * p), "alloc order");
@@ -129,6 +132,9 @@ rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, in
   }
   return RF_OK;
 }
+
+// quantisation headroom (R32): 2 guard bits under MAE
+int mae_guard(const rf_params* prm) { return prm->criterion == RF_CRITERION_MAE ? 2 : 0; }
 
 int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
 
@@ -194,7 +200,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   }
   Scratch sc(s);
   rf::DevData d;
-  st = prepare(dX, dy, n, p, prm->target, 1, true, d, sc, s);
+  st = prepare(dX, dy, n, p, prm->target, 1, true, d, sc, s, mae_guard(prm));
   if (st) return st;
 
   const int32_t* dfold = dfold_in;
@@ -258,6 +264,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   a.ntr_max = ntr_max; a.nte_max = nte_max;
   a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
   a.extra = prm->split_mode == RF_SPLIT_EXTRA;
+  a.mae = prm->criterion == RF_CRITERION_MAE;
   a.max_depth = prm->max_depth; a.n_mtry = nmd;
   for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
@@ -274,6 +281,8 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     }
     if (best_wpb == 0) large = true;
   }
+  if (large && a.mae)
+    return fail(RF_E_UNSUPPORTED, "MAE criterion: training sets of <= 255 rows and p <= 64 only (R32)");
   if (large) {
     for (int c = 32; c >= 1; --c)
       if (g % c == 0) { Cw = c; break; }
@@ -386,7 +395,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   const int T = tree_hi - tree_lo;
   Scratch sc(s);
   rf::DevData d;
-  st = prepare(dX, dy, n, p, prm->target, prm->target == RF_TARGET_LOG, true, d, sc, s);
+  st = prepare(dX, dy, n, p, prm->target, prm->target == RF_TARGET_LOG, true, d, sc, s, mae_guard(prm));
   if (st) return st;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -431,6 +440,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     a.ord = td.ord; a.lrank = td.lrank; a.ntr_max = (int)n; a.nte_max = 0;
     a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
     a.extra = prm->split_mode == RF_SPLIT_EXTRA;
+    a.mae = prm->criterion == RF_CRITERION_MAE;
     a.max_depth = prm->max_depth; a.n_mtry = 1; a.mtrys[0] = (int)mtry;
     a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
     a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;
@@ -448,6 +458,10 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
       cudaError_t e = rf::launch_small_tree(a, s);
       if (e != cudaSuccess) { drop(); return cuda_fail(e, "small_tree fit"); }
     }
+  }
+  if (!small && prm->criterion == RF_CRITERION_MAE) {
+    drop();
+    return fail(RF_E_UNSUPPORTED, "MAE criterion: training sets of <= 255 rows and p <= 64 only (R32)");
   }
   if (!small) {
     rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,

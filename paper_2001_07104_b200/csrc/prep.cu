@@ -55,7 +55,7 @@ __global__ void k_prep_y(const double* __restrict__ y, double* __restrict__ t, i
   }
 }
 
-__device__ __forceinline__ int quant_F(unsigned long long maxbits, int n) {
+__device__ __forceinline__ int quant_F(unsigned long long maxbits, int n, int guard) {
   double M = __longlong_as_double((long long)maxbits);
   if (M == 0.0) return 0;
   int ex;
@@ -63,12 +63,12 @@ __device__ __forceinline__ int quant_F(unsigned long long maxbits, int n) {
   int eM = (fr == 0.5) ? ex - 1 : ex;
   int c = 0;
   while ((1ull << c) < (unsigned long long)n) ++c;
-  return 62 - c - eM;
+  return 62 - c - eM - guard;  // guard = 2 under MAE (R32)
 }
 
-__global__ void k_quant(const double* __restrict__ t, int n, const unsigned long long* maxbits,
+__global__ void k_quant(const double* __restrict__ t, int n, const unsigned long long* maxbits, int guard,
                         int64_t* __restrict__ tq, int32_t* Fout) {
-  const int F = quant_F(*maxbits, n);
+  const int F = quant_F(*maxbits, n, guard);
   if (blockIdx.x == 0 && threadIdx.x == 0) *Fout = F;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     tq[i] = __double2ll_rn(scalbn(t[i], F));
@@ -167,7 +167,7 @@ __global__ void k_rank_sorted(const unsigned long long* __restrict__ skeys,
 }  // namespace
 
 cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int target,
-                         int require_pos, DevData& d, double* scratch_t, cudaStream_t s) {
+                         int require_pos, int guard, DevData& d, double* scratch_t, cudaStream_t s) {
   unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(scratch_t + n);
   cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), s);
   const size_t total = (size_t)n * p;
@@ -177,7 +177,7 @@ cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int t
   int gy = std::min((n + 255) / 256, 148 * 8);
   k_prep_y<<<gy > 0 ? gy : 1, 256, 0, s>>>(dy, scratch_t, n, target, require_pos, maxbits, d.err);
   note_launch();
-  k_quant<<<gy > 0 ? gy : 1, 256, 0, s>>>(scratch_t, n, maxbits, d.tq, d.F);
+  k_quant<<<gy > 0 ? gy : 1, 256, 0, s>>>(scratch_t, n, maxbits, guard, d.tq, d.F);
   note_launch();
   return cudaGetLastError();
 }

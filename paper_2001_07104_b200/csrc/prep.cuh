@@ -20,9 +20,10 @@ struct DevData {
 };
 
 // X -> canonical copy, checks finiteness; y -> t (ln if LOG) -> F, t_q.
-// require_pos: y > 0 required (LOG target or CV).
+// require_pos: y > 0 required (LOG target or CV).  guard: extra headroom bits of
+// the quantisation (2 under the MAE criterion, R32: F = 62 - ceil(log2 n) - e - 2).
 cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int target,
-                         int require_pos, DevData& d, double* scratch_t, cudaStream_t s);
+                         int require_pos, int guard, DevData& d, double* scratch_t, cudaStream_t s);
 // stable per-feature order + dense ranks (needs workspace for large n)
 cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t presort_ws_bytes(int n, int p);

@@ -17,6 +17,15 @@
 //   (node, slot) segment is the boundary of its random threshold, given as a
 //   dense-rank threshold found by a binary search in a shared-memory table of
 //   the task's distinct values; everything else is shared.
+//   MAE criterion (R32): the candidates are the same; a
+//   candidate's cost D = 2 (SAD_L + SAD_R), the doubled weighted absolute
+//   deviations of the children from their weighted medians, is exact in
+//   uint64 (2 guard bits of quantisation keep it below 2^63) and is found by
+//   one walk of the node's rows in t_q order (an extra row list, partitioned
+//   like the feature lists): the walk stops at both children's weighted
+//   medians and SAD = m2 (2 W_<=k - W) + 2 (S - 2 S_<=k) needs only the
+//   cumulative sums there.  Best = lowest D (key ~D), same tie-break; leaves
+//   hold the weighted median (a second walk per node after the mark pass).
 //
 // Per level the warp runs three lane-serial passes (each lane owns a
 // contiguous chunk; lane totals are combined by one warp scan):
@@ -74,6 +83,7 @@ struct CtaSmem {
   SA<double2> rcp2;   // [256] (w, RN(1/w))
   SA<double> xte;     // [nte_max][p]
   SA<double> xs;      // ExtraTrees: [p][ntr_max] distinct training values of x_f by dense rank
+  SA<uint8_t> tord;   // MAE: [ntr_max] local rows in (t_q, local index) order
 };
 
 struct NodeSet {  // open nodes of one level
@@ -106,6 +116,8 @@ struct WarpSmem {
   SA<uint32_t> thrIdx; // fit mode: threshold rank
   SA<uint32_t> desc;   // [ntr_max] partition descriptor per position (shared by all lists);
                        // aliases bkey (free once the level's thresholds are used, (g))
+  SA<int64_t> med2;    // MAE: [NM][2] doubled weighted medians of the children (or of the node)
+  SA<uint64_t> bD;     // MAE fit: [NM] cost D of the chosen split (importance)
 };
 
 constexpr uint8_t kNone = 0xFF;
@@ -114,13 +126,15 @@ __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
 // per-feature stride of the row lists: a multiple of 4 (32-bit list words in (g))
 __host__ __device__ inline int stride_of(int ntr_max) { return (ntr_max + 3) & ~3; }
 
-__host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_max, int nte_max, bool extra) {
+__host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_max, int nte_max, bool extra,
+                                          bool mae) {
   s.ord = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.lrank = c.take<uint8_t>((size_t)p * ntr_max, 16);
   s.tq = c.take<int64_t>(ntr_max, 16);
   s.rcp2 = c.take<double2>(256, 16);
   s.xte = c.take<double>((size_t)nte_max * p, 16);
   s.xs = extra ? c.take<double>((size_t)p * ntr_max, 16) : SA<double>{0u};
+  s.tord = mae ? c.take<uint8_t>(ntr_max, 16) : SA<uint8_t>{0u};
 }
 
 __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
@@ -132,12 +146,16 @@ __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
   s.bfs = c.take<uint16_t>(NM, 4);
 }
 
+// row lists per tree: the p feature lists, plus the t_q-ordered list under MAE (list p)
+__host__ __device__ inline int nlists_of(int p, bool mae) { return p + (mae ? 1 : 0); }
+
 __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool extra,
-                                           bool fit) {
+                                           bool fit, bool mae) {
   const int NM = nmax_of(ntr_max);
+  const int P = nlists_of(p, mae);
   s.w = c.take<uint8_t>((ntr_max + 3) / 4 * 4, 16);
-  s.listA = c.take<uint8_t>((size_t)p * ntr_max, 16);
-  s.listB = c.take<uint8_t>((size_t)p * ntr_max, 16);
+  s.listA = c.take<uint8_t>((size_t)P * ntr_max, 16);
+  s.listB = c.take<uint8_t>((size_t)P * ntr_max, 16);
   s.pnA = c.take<uint8_t>(ntr_max, 4);
   s.pnB = c.take<uint8_t>(ntr_max, 4);
   s.side = c.take<uint8_t>(ntr_max, 4);
@@ -155,6 +173,8 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.chBase = c.take<uint16_t>(NM, 4);
   s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
   s.desc = SA<uint32_t>{s.bkey.off};  // ntr_max * 4 <= NM * 8 bytes
+  s.med2 = mae ? c.take<int64_t>((size_t)NM * 2, 8) : SA<int64_t>{0u};
+  s.bD = (mae && fit) ? c.take<uint64_t>(NM, 8) : SA<uint64_t>{0u};
 }
 
 // ---------------------------------------------------------------- warp ops --
@@ -235,6 +255,89 @@ __device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsig
   return k1 > k2 || (k1 == k2 && a1 < a2);
 }
 
+// ------------------------------------------------------- MAE criterion (R32) --
+// Doubled weighted median of a row set walked in t_q order (scikit-learn's rule, the
+// oracle's median2): k = the first element with 2 cum_k >= W; m2 = t_k + t_k+1 if
+// 2 cum_k == W, else 2 t_k.  The tracker also keeps W_<=k and S_<=k, from which
+// the doubled absolute-deviation sum is SAD2 = sum w |2t - m2|
+//   = m2 (2 W_<=k - W) + 2 (S - 2 S_<=k)
+// (rows up to k lie at or below m2 / 2, the rest at or above).  All exact in
+// (modular) 64-bit integers: |t_q| <= 2^(60 - ceil(log2 n)) under 2 guard bits.
+struct MedTrack {
+  uint32_t W;          // total weight of the set
+  uint32_t cum;        // running weight
+  int64_t sum;         // running weighted sum
+  uint32_t Wk;         // weight up to and including k
+  int64_t Sk;          // weighted sum up to and including k
+  int64_t m2;          // doubled median
+  int state;           // 0 searching, 1 waiting for t_k+1, 2 done
+};
+
+__device__ __forceinline__ void med_init(MedTrack& m, uint32_t W) {
+  m.W = W; m.cum = 0; m.sum = 0; m.Wk = 0; m.Sk = 0; m.m2 = 0; m.state = W ? 0 : 2;
+}
+
+__device__ __forceinline__ void med_push(MedTrack& m, uint32_t wv, int64_t t) {
+  if (m.state == 0) {
+    m.cum += wv;
+    m.sum += (int64_t)wv * t;
+    if (2u * m.cum >= m.W) {
+      m.Wk = m.cum; m.Sk = m.sum;
+      if (2u * m.cum == m.W) { m.m2 = t; m.state = 1; }
+      else { m.m2 = 2 * t; m.state = 2; }
+    }
+  } else if (m.state == 1) {
+    m.m2 += t;
+    m.state = 2;
+  }
+}
+
+// SAD2 of the tracked set with total weighted sum S
+__device__ __forceinline__ uint64_t med_sad2(const MedTrack& m, int64_t S) {
+  return (uint64_t)m.m2 * (uint64_t)(2u * m.Wk - m.W) + 2ull * (uint64_t)(S - 2 * m.Sk);
+}
+
+// Search key of one MAE candidate: ~D with D = SAD2(left) + SAD2(right) < 2^63, so the
+// key is > 0 and "larger key = better" keeps the MSE path's reduction and tie-break (R9).
+// tl: the node's rows in t order (len ln); left rows are those with lrank_f <= thr.
+__device__ __noinline__ unsigned long long mae_key(SA<uint8_t> tl, int ln, SA<uint8_t> lr, uint32_t thr,
+                                                   SA<uint8_t> w, SA<int64_t> tq, uint32_t WL, int64_t SL,
+                                                   uint32_t WR, int64_t SR) {
+  MedTrack mL, mR;
+  med_init(mL, WL);
+  med_init(mR, WR);
+  #pragma unroll 1
+  for (int i = 0; i < ln; ++i) {
+    const uint8_t r = tl[i];
+    const uint32_t wv = w[r];
+    const int64_t t = tq[r];
+    if ((uint32_t)lr[r] <= thr) med_push(mL, wv, t); else med_push(mR, wv, t);
+    if (mL.state == 2 && mR.state == 2) break;
+  }
+  return ~(med_sad2(mL, SL) + med_sad2(mR, SR));
+}
+
+// Doubled weighted median (and, if sad2 != null, the doubled SAD) of the rows of a t-ordered
+// segment selected by sel: 0 = all rows, 1 = side[r] != 0 (left child), 2 = side[r] == 0.
+// Rows with weight 0 are absent (w = 0 adds nothing).
+__device__ __noinline__ int64_t seg_median2(SA<uint8_t> tl, int ln, SA<uint8_t> w, SA<int64_t> tq,
+                                            SA<uint8_t> side, int sel, uint32_t W, int64_t S, uint64_t* sad2) {
+  MedTrack m;
+  med_init(m, W);
+  #pragma unroll 1
+  for (int i = 0; i < ln && m.state != 2; ++i) {
+    const uint8_t r = tl[i];
+    if (sel == 1 && !side[r]) continue;
+    if (sel == 2 && side[r]) continue;
+    const uint32_t wv = w[r];
+    if (wv) med_push(m, wv, tq[r]);
+  }
+  if (sad2) *sad2 = med_sad2(m, S);
+  return m.m2;
+}
+
+__device__ __noinline__ double median_leaf(int64_t m2, int F) { return scalbn(__ll2double_rn(m2), -F - 1); }
+
 // ------------------------------------------------- profiling build only --
 // RF_PHASE_TIMING: lane 0 of every warp adds the clock64 delta since the previous
 // mark to g_phase_cyc[i] (phase names: DESIGN.md sec. 6).  Compiled out otherwise.
@@ -253,8 +356,8 @@ __device__ unsigned long long g_phase_cyc[kPhases];
 #endif
 
 // -------------------------------------------------------------- the kernel --
-// TM: max test rows per lane.  kExtra: ExtraTrees split mode (R29).
-template <bool kFit, int TM, bool kExtra>
+// TM: max test rows per lane.  kExtra: ExtraTrees split mode (R29).  kMae: MAE criterion (R32).
+template <bool kFit, int TM, bool kExtra, bool kMae>
 __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -276,16 +379,16 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 
   Carve cv;
   CtaSmem cs;
-  carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max, extra);
+  carve_cta(cv, cs, p, ntr_max, kFit ? 0 : a.nte_max, extra, kMae);
   WarpSmem ws;
   {
     const size_t cta_bytes = (cv.off + 15) / 16 * 16;
     Carve cw;
     WarpSmem dummy;
-    carve_warp(cw, dummy, p, ntr_max, extra, kFit);
+    carve_warp(cw, dummy, p, ntr_max, extra, kFit, kMae);
     const size_t per_warp = (cw.off + 15) / 16 * 16;
     Carve mine(cta_bytes + per_warp * warp);
-    carve_warp(mine, ws, p, ntr_max, extra, kFit);
+    carve_warp(mine, ws, p, ntr_max, extra, kFit, kMae);
   }
 
   const int ntr = a.ntr[tl];
@@ -307,6 +410,21 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     }
     #pragma unroll 1
     for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
+    if (kMae) {
+      // t order of the training rows: rank of (t_q, local index) by counting (n_tr <= 255)
+      __syncthreads();
+      #pragma unroll 1
+      for (int i = threadIdx.x; i < ntr; i += blockDim.x) {
+        const int64_t ti = cs.tq[i];
+        int rk = 0;
+        #pragma unroll 1
+        for (int j = 0; j < ntr; ++j) {
+          const int64_t tj = cs.tq[j];
+          rk += (tj < ti) || (tj == ti && j < i);
+        }
+        cs.tord[rk] = (uint8_t)i;
+      }
+    }
     #pragma unroll 1
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
       cs.rcp2[i] = make_double2((double)i, i ? __ddiv_rn(1.0, (double)i) : 0.0);
@@ -390,7 +508,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     uint32_t tcur = 0;  // packed: test row s -> open node (byte s), 0xFF = finished
     const bool root_leaf = (a.max_depth == 0) || ((int)D < a.min_split) || (mn == mx);
     if (root_leaf) {
-      const double v = leaf_value(S, Wroot, F);
+      const double v = kMae ? median_leaf(seg_median2(cs.tord, ntr, ws.w, cs.tq, ws.w, 0, Wroot, S, nullptr), F)
+                            : leaf_value(S, Wroot, F);
 #pragma unroll
       for (int s = 0; s < TM; ++s)
         if (lane + 32 * s < nte) acc[s] += v;
@@ -416,14 +535,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
     SA<uint8_t> pn2 = ws.pnB;
     NodeSet cur = ws.cur, nxt = ws.nxt;
     #pragma unroll 1
-    for (int f = 0; f < p; ++f) {
+    for (int f = 0; f < nlists_of(p, kMae); ++f) {
       uint32_t off = 0;
       #pragma unroll 1
       for (int c = 0; c < ntr; c += 32) {
         const int j = c + lane;
         uint8_t r = 0;
         bool keep = false;
-        if (j < ntr) { r = cs.ord[f * ntr_max + j]; keep = ws.w[r] != 0; }
+        if (j < ntr) { r = (kMae && f == p) ? cs.tord[j] : cs.ord[f * ntr_max + j]; keep = ws.w[r] != 0; }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (keep) L[f * ntr_max + off + __popc(bal & lanemask_lt())] = r;
         off += __popc(bal);
@@ -651,8 +770,12 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           const double gl = div_small(__dmul_rn(dSL, dSL), yl.x, yl.y);
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
           const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
-          const unsigned long long key =
-              cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
+          unsigned long long key;
+          if (kMae)  // R32: left = rows of the node with rank <= the boundary's rank
+            key = cand ? mae_key(L + (p * ntr_max + st), ln, cs.lrank + lbase, rkr, ws.w, cs.tq, WL, SL, WR, SR)
+                       : 0ull;
+          else
+            key = cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
           const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);  // draw slot, position (R9)
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
@@ -746,6 +869,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
           } else {
             thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
           }
+          if (kMae && kFit) ws.bD[k] = ~key;  // cost D of the chosen split (importance)
           ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
           ws.baux[k] = ((uint32_t)f << 8) | (uint32_t)bp | 0x80000000u;  // feature, boundary, split flag
           if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
@@ -775,6 +899,31 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
       }
       __syncwarp();
       PT_MARK(7);
+
+      // ---------------- (d') MAE (R32): weighted medians of the children of split nodes (leaf
+      // values) and of unsplit open nodes, by one walk of the node's t-ordered rows each
+      if (kMae) {
+        #pragma unroll 1
+        for (int k = lane; k < nOpen; k += 32) {
+          const SA<uint8_t> tl = L + (p * ntr_max + cur.start[k]);
+          const int ln = cur.len[k];
+          const uint32_t aux = ws.baux[k];
+          if (aux & 0x80000000u) {
+            const uint32_t WLv = ws.bW[k];
+            const int64_t SLv = (int64_t)ws.bS[k];
+            ws.med2[2 * k] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 1, WLv, SLv, nullptr);
+            ws.med2[2 * k + 1] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 2, cur.W[k] - WLv, cur.S[k] - SLv, nullptr);
+            if (kFit && a.imp) {  // importance: (SAD2(node) - D) 2^(-F-1) (R30, R32)
+              uint64_t sad = 0;
+              seg_median2(tl, ln, ws.w, cs.tq, ws.side, 0, cur.W[k], cur.S[k], &sad);
+              ws.bD[k] = sad - ws.bD[k];
+            }
+          } else {
+            ws.med2[2 * k] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 0, cur.W[k], cur.S[k], nullptr);
+          }
+        }
+        __syncwarp();
+      }
 
       // ---------------- (e) children, node emission, next-level tables
       int nSplitTotal = 0, nOpenNext = 0, Nnext = 0, NL = 0;
@@ -819,7 +968,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               ws.chOpen[2 * k] = (uint8_t)oi;
               ++oi; ps += lenL;
             } else {
-              vL = leaf_value(SLv, WLv, F);
+              vL = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(SLv, WLv, F);
               ws.chOpen[2 * k] = kNone;
             }
             if (openR) {
@@ -828,7 +977,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               nxt.heap[oi] = 2ull * cur.heap[k] + 1ull; nxt.bfs[oi] = (uint16_t)(childBase + 1);
               ws.chOpen[2 * k + 1] = (uint8_t)oi;
             } else {
-              vR = leaf_value(SRv, WRv, F);
+              vR = kMae ? median_leaf(ws.med2[2 * k + 1], F) : leaf_value(SRv, WRv, F);
               ws.chOpen[2 * k + 1] = kNone;
             }
             ws.chVal[2 * k] = vL;
@@ -853,12 +1002,13 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
               ti[me] = ws.thrIdx[k];
               if (!openL) { Node16 l; l.feat = -1; l.left = 0; l.v = vL; tn[childBase] = l; ti[childBase] = 0; }
               if (!openR) { Node16 r; r.feat = -1; r.left = 0; r.v = vR; tn[childBase + 1] = r; ti[childBase + 1] = 0; }
-              if (a.imp)  // feature importance (MDI, NEXT-3)
-                atomicAdd(&a.imp[tree_slot * p + nd.feat], mdi_decrease(WLv, SLv, WRv, SRv, F));
+              if (a.imp)  // feature importance (MDI, NEXT-3; MAE: R32)
+                atomicAdd(&a.imp[tree_slot * p + nd.feat],
+                          kMae ? scalbn(__ull2double_rn(ws.bD[k]), -F - 1) : mdi_decrease(WLv, SLv, WRv, SRv, F));
             }
           } else if (act) {
             // open node without any candidate split: leaf (R11)
-            const double v = leaf_value(cur.S[k], cur.W[k], F);
+            const double v = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(cur.S[k], cur.W[k], F);
             ws.chVal[2 * k] = v;
             ws.bS[k] = 0ull;  // partition record: not split
             if (kFit) {
@@ -963,7 +1113,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         // 4 (c % nc4) .. +3 (c / nc4 exactly via a float reciprocal: c < 2^16).  Four
         // ballots give each element its rank among the left rows before it.
         const int nc4 = (N + 3) >> 2;
-        const int C = (p - 1) * nc4;
+        const int C = (nlists_of(p, kMae) - 1) * nc4;
         const float inv4 = 1.0f / (float)nc4;
         carry = 0;
         #pragma unroll 1
@@ -1046,19 +1196,23 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
 size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   Carve c;
   CtaSmem cs;
-  carve_cta(c, cs, a.p, stride_of(a.ntr_max), a.fit_mode ? 0 : a.nte_max, a.extra != 0);
+  carve_cta(c, cs, a.p, stride_of(a.ntr_max), a.fit_mode ? 0 : a.nte_max, a.extra != 0, a.mae != 0);
   const size_t cta = (c.off + 15) / 16 * 16;
   Carve w;
   WarpSmem ws;
-  carve_warp(w, ws, a.p, stride_of(a.ntr_max), a.extra != 0, a.fit_mode != 0);
+  carve_warp(w, ws, a.p, stride_of(a.ntr_max), a.extra != 0, a.fit_mode != 0, a.mae != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
 }
 
-// calls fn(kernel) with the variant for (fit mode, test rows per lane, split mode)
+// calls fn(kernel) with the variant for (fit mode, test rows per lane, split mode, criterion)
+template <bool kFit, int TM, bool kExtra, typename Fn>
+static auto with_crit(const SmallArgs& a, Fn&& fn) {
+  return a.mae ? fn(small_tree_kernel<kFit, TM, kExtra, true>) : fn(small_tree_kernel<kFit, TM, kExtra, false>);
+}
 template <bool kFit, int TM, typename Fn>
 static auto with_split(const SmallArgs& a, Fn&& fn) {
-  return a.extra ? fn(small_tree_kernel<kFit, TM, true>) : fn(small_tree_kernel<kFit, TM, false>);
+  return a.extra ? with_crit<kFit, TM, true>(a, fn) : with_crit<kFit, TM, false>(a, fn);
 }
 template <typename Fn>
 static auto with_variant(const SmallArgs& a, Fn&& fn) {

@@ -35,6 +35,7 @@ struct SmallArgs {
   uint64_t seed;
   int bootstrap, min_split, max_depth;
   int extra;                // ExtraTrees split mode (R29): one random threshold per drawn feature
+  int mae;                  // MAE criterion (R32): absolute deviations from weighted medians
   int n_mtry;
   int mtrys[kMaxMtry];
   int tree_lo, tree_hi;     // trees [tree_lo, tree_hi)

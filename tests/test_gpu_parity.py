@@ -519,3 +519,88 @@ def test_errors():
     with pytest.raises(rfg.RFError) as e:
         rfg.cross_validate_grid(X, y - 10, 4, 1, [2], [1])
     assert e.value.code == rfg.E_NONPOSITIVE_Y
+
+
+# ------------------------------------------------ MAE criterion (NEXT-4, R32) ---
+MAE_CASES = [
+    ("paper_time_m12", lambda: datagen.paper_shaped(189, "K20", "time"), dict(mtry=12, target=1)),
+    ("paper_time_m3", lambda: datagen.paper_shaped(189, "V100", "time"), dict(mtry=3, target=1)),
+    ("paper_power", lambda: datagen.paper_shaped(168, "P100", "power"), dict(mtry=4)),
+    ("ties", lambda: datagen.tiny(200, 5, 3, distinct=6), dict(mtry=2)),
+    ("target_ties", lambda: (datagen.tiny(150, 4, 4)[0], np.round(datagen.tiny(150, 4, 4)[1], 0)), dict(mtry=3)),
+    ("noboot", lambda: datagen.tiny(120, 4, 5), dict(mtry=4, bootstrap=False)),
+    ("depth3", lambda: datagen.paper_shaped(189, "TitanXp", "time"), dict(mtry=5, max_depth=3, target=1)),
+    ("mss5", lambda: datagen.tiny(150, 6, 8, distinct=20), dict(mtry=3, min_samples_split=5)),
+    ("n255", lambda: datagen.tiny(255, 3, 9), dict(mtry=1)),
+    ("n2", lambda: (np.array([[0.0], [1.0]]), np.array([1.0, 3.0])), dict(mtry=1)),
+    ("const", lambda: (datagen.tiny(40, 3, 1)[0], np.full(40, 2.5)), dict(mtry=2)),
+    ("p40", lambda: datagen.tiny(90, 40, 6, distinct=30), dict(mtry=13)),
+    # ExtraTrees + MAE: the paper's best models (T4/T5 P:858-861)
+    ("extra_time_m12", lambda: datagen.paper_shaped(189, "K20", "time"), dict(mtry=12, target=1, bootstrap=False,
+                                                                             split_mode=2)),
+    ("extra_power_boot", lambda: datagen.paper_shaped(168, "GTX1650", "power"), dict(mtry=4, split_mode=2)),
+    ("extra_ties", lambda: datagen.tiny(200, 5, 3, distinct=6), dict(mtry=2, split_mode=2, bootstrap=False)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", MAE_CASES, ids=[c[0] for c in MAE_CASES])
+def test_mae_fit_structures_bit_exact(name, data, kw):
+    """Structures, medians (leaf values) and leaf row sets bit-exact; the MAE costs are exact
+    integers on both sides, so the chosen splits cannot differ."""
+    X, y = data()
+    of = oracle.fit(X, y, ntree=16, seed=31, leaf_rows=True, criterion=1, **kw)
+    gf = rfg.fit(X, y, ntree=16, seed=31, debug=True, criterion=rfg.CRITERION_MAE, **kw)
+    _compare_forest(gf, of, X)
+    Q = np.random.default_rng(1).permuted(np.concatenate([X, X]), axis=0)  # columns shuffled independently
+    np.testing.assert_allclose(rfg.predict(gf, Q), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
+def test_mae_fit_many_seeds_paper_shaped():
+    X, y = datagen.paper_shaped(189, "GTX1650", "time")
+    for seed in range(4):
+        for sm in (0, 2):
+            of = oracle.fit(X, y, ntree=32, seed=seed, mtry=3, target=1, split_mode=sm, criterion=1)
+            gf = rfg.fit(X, y, ntree=32, seed=seed, mtry=3, target=1, split_mode=sm, criterion=1)
+            _compare_forest(gf, of, X)
+
+
+@pytest.mark.parametrize("custom,split_mode,boot", [(True, 0, True), (False, 0, True), (True, 2, False)])
+def test_mae_cv_parity(custom, split_mode, boot):
+    X, y = datagen.paper_shaped(189 if custom else 168, "V100", "time" if custom else "power")
+    f = oracle.make_folds(y, 10, 2, seed=9, custom=custom)
+    kw = dict(fold_ids=f, target=1 if custom else 0, seed=9, bootstrap=boot, split_mode=split_mode,
+              want_pred=True, criterion=1)
+    fm_o, pr_o = oracle.cv_grid(X, y, 10, 2, [4, 12], [12, 3], **kw)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 10, 2, [4, 12], [12, 3], **kw)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
+    # device twin
+    fm_d = rfg.cross_validate_grid(_cuda(X), _cuda(y), 10, 2, [4, 12], [12, 3], fold_ids=_cuda(f, torch.int32),
+                                   target=kw["target"], seed=9, bootstrap=boot, split_mode=split_mode,
+                                   criterion=1)
+    np.testing.assert_allclose(fm_d.cpu().numpy(), fm_o, rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("split_mode", [0, 2])
+def test_mae_importance_parity(split_mode):
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    kw = dict(mtry=6, target=1, split_mode=split_mode, bootstrap=split_mode == 0, criterion=1)
+    of = oracle.fit(X, y, ntree=8, seed=23, **kw)
+    gf = rfg.fit(X, y, ntree=8, seed=23, **kw)
+    _compare_forest(gf, of, X)
+    imp, raw = gf.importance(raw=True)
+    np.testing.assert_allclose(raw, np.stack([t.imp_raw for t in of.trees]), rtol=1e-12, atol=0)
+    np.testing.assert_allclose(imp, of.importance(), rtol=0, atol=1e-12)
+
+
+def test_mae_unsupported_shapes():
+    X, y = datagen.paper_shaped(600, "K20", "time")
+    with pytest.raises(rfg.RFError) as e:  # n_tr > 255: no CTA-resident MAE path
+        rfg.fit(X, y, ntree=2, mtry=3, target=1, criterion=1)
+    assert e.value.code == rfg.E_UNSUPPORTED
+    with pytest.raises(rfg.RFError) as e:  # histogram mode has no MAE variant (R32)
+        rfg.fit(X[:100], y[:100], ntree=2, mtry=3, target=1, split_mode=rfg.SPLIT_HIST256, criterion=1)
+    assert e.value.code == rfg.E_UNSUPPORTED
+    with pytest.raises(rfg.RFError) as e:
+        rfg.cross_validate_grid(X, y, 2, 1, [2], [3], target=1, criterion=1)
+    assert e.value.code == rfg.E_UNSUPPORTED
