@@ -13,6 +13,12 @@
 namespace rf {
 namespace {
 
+// Tree walks are chains of dependent loads (node -> feature -> child), so one walk at a
+// time leaves the SM waiting on L2 latency.  Each thread walks kG trees at once (kG
+// independent chains in flight), then adds their leaf values in tree order, so the sum is
+// bit-identical to walking the trees one by one.
+constexpr int kG = 8;
+
 __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ nodes,
                                                  const uint64_t* __restrict__ tree_off, int T,
                                                  const double* __restrict__ X, long long n, int p,
@@ -21,14 +27,33 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
        r += (long long)gridDim.x * blockDim.x) {
     const double* x = X + r * p;
     double s = 0.0;
-    for (int t = 0; t < T; ++t) {
-      const Node16* tn = nodes + tree_off[t];
-      uint32_t i = 0;
-      Node16 nd = tn[0];
-      while (nd.feat >= 0) {
-        i = nd.left + ((x[nd.feat] <= nd.v) ? 0u : 1u);
-        nd = tn[i];
+    int t = 0;
+    for (; t + kG <= T; t += kG) {
+      const Node16* tn[kG];
+      Node16 nd[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        tn[g] = nodes + __ldg(tree_off + t + g);
+        nd[g] = tn[g][0];
       }
+      bool open = true;
+      while (open) {
+        open = false;
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          if (nd[g].feat >= 0) {
+            nd[g] = tn[g][nd[g].left + ((__ldg(x + nd[g].feat) <= nd[g].v) ? 0u : 1u)];
+            open = true;
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) s += nd[g].v;
+    }
+    for (; t < T; ++t) {
+      const Node16* tn = nodes + tree_off[t];
+      Node16 nd = tn[0];
+      while (nd.feat >= 0) nd = tn[nd.left + ((__ldg(x + nd.feat) <= nd.v) ? 0u : 1u)];
       s += nd.v;
     }
     if (mode == 1) s = s / (double)T;
