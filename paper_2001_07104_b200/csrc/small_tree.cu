@@ -717,13 +717,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         // pass 1: lane totals
         uint32_t lw = 0;
         uint64_t ls = 0;
+        // the next element's row id is loaded while this element's weight and target load
+        uint8_t r1 = L[lbase + st + i];
         #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
-          const uint8_t r = L[lbase + st + i];
+          const uint8_t r = r1;
           const uint32_t wv = act ? (uint32_t)ws.w[r] : 0u;
-          lw += wv;
-          ls += (uint64_t)((int64_t)wv * cs.tq[r]);
+          const int64_t tv = cs.tq[r];
           if (++i == ln && c + 1 < cnt) {
             i = 0;
             if (++j == m) {
@@ -735,6 +736,9 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
             f = ws.feat[k * p + j];
             lbase = f * ntr_max;
           }
+          r1 = L[lbase + st + min(i, ln - 1)];
+          lw += wv;
+          ls += (uint64_t)((int64_t)wv * tv);
         }
         uint32_t tW;
         uint64_t tS;
@@ -754,16 +758,22 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
         uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
         uint8_t r = L[lbase + st + i];
         uint32_t rkr = cs.lrank[lbase + r];
+        // the element's weight and target are loaded one iteration ahead (off the
+        // critical path of the prefix sums -> reciprocal table -> fp64 score chain)
+        uint32_t wr = ws.w[r];
+        int64_t tr = cs.tq[r];
         int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
         #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
-          const uint32_t wv = act ? (uint32_t)ws.w[r] : 0u;
+          const uint32_t wv = act ? wr : 0u;
           cW += wv;
-          cS += (uint64_t)((int64_t)wv * cs.tq[r]);
+          cS += (uint64_t)((int64_t)wv * tr);
           const bool hasNext = i + 1 < ln;
           uint8_t rn = L[lbase + st + (hasNext ? i + 1 : i)];
           uint32_t rkn = cs.lrank[lbase + rn];
+          wr = ws.w[rn];
+          tr = cs.tq[rn];
           const uint32_t WL = cW - segW;
           const int64_t SL = (int64_t)(cS - segS);
           const uint32_t WR = Wk - WL;
@@ -805,6 +815,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallA
             segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
             rn = L[lbase + st];
             rkn = cs.lrank[lbase + rn];
+            wr = ws.w[rn];
+            tr = cs.tq[rn];
           } else if (act) {
             ++i;
           }
