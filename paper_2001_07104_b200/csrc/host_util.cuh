@@ -2,15 +2,32 @@
 // stream-ordered scratch allocations and per-kernel CUDA-event profiling.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdint>
 #include <vector>
 
 namespace rf {
+
+// Keep freed scratch memory in the device's default pool (release threshold = max):
+// with the default threshold 0 the pool returns its memory to the driver at every
+// synchronisation, and the next call maps it again (a 128-tree large-path batch
+// allocates ~5 GB: re-mapping it cost ~1.5 s per rf_fit call).  Once per device.
+inline void retain_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
 
 // stream-ordered scratch allocations (cudaMallocAsync pool), freed at scope exit
 struct Scratch {
   cudaStream_t s;
   std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+  explicit Scratch(cudaStream_t st) : s(st) { retain_pool(); }
   ~Scratch() {
     for (void* p : ptrs) cudaFreeAsync(p, s);
   }

@@ -112,6 +112,8 @@ struct Batch {
   uint32_t* keys;           // [B][2]
   uint8_t* w;               // [B][n] by global row
   uint8_t* side;            // [B][n]
+  uint32_t* sideBits;       // [B][nbw] go-left bit per row (fused partition path) or null
+  int nbw;                  // words per tree in sideBits = ceil(n / 32)
   uint32_t* L[2];           // [B][p][ntr]
   uint32_t* posNode[2];     // [B*ntr] concatenated positions -> node
   Nodes nd[2];
@@ -462,6 +464,150 @@ __global__ void __launch_bounds__(kThreads) k_search_eval(Batch b, int cur, long
   }
 }
 
+// Single-pass search (decoupled look-back): a CTA takes the next tile id from a counter,
+// sums its elements (pass 1, caching each element's weight and target in shared memory),
+// publishes the tile aggregate, then walks back over the predecessors' published
+// aggregates / inclusive prefixes for its exclusive prefix -- no separate totals kernel
+// and no device-wide scan, and pass 2 reads the cached weights/targets instead of
+// gathering them again.  Tile ids follow CTA start order, and every CTA publishes its
+// aggregate before it waits, so the look-back cannot deadlock.  Flags carry a per-level
+// epoch ((epoch << 2) | state; state 1 = aggregate, 2 = inclusive), so the status
+// array is never reset.
+struct TileStat {
+  unsigned long long aw, as, iw, is;  // aggregate (W, S), inclusive prefix (W, S)
+};
+
+__global__ void __launch_bounds__(kThreads) k_search_fused(Batch b, int cur, long long E, unsigned long long* ncand,
+                                                           uint32_t* tileCtr, TileStat* stat, uint32_t* flags,
+                                                           uint32_t epoch) {
+  __shared__ uint32_t s_tile;
+  __shared__ WS2 s_pref;
+  __shared__ long long s_t[kTile];
+  __shared__ uint8_t s_w[kTile];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tileCtr, 1u);
+  __syncthreads();
+  const long long tile = s_tile;
+  const Nodes& nd = b.nd[cur];
+  const uint32_t* posNode = b.posNode[cur];
+  const uint32_t* L = b.L[cur & 1];
+  const long long e0 = tile * kTile + (long long)threadIdx.x * kKC;
+  const long long e1 = min(e0 + kKC, E);
+  const int cbase = threadIdx.x * kKC;
+  // pass 1: thread totals (weights and targets cached)
+  unsigned long long lw = 0, ls = 0;
+  Cursor c0;
+  if (e0 < e1) {
+    cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
+    Cursor c = c0;
+    const uint8_t* w = b.w + (size_t)c.t * b.n;
+    for (long long e = e0; e < e1; ++e) {
+      const uint32_t r = L[c.listBase + c.i];
+      const uint32_t wv = w[r];
+      const long long tv = b.tq[r];
+      s_w[cbase + (int)(e - e0)] = (uint8_t)wv;
+      s_t[cbase + (int)(e - e0)] = tv;
+      lw += wv;
+      ls += (unsigned long long)((long long)wv * tv);
+      if (++c.i == c.len && e + 1 < e1) cursor_next_segment(b, nd, c);
+    }
+  }
+  using BS = cub::BlockScan<WS2, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  WS2 ex, agg;
+  BS(tmp).ExclusiveScan(WS2{lw, ls}, ex, WS2{0ull, 0ull}, WS2Sum(), agg);
+  if (threadIdx.x == 0) {
+    volatile TileStat* vs = stat;
+    volatile uint32_t* vf = flags;
+    unsigned long long pw = 0, ps = 0;
+    if (tile == 0) {
+      vs[0].iw = agg.w; vs[0].is = agg.s;
+      __threadfence();
+      vf[0] = (epoch << 2) | 2u;
+    } else {
+      vs[tile].aw = agg.w; vs[tile].as = agg.s;
+      __threadfence();
+      vf[tile] = (epoch << 2) | 1u;
+      for (long long k = tile - 1; k >= 0; --k) {
+        uint32_t fl;
+        do { fl = vf[k]; } while ((fl >> 2) != epoch || (fl & 3u) == 0u);
+        __threadfence();
+        if (fl & 2u) { pw += vs[k].iw; ps += vs[k].is; break; }
+        pw += vs[k].aw; ps += vs[k].as;
+      }
+      vs[tile].iw = pw + agg.w; vs[tile].is = ps + agg.s;
+      __threadfence();
+      vf[tile] = (epoch << 2) | 2u;
+    }
+    s_pref = WS2{pw, ps};
+  }
+  __syncthreads();
+  unsigned long long cW = s_pref.w + ex.w, cS = s_pref.s + ex.s;
+  unsigned int nc = 0;
+  if (e0 < e1) {  // pass 2 (no early return: the candidate count below is a full-warp shuffle)
+  Cursor c = c0;
+  unsigned long long segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
+  unsigned long long segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
+  unsigned long long rkey = 0ull, raux = ~0ull;
+  int rg = c.g;
+  const uint32_t* grank = b.grank;
+  uint32_t r = L[c.listBase + c.i];
+  uint32_t rk = grank[(size_t)c.f * b.n + r];
+  for (long long e = e0; e < e1; ++e) {
+    const uint32_t wv = s_w[cbase + (int)(e - e0)];
+    cW += wv;
+    cS += (unsigned long long)((long long)wv * s_t[cbase + (int)(e - e0)]);
+    const bool hasNext = c.i + 1 < c.len;
+    uint32_t rn = r, rkn = rk;
+    if (hasNext) {
+      rn = L[c.listBase + c.i + 1];
+      bool cand;
+      if (b.extra) {
+        cand = (uint32_t)c.i == c.xb;  // the segment's one candidate (R29)
+      } else {
+        rkn = grank[(size_t)c.f * b.n + rn];
+        cand = rkn != rk;
+      }
+      if (cand) {
+        const unsigned long long WL = cW - segW;
+        const long long SL = (long long)(cS - segS);
+        const unsigned long long WR = (unsigned long long)c.W - WL;
+        const long long SR = c.S - SL;
+        const double G = split_gain((long long)WL, SL, (long long)WR, SR);
+        const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
+        const unsigned long long aux = ((unsigned long long)c.j << 32) | (unsigned long long)c.i;  // R9
+        ++nc;
+        if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
+      }
+    }
+    if (e + 1 < e1) {
+      if (!hasNext) {
+        const int pg = c.g;
+        cursor_next_segment(b, nd, c);
+        if (c.g != pg) {
+          if (rkey) cas128(&b.best[pg], rkey, raux);
+          rkey = 0ull; raux = ~0ull;
+          rg = c.g;
+        }
+        segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
+        segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
+        rn = L[c.listBase];
+        rkn = grank[(size_t)c.f * b.n + rn];
+      } else {
+        ++c.i;
+      }
+    }
+    r = rn;
+    rk = rkn;
+  }
+  if (rkey) cas128(&b.best[rg], rkey, raux);
+  }
+  if (ncand) {
+    unsigned long long v = nc;
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(ncand, v);
+  }
+}
+
 __global__ void k_decide(Batch b, int cur, int NO) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= NO) return;
@@ -499,7 +645,11 @@ __global__ void k_mark(Batch b, int cur, int NP) {
       const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + start;
       const uint32_t r = L[i];
       const bool left = i <= bi;
-      b.side[(size_t)t * b.n + r] = left ? 1 : 0;
+      if (b.sideBits) {
+        if (left) atomicOr(&b.sideBits[(size_t)t * b.nbw + (r >> 5)], 1u << (r & 31u));
+      } else {
+        b.side[(size_t)t * b.n + r] = left ? 1 : 0;
+      }
       const long long tv = b.tq[r];
       const long long ref = b.tq[left ? L[0] : L[bi + 1]];
       if (tv != ref) b.nc[2 * g + (left ? 0 : 1)] = 1;
@@ -1046,6 +1196,136 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
   }
 }
 
+// ---- fused multi-list partition (exact and ExtraTrees modes) -------------------
+// The per-position split information is list independent, so it is computed once per
+// level (k_part_desc) instead of once per (list, position); the go-left flags are one
+// bit per row, staged in shared memory per tree (no global gathers); one CTA streams
+// a group of G lists of one tree through the position space in chunks of 1024 with a
+// running carry per list (no count pass, no device-wide scan, each list read once).
+// The four lists of a scan step share one 64-bit block scan (16-bit fields).
+constexpr int kPLThreads = 256, kPLItems = 4, kPLChunk = kPLThreads * kPLItems, kPLMaxG = 8;
+
+// desc[q] for current position q: x = left rows of the earlier split nodes of the tree
+// (leftBefore at the node start, the same in every list), y = node start (tree-local)
+// | bit 31 = split, z / w = first next-level position (tree-local) of the left / right
+// child or ~0 if that child is not open.
+__global__ void k_part_desc(Batch b, int cur, int NP, const uint32_t* __restrict__ nextPos0,
+                            const uint32_t* __restrict__ nlBase, uint4* __restrict__ desc) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= NP) return;
+  const Nodes& nd = b.nd[cur];
+  const uint32_t g = b.posNode[cur][q];
+  if (!b.best[g].key) {
+    desc[q] = make_uint4(0u, 0u, ~0u, ~0u);
+    return;
+  }
+  const uint32_t t = nd.tree[g];
+  const U4S sc = b.chScan[g];
+  const uint32_t nl = b.chVal[g].nl, fl = b.chFlags[g];
+  const uint32_t cL = sc.pos - nextPos0[t];
+  desc[q] = make_uint4(sc.nl - nlBase[t], nd.start[g] | 0x80000000u, (fl & 1u) ? cL : ~0u,
+                       (fl & 2u) ? cL + ((fl & 1u) ? nl : 0u) : ~0u);
+}
+
+__global__ void __launch_bounds__(kPLThreads) k_part_lists(Batch b, int cur, int G, const uint4* __restrict__ desc) {
+  extern __shared__ uint32_t sbits[];
+  const int t = blockIdx.x, f0 = blockIdx.y * G;
+  const int nf = min(G, b.nl - f0);
+  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
+  if (N == 0 || nf <= 0) return;
+  const uint32_t* gb = b.sideBits + (size_t)t * b.nbw;
+  for (int i = threadIdx.x; i < b.nbw; i += kPLThreads) sbits[i] = gb[i];
+  __syncthreads();
+  using BS = cub::BlockScan<unsigned long long, kPLThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  uint32_t carry[kPLMaxG];
+#pragma unroll
+  for (int l = 0; l < kPLMaxG; ++l) carry[l] = 0;
+  const uint32_t* Lsrc = b.L[cur & 1] + ((size_t)t * b.nl + f0) * b.ntr;
+  uint32_t* Ldst = b.L[(cur & 1) ^ 1] + ((size_t)t * b.nl + f0) * b.ntr;
+  for (uint32_t base = 0; base < N; base += kPLChunk) {
+    const uint32_t i0 = base + threadIdx.x * kPLItems;
+    uint4 d[kPLItems];
+#pragma unroll
+    for (int it = 0; it < kPLItems; ++it)
+      d[it] = (i0 + it < N) ? desc[pos0 + i0 + it] : make_uint4(0u, 0u, ~0u, ~0u);
+#pragma unroll
+    for (int fg = 0; fg < kPLMaxG; fg += 4) {
+      if (fg >= nf) break;
+      uint32_t rr[4][kPLItems];
+      uint32_t lmask = 0;  // bit 4l + it: element it of list fg + l goes left (split nodes only)
+      unsigned long long packed = 0;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int it = 0; it < kPLItems; ++it) {
+          rr[l][it] = 0;
+          if (fg + l < nf && i0 + it < N) {
+            const uint32_t r = Lsrc[(size_t)(fg + l) * b.ntr + i0 + it];
+            rr[l][it] = r;
+            const uint32_t lf = (d[it].y >> 31) & (sbits[r >> 5] >> (r & 31u)) & 1u;
+            lmask |= lf << (4 * l + it);
+            c += lf;
+          }
+        }
+        packed |= (unsigned long long)c << (16 * l);
+      }
+      unsigned long long ex, tot;
+      BS(tmp).ExclusiveSum(packed, ex, tot);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if (fg + l >= nf) break;
+        uint32_t lb = carry[fg + l] + (uint32_t)((ex >> (16 * l)) & 0xFFFFull);
+#pragma unroll
+        for (int it = 0; it < kPLItems; ++it) {
+          const uint32_t i = i0 + it;
+          if (i >= N || !(d[it].y >> 31)) continue;
+          const bool left = (lmask >> (4 * l + it)) & 1u;
+          const uint32_t wl = lb - d[it].x;  // left rows of this node before i (this list)
+          const uint32_t dst = left ? d[it].z : d[it].w;
+          if (dst != ~0u) Ldst[(size_t)(fg + l) * b.ntr + dst + (left ? wl : (i - (d[it].y & 0x7FFFFFFFu)) - wl)] =
+              rr[l][it];
+          lb += left ? 1u : 0u;
+        }
+        carry[fg + l] += (uint32_t)((tot >> (16 * l)) & 0xFFFFull);
+      }
+      __syncthreads();  // tmp reuse
+    }
+  }
+}
+
+// next-level position -> node map (one warp per next-level open node)
+__global__ void k_fill_posnode(Batch b, int nxt, const uint32_t* __restrict__ counters) {
+  const Nodes& nx = b.nd[nxt];
+  const uint32_t NOn = counters[0];
+  const int lane = threadIdx.x & 31;
+  for (uint32_t oi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; oi < NOn; oi += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t base = b.tPos0[nx.tree[oi]] + nx.start[oi], len = nx.len[oi];
+    for (uint32_t i = lane; i < len; i += 32) b.posNode[nxt][base + i] = oi;
+  }
+}
+
+// debug: leaf of every in-bag row that stops at this level (list 0 order)
+__global__ void k_part_debug_rows(Batch b, int cur, int NP) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= NP) return;
+  const Nodes& nd = b.nd[cur];
+  const uint32_t g = b.posNode[cur][q];
+  const uint32_t t = nd.tree[g];
+  const uint32_t r = b.L[cur & 1][(size_t)t * b.nl * b.ntr + (q - b.tPos0[t])];
+  if (!b.best[g].key) {
+    b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
+    return;
+  }
+  const bool left = (b.sideBits[(size_t)t * b.nbw + (r >> 5)] >> (r & 31u)) & 1u;
+  const uint32_t fl = b.chFlags[g];
+  if (!(left ? (fl & 1u) : (fl & 2u))) {
+    const uint32_t cb = b.out[(size_t)t * b.cap + nd.bfs[g]].left;
+    b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)(cb + (left ? 0u : 1u));
+  }
+}
+
 __global__ void k_init_level0(Batch b, const uint32_t* rootInfo, uint32_t* counters /*[2]: NO, NP*/) {
   // single thread: root nodes of non-leaf trees, per-tree position spaces
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -1141,7 +1421,12 @@ struct HistBufs {  // histogram mode: per-chunk-of-nodes histograms and work-ite
   uint32_t* pref = nullptr; // [cap + 1]
 };
 
-struct PartBufs {  // partition tiles
+struct PartBufs {  // per-level scratch: search look-back status, partition tiles
+  uint32_t* tileCtr = nullptr;  // search: next tile id
+  TileStat* stat = nullptr;     // search: [tiles_max] published aggregates / prefixes
+  uint32_t* flags = nullptr;    // search: [tiles_max] (epoch << 2) | state, zeroed once
+  uint32_t* epoch = nullptr;    // host: last search epoch
+  uint4* desc = nullptr;     // [npmax] per-position split descriptors (fused path)
   uint32_t* tab = nullptr;   // [2 B]
   uint32_t* cnt = nullptr;   // [max tiles]
   uint32_t* pref = nullptr;  // [max tiles]
@@ -1153,6 +1438,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
                      void* cub_tmp, size_t cub_bytes, uint32_t* rootInfo, uint32_t* counters, uint32_t* hcounters,
                      uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp, const HistBufs& hb,
                      const PartBufs& pb, unsigned long long* ncand, cudaStream_t s, std::string& err) {
+  // fused partition: lists per CTA so that the grid covers the SMs at least twice
+  int G = kPLMaxG;
+  while (G > 1 && (long long)b.B * ((b.nl + G - 1) / G) < 2 * 148) G >>= 1;
+  const size_t plSmem = (size_t)b.nbw * 4;
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
   LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
   if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
@@ -1198,14 +1487,13 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       const long long tiles = (E + kTile - 1) / kTile;
       {
         ProfScope ps("large_search", s);
-        k_search_tot<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E);
-        tb = cub_bytes;
-        LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, b.tileTot, b.tileTot, WS2Sum(), WS2{0ull, 0ull},
-                                           (int)tiles, s));
-        k_search_eval<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand);
-        note_launch(2);
+        const uint32_t epoch = ++*pb.epoch;
+        LCK(cudaMemsetAsync(pb.tileCtr, 0, 4, s));
+        k_search_fused<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand, pb.tileCtr, pb.stat, pb.flags, epoch);
+        note_launch();
       }
       k_decide<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
+      if (b.sideBits) LCK(cudaMemsetAsync(b.sideBits, 0, (size_t)b.B * b.nbw * 4, s));
       k_mark<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
       note_launch(2);
     } else {
@@ -1239,7 +1527,17 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     k_tree_update<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, (int)NO, nextNode0, nextPos0, nlBase);
     k_children_write<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, nextNode0, nextPos0, nlBase, depth);
     note_launch(2);
-    {
+    if (b.sideBits) {
+      ProfScope ps("large_partition", s);
+      k_part_desc<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP, nextPos0, nlBase, pb.desc);
+      note_launch();
+      if (b.leaf_of_row) {
+        k_part_debug_rows<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
+        note_launch();
+      }
+      k_part_lists<<<dim3((unsigned)b.B, (unsigned)((b.nl + G - 1) / G)), kPLThreads, plSmem, s>>>(b, cur, G, pb.desc);
+      note_launch();
+    } else {
       ProfScope ps("large_partition", s);
       // tile table of the current level (per-tree position counts read back at the level start)
       uint32_t tiles = 0;
@@ -1262,6 +1560,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     }
     k_set_next_tree_tables<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, nextNode0, nextPos0, counters);
     note_launch();
+    if (b.sideBits) {  // next-level position -> node map (the fused partition does not write it)
+      k_fill_posnode<<<std::min<unsigned>(nblk(2 * NO * 32, 256), 148 * 16), 256, 0, s>>>(b, cur ^ 1, counters);
+      note_launch();
+    }
     LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
     LCK(cudaMemcpyAsync(htPos0, b.tPos0, (size_t)(b.B + 1) * 4, cudaMemcpyDeviceToHost, s));
     LCK(cudaStreamSynchronize(s));
@@ -1458,6 +1760,11 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(sc.alloc(&b.keys, (size_t)2 * B));
   LCK(sc.alloc(&b.w, (size_t)B * n + 4));
   LCK(sc.alloc(&b.side, (size_t)B * n));
+  // fused partition path (exact / ExtraTrees): go-left bits per row, staged per tree in
+  // shared memory by the partition CTAs (n <= 2^20 rows: <= 128 KB)
+  b.nbw = (n + 31) / 32;
+  const bool fused_part = !hist && n <= (1 << 20);
+  if (fused_part) LCK(sc.alloc(&b.sideBits, (size_t)B * b.nbw));
   for (int i = 0; i < 2; ++i) {
     LCK(sc.alloc(&b.L[i], (size_t)B * nlists * ntr));
     LCK(sc.alloc(&b.posNode[i], (size_t)pl.npmax));
@@ -1499,6 +1806,16 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   PartBufs pbufs;
   const long long max_tiles = (long long)nlists * (B + pl.npmax / kPartTile + 1) + 1;
   LCK(sc.alloc(&pbufs.tab, (size_t)2 * B));
+  uint32_t search_epoch = 0;
+  pbufs.epoch = &search_epoch;
+  LCK(sc.alloc(&pbufs.tileCtr, 1));
+  LCK(sc.alloc(&pbufs.stat, (size_t)pl.tiles_max + 1));
+  LCK(sc.alloc(&pbufs.flags, (size_t)pl.tiles_max + 1));
+  LCK(cudaMemsetAsync(pbufs.flags, 0, ((size_t)pl.tiles_max + 1) * 4, s));
+  if (fused_part) {
+    LCK(sc.alloc(&pbufs.desc, (size_t)pl.npmax));
+    LCK(cudaFuncSetAttribute(k_part_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
+  }
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
   struct HostFree {
