@@ -499,10 +499,9 @@ __global__ void __launch_bounds__(kThreads) k_search_fused(Batch b, int cur, lon
   if (e0 < e1) {
     cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
     Cursor c = c0;
-    const uint8_t* w = b.w + (size_t)c.t * b.n;
     for (long long e = e0; e < e1; ++e) {
       const uint32_t r = L[c.listBase + c.i];
-      const uint32_t wv = w[r];
+      const uint32_t wv = b.w[(size_t)c.t * b.n + r];  // (the chunk may span trees)
       const long long tv = b.tq[r];
       s_w[cbase + (int)(e - e0)] = (uint8_t)wv;
       s_t[cbase + (int)(e - e0)] = tv;
@@ -515,30 +514,56 @@ __global__ void __launch_bounds__(kThreads) k_search_fused(Batch b, int cur, lon
   __shared__ typename BS::TempStorage tmp;
   WS2 ex, agg;
   BS(tmp).ExclusiveScan(WS2{lw, ls}, ex, WS2{0ull, 0ull}, WS2Sum(), agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-wide look-back: 32 predecessors per step; aggregates are summed until the
+    // nearest published inclusive prefix (tile 0 always publishes one)
     volatile TileStat* vs = stat;
     volatile uint32_t* vf = flags;
+    const int lane = threadIdx.x;
     unsigned long long pw = 0, ps = 0;
     if (tile == 0) {
-      vs[0].iw = agg.w; vs[0].is = agg.s;
-      __threadfence();
-      vf[0] = (epoch << 2) | 2u;
-    } else {
-      vs[tile].aw = agg.w; vs[tile].as = agg.s;
-      __threadfence();
-      vf[tile] = (epoch << 2) | 1u;
-      for (long long k = tile - 1; k >= 0; --k) {
-        uint32_t fl;
-        do { fl = vf[k]; } while ((fl >> 2) != epoch || (fl & 3u) == 0u);
+      if (lane == 0) {
+        vs[0].iw = agg.w; vs[0].is = agg.s;
         __threadfence();
-        if (fl & 2u) { pw += vs[k].iw; ps += vs[k].is; break; }
-        pw += vs[k].aw; ps += vs[k].as;
+        vf[0] = (epoch << 2) | 2u;
       }
-      vs[tile].iw = pw + agg.w; vs[tile].is = ps + agg.s;
-      __threadfence();
-      vf[tile] = (epoch << 2) | 2u;
+    } else {
+      if (lane == 0) {
+        vs[tile].aw = agg.w; vs[tile].as = agg.s;
+        __threadfence();
+        vf[tile] = (epoch << 2) | 1u;
+      }
+      for (long long k = tile - 1;; k -= 32) {
+        const long long kk = k - lane;
+        uint32_t fl = 0;
+        if (kk >= 0) {
+          do { fl = vf[kk]; } while ((fl >> 2) != epoch || (fl & 3u) == 0u);
+        }
+        __syncwarp();
+        __threadfence();
+        const unsigned incl = __ballot_sync(0xffffffffu, kk >= 0 && (fl & 2u));
+        const int stop = incl ? __ffs(incl) - 1 : 31;
+        unsigned long long vw = 0, vsum = 0;
+        if (kk >= 0 && lane <= stop) {
+          if ((fl & 2u) && lane == stop) { vw = vs[kk].iw; vsum = vs[kk].is; }
+          else { vw = vs[kk].aw; vsum = vs[kk].as; }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+          vw += __shfl_xor_sync(0xffffffffu, vw, d);
+          vsum += __shfl_xor_sync(0xffffffffu, vsum, d);
+        }
+        pw += vw;
+        ps += vsum;
+        if (incl) break;
+      }
+      if (lane == 0) {
+        vs[tile].iw = pw + agg.w; vs[tile].is = ps + agg.s;
+        __threadfence();
+        vf[tile] = (epoch << 2) | 2u;
+      }
     }
-    s_pref = WS2{pw, ps};
+    if (lane == 0) s_pref = WS2{pw, ps};
   }
   __syncthreads();
   unsigned long long cW = s_pref.w + ex.w, cS = s_pref.s + ex.s;
@@ -686,7 +711,11 @@ __global__ void k_mark(Batch b, int cur, int NP) {
 // the candidate after cut c is valid iff WL > 0 and WR > 0; threshold = cut
 // value, threshold index = c; ties -> first drawn feature (R9), then lowest c.
 constexpr int kHistThreads = 256;
+#ifdef RF_HIST_ATOMICS
 constexpr int kHistChunk = 8192;  // rows per histogram work item
+#else
+constexpr int kHistChunk = 1024;  // rows per histogram work item (rows and drawn bins staged in smem)
+#endif
 
 // one CTA per feature: cuts from the task's training rows sorted by x_f
 __global__ void k_cuts(const double* __restrict__ X, int p, const uint32_t* __restrict__ order, int ntr,
@@ -768,6 +797,7 @@ __global__ void k_hist_zero(Batch b, int cur, int g0, int g1, uint32_t* hW, unsi
   for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) { hW[base + i] = 0u; hS[base + i] = 0ull; }
 }
 
+#ifdef RF_HIST_ATOMICS
 // work item = (node, chunk of <= kHistChunk rows): shared-memory histograms of the drawn features
 __global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, int g0, int g1,
                                                              const uint32_t* itemPref, uint32_t* hW,
@@ -817,6 +847,113 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, i
     }
   }
 }
+
+size_t hist_build_smem(int m) { return (size_t)m * 256 * 12 + (size_t)m * 4 + 16; }
+#else
+// Work item = (node, chunk of <= kHistChunk rows).  Shared-memory atomics run at about
+// 2 cycles per lane (B300_MICROARCH: ATOMS spread-address), i.e. ~4 cycles per
+// (row, feature) for the (W, S) pair; instead each warp owns whole features with a
+// private 256-bin histogram and aggregates 32 rows at a time in registers: a warp
+// bitonic sort by bin, a segmented sum over equal bins, and one plain read-modify-write
+// per distinct bin by the run's last lane (no other lane or warp touches that bin).
+// The chunk's rows, weights, w*t_q and drawn bins are staged in shared memory once.
+// Sums are exact integers, so the result equals the atomic version bit for bit.
+__device__ __forceinline__ void hist_sort_step(int lane, int k, int j, uint32_t& key, uint32_t& wv,
+                                               unsigned long long& sv) {
+  const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, j);
+  const uint32_t ow = __shfl_xor_sync(0xffffffffu, wv, j);
+  const unsigned long long os = __shfl_xor_sync(0xffffffffu, sv, j);
+  const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+  if (lower == up ? ok < key : ok > key) { key = ok; wv = ow; sv = os; }
+}
+
+__global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, int g0, int g1,
+                                                             const uint32_t* itemPref, uint32_t* hW,
+                                                             unsigned long long* hS) {
+  extern __shared__ __align__(16) char sm[];
+  constexpr int R = kHistChunk, NW = kHistThreads / 32;
+  unsigned long long* sSv = reinterpret_cast<unsigned long long*>(sm);      // [R] w * t_q
+  unsigned long long* pS = sSv + R;                                          // [NW][256]
+  uint32_t* pW = reinterpret_cast<uint32_t*>(pS + NW * 256);                 // [NW][256]
+  uint32_t* sWv = pW + NW * 256;                                             // [R]
+  int* sF = reinterpret_cast<int*>(sWv + R);                                 // [m]
+  uint8_t* sB = reinterpret_cast<uint8_t*>(sF + b.m);                        // [m][R]
+  const int item = blockIdx.x;
+  int lo = g0, hi = g1;  // node: last g with itemPref[g - g0] <= item
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)itemPref[mid - g0] <= item) lo = mid; else hi = mid;
+  }
+  const int g = lo;
+  const uint32_t c = (uint32_t)(item - (int)itemPref[g - g0]);
+  const Nodes& nd = b.nd[cur];
+  const int t = (int)nd.tree[g];
+  const uint32_t start = nd.start[g], len = nd.len[g];
+  const uint32_t i0 = c * R, nr = min(len - i0, (uint32_t)R);
+  for (int j = threadIdx.x; j < b.m; j += blockDim.x) sF[j] = b.feat[(size_t)g * b.m + j];
+  __syncthreads();
+  const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr + start + i0;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) {
+    const uint32_t r = L[i];
+    const uint32_t wv = w[r];
+    sWv[i] = wv;
+    sSv[i] = (unsigned long long)((long long)wv * b.tq[r]);
+    const uint8_t* br = b.bins + (size_t)r * b.p;
+    for (int j = 0; j < b.m; ++j) sB[j * R + i] = br[sF[j]];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* hw = pW + warp * 256;
+  unsigned long long* hs = pS + warp * 256;
+  const size_t base = (size_t)(g - g0) * b.m * 256;
+  const bool single = len <= (uint32_t)R;
+  for (int j = warp; j < b.m; j += NW) {
+    for (int q = lane; q < 256; q += 32) { hw[q] = 0u; hs[q] = 0ull; }
+    __syncwarp();
+    for (uint32_t i = 0; i < nr; i += 32) {
+      const uint32_t e = i + lane;
+      uint32_t key = 256u, wv = 0u;
+      unsigned long long sv = 0ull;
+      if (e < nr) { key = sB[j * R + e]; wv = sWv[e]; sv = sSv[e]; }
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int d = k >> 1; d > 0; d >>= 1) hist_sort_step(lane, k, d, key, wv, sv);
+      // inclusive segmented sums over runs of equal keys (keys ascending across lanes)
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t okey = __shfl_up_sync(0xffffffffu, key, d);
+        const uint32_t ow = __shfl_up_sync(0xffffffffu, wv, d);
+        const unsigned long long os = __shfl_up_sync(0xffffffffu, sv, d);
+        if (lane >= d && okey == key) { wv += ow; sv += os; }
+      }
+      const uint32_t nkey = __shfl_down_sync(0xffffffffu, key, 1);
+      if (key < 256u && (lane == 31 || nkey != key)) {  // last lane of the run
+        hw[key] += wv;
+        hs[key] += sv;
+      }
+      __syncwarp();
+    }
+    const size_t ob = base + (size_t)j * 256;
+    for (int q = lane; q < 256; q += 32) {
+      if (single) {
+        hW[ob + q] = hw[q];
+        hS[ob + q] = hs[q];
+      } else if (hw[q]) {
+        atomicAdd(&hW[ob + q], hw[q]);
+        atomicAdd(&hS[ob + q], hs[q]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t hist_build_smem(int m) {
+  return (size_t)kHistChunk * 8 + (size_t)(kHistThreads / 32) * 256 * 12 + (size_t)kHistChunk * 4 + (size_t)m * 4 +
+         (size_t)m * kHistChunk;
+}
+#endif
 
 // one CTA per node: best cut over the drawn features (warp per feature, 8 bins per lane)
 __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int g1, const uint32_t* hW,
@@ -1499,7 +1636,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     } else {
       k_hist_reset<<<nblk(NO, 256), 256, 0, s>>>(b, (int)NO);
       note_launch();
-      const size_t hsm = (size_t)b.m * 256 * 12 + (size_t)b.m * 4 + 16;
+      const size_t hsm = hist_build_smem(b.m);
       ProfScope ps("hist_search", s);
       for (long long g0 = 0; g0 < NO; g0 += hb.cap) {
         const long long g1 = std::min<long long>(NO, g0 + hb.cap);
@@ -1744,9 +1881,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&hb.nch, (size_t)hb.cap + 1));
     LCK(sc.alloc(&hb.pref, (size_t)hb.cap + 1));
     LCK(cudaMemsetAsync(hb.nch, 0, ((size_t)hb.cap + 1) * 4, s));
-    const size_t hsm = (size_t)mtry * 256 * 12 + (size_t)mtry * 4 + 16;
+    const size_t hsm = hist_build_smem(mtry);
     if (hsm > 227 * 1024) {
-      err = "histogram mode: mtry too large for the shared-memory histograms (mtry <= 73)";
+      err = "histogram mode: mtry too large for the shared-memory staging of the drawn bins";
       return RF_E_UNSUPPORTED;
     }
     LCK(cudaFuncSetAttribute(k_hist_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
