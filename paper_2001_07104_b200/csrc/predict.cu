@@ -10,6 +10,8 @@
 #include "host_util.cuh"
 #include "predict.cuh"
 
+#include <algorithm>
+
 namespace rf {
 namespace {
 
@@ -17,15 +19,20 @@ namespace {
 // time leaves the SM waiting on L2 latency.  Each thread walks kG trees at once (kG
 // independent chains in flight), then adds their leaf values in tree order, so the sum is
 // bit-identical to walking the trees one by one.
+// The feature values are read from a feature-major copy of the row block (XT[f][r]):
+// the 32 lanes of a warp are 32 consecutive rows, and wherever they visit the same
+// node (the top levels of every tree) they read the same feature, i.e. 256 contiguous
+// bytes instead of 32 separate 512-byte-strided lines (ncu: L1 throughput was the
+// limiter of the row-major version).
 constexpr int kG = 8;
 
 __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ nodes,
                                                  const uint64_t* __restrict__ tree_off, int T,
-                                                 const double* __restrict__ X, long long n, int p,
+                                                 const double* __restrict__ XT, long long n, int p,
                                                  int mode, double* __restrict__ out) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
        r += (long long)gridDim.x * blockDim.x) {
-    const double* x = X + r * p;
+    const double* x = XT + r;  // feature f of row r at x[f * n]
     double s = 0.0;
     int t = 0;
     for (; t + kG <= T; t += kG) {
@@ -42,7 +49,7 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
 #pragma unroll
         for (int g = 0; g < kG; ++g) {
           if (nd[g].feat >= 0) {
-            nd[g] = tn[g][nd[g].left + ((__ldg(x + nd[g].feat) <= nd[g].v) ? 0u : 1u)];
+            nd[g] = tn[g][nd[g].left + ((__ldg(x + (size_t)nd[g].feat * n) <= nd[g].v) ? 0u : 1u)];
             open = true;
           }
         }
@@ -53,12 +60,30 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
     for (; t < T; ++t) {
       const Node16* tn = nodes + tree_off[t];
       Node16 nd = tn[0];
-      while (nd.feat >= 0) nd = tn[nd.left + ((__ldg(x + nd.feat) <= nd.v) ? 0u : 1u)];
+      while (nd.feat >= 0) nd = tn[nd.left + ((__ldg(x + (size_t)nd.feat * n) <= nd.v) ? 0u : 1u)];
       s += nd.v;
     }
     if (mode == 1) s = s / (double)T;
     if (mode == 2) s = exp(s / (double)T);
     out[r] = s;
+  }
+}
+
+// rows [r0, r0 + cn) of X (row-major, n x p) -> XT (p x cn, feature-major), 32 x 32 tiles
+__global__ void k_transpose(const double* __restrict__ X, long long r0, long long cn, int p, double* __restrict__ XT) {
+  __shared__ double tile[32][33];
+  const long long rb = blockIdx.x * 32LL;
+  const int fb = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const long long r = rb + k;
+    const int f = fb + threadIdx.x;
+    if (r < cn && f < p) tile[k][threadIdx.x] = X[(r0 + r) * p + f];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int f = fb + k;
+    const long long r = rb + threadIdx.x;
+    if (r < cn && f < p) XT[(size_t)f * cn + r] = tile[threadIdx.x][k];
   }
 }
 
@@ -124,11 +149,22 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     note_launch();
     return cudaGetLastError();
   }
-  long long blocks = (n + 255) / 256;
-  if (blocks > 148LL * 64) blocks = 148LL * 64;
-  k_predict<<<(unsigned)blocks, 256, 0, s>>>(nodes, tree_off, T, X, n, p, mode, out);
-  note_launch();
-  return cudaGetLastError();
+  // row blocks of <= ~512 MB transposed at a time
+  const long long chunk = std::max<long long>(4096, (512LL << 20) / (8LL * p));
+  Scratch sc(s);
+  double* XT;
+  cudaError_t e = sc.alloc(&XT, (size_t)std::min(n, chunk) * p);
+  if (e != cudaSuccess) return e;
+  for (long long r0 = 0; r0 < n; r0 += chunk) {
+    const long long cn = std::min(chunk, n - r0);
+    k_transpose<<<dim3((unsigned)((cn + 31) / 32), (unsigned)((p + 31) / 32)), dim3(32, 8), 0, s>>>(X, r0, cn, p, XT);
+    long long blocks = (cn + 255) / 256;
+    if (blocks > 148LL * 64) blocks = 148LL * 64;
+    k_predict<<<(unsigned)blocks, 256, 0, s>>>(nodes, tree_off, T, XT, cn, p, mode, out + r0);
+    note_launch(2);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t predict_finalize(const double* partial, long long n, int T, int target, double* out,
