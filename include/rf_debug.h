@@ -25,6 +25,12 @@ RF_API rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates);
    them; the normal build returns RF_E_UNSUPPORTED.  reset != 0 zeroes the
    counters after reading.  Synchronises the current device. */
 RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
+/* Test switches of this process (parity of alternative kernel paths):
+   "large_tiled_partition" = 1 makes the large path use the tiled count ->
+   scan -> scatter partition (otherwise only taken for the histogram mode and
+   n > 2^20) instead of the fused multi-list partition.  Unknown names return
+   RF_E_ARG. */
+RF_API rf_status rf_debug_set_option(const char* name, int64_t value);
 #ifdef __cplusplus
 }
 #endif

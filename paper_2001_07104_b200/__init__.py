@@ -39,7 +39,7 @@ ABI_SYMBOLS = [
     "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
     "rf_last_profile", "rf_set_profiling",
-    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles",
+    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles", "rf_debug_set_option",
 ]
 
 
@@ -106,6 +106,7 @@ def lib():
             "rf_debug_philox_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_counters": ([P, P], C.c_int),
             "rf_debug_phase_cycles": ([P, C.c_int], C.c_int),
+            "rf_debug_set_option": ([C.c_char_p, C.c_int64], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -447,6 +448,11 @@ def phase_cycles(reset=True):
     out = np.zeros(16, np.uint64)
     _check(lib().rf_debug_phase_cycles(_ptr(out), 1 if reset else 0))
     return dict(zip(PHASE_NAMES, out.tolist()))
+
+
+def debug_set_option(name: str, value: int):
+    """Test switch of alternative kernel paths (rf_debug_set_option)."""
+    _check(lib().rf_debug_set_option(name.encode(), int(value)))
 
 
 def candidate_count():

@@ -1061,6 +1061,15 @@ rf_status rf_debug_phase_cycles(uint64_t* out16, int reset) {
   return RF_OK;
 }
 
+rf_status rf_debug_set_option(const char* name, int64_t value) {
+  if (!name) return fail(RF_E_ARG, "name is NULL");
+  if (!strcmp(name, "large_tiled_partition")) {
+    rf::g_opt_tiled_partition = value != 0;
+    return RF_OK;
+  }
+  return fail(RF_E_ARG, "unknown option");
+}
+
 rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, uint64_t n, void* stream) {
   if (rf_status st = check_device()) return st;
   CK(rf::device_philox(dctr_key, dout, (int)n, static_cast<cudaStream_t>(stream)), "philox");

@@ -42,6 +42,13 @@ namespace rf {
 namespace {
 
 constexpr int kThreads = 128;
+// resident-CTA hints of the two streaming kernels (A/B variants via RF_DEFS)
+#ifndef RF_SEARCH_MINB
+#define RF_SEARCH_MINB 8
+#endif
+#ifndef RF_PART_MINB
+#define RF_PART_MINB 3
+#endif
 constexpr int kKC = 16;  // elements per thread in the search tiles
 constexpr int kTile = kThreads * kKC;
 
@@ -362,7 +369,7 @@ struct TileStat {
   unsigned long long aw, as, iw, is;  // aggregate (W, S), inclusive prefix (W, S)
 };
 
-__global__ void __launch_bounds__(kThreads) k_search_fused(Batch b, int cur, long long E, unsigned long long* ncand,
+__global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch b, int cur, long long E, unsigned long long* ncand,
                                                            uint32_t* tileCtr, TileStat* stat, uint32_t* flags,
                                                            uint32_t epoch) {
   __shared__ uint32_t s_tile;
@@ -1252,7 +1259,7 @@ __global__ void k_part_desc(Batch b, int cur, int NP, const uint32_t* __restrict
                        (fl & 2u) ? cL + ((fl & 1u) ? nl : 0u) : ~0u);
 }
 
-__global__ void __launch_bounds__(kPLThreads) k_part_lists(Batch b, int cur, int G, const uint4* __restrict__ desc) {
+__global__ void __launch_bounds__(kPLThreads, RF_PART_MINB) k_part_lists(Batch b, int cur, int G, const uint4* __restrict__ desc) {
   extern __shared__ uint32_t sbits[];
   const int t = blockIdx.x, f0 = blockIdx.y * G;
   const int nf = min(G, b.nl - f0);
@@ -1652,6 +1659,8 @@ __global__ void k_chunk_predict(const Node16* __restrict__ nodes, uint64_t cap, 
 
 }  // namespace
 
+int g_opt_tiled_partition = 0;
+
 static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
                              int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
                              cudaStream_t s, Scratch& sc, Node16** nodes_out, uint32_t** thr_out,
@@ -1788,7 +1797,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   // fused partition path (exact / ExtraTrees): go-left bits per row, staged per tree in
   // shared memory by the partition CTAs (n <= 2^20 rows: <= 128 KB)
   b.nbw = (n + 31) / 32;
-  const bool fused_part = !hist && n <= (1 << 20);
+  const bool fused_part = !hist && n <= (1 << 20) && !g_opt_tiled_partition;
   if (fused_part) LCK(sc.alloc(&b.sideBits, (size_t)B * b.nbw));
   for (int i = 0; i < 2; ++i) {
     LCK(sc.alloc(&b.L[i], (size_t)B * nlists * ntr));

@@ -11,6 +11,9 @@
 
 namespace rf {
 
+// test switch (rf_debug_set_option "large_tiled_partition"): force the tiled partition
+extern int g_opt_tiled_partition;
+
 // Grows trees [tree_lo, tree_hi) of task 0 over all rows.  Outputs (scratch
 // owned by `sc`): per-tree BFS node blocks of capacity *cap, node counts.
 rf_status fit_large(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,

@@ -604,3 +604,26 @@ def test_mae_unsupported_shapes():
     with pytest.raises(rfg.RFError) as e:
         rfg.cross_validate_grid(X, y, 2, 1, [2], [3], target=1, criterion=1)
     assert e.value.code == rfg.E_UNSUPPORTED
+
+
+# ------------------------------------------- alternative large-path kernels ---
+def test_large_partition_paths_agree():
+    """The fused multi-list partition (default for n <= 2^20) and the tiled count/scan/scatter
+    partition (histogram mode, n > 2^20) grow identical forests; the tiled one also matches the
+    oracle, leaf row sets included."""
+    X, y = datagen.scaled(20_000, 64)
+    a = rfg.fit(X, y, ntree=4, mtry=21, target=1, seed=3).export()
+    rfg.debug_set_option("large_tiled_partition", 1)
+    try:
+        b = rfg.fit(X, y, ntree=4, mtry=21, target=1, seed=3).export()
+        Xs, ys = datagen.tiny(600, 5, 17, distinct=40)
+        of = oracle.fit(Xs, ys, ntree=4, seed=5, mtry=3, leaf_rows=True)
+        gf = rfg.fit(Xs, ys, ntree=4, seed=5, mtry=3, debug=True)
+        _compare_forest(gf, of, Xs)
+    finally:
+        rfg.debug_set_option("large_tiled_partition", 0)
+    for key in ("feature", "left", "thr_index", "tree_off"):
+        assert np.array_equal(a[key], b[key]), key
+    assert np.array_equal(a["value"].view(np.int64), b["value"].view(np.int64))
+    with pytest.raises(rfg.RFError):
+        rfg.debug_set_option("no_such_option", 1)
