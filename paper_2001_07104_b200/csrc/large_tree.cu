@@ -374,9 +374,13 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
                                                            uint32_t epoch) {
   __shared__ uint32_t s_tile;
   __shared__ WS2 s_pref;
+  __shared__ int s_local;  // 1: the tile contains a segment start, its prefix is known locally
   __shared__ long long s_t[kTile];
   __shared__ uint8_t s_w[kTile];
-  if (threadIdx.x == 0) s_tile = atomicAdd(tileCtr, 1u);
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(tileCtr, 1u);
+    s_local = 0;
+  }
   __syncthreads();
   const long long tile = s_tile;
   const Nodes& nd = b.nd[cur];
@@ -385,13 +389,22 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   const long long e0 = tile * kTile + (long long)threadIdx.x * kKC;
   const long long e1 = min(e0 + kKC, E);
   const int cbase = threadIdx.x * kKC;
-  // pass 1: thread totals (weights and targets cached)
+  // pass 1: thread totals (weights and targets cached).  The absolute prefix at every
+  // segment start is known from the node prefixes (m bW[g] + j W[g]), so a tile that
+  // contains a segment start derives its own prefix and skips the look-back.
   unsigned long long lw = 0, ls = 0;
+  bool has_start = false;
+  unsigned long long sbW = 0, sbS = 0;  // segment base minus the thread's sum before that start
   Cursor c0;
   if (e0 < e1) {
     cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
     Cursor c = c0;
     for (long long e = e0; e < e1; ++e) {
+      if (!has_start && c.i == 0) {
+        has_start = true;
+        sbW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W - lw;
+        sbS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S - ls;
+      }
       const uint32_t r = L[c.listBase + c.i];
       const uint32_t wv = b.w[(size_t)c.t * b.n + r];  // (the chunk may span trees)
       const long long tv = b.tq[r];
@@ -406,7 +419,19 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   __shared__ typename BS::TempStorage tmp;
   WS2 ex, agg;
   BS(tmp).ExclusiveScan(WS2{lw, ls}, ex, WS2{0ull, 0ull}, WS2Sum(), agg);
-  if (threadIdx.x < 32) {
+  if (has_start) {  // every such thread derives the same value (benign identical writes)
+    s_pref = WS2{sbW - ex.w, sbS - ex.s};
+    s_local = 1;
+  }
+  __syncthreads();
+  if (s_local) {
+    if (threadIdx.x == 0) {
+      volatile TileStat* vs = stat;
+      vs[tile].iw = s_pref.w + agg.w; vs[tile].is = s_pref.s + agg.s;
+      __threadfence();
+      reinterpret_cast<volatile uint32_t*>(flags)[tile] = (epoch << 2) | 2u;
+    }
+  } else if (threadIdx.x < 32) {
     // warp-wide look-back: 32 predecessors per step; aggregates are summed until the
     // nearest published inclusive prefix (tile 0 always publishes one)
     volatile TileStat* vs = stat;

@@ -69,6 +69,64 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
   }
 }
 
+// Shared-memory variant (p <= kSmemMaxP): a CTA stages its 128 rows feature-major in
+// shared memory (row stride 129 doubles: at most 2-way bank conflicts both when staging
+// and when 32 lanes read 32 rows of any features), so the L1 serves only the node loads
+// (ncu of the global-memory variants: L1 throughput was the limiter, half of it the
+// feature loads).  Same 8-tree interleaving and tree-order sums.
+constexpr int kSmemRows = 128, kSmemStride = 129, kSmemMaxP = 96;
+
+__global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __restrict__ nodes,
+                                                           const uint64_t* __restrict__ tree_off, int T,
+                                                           const double* __restrict__ X, long long n, int p,
+                                                           int mode, double* __restrict__ out) {
+  extern __shared__ double xs[];  // [p][kSmemStride]
+  const long long r0 = (long long)blockIdx.x * kSmemRows;
+  const int nr = (int)min((long long)kSmemRows, n - r0);
+  const double* Xb = X + r0 * p;
+  for (int q = threadIdx.x; q < nr * p; q += kSmemRows) {
+    const int i = q / p, f = q - i * p;
+    xs[f * kSmemStride + i] = Xb[q];
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= nr) return;
+  const double* x = xs + i;  // feature f at x[f * kSmemStride]
+  double s = 0.0;
+  int t = 0;
+  for (; t + kG <= T; t += kG) {
+    const Node16* tn[kG];
+    Node16 nd[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+      tn[g] = nodes + __ldg(tree_off + t + g);
+      nd[g] = tn[g][0];
+    }
+    bool open = true;
+    while (open) {
+      open = false;
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        if (nd[g].feat >= 0) {
+          nd[g] = tn[g][nd[g].left + ((x[nd[g].feat * kSmemStride] <= nd[g].v) ? 0u : 1u)];
+          open = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kG; ++g) s += nd[g].v;
+  }
+  for (; t < T; ++t) {
+    const Node16* tn = nodes + tree_off[t];
+    Node16 nd = tn[0];
+    while (nd.feat >= 0) nd = tn[nd.left + ((x[nd.feat * kSmemStride] <= nd.v) ? 0u : 1u)];
+    s += nd.v;
+  }
+  if (mode == 1) s = s / (double)T;
+  if (mode == 2) s = exp(s / (double)T);
+  out[r0 + i] = s;
+}
+
 // rows [r0, r0 + cn) of X (row-major, n x p) -> XT (p x cn, feature-major), 32 x 32 tiles
 __global__ void k_transpose(const double* __restrict__ X, long long r0, long long cn, int p, double* __restrict__ XT) {
   __shared__ double tile[32][33];
@@ -149,7 +207,16 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     note_launch();
     return cudaGetLastError();
   }
-  // row blocks of <= ~512 MB transposed at a time
+  if (p <= kSmemMaxP) {
+    const size_t smem = (size_t)p * kSmemStride * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_predict_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_predict_smem<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p,
+                                                                                      mode, out);
+    note_launch();
+    return cudaGetLastError();
+  }
+  // wide rows: blocks of <= ~512 MB transposed at a time
   const long long chunk = std::max<long long>(4096, (512LL << 20) / (8LL * p));
   Scratch sc(s);
   double* XT;
