@@ -361,7 +361,7 @@ __device__ unsigned long long g_phase_cyc[kPhases];
 // -------------------------------------------------------------- the kernel --
 // TM: max test rows per lane.  kExtra: ExtraTrees split mode (R29).  kMae: MAE criterion (R32).
 template <bool kFit, int TM, bool kExtra, bool kMae>
-__global__ void __launch_bounds__(32 * kSmallMaxWpb, 2) small_tree_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)) small_tree_kernel(SmallArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int p = a.p;

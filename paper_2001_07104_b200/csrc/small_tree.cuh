@@ -10,7 +10,11 @@ constexpr int kSmallMaxRows = 255;  // n_tr <= 255: u8 local indices, u8 bootstr
 constexpr int kSmallMaxP = 64;
 constexpr int kSmallKMax = 8;       // ceil(255 / 32)
 constexpr int kMaxMtry = 16;        // grid points per launch
-constexpr int kSmallMaxWpb = 7;     // warps per CTA (launch bound 224 threads x 2 CTAs/SM)
+#ifndef RF_SMALL_MAXWPB
+#define RF_SMALL_MAXWPB 7
+#endif
+// warps per CTA (launch bound 32 x kSmallMaxWpb threads; 128 registers at 7 x 2 CTAs/SM)
+constexpr int kSmallMaxWpb = RF_SMALL_MAXWPB;
 
 struct SmallArgs {
   // dataset (device)
