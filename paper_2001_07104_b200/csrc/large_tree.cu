@@ -122,6 +122,7 @@ struct Batch {
   const uint32_t* tr_rows;  // training rows (ascending)
   uint32_t* keys;           // [B][2]
   uint8_t* w;               // [B][n] by global row
+  long long* wt;            // [B][n] (t_q << 8) | w per training row (exact when ceil(log2 n) >= 9), or null
   uint8_t* side;            // [B][n]
   uint32_t* sideBits;       // [B][nbw] go-left bit per row (fused partition path) or null
   int nbw;                  // words per tree in sideBits = ceil(n / 32)
@@ -178,6 +179,19 @@ __global__ void k_keys_boot(Batch b, uint64_t seed, int task, int bootstrap) {
       old = atomicAdd(reinterpret_cast<unsigned int*>(w + (r1 & ~3u)), 1u << ((r1 & 3u) * 8));
       if (((old >> ((r1 & 3u) * 8)) & 0xFFu) == 0xFFu) atomicOr(b.err, kErrOverflow);
     }
+  }
+}
+
+// packed (t_q << 8) | w per training row of each tree: one 8-byte gather per search
+// element instead of two.  |t_q| <= 2^(62 - ceil(log2 n)) (R7), so for n > 256 the
+// shifted target stays below 2^61 and the packing is exact.
+__global__ void k_pack_wt(Batch b) {
+  const int t = blockIdx.y;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  long long* wt = b.wt + (size_t)t * b.n;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) {
+    const uint32_t r = b.tr_rows[j];
+    wt[r] = (long long)((unsigned long long)b.tq[r] << 8) | (long long)w[r];
   }
 }
 
@@ -406,8 +420,16 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         sbS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S - ls;
       }
       const uint32_t r = L[c.listBase + c.i];
-      const uint32_t wv = b.w[(size_t)c.t * b.n + r];  // (the chunk may span trees)
-      const long long tv = b.tq[r];
+      uint32_t wv;
+      long long tv;
+      if (b.wt) {  // (the chunk may span trees)
+        const long long v = b.wt[(size_t)c.t * b.n + r];
+        wv = (uint32_t)(v & 0xFF);
+        tv = v >> 8;
+      } else {
+        wv = b.w[(size_t)c.t * b.n + r];
+        tv = b.tq[r];
+      }
       s_w[cbase + (int)(e - e0)] = (uint8_t)wv;
       s_t[cbase + (int)(e - e0)] = tv;
       lw += wv;
@@ -1506,6 +1528,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     dim3 g(nblk((b.ntr + 1) / 2, 256) > 64 ? 64 : nblk((b.ntr + 1) / 2, 256), b.B);
     k_keys_boot<<<g, 256, 0, s>>>(b, seed, task, bootstrap);
     note_launch();
+    if (b.wt) {
+      k_pack_wt<<<dim3(std::min<unsigned>(nblk(b.ntr, 256), 64), b.B), 256, 0, s>>>(b);
+      note_launch();
+    }
   }
   k_inbag_lists<<<b.B * b.nl, kThreads, 0, s>>>(b, task_order);
   note_launch();
@@ -1818,6 +1844,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.tr_rows = tr_rows_in;
   LCK(sc.alloc(&b.keys, (size_t)2 * B));
   LCK(sc.alloc(&b.w, (size_t)B * n + 4));
+  if (!hist && n > 256) LCK(sc.alloc(&b.wt, (size_t)B * n));
   LCK(sc.alloc(&b.side, (size_t)B * n));
   // fused partition path (exact / ExtraTrees): go-left bits per row, staged per tree in
   // shared memory by the partition CTAs (n <= 2^20 rows: <= 128 KB)

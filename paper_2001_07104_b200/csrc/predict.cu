@@ -3,9 +3,11 @@
 // outputs the mean of its trees; exp() for LOG targets).
 //
 // One thread per query row walks every tree of the flattened BFS forest
-// (16-byte nodes, one 128-bit load per visit) and sums the leaf values in
-// tree order.  The forest (C1/C2: ~2 MB) stays L1/L2-resident; rows are read
-// with 8-byte loads.  Tuned variants live beside it (predict_kernel_*).
+// (16-byte nodes, one 128-bit load per visit), several trees at a time, and sums
+// the leaf values in tree order (bit-identical to walking them one by one).  The
+// forest (C5: 64 MB) stays L2-resident; the rows' features come from shared memory
+// (p <= 96) or from a feature-major copy of the row block (wider rows).  Few rows
+// (single-query latency) take a CTA per row with threads over trees.
 #include "common.cuh"
 #include "host_util.cuh"
 #include "predict.cuh"
@@ -74,7 +76,10 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
 // and when 32 lanes read 32 rows of any features), so the L1 serves only the node loads
 // (ncu of the global-memory variants: L1 throughput was the limiter, half of it the
 // feature loads).  Same 8-tree interleaving and tree-order sums.
-constexpr int kSmemRows = 128, kSmemStride = 129, kSmemMaxP = 96;
+#ifndef RF_PRED_SMEM_G
+#define RF_PRED_SMEM_G 12
+#endif
+constexpr int kSmemRows = 128, kSmemStride = 129, kSmemMaxP = 96, kGs = RF_PRED_SMEM_G;
 
 __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __restrict__ nodes,
                                                            const uint64_t* __restrict__ tree_off, int T,
@@ -94,11 +99,11 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
   const double* x = xs + i;  // feature f at x[f * kSmemStride]
   double s = 0.0;
   int t = 0;
-  for (; t + kG <= T; t += kG) {
-    const Node16* tn[kG];
-    Node16 nd[kG];
+  for (; t + kGs <= T; t += kGs) {
+    const Node16* tn[kGs];
+    Node16 nd[kGs];
 #pragma unroll
-    for (int g = 0; g < kG; ++g) {
+    for (int g = 0; g < kGs; ++g) {
       tn[g] = nodes + __ldg(tree_off + t + g);
       nd[g] = tn[g][0];
     }
@@ -106,7 +111,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
     while (open) {
       open = false;
 #pragma unroll
-      for (int g = 0; g < kG; ++g) {
+      for (int g = 0; g < kGs; ++g) {
         if (nd[g].feat >= 0) {
           nd[g] = tn[g][nd[g].left + ((x[nd[g].feat * kSmemStride] <= nd[g].v) ? 0u : 1u)];
           open = true;
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
       }
     }
 #pragma unroll
-    for (int g = 0; g < kG; ++g) s += nd[g].v;
+    for (int g = 0; g < kGs; ++g) s += nd[g].v;
   }
   for (; t < T; ++t) {
     const Node16* tn = nodes + tree_off[t];

@@ -11,9 +11,11 @@ constexpr int kSmallMaxP = 64;
 constexpr int kSmallKMax = 8;       // ceil(255 / 32)
 constexpr int kMaxMtry = 16;        // grid points per launch
 #ifndef RF_SMALL_MAXWPB
-#define RF_SMALL_MAXWPB 7
+#define RF_SMALL_MAXWPB 16
 #endif
-// warps per CTA (launch bound 32 x kSmallMaxWpb threads; 128 registers at 7 x 2 CTAs/SM)
+// warps per CTA (launch bound 32 x kSmallMaxWpb threads, 128 registers); the host picks the
+// count with the most resident warps (A/B on the full study: up to 16 warps in one CTA per SM
+// beat 2 CTAs x 7 warps by 5 %)
 constexpr int kSmallMaxWpb = RF_SMALL_MAXWPB;
 
 struct SmallArgs {

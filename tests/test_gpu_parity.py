@@ -627,3 +627,17 @@ def test_large_partition_paths_agree():
     assert np.array_equal(a["value"].view(np.int64), b["value"].view(np.int64))
     with pytest.raises(rfg.RFError):
         rfg.debug_set_option("no_such_option", 1)
+
+
+def test_predict_c5_shape():
+    """Config 5 shape: forest grown on scaled(20k, 64) with max_depth 12 (30 trees: two
+    12-tree groups of the batched kernel plus a remainder), 200k query rows through the
+    batched kernel (device and host entry points) vs the oracle, <= 1e-9 relative."""
+    X, y = datagen.scaled(20_000, 64)
+    of = oracle.fit(X, y, ntree=30, seed=9, mtry=21, target=1, max_depth=12)
+    gf = rfg.fit(X, y, ntree=30, seed=9, mtry=21, target=1, max_depth=12)
+    _compare_forest(gf, of, X)
+    Q = datagen.queries(200_000, 64)
+    want = oracle.predict(of, Q)
+    np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), want, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(rfg.predict(gf, Q[:777]), want[:777], rtol=RTOL, atol=0)
