@@ -280,7 +280,7 @@ def run_ours(args):
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (fp64 pipe ops)",
                     "frac": achieved / peak, "traffic": SMALL_TREE_DRAM_BYTES_PER_LAUNCH,
                     "traffic_source": "ncu --set full, one launch (one dataset, 614,400 trees): dram read + write "
-                                      "bytes (profiles/r01b_small_tree_ncu.txt); the working set is on chip",
+                                      "bytes (profiles/r01r_small_tree_ncu.txt); the working set is on chip",
                     "kernel": "small_tree_kernel",
                     "kernel_ms_per_step": kern_ms / args.steps, "launches_per_step": kern_n / args.steps,
                     "kernel_share_of_step": kern_ms / max(dev_ms, 1e-9),
@@ -341,9 +341,9 @@ def measure_e2e(rfg, ds, args, skw):
 # fp64 arithmetic per evaluated candidate split: 2 squares (DMUL),
 # 2 correctly rounded divisions by W <= 255 as DMUL + 2 DFMA each (Markstein), 1 DADD
 FP64_OPS_PER_CANDIDATE = 9
-# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (1.64 MB + 0.72 MB),
-# from the round-1 ncu --set full capture (gpurun_out/r01a_small_tree.ncu-rep)
-SMALL_TREE_DRAM_BYTES_PER_LAUNCH = 2.36e6
+# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (1.70 MB + 0.56 MB),
+# from the round-1 final ncu --set full capture (profiles/r01r_small_tree_ncu.txt)
+SMALL_TREE_DRAM_BYTES_PER_LAUNCH = 2.26e6
 FP64_PEAK_TOPS = 148 * 64 * 1.965e9 / 1e12
 
 

@@ -1374,6 +1374,55 @@ __global__ void __launch_bounds__(kPLThreads, RF_PART_MINB) k_part_lists(Batch b
   }
 }
 
+#ifdef RF_PART_WARP
+// Warp-per-list variant: a CTA of kPWWarps warps shares one tree's go-left bitmap; each
+// warp streams one list through the position space 32 x kPWSteps positions at a time
+// (all loads of a step issued before use); a ballot gives every element its rank among
+// the left rows before it -- no block scans, no barriers after the bitmap load.
+constexpr int kPWWarps = 8, kPWSteps = 4;
+
+__global__ void __launch_bounds__(32 * kPWWarps) k_part_lists_warp(Batch b, int cur, const uint4* __restrict__ desc) {
+  extern __shared__ uint32_t sbits[];
+  const int t = blockIdx.x;
+  const int f = blockIdx.y * kPWWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
+  if (N == 0) return;
+  const uint32_t* gb = b.sideBits + (size_t)t * b.nbw;
+  for (int i = threadIdx.x; i < b.nbw; i += blockDim.x) sbits[i] = gb[i];
+  __syncthreads();
+  if (f >= b.nl) return;
+  const uint32_t* Lsrc = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr;
+  uint32_t* Ldst = b.L[(cur & 1) ^ 1] + ((size_t)t * b.nl + f) * b.ntr;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < N; base += 32 * kPWSteps) {
+    uint4 d[kPWSteps];
+    uint32_t r[kPWSteps];
+#pragma unroll
+    for (int k = 0; k < kPWSteps; ++k) {
+      const uint32_t i = base + 32 * k + lane;
+      d[k] = i < N ? desc[pos0 + i] : make_uint4(0u, 0u, ~0u, ~0u);
+      r[k] = i < N ? Lsrc[i] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kPWSteps; ++k) {
+      const uint32_t i = base + 32 * k + lane;
+      const bool sp = (d[k].y >> 31) != 0u;
+      const bool left = sp && ((sbits[r[k] >> 5] >> (r[k] & 31u)) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, left);
+      const uint32_t lb = carry + (uint32_t)__popc(bal & lt);  // left rows of this list before i
+      if (sp) {
+        const uint32_t wl = lb - d[k].x;
+        const uint32_t dst = left ? d[k].z : d[k].w;
+        if (dst != ~0u) Ldst[dst + (left ? wl : (i - (d[k].y & 0x7FFFFFFFu)) - wl)] = r[k];
+      }
+      carry += (uint32_t)__popc(bal);
+    }
+  }
+}
+#endif
+
 // next-level position -> node map (one warp per next-level open node)
 __global__ void k_fill_posnode(Batch b, int nxt, const uint32_t* __restrict__ counters) {
   const Nodes& nx = b.nd[nxt];
@@ -1618,7 +1667,13 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
         k_part_debug_rows<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
         note_launch();
       }
+#ifdef RF_PART_WARP
+      k_part_lists_warp<<<dim3((unsigned)b.B, (unsigned)((b.nl + kPWWarps - 1) / kPWWarps)), 32 * kPWWarps, plSmem, s>>>(
+          b, cur, pb.desc);
+      (void)G;
+#else
       k_part_lists<<<dim3((unsigned)b.B, (unsigned)((b.nl + G - 1) / G)), kPLThreads, plSmem, s>>>(b, cur, G, pb.desc);
+#endif
       note_launch();
     } else {
       ProfScope ps("large_partition", s);
@@ -1900,6 +1955,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   if (fused_part) {
     LCK(sc.alloc(&pbufs.desc, (size_t)pl.npmax));
     LCK(cudaFuncSetAttribute(k_part_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
+#ifdef RF_PART_WARP
+    LCK(cudaFuncSetAttribute(k_part_lists_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
+#endif
   }
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
