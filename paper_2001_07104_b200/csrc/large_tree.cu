@@ -24,9 +24,9 @@
 //   children    scans over nodes: BFS ids per tree, open children, positions;
 //               next-level node tables; BFS node emission
 //   partition   per-position split descriptors, go-left bits per row staged in
-//               shared memory; one CTA streams a group of lists of one tree with
-//               running per-list carries (the tiled count/scan/scatter variant
-//               remains for the histogram mode's single list and n > 2^20)
+//               shared memory; one warp streams each list with a running carry and
+//               ballot ranks (the tiled count/scan/scatter variant remains for the
+//               histogram mode's single list and n > 2^20)
 // Per-level sizes are read back once per round (one small D2H).
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -42,12 +42,10 @@ namespace rf {
 namespace {
 
 constexpr int kThreads = 128;
-// resident-CTA hints of the two streaming kernels (A/B variants via RF_DEFS)
+// resident-CTA hint of the split search (A/B via RF_DEFS: 8 per SM beat 1, 10, 12; gathering the
+// ranks in pass 1 with the weights instead of in pass 2 measured 39 % slower)
 #ifndef RF_SEARCH_MINB
 #define RF_SEARCH_MINB 8
-#endif
-#ifndef RF_PART_MINB
-#define RF_PART_MINB 3
 #endif
 constexpr int kKC = 16;  // elements per thread in the search tiles
 constexpr int kTile = kThreads * kKC;
@@ -565,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   }
   if (rkey) cas128(&b.best[rg], rkey, raux);
   }
+
   if (ncand) {
     unsigned long long v = nc;
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -1278,11 +1277,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
 // ---- fused multi-list partition (exact and ExtraTrees modes) -------------------
 // The per-position split information is list independent, so it is computed once per
 // level (k_part_desc) instead of once per (list, position); the go-left flags are one
-// bit per row, staged in shared memory per tree (no global gathers); one CTA streams
-// a group of G lists of one tree through the position space in chunks of 1024 with a
-// running carry per list (no count pass, no device-wide scan, each list read once).
-// The four lists of a scan step share one 64-bit block scan (16-bit fields).
-constexpr int kPLThreads = 256, kPLItems = 4, kPLChunk = kPLThreads * kPLItems, kPLMaxG = 8;
+// bit per row, staged in shared memory per tree (no global gathers); each list is
+// streamed once by one warp with a running carry (no count pass, no device-wide scan).
 
 // desc[q] for current position q: x = left rows of the earlier split nodes of the tree
 // (leftBefore at the node start, the same in every list), y = node start (tree-local)
@@ -1306,79 +1302,11 @@ __global__ void k_part_desc(Batch b, int cur, int NP, const uint32_t* __restrict
                        (fl & 2u) ? cL + ((fl & 1u) ? nl : 0u) : ~0u);
 }
 
-__global__ void __launch_bounds__(kPLThreads, RF_PART_MINB) k_part_lists(Batch b, int cur, int G, const uint4* __restrict__ desc) {
-  extern __shared__ uint32_t sbits[];
-  const int t = blockIdx.x, f0 = blockIdx.y * G;
-  const int nf = min(G, b.nl - f0);
-  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
-  if (N == 0 || nf <= 0) return;
-  const uint32_t* gb = b.sideBits + (size_t)t * b.nbw;
-  for (int i = threadIdx.x; i < b.nbw; i += kPLThreads) sbits[i] = gb[i];
-  __syncthreads();
-  using BS = cub::BlockScan<unsigned long long, kPLThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  uint32_t carry[kPLMaxG];
-#pragma unroll
-  for (int l = 0; l < kPLMaxG; ++l) carry[l] = 0;
-  const uint32_t* Lsrc = b.L[cur & 1] + ((size_t)t * b.nl + f0) * b.ntr;
-  uint32_t* Ldst = b.L[(cur & 1) ^ 1] + ((size_t)t * b.nl + f0) * b.ntr;
-  for (uint32_t base = 0; base < N; base += kPLChunk) {
-    const uint32_t i0 = base + threadIdx.x * kPLItems;
-    uint4 d[kPLItems];
-#pragma unroll
-    for (int it = 0; it < kPLItems; ++it)
-      d[it] = (i0 + it < N) ? desc[pos0 + i0 + it] : make_uint4(0u, 0u, ~0u, ~0u);
-#pragma unroll
-    for (int fg = 0; fg < kPLMaxG; fg += 4) {
-      if (fg >= nf) break;
-      uint32_t rr[4][kPLItems];
-      uint32_t lmask = 0;  // bit 4l + it: element it of list fg + l goes left (split nodes only)
-      unsigned long long packed = 0;
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        uint32_t c = 0;
-#pragma unroll
-        for (int it = 0; it < kPLItems; ++it) {
-          rr[l][it] = 0;
-          if (fg + l < nf && i0 + it < N) {
-            const uint32_t r = Lsrc[(size_t)(fg + l) * b.ntr + i0 + it];
-            rr[l][it] = r;
-            const uint32_t lf = (d[it].y >> 31) & (sbits[r >> 5] >> (r & 31u)) & 1u;
-            lmask |= lf << (4 * l + it);
-            c += lf;
-          }
-        }
-        packed |= (unsigned long long)c << (16 * l);
-      }
-      unsigned long long ex, tot;
-      BS(tmp).ExclusiveSum(packed, ex, tot);
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        if (fg + l >= nf) break;
-        uint32_t lb = carry[fg + l] + (uint32_t)((ex >> (16 * l)) & 0xFFFFull);
-#pragma unroll
-        for (int it = 0; it < kPLItems; ++it) {
-          const uint32_t i = i0 + it;
-          if (i >= N || !(d[it].y >> 31)) continue;
-          const bool left = (lmask >> (4 * l + it)) & 1u;
-          const uint32_t wl = lb - d[it].x;  // left rows of this node before i (this list)
-          const uint32_t dst = left ? d[it].z : d[it].w;
-          if (dst != ~0u) Ldst[(size_t)(fg + l) * b.ntr + dst + (left ? wl : (i - (d[it].y & 0x7FFFFFFFu)) - wl)] =
-              rr[l][it];
-          lb += left ? 1u : 0u;
-        }
-        carry[fg + l] += (uint32_t)((tot >> (16 * l)) & 0xFFFFull);
-      }
-      __syncthreads();  // tmp reuse
-    }
-  }
-}
-
-#ifdef RF_PART_WARP
-// Warp-per-list variant: a CTA of kPWWarps warps shares one tree's go-left bitmap; each
-// warp streams one list through the position space 32 x kPWSteps positions at a time
-// (all loads of a step issued before use); a ballot gives every element its rank among
-// the left rows before it -- no block scans, no barriers after the bitmap load.
+// Warp per list: a CTA of kPWWarps warps shares one tree's go-left bitmap; each warp
+// streams one list through the position space 32 x kPWSteps positions at a time (all
+// loads of a step issued before use); a ballot gives every element its rank among the
+// left rows before it -- no block scans, no barriers after the bitmap load.  (A/B against
+// a CTA-per-list-group version with 64-bit block scans over four lists: -22 % time.)
 constexpr int kPWWarps = 8, kPWSteps = 4;
 
 __global__ void __launch_bounds__(32 * kPWWarps) k_part_lists_warp(Batch b, int cur, const uint4* __restrict__ desc) {
@@ -1421,7 +1349,6 @@ __global__ void __launch_bounds__(32 * kPWWarps) k_part_lists_warp(Batch b, int 
     }
   }
 }
-#endif
 
 // next-level position -> node map (one warp per next-level open node)
 __global__ void k_fill_posnode(Batch b, int nxt, const uint32_t* __restrict__ counters) {
@@ -1566,9 +1493,6 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
                      void* cub_tmp, size_t cub_bytes, uint32_t* rootInfo, uint32_t* counters, uint32_t* hcounters,
                      uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp, const HistBufs& hb,
                      const PartBufs& pb, unsigned long long* ncand, cudaStream_t s, std::string& err) {
-  // fused partition: lists per CTA so that the grid covers the SMs at least twice
-  int G = kPLMaxG;
-  while (G > 1 && (long long)b.B * ((b.nl + G - 1) / G) < 2 * 148) G >>= 1;
   const size_t plSmem = (size_t)b.nbw * 4;
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
   LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
@@ -1667,13 +1591,8 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
         k_part_debug_rows<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
         note_launch();
       }
-#ifdef RF_PART_WARP
       k_part_lists_warp<<<dim3((unsigned)b.B, (unsigned)((b.nl + kPWWarps - 1) / kPWWarps)), 32 * kPWWarps, plSmem, s>>>(
           b, cur, pb.desc);
-      (void)G;
-#else
-      k_part_lists<<<dim3((unsigned)b.B, (unsigned)((b.nl + G - 1) / G)), kPLThreads, plSmem, s>>>(b, cur, G, pb.desc);
-#endif
       note_launch();
     } else {
       ProfScope ps("large_partition", s);
@@ -1954,10 +1873,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(cudaMemsetAsync(pbufs.flags, 0, ((size_t)pl.tiles_max + 1) * 4, s));
   if (fused_part) {
     LCK(sc.alloc(&pbufs.desc, (size_t)pl.npmax));
-    LCK(cudaFuncSetAttribute(k_part_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
-#ifdef RF_PART_WARP
     LCK(cudaFuncSetAttribute(k_part_lists_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
-#endif
   }
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
