@@ -135,6 +135,9 @@ RF_API rf_status rf_predict_partial_dev(const rf_forest* f, const double* dX, ui
 /* Finish a reduced partial: yhat = partial / ntree_total, exp if LOG. */
 RF_API rf_status rf_predict_finalize_dev(const double* dpartial, uint64_t n, uint32_t ntree_total,
                                   uint32_t target, double* dyhat, void* stream);
+/* Host twin of rf_predict_partial_dev (host X in, host partial[n] out; synchronous). */
+RF_API rf_status rf_predict_partial(const rf_forest* f, const double* X, uint64_t n, uint32_t p,
+                                    double* partial);
 
 /* rf_make_folds: fold ids [repeats][n] in {-1 (always train), 0..k-1}.
    Plain (custom = 0): rows ordered by Philox keys (seed, rep), contiguous
@@ -233,6 +236,17 @@ RF_API rf_status rf_cv_finalize_dev(const double* dy, uint64_t n, uint32_t targe
                              uint32_t repeats, const int32_t* dfold_ids, const uint32_t* ntrees,
                              uint32_t n_ntree, uint32_t n_mtry, const double* dreduced,
                              double* dfold_mape, double* dpred, void* stream);
+/* Host twins of the tree-sharded CV pair (host buffers in and out, synchronous; fold_ids
+   are required, [repeats][n]; partial / reduced [n_mtry][n_ntree][repeats][n]; fold_mape
+   [n_mtry][n_ntree][repeats][k]; pred may be NULL).  Device: prm->device. */
+RF_API rf_status rf_cv_partial(const double* X, uint64_t n, uint32_t p, const double* y,
+                               const rf_params* prm, uint32_t k, uint32_t repeats,
+                               const int32_t* fold_ids, const uint32_t* ntrees, uint32_t n_ntree,
+                               const uint32_t* mtrys, uint32_t n_mtry, double* partial);
+RF_API rf_status rf_cv_finalize(const double* y, uint64_t n, uint32_t target, uint32_t k,
+                                uint32_t repeats, const int32_t* fold_ids, const uint32_t* ntrees,
+                                uint32_t n_ntree, uint32_t n_mtry, const double* reduced,
+                                double* fold_mape, double* pred, int32_t device);
 
 RF_API void rf_forest_free(rf_forest* f);
 RF_API const char* rf_last_error(void);

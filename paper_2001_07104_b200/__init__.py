@@ -36,7 +36,7 @@ ABI_SYMBOLS = [
     "rf_predict_partial_dev", "rf_predict_finalize_dev", "rf_make_folds", "rf_make_folds_dev",
     "rf_make_folds_masked_dev", "rf_nested_cv", "rf_nested_cv_dev", "rf_error_buckets", "rf_error_buckets_dev",
     "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
-    "rf_cv_finalize_dev", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
+    "rf_cv_finalize_dev", "rf_predict_partial", "rf_cv_partial", "rf_cv_finalize", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
     "rf_last_profile", "rf_set_profiling",
     "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles", "rf_debug_set_option",
@@ -79,6 +79,9 @@ def lib():
             "rf_predict_dev": ([P, P, u64, u32, P, P], C.c_int),
             "rf_predict_partial_dev": ([P, P, u64, u32, P, P], C.c_int),
             "rf_predict_finalize_dev": ([P, u64, u32, u32, P, P], C.c_int),
+            "rf_predict_partial": ([P, P, u64, u32, P], C.c_int),
+            "rf_cv_partial": ([P, u64, u32, P, pp, u32, u32, P, P, u32, P, u32, P], C.c_int),
+            "rf_cv_finalize": ([P, u64, u32, u32, u32, P, P, u32, u32, P, P, P, i32], C.c_int),
             "rf_make_folds": ([P, u64, u32, u32, u64, u32, P], C.c_int),
             "rf_make_folds_dev": ([P, u64, u32, u32, u64, u32, P, P], C.c_int),
             "rf_make_folds_masked_dev": ([P, u64, u32, u32, u64, u32, P, P, P], C.c_int),
@@ -265,6 +268,14 @@ def predict(forest: Forest, X, out=None):
 
 
 def predict_partial(forest: Forest, X, out=None):
+    """Sum over this forest's trees of the leaf values (tree-shard partial): CUDA tensors in and
+    out (rf_predict_partial_dev), or host arrays (rf_predict_partial)."""
+    if not _is_torch(X):
+        X = _host(X, np.float64)
+        n, p = X.shape
+        out = np.zeros(n, np.float64)
+        _check(lib().rf_predict_partial(forest.handle, _ptr(X), n, p, _ptr(out)))
+        return out
     torch = _torch()
     n, p = X.shape
     out = torch.empty(n, dtype=torch.float64, device=X.device) if out is None else out
@@ -386,23 +397,39 @@ def cross_validate(X, y, k, repeats=1, fold_ids=None, *, ntree=100, mtry=0, **kw
 def cv_partial(X, y, k, repeats, fold_ids, ntrees, mtrys, *, tree_begin, tree_end, min_samples_split=2,
                max_depth=-1, bootstrap=True, target=TARGET_IDENTITY, seed=0, out=None, split_mode=SPLIT_EXACT,
                criterion=CRITERION_MSE):
-    """Tree-sharded CV partial sums [n_mtry, n_ntree, repeats, n] (device tensors)."""
-    torch = _torch()
+    """Tree-sharded CV partial sums [n_mtry, n_ntree, repeats, n] (device tensors, or host arrays
+    through rf_cv_partial)."""
     prm = params(ntree=max(ntrees), min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), target=target, seed=seed, tree_begin=tree_begin, tree_end=tree_end,
                  split_mode=split_mode, criterion=criterion)
     nt, mt = _u32(ntrees), _u32(mtrys)
     n, p = X.shape
+    if not _is_torch(X):
+        X, y, fid = _host(X, np.float64), _host(y, np.float64), _host(fold_ids, np.int32)
+        out = np.zeros((len(mt), len(nt), repeats, n), np.float64)
+        _check(lib().rf_cv_partial(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats, _ptr(fid), _ptr(nt), len(nt),
+                                   _ptr(mt), len(mt), _ptr(out)))
+        return out
+    torch = _torch()
     out = torch.empty((len(mt), len(nt), repeats, n), dtype=torch.float64, device=X.device) if out is None else out
     _check(lib().rf_cv_partial_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats, _ptr(fold_ids), _ptr(nt),
                                    len(nt), _ptr(mt), len(mt), _ptr(out), _stream()))
     return out
 
 
-def cv_finalize(y, k, repeats, fold_ids, ntrees, n_mtry, reduced, *, target=TARGET_IDENTITY, want_pred=False):
-    torch = _torch()
+def cv_finalize(y, k, repeats, fold_ids, ntrees, n_mtry, reduced, *, target=TARGET_IDENTITY, want_pred=False,
+                device=0):
+    """Fold MAPEs (and predictions) from all-reduced partial sums (rf_cv_finalize[_dev])."""
     n = y.shape[0]
     nt = _u32(ntrees)
+    if not _is_torch(y):
+        y, fid, red = _host(y, np.float64), _host(fold_ids, np.int32), _host(reduced, np.float64)
+        fm = np.zeros((n_mtry, len(nt), repeats, k), np.float64)
+        pr = np.zeros((n_mtry, len(nt), repeats, n), np.float64) if want_pred else None
+        _check(lib().rf_cv_finalize(_ptr(y), n, target, k, repeats, _ptr(fid), _ptr(nt), len(nt), n_mtry, _ptr(red),
+                                    _ptr(fm), _ptr(pr), device))
+        return (fm, pr) if want_pred else fm
+    torch = _torch()
     fm = torch.empty((n_mtry, len(nt), repeats, k), dtype=torch.float64, device=y.device)
     pr = torch.empty((n_mtry, len(nt), repeats, n), dtype=torch.float64, device=y.device) if want_pred else None
     _check(lib().rf_cv_finalize_dev(_ptr(y), n, target, k, repeats, _ptr(fold_ids), _ptr(nt), len(nt), n_mtry,

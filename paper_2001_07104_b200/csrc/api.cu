@@ -310,6 +310,16 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   }
   a.Cw = Cw;
   a.nsub = nsub = (T + Cw - 1) / Cw;
+  {
+    // a launch with fewer warp jobs than resident warp slots (e.g. C1: 1,000 single-tree
+    // jobs) spreads its jobs over all SMs with smaller CTAs instead of filling a few SMs
+    const long long jobs = (long long)nmd * ntask * nsub;
+    if (jobs < resident) {
+      int w = best_wpb;
+      while (w > 1 && (long long)nmd * ntask * ((nsub + w - 1) / w) < 148) --w;
+      a.wpb = w;
+    }
+  }
   CK(sc.alloc(&partial, (size_t)nmd * ntask * a.nsub * nte_max), "alloc partial");
   a.partial = partial;
   {
@@ -914,6 +924,75 @@ rf_status rf_cv_finalize_dev(const double* dy, uint64_t n, uint32_t target, uint
   if (dpred) CK(cudaMemsetAsync(dpred, 0xFF, (size_t)n_mtry * n_ntree * repeats * n * 8, s), "memset");
   CK(rf::finalize_cv(dreduced, dy, dfold_ids, (int)n, (int)k, (int)repeats, (int)n_mtry, (int)n_ntree,
                      nt.data(), (int)target, dfold_mape, dpred, s), "finalize");
+  return RF_OK;
+}
+
+rf_status rf_predict_partial(const rf_forest* f, const double* X, uint64_t n, uint32_t p, double* partial) {
+  if (rf_status st = check_device()) return st;
+  if (!f) return fail(RF_E_ARG, "forest is NULL");
+  if (n == 0) return RF_OK;
+  CK(cudaSetDevice(f->device), "set device");
+  cudaStream_t s = host_stream(f->device);
+  Scratch sc(s);
+  double *dX, *dp;
+  CK(sc.alloc(&dX, n * p), "alloc");
+  CK(sc.alloc(&dp, n), "alloc");
+  CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+  return predict_core(f, dX, n, p, dp, 0, s, partial);
+}
+
+rf_status rf_cv_partial(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
+                        uint32_t k, uint32_t repeats, const int32_t* fold_ids, const uint32_t* ntrees,
+                        uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry, double* partial) {
+  if (rf_status st = check_device()) return st;
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  if (!fold_ids || !partial) return fail(RF_E_ARG, "fold ids and partial required");
+  CK(cudaSetDevice(prm->device), "set device");
+  cudaStream_t s = host_stream(prm->device);
+  Scratch sc(s);
+  double *dX, *dy, *dp;
+  int32_t* df;
+  const size_t np_ = (size_t)n_mtry * n_ntree * repeats * n;
+  CK(sc.alloc(&dX, n * p), "alloc");
+  CK(sc.alloc(&dy, n), "alloc");
+  CK(sc.alloc(&dp, np_), "alloc");
+  CK(sc.alloc(&df, n * repeats), "alloc");
+  CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+  CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+  CK(cudaMemcpyAsync(df, fold_ids, n * repeats * 4, cudaMemcpyHostToDevice, s), "h2d");
+  rf_status st = rf_cv_partial_dev(dX, n, p, dy, prm, k, repeats, df, ntrees, n_ntree, mtrys, n_mtry, dp, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(partial, dp, np_ * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
+  return RF_OK;
+}
+
+rf_status rf_cv_finalize(const double* y, uint64_t n, uint32_t target, uint32_t k, uint32_t repeats,
+                         const int32_t* fold_ids, const uint32_t* ntrees, uint32_t n_ntree, uint32_t n_mtry,
+                         const double* reduced, double* fold_mape, double* pred, int32_t device) {
+  if (rf_status st = check_device()) return st;
+  if (!fold_ids || !reduced || !fold_mape) return fail(RF_E_ARG, "fold ids, reduced and fold_mape required");
+  if (n == 0) return fail(RF_E_EMPTY, "n == 0");
+  CK(cudaSetDevice(device), "set device");
+  cudaStream_t s = host_stream(device);
+  Scratch sc(s);
+  double *dy, *dr, *dm, *dpr = nullptr;
+  int32_t* df;
+  const size_t np_ = (size_t)n_mtry * n_ntree * repeats * n, nm = (size_t)n_mtry * n_ntree * repeats * k;
+  CK(sc.alloc(&dy, n), "alloc");
+  CK(sc.alloc(&dr, np_), "alloc");
+  CK(sc.alloc(&dm, nm), "alloc");
+  CK(sc.alloc(&df, n * repeats), "alloc");
+  if (pred) CK(sc.alloc(&dpr, np_), "alloc");
+  CK(cudaMemcpyAsync(dy, y, n * 8, cudaMemcpyHostToDevice, s), "h2d");
+  CK(cudaMemcpyAsync(dr, reduced, np_ * 8, cudaMemcpyHostToDevice, s), "h2d");
+  CK(cudaMemcpyAsync(df, fold_ids, n * repeats * 4, cudaMemcpyHostToDevice, s), "h2d");
+  rf_status st = rf_cv_finalize_dev(dy, n, target, k, repeats, df, ntrees, n_ntree, n_mtry, dr, dm, dpr, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(fold_mape, dm, nm * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  if (pred) CK(cudaMemcpyAsync(pred, dpr, np_ * 8, cudaMemcpyDeviceToHost, s), "d2h");
+  CK(cudaStreamSynchronize(s), "sync");
   return RF_OK;
 }
 

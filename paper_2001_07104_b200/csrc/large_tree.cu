@@ -43,7 +43,8 @@ namespace {
 
 constexpr int kThreads = 128;
 // resident-CTA hint of the split search (A/B via RF_DEFS: 8 per SM beat 1, 10, 12; gathering the
-// ranks in pass 1 with the weights instead of in pass 2 measured 39 % slower)
+// ranks in pass 1 with the weights instead of in pass 2 measured 39 % slower, and walking the
+// cursor first to issue a thread's 16 weight/target gathers back to back 18 % slower)
 #ifndef RF_SEARCH_MINB
 #define RF_SEARCH_MINB 8
 #endif
@@ -408,37 +409,6 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   bool has_start = false;
   unsigned long long sbW = 0, sbS = 0;  // segment base minus the thread's sum before that start
   Cursor c0;
-#ifdef RF_SEARCH_BATCH
-  if (e0 < e1 && b.wt) {
-    // walk the cursor first (row ids are L1-resident list reads), parking each element's
-    // gather index in s_t; then issue the weight/target gathers back to back
-    cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
-    Cursor c = c0;
-    const int cnt = (int)(e1 - e0);
-    int kst = -1;
-    unsigned long long bW0 = 0, bS0 = 0;
-    for (int k = 0; k < cnt; ++k) {
-      if (kst < 0 && c.i == 0) {
-        kst = k;
-        bW0 = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
-        bS0 = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
-      }
-      s_t[cbase + k] = (long long)((size_t)c.t * b.n + L[c.listBase + c.i]);
-      if (++c.i == c.len && k + 1 < cnt) cursor_next_segment(b, nd, c);
-    }
-#pragma unroll 4
-    for (int k = 0; k < cnt; ++k) {
-      const long long v = b.wt[(size_t)s_t[cbase + k]];
-      const uint32_t wv = (uint32_t)(v & 0xFF);
-      const long long tv = v >> 8;
-      if (k == kst) { has_start = true; sbW = bW0 - lw; sbS = bS0 - ls; }
-      s_w[cbase + k] = (uint8_t)wv;
-      s_t[cbase + k] = tv;
-      lw += wv;
-      ls += (unsigned long long)((long long)wv * tv);
-    }
-  } else
-#endif
   if (e0 < e1) {
     cursor_locate(b, nd, posNode, b.tPos0, e0, c0);
     Cursor c = c0;

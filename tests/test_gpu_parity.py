@@ -233,6 +233,15 @@ def test_cv_tree_shard_partial_finalize():
     fm = rfg.cv_finalize(yd, 10, 2, folds, ntrees, len(mtrys), tot, target=1).cpu().numpy()
     want = oracle.cv_grid(X, y, 10, 2, ntrees, mtrys, fold_ids=folds.cpu().numpy(), target=1, seed=3)
     np.testing.assert_allclose(fm, want, rtol=RTOL, atol=0)
+    # host twins (rf_cv_partial / rf_cv_finalize / rf_predict_partial)
+    fh = folds.cpu().numpy()
+    toth = sum(rfg.cv_partial(X, y, 10, 2, fh, ntrees, mtrys, tree_begin=lo, tree_end=hi, target=1, seed=3)
+               for lo, hi in [(0, 16), (16, 32)])
+    np.testing.assert_allclose(rfg.cv_finalize(y, 10, 2, fh, ntrees, len(mtrys), toth, target=1), want,
+                               rtol=RTOL, atol=0)
+    f = rfg.fit(X, y, ntree=12, seed=3, mtry=3, target=1)
+    ph = rfg.predict_partial(f, X[:50])
+    np.testing.assert_allclose(np.exp(ph / 12), rfg.predict(f, X[:50]), rtol=1e-12, atol=0)
 
 
 def test_cv_full_study_config_sampled():
