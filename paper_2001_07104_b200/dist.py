@@ -21,7 +21,7 @@ import torch
 import torch.distributed as dist
 
 from . import (TARGET_IDENTITY, cross_validate_grid, cv_finalize, cv_partial, fit, forest_import,
-               predict_finalize, predict_partial)
+               predict, predict_finalize, predict_partial)
 
 
 def shard(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -146,6 +146,17 @@ def fit_sharded(X, y, *, ntree, group=None, **kw):
     dev_index = dev.index if dev.type == "cuda" and dev.index is not None else 0
     return forest_import(feature, left, value, thr_index, off.astype(np.uint64), e["p"], e["F"], e["target"],
                          device=dev_index)
+
+
+def predict_row_sharded(forest, X, group=None, gather=True):
+    """Row-sharded batched inference: the forest is replicated, rank r
+    predicts rows shard(n, r, world) of X (device tensor, the full query block or already
+    this rank's rows with gather=False); no data-path collective, optionally one all_gather
+    of the predictions in row order."""
+    rank, world = _world(group)
+    lo, hi = shard(X.shape[0], rank, world) if gather else (0, X.shape[0])
+    mine = predict(forest, X[lo:hi].contiguous())
+    return gather_rows(mine, group) if gather else mine
 
 
 def predict_tree_sharded(local_forest, X, ntree_total, target, group=None):

@@ -126,3 +126,22 @@ def _gather_rows(rank, world):
 
 def test_gather_rows_importance_shards():
     run_world(_gather_rows)
+
+
+def _row_sharded_predict(rank, world):
+    # host logic of the row-sharded inference driver (C5): the per-rank prediction is stubbed
+    # with the oracle (no GPU here); rows are sharded unevenly and gathered in row order
+    import paper_2001_07104_b200.dist as D
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    f = oracle.fit(X, y, ntree=6, mtry=4, seed=2, target=1)
+    D.predict = lambda forest, Xs: torch.as_tensor(oracle.predict(f, Xs.numpy()))
+    Q = torch.as_tensor(X[:101])
+    got = D.predict_row_sharded(None, Q)
+    assert np.array_equal(got.numpy(), oracle.predict(f, X[:101]))
+    lo, hi = D.shard(101, rank, world)
+    mine = D.predict_row_sharded(None, Q[lo:hi], gather=False)
+    assert np.array_equal(mine.numpy(), oracle.predict(f, X[lo:hi]))
+
+
+def test_row_sharded_predict():
+    run_world(_row_sharded_predict)
