@@ -763,10 +763,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         uint32_t wr = ws.w[r];
         int64_t tr = cs.tq[r];
         int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
-#ifdef RF_RCP_AHEAD
         // reciprocal-table entries of the next element, loaded one iteration ahead
         double2 ylN = cs.rcp2[(cW + wr - segW) & 0xFFu], yrN = cs.rcp2[(Wk - (cW + wr - segW)) & 0xFFu];
-#endif
         #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
@@ -783,11 +781,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const uint32_t WR = Wk - WL;
           const int64_t SR = Sk - SL;
           const double dSL = __ll2double_rn(SL), dSR = __ll2double_rn(SR);
-#ifdef RF_RCP_AHEAD
           const double2 yl = ylN, yr = yrN;  // = rcp2[WL], rcp2[WR] for active lanes
-#else
-          const double2 yl = cs.rcp2[WL & 0xFFu], yr = cs.rcp2[WR & 0xFFu];
-#endif
           const double gl = div_small(__dmul_rn(dSL, dSL), yl.x, yl.y);
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
           const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
@@ -828,13 +822,11 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           } else if (act) {
             ++i;
           }
-#ifdef RF_RCP_AHEAD
           {
             const uint32_t WLn = cW + wr - segW;
             ylN = cs.rcp2[WLn & 0xFFu];
             yrN = cs.rcp2[(Wk - WLn) & 0xFFu];
           }
-#endif
           r = rn;
           rkr = rkn;
         }
