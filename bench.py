@@ -13,9 +13,11 @@ cross-rank gather of the fold-MAPE tables (a11).
 Multi-GPU (weak scaling): rank r runs repeats [30 r, 30 r + 30) of a
 30 N-repeat study (task sharding, no data-path collective besides the final
 all_gather of MAPE tables).  value = trees grown by all ranks / max over
-ranks of the device time.
+ranks of the device time.  Within a rank the ten datasets run on ten CUDA
+streams (--streams 1: one after another).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--split exact|extra]
+                  [--streams S] [--no-cpu-baseline] [--no-e2e]
 """
 from __future__ import annotations
 
