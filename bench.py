@@ -307,6 +307,11 @@ def run_ours(args):
                     "traffic_source": "ncu --set full, one launch (one dataset, 614,400 trees): dram read + write "
                                       "bytes (profiles/r01r_small_tree_ncu.txt); the working set is on chip",
                     "kernel": "small_tree_kernel",
+                    "ncu_context": {"ipc": 2.54, "issue_slots_busy_pct": 63.7, "warps_per_sm": 16,
+                                    "top_stalls": "wait 35 %, short_scoreboard 19 %",
+                                    "source": "profiles/r01r_small_tree_ncu.txt (latency-bound: the fp64 "
+                                              "pipe fraction is low because each candidate also costs "
+                                              "shared-memory scans and per-level node work)"},
                     "kernel_ms_per_step": kern_busy_ms / args.steps, "launches_per_step": kern_n / args.steps,
                     "kernel_share_of_step": kern_busy_ms / max(dev_ms, 1e-9),
                     "kernel_launch_spans_ms_per_step": kern_ms / args.steps,

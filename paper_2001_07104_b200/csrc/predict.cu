@@ -6,7 +6,7 @@
 // (16-byte nodes, one 128-bit load per visit), several trees at a time, and sums
 // the leaf values in tree order (bit-identical to walking them one by one).  The
 // forest (C5: 64 MB) stays L2-resident; the rows' features come from shared memory
-// (p <= 96) or from a feature-major copy of the row block (wider rows).  Few rows
+// (p <= 192, fp32 with an exact fp64 fallback) or from a feature-major copy of the row block (wider rows).  Few rows
 // (single-query latency) take a CTA per row with threads over trees.
 #include "common.cuh"
 #include "host_util.cuh"
@@ -72,31 +72,46 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
 }
 
 // Shared-memory variant (p <= kSmemMaxP): a CTA stages its 128 rows feature-major in
-// shared memory (row stride 129 doubles: at most 2-way bank conflicts both when staging
-// and when 32 lanes read 32 rows of any features), so the L1 serves only the node loads
-// (ncu of the global-memory variants: L1 throughput was the limiter, half of it the
-// feature loads).  Same 8-tree interleaving and tree-order sums.
+// shared memory (row stride 129 words: conflict-free when 32 lanes read one feature of 32
+// rows), so the L1 serves only the node loads (ncu of the global-memory variants: L1
+// throughput was the limiter, half of it the feature loads).  Same interleaving of trees
+// and tree-order sums.  (A/B: fp32 staging + exact fallback beat fp64 staging by 24 %, 12
+// trees per thread beat 8 and 16.)
 #ifndef RF_PRED_SMEM_G
 #define RF_PRED_SMEM_G 12
 #endif
-constexpr int kSmemRows = 128, kSmemStride = 129, kSmemMaxP = 96, kGs = RF_PRED_SMEM_G;
+constexpr int kSmemRows = 128, kSmemMaxP = 192, kGs = RF_PRED_SMEM_G;
+
+// Features staged as fp32 (half the shared memory per row -> more resident warps).  The
+// comparison stays exact: rounding to nearest is monotonic, so float(x) < float(thr)
+// implies x <= thr and float(x) > float(thr) implies x > thr; only float(x) ==
+// float(thr) is undecided, and then the fp64 value is read from X.
+constexpr int kSmemStrideF = 129;
+
+__device__ __forceinline__ bool le_exact(float xf, double thr, const double* xrow, int f) {
+  const float tf = __double2float_rn(thr);
+  if (xf < tf) return true;
+  if (xf > tf) return false;
+  return __ldg(xrow + f) <= thr;
+}
 
 __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __restrict__ nodes,
                                                            const uint64_t* __restrict__ tree_off, int T,
                                                            const double* __restrict__ X, long long n, int p,
                                                            int mode, double* __restrict__ out) {
-  extern __shared__ double xs[];  // [p][kSmemStride]
+  extern __shared__ float xsf[];  // [p][kSmemStrideF]
   const long long r0 = (long long)blockIdx.x * kSmemRows;
   const int nr = (int)min((long long)kSmemRows, n - r0);
   const double* Xb = X + r0 * p;
   for (int q = threadIdx.x; q < nr * p; q += kSmemRows) {
     const int i = q / p, f = q - i * p;
-    xs[f * kSmemStride + i] = Xb[q];
+    xsf[f * kSmemStrideF + i] = __double2float_rn(Xb[q]);
   }
   __syncthreads();
   const int i = threadIdx.x;
   if (i >= nr) return;
-  const double* x = xs + i;  // feature f at x[f * kSmemStride]
+  const float* x = xsf + i;  // feature f at x[f * kSmemStrideF]
+  const double* xrow = Xb + (size_t)i * p;
   double s = 0.0;
   int t = 0;
   for (; t + kGs <= T; t += kGs) {
@@ -113,7 +128,8 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
 #pragma unroll
       for (int g = 0; g < kGs; ++g) {
         if (nd[g].feat >= 0) {
-          nd[g] = tn[g][nd[g].left + ((x[nd[g].feat * kSmemStride] <= nd[g].v) ? 0u : 1u)];
+          const int f = nd[g].feat;
+          nd[g] = tn[g][nd[g].left + (le_exact(x[f * kSmemStrideF], nd[g].v, xrow, f) ? 0u : 1u)];
           open = true;
         }
       }
@@ -124,14 +140,16 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
   for (; t < T; ++t) {
     const Node16* tn = nodes + tree_off[t];
     Node16 nd = tn[0];
-    while (nd.feat >= 0) nd = tn[nd.left + ((x[nd.feat * kSmemStride] <= nd.v) ? 0u : 1u)];
+    while (nd.feat >= 0) {
+      const int f = nd.feat;
+      nd = tn[nd.left + (le_exact(x[f * kSmemStrideF], nd.v, xrow, f) ? 0u : 1u)];
+    }
     s += nd.v;
   }
   if (mode == 1) s = s / (double)T;
   if (mode == 2) s = exp(s / (double)T);
   out[r0 + i] = s;
 }
-
 // rows [r0, r0 + cn) of X (row-major, n x p) -> XT (p x cn, feature-major), 32 x 32 tiles
 __global__ void k_transpose(const double* __restrict__ X, long long r0, long long cn, int p, double* __restrict__ XT) {
   __shared__ double tile[32][33];
@@ -213,7 +231,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     return cudaGetLastError();
   }
   if (p <= kSmemMaxP) {
-    const size_t smem = (size_t)p * kSmemStride * 8;
+    const size_t smem = (size_t)p * kSmemStrideF * 4;
     cudaError_t e = cudaFuncSetAttribute(k_predict_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_predict_smem<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p,

@@ -140,13 +140,15 @@ __host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_m
   s.tord = mae ? c.take<uint8_t>(ntr_max, 16) : SA<uint8_t>{0u};
 }
 
-__host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM) {
+// BFS ids are needed only when nodes are emitted (fit mode); CV mode routes test rows by
+// open-node index and leaves them out (saves shared memory: 16 warps fit on the C2 shapes)
+__host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM, bool fit) {
   s.start = c.take<uint8_t>(NM, 4);
   s.len = c.take<uint8_t>(NM, 4);
   s.W = c.take<uint16_t>(NM, 4);
   s.S = c.take<int64_t>(NM, 8);
   s.heap = c.take<uint64_t>(NM, 8);
-  s.bfs = c.take<uint16_t>(NM, 4);
+  s.bfs = fit ? c.take<uint16_t>(NM, 4) : SA<uint16_t>{0u};
 }
 
 // row lists per tree: the p feature lists, plus the t_q-ordered list under MAE (list p)
@@ -162,8 +164,8 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.pnA = c.take<uint8_t>(ntr_max, 4);
   s.pnB = c.take<uint8_t>(ntr_max, 4);
   s.side = c.take<uint8_t>(ntr_max, 4);
-  carve_nodeset(c, s.cur, NM);
-  carve_nodeset(c, s.nxt, NM);
+  carve_nodeset(c, s.cur, NM, fit);
+  carve_nodeset(c, s.nxt, NM, fit);
   s.feat = c.take<uint8_t>((size_t)NM * p, 4);
   s.xb = extra ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
   s.bkey = c.take<unsigned long long>(NM, 16);  // 16-aligned: desc aliases it (uint4 loads)
@@ -173,7 +175,7 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.ncb = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chOpen = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chVal = c.take<double>((size_t)NM * 2, 8);
-  s.chBase = c.take<uint16_t>(NM, 4);
+  s.chBase = fit ? c.take<uint16_t>(NM, 4) : SA<uint16_t>{0u};
   s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
   s.desc = SA<uint32_t>{s.bkey.off};  // ntr_max * 4 <= NM * 8 bytes
   s.med2 = mae ? c.take<int64_t>((size_t)NM * 2, 8) : SA<int64_t>{0u};
@@ -555,7 +557,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
     for (int i = lane; i < (int)D; i += 32) pn[i] = 0;
     if (lane == 0) {
       cur.start[0] = 0; cur.len[0] = (uint8_t)D; cur.W[0] = (uint16_t)Wroot; cur.S[0] = S;
-      cur.heap[0] = 1ull; cur.bfs[0] = 0;
+      cur.heap[0] = 1ull;
+      if (kFit) cur.bfs[0] = 0;
     }
     __syncwarp();
 
@@ -981,14 +984,15 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const uint32_t eL = wscan_u32(sp ? nl : 0u, tL);
           if (sp) {
             const uint32_t childBase = curBase + levelCount + 2 * (carrySplit + eSp);
-            ws.chBase[k] = (uint16_t)childBase;
+            if (kFit) ws.chBase[k] = (uint16_t)childBase;
             uint32_t oi = carryOpen + eOpen;
             uint32_t ps = carryPos + ePos;
             double vL = 0.0, vR = 0.0;
             if (openL) {
               nxt.start[oi] = (uint8_t)ps; nxt.len[oi] = (uint8_t)lenL;
               nxt.W[oi] = (uint16_t)WLv; nxt.S[oi] = SLv;
-              nxt.heap[oi] = 2ull * cur.heap[k]; nxt.bfs[oi] = (uint16_t)childBase;
+              nxt.heap[oi] = 2ull * cur.heap[k];
+              if (kFit) nxt.bfs[oi] = (uint16_t)childBase;
               ws.chOpen[2 * k] = (uint8_t)oi;
               ++oi; ps += lenL;
             } else {
@@ -998,7 +1002,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             if (openR) {
               nxt.start[oi] = (uint8_t)ps; nxt.len[oi] = (uint8_t)lenR;
               nxt.W[oi] = (uint16_t)WRv; nxt.S[oi] = SRv;
-              nxt.heap[oi] = 2ull * cur.heap[k] + 1ull; nxt.bfs[oi] = (uint16_t)(childBase + 1);
+              nxt.heap[oi] = 2ull * cur.heap[k] + 1ull;
+              if (kFit) nxt.bfs[oi] = (uint16_t)(childBase + 1);
               ws.chOpen[2 * k + 1] = (uint8_t)oi;
             } else {
               vR = kMae ? median_leaf(ws.med2[2 * k + 1], F) : leaf_value(SRv, WRv, F);

@@ -650,3 +650,22 @@ def test_predict_c5_shape():
     want = oracle.predict(of, Q)
     np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), want, rtol=RTOL, atol=0)
     np.testing.assert_allclose(rfg.predict(gf, Q[:777]), want[:777], rtol=RTOL, atol=0)
+
+
+def test_predict_threshold_ties():
+    """Batched inference on query values at and next to the split thresholds (x == thr goes
+    left; neighbours one ulp away, which share the threshold's fp32 rounding, must be decided
+    in fp64) -- thresholds taken from the oracle's forest."""
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    of = oracle.fit(X, y, ntree=40, seed=4, mtry=4, target=1)
+    gf = rfg.fit(X, y, ntree=40, seed=4, mtry=4, target=1)
+    _compare_forest(gf, of, X)
+    rnd = np.random.default_rng(0)
+    feats = np.concatenate([t.feature[t.feature >= 0] for t in of.trees])
+    thrs = np.concatenate([t.thr_value[t.feature >= 0] for t in of.trees])
+    Q = np.repeat(X[rnd.integers(0, len(X), 2000)], 1, axis=0).copy()
+    for r in range(len(Q)):
+        for _ in range(6):
+            k = rnd.integers(0, len(feats))
+            Q[r, feats[k]] = [thrs[k], np.nextafter(thrs[k], np.inf), np.nextafter(thrs[k], -np.inf)][r % 3]
+    np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), oracle.predict(of, Q), rtol=RTOL, atol=0)
