@@ -84,6 +84,7 @@ struct CtaSmem {
   SA<double> xte;     // [nte_max][p]
   SA<double> xs;      // ExtraTrees: [p][ntr_max] distinct training values of x_f by dense rank
   SA<uint8_t> tord;   // MAE: [ntr_max] local rows in (t_q, local index) order
+  SA<uint32_t> trr;   // [ntr_max] global row of each local row (threshold values, decide step)
 };
 
 struct NodeSet {  // open nodes of one level
@@ -138,6 +139,7 @@ __host__ __device__ inline void carve_cta(Carve& c, CtaSmem& s, int p, int ntr_m
   s.xte = c.take<double>((size_t)nte_max * p, 16);
   s.xs = extra ? c.take<double>((size_t)p * ntr_max, 16) : SA<double>{0u};
   s.tord = mae ? c.take<uint8_t>(ntr_max, 16) : SA<uint8_t>{0u};
+  s.trr = c.take<uint32_t>(ntr_max, 16);
 }
 
 // BFS ids are needed only when nodes are emitted (fit mode); CV mode routes test rows by
@@ -414,7 +416,11 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
       if (extra) cs.xs[f * ntr_max + gr[(size_t)f * a.ntr_stride + j]] = a.X[(size_t)tr_rows[j] * p + f];
     }
     #pragma unroll 1
-    for (int i = threadIdx.x; i < ntr; i += blockDim.x) cs.tq[i] = a.tq[tr_rows[i]];
+    for (int i = threadIdx.x; i < ntr; i += blockDim.x) {
+      const uint32_t g = tr_rows[i];
+      cs.trr[i] = g;
+      cs.tq[i] = a.tq[g];
+    }
     if (kMae) {
       // t order of the training rows: rank of (t_q, local index) by counting (n_tr <= 255)
       __syncthreads();
@@ -886,7 +892,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const int j = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
           const int f = ws.feat[k * p + j];
           const uint8_t ra = L[f * ntr_max + bp], rb = L[f * ntr_max + bp + 1];
-          const uint32_t ga = tr_rows[ra], gb = tr_rows[rb];
+          const uint32_t ga = cs.trr[ra], gb = cs.trr[rb];
           double thr;
           if (extra) {  // the drawn threshold of slot j (R29), recomputed from the segment's range
             const int st = cur.start[k], fb = f * ntr_max;
