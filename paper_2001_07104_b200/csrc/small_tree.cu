@@ -1011,11 +1011,17 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             openL = !capd && (int)lenL >= a.min_split && ws.ncb[2 * k];
             openR = !capd && (int)lenR >= a.min_split && ws.ncb[2 * k + 1];
           }
-          uint32_t tSp, tOpen, tPos, tL;
-          const uint32_t eSp = wscan_u32(sp ? 1u : 0u, tSp);
-          const uint32_t eOpen = wscan_u32((openL ? 1u : 0u) + (openR ? 1u : 0u), tOpen);
-          const uint32_t ePos = wscan_u32((openL ? lenL : 0u) + (openR ? lenR : 0u), tPos);
-          const uint32_t eL = wscan_u32(sp ? nl : 0u, tL);
+          // the four counters share one warp scan, one byte each: every total is <= 255
+          // (splits and open children <= N/2 < 128, positions and left rows <= N <= 255)
+          uint32_t tPacked;
+          const uint32_t ePacked = wscan_u32((sp ? 1u : 0u) | (((openL ? 1u : 0u) + (openR ? 1u : 0u)) << 8) |
+                                                 (((openL ? lenL : 0u) + (openR ? lenR : 0u)) << 16) |
+                                                 ((sp ? nl : 0u) << 24),
+                                             tPacked);
+          const uint32_t eSp = ePacked & 0xFFu, eOpen = (ePacked >> 8) & 0xFFu, ePos = (ePacked >> 16) & 0xFFu,
+                         eL = ePacked >> 24;
+          const uint32_t tSp = tPacked & 0xFFu, tOpen = (tPacked >> 8) & 0xFFu, tPos = (tPacked >> 16) & 0xFFu,
+                         tL = tPacked >> 24;
           if (sp) {
             const uint32_t childBase = curBase + levelCount + 2 * (carrySplit + eSp);
             if (kFit) ws.chBase[k] = (uint16_t)childBase;
