@@ -241,20 +241,21 @@ __device__ __noinline__ int64_t wmax_i64(int64_t v) {
 
 // Rarely executed helpers are out of line: the kernel's hot per-level code must fit
 // the instruction caches (ncu showed no_instruction stalls with everything inlined).
-__device__ __noinline__ double leaf_value(int64_t S, uint32_t W, int F) {
-  return scalbn(__ddiv_rn(__ll2double_rn(S), __uint2double_rn(W)), -F);
-}
-
-__device__ __noinline__ void philox_pair_ool(uint32_t k0, uint32_t k1, uint32_t b, uint32_t c1, uint32_t c2,
-                                             uint32_t c3, uint64_t& d0, uint64_t& d1) {
-  philox_pair(k0, k1, b, c1, c2, c3, d0, d1);
-}
-
 // RN(a / w) for an integer 1 <= w <= 255 with y = RN(1/w): one Markstein correction
 __device__ __forceinline__ double div_small(double a, double dw, double y) {
   const double q = __dmul_rn(a, y);
   const double r = __fma_rn(-dw, q, a);
   return __fma_rn(r, y, q);
+}
+
+// leaf value fl(fl(S) / W) 2^-F (R13), the division by the reciprocal table (W <= 255)
+__device__ __noinline__ double leaf_value(int64_t S, double2 wy, int F) {
+  return scalbn(div_small(__ll2double_rn(S), wy.x, wy.y), -F);
+}
+
+__device__ __noinline__ void philox_pair_ool(uint32_t k0, uint32_t k1, uint32_t b, uint32_t c1, uint32_t c2,
+                                             uint32_t c3, uint64_t& d0, uint64_t& d1) {
+  philox_pair(k0, k1, b, c1, c2, c3, d0, d1);
 }
 
 // total order of candidates: key (G bits + 1) descending, aux (draw slot, position) ascending (R9)
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
     const bool root_leaf = (a.max_depth == 0) || ((int)D < a.min_split) || (mn == mx);
     if (root_leaf) {
       const double v = kMae ? median_leaf(seg_median2(cs.tord, ntr, ws.w, cs.tq, ws.w, 0, Wroot, S, nullptr), F)
-                            : leaf_value(S, Wroot, F);
+                            : leaf_value(S, cs.rcp2[Wroot], F);
 #pragma unroll
       for (int s = 0; s < TM; ++s)
         if (lane + 32 * s < nte) acc[s] += v;
@@ -1036,7 +1037,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               ws.chOpen[2 * k] = (uint8_t)oi;
               ++oi; ps += lenL;
             } else {
-              vL = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(SLv, WLv, F);
+              vL = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(SLv, cs.rcp2[WLv], F);
               ws.chOpen[2 * k] = kNone;
             }
             if (openR) {
@@ -1046,7 +1047,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               if (kFit) nxt.bfs[oi] = (uint16_t)(childBase + 1);
               ws.chOpen[2 * k + 1] = (uint8_t)oi;
             } else {
-              vR = kMae ? median_leaf(ws.med2[2 * k + 1], F) : leaf_value(SRv, WRv, F);
+              vR = kMae ? median_leaf(ws.med2[2 * k + 1], F) : leaf_value(SRv, cs.rcp2[WRv], F);
               ws.chOpen[2 * k + 1] = kNone;
             }
             ws.chVal[2 * k] = vL;
@@ -1077,7 +1078,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             }
           } else if (act) {
             // open node without any candidate split: leaf (R11)
-            const double v = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(cur.S[k], cur.W[k], F);
+            const double v = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(cur.S[k], cs.rcp2[cur.W[k]], F);
             ws.chVal[2 * k] = v;
             ws.bS[k] = 0ull;  // partition record: not split
             if (kFit) {
