@@ -305,11 +305,11 @@ def run_ours(args):
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (fp64 pipe ops)",
                     "frac": achieved / peak, "traffic": SMALL_TREE_DRAM_BYTES_PER_LAUNCH,
                     "traffic_source": "ncu --set full, one launch (one dataset, 614,400 trees): dram read + write "
-                                      "bytes (profiles/r01r_small_tree_ncu.txt); the working set is on chip",
+                                      "bytes (profiles/r02i_small_tree_ncu.txt); the working set is on chip",
                     "kernel": "small_tree_kernel",
-                    "ncu_context": {"ipc": 2.54, "issue_slots_busy_pct": 63.7, "warps_per_sm": 16,
-                                    "top_stalls": "wait 35 %, short_scoreboard 19 %",
-                                    "source": "profiles/r01r_small_tree_ncu.txt (latency-bound: the fp64 "
+                    "ncu_context": {"ipc": 2.55, "issue_slots_busy_pct": 63.8, "warps_per_sm": 16,
+                                    "top_stalls": "wait 37 %, short_scoreboard 17 %",
+                                    "source": "profiles/r02i_small_tree_ncu.txt (latency-bound: the fp64 "
                                               "pipe fraction is low because each candidate also costs "
                                               "shared-memory scans and per-level node work)"},
                     "kernel_ms_per_step": kern_busy_ms / args.steps, "launches_per_step": kern_n / args.steps,
@@ -373,9 +373,9 @@ def measure_e2e(rfg, ds, args, skw):
 # fp64 arithmetic per evaluated candidate split: 2 squares (DMUL),
 # 2 correctly rounded divisions by W <= 255 as DMUL + 2 DFMA each (Markstein), 1 DADD
 FP64_OPS_PER_CANDIDATE = 9
-# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (1.70 MB + 0.56 MB),
-# from the round-1 final ncu --set full capture (profiles/r01r_small_tree_ncu.txt)
-SMALL_TREE_DRAM_BYTES_PER_LAUNCH = 2.26e6
+# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (1.75 MB + 0.50 MB),
+# from the round-1 final ncu --set full capture (profiles/r02i_small_tree_ncu.txt)
+SMALL_TREE_DRAM_BYTES_PER_LAUNCH = 2.25e6
 FP64_PEAK_TOPS = 148 * 64 * 1.965e9 / 1e12
 
 
