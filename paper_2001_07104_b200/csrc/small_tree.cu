@@ -835,8 +835,12 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
-            // end of segment: next feature slot or next node
+            // end of segment: next feature slot or next node.  Segments are contiguous in the
+            // flattened order and each holds all rows of its node, so the next segment's base
+            // is this one's plus the node's sums (W_k, S_k)
             i = 0;
+            segW += Wk;
+            segS += (uint64_t)Sk;
             if (++j == m) {
               j = 0;
               // node k complete inside this lane (no other lane reads its bW/bS any more)
@@ -853,8 +857,6 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             f = ws.feat[k * p + j];
             if (extra) xbj = ws.xb[k * p + j];
             lbase = f * ntr_max;
-            segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
-            segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
             rn = L[lbase + st];
             rkn = cs.lrank[lbase + rn];
             wr = ws.w[rn];
