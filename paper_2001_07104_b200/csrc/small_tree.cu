@@ -548,16 +548,29 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
     NodeSet cur = ws.cur, nxt = ws.nxt;
     #pragma unroll 1
     for (int f = 0; f < nlists_of(p, kMae); ++f) {
+      // four entries per lane (one 32-bit word of the order), four ballots per step
+      const SA<uint8_t> src = (kMae && f == p) ? cs.tord : cs.ord + f * ntr_max;
+      const unsigned lt = lanemask_lt();
       uint32_t off = 0;
       #pragma unroll 1
-      for (int c = 0; c < ntr; c += 32) {
-        const int j = c + lane;
-        uint8_t r = 0;
-        bool keep = false;
-        if (j < ntr) { r = (kMae && f == p) ? cs.tord[j] : cs.ord[f * ntr_max + j]; keep = ws.w[r] != 0; }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) L[f * ntr_max + off + __popc(bal & lanemask_lt())] = r;
-        off += __popc(bal);
+      for (int c = 0; c < ntr; c += 128) {
+        const int j = c + 4 * lane;
+        const uint32_t rows4 = j < ntr ? *reinterpret_cast<const uint32_t*>(src.ptr() + j) : 0u;
+        bool keep[4];
+        unsigned bal[4];
+        uint32_t before = off;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          keep[q] = j + q < ntr && ws.w[(rows4 >> (8 * q)) & 0xFFu] != 0;
+          bal[q] = __ballot_sync(0xffffffffu, keep[q]);
+          before += __popc(bal[q] & lt);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (keep[q]) L[f * ntr_max + before] = (uint8_t)(rows4 >> (8 * q));
+          before += keep[q] ? 1u : 0u;
+        }
+        off += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
       }
     }
     #pragma unroll 1
