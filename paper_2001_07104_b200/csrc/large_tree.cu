@@ -122,6 +122,10 @@ struct Batch {
   uint32_t* keys;           // [B][2]
   uint8_t* w;               // [B][n] by global row
   long long* wt;            // [B][n] (t_q << 8) | w per training row (exact when ceil(log2 n) >= 9), or null
+  // list entries: row | (low 15 bits of its rank of x_f) << 17 when n <= 2^17 (exact and
+  // ExtraTrees modes), else the row; every reader masks with rowMask
+  int packRank;
+  uint32_t rowMask;
   uint8_t* side;            // [B][n]
   uint32_t* sideBits;       // [B][nbw] go-left bit per row (fused partition path) or null
   int nbw;                  // words per tree in sideBits = ceil(n / 32)
@@ -212,7 +216,7 @@ __global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /
     if (j < b.ntr) { r = src[j]; keep = w[r] != 0; }
     uint32_t ex, tot;
     BS(tmp).ExclusiveSum(keep, ex, tot);
-    if (keep) dst[carry + ex] = r;
+    if (keep) dst[carry + ex] = b.packRank ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
@@ -305,14 +309,14 @@ __global__ void k_extra_bounds(Batch b, int cur, long long NQ) {
   const uint32_t len = nd.len[g];
   const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
   const double* Xf = b.X + f;
-  const double lo = Xf[(size_t)L[0] * b.p], hi = Xf[(size_t)L[len - 1] * b.p];
+  const double lo = Xf[(size_t)(L[0] & b.rowMask) * b.p], hi = Xf[(size_t)(L[len - 1] & b.rowMask) * b.p];
   uint32_t bnd = ~0u;
   if (lo < hi) {
     const double thr = extra_thr(b.keys[2 * t], b.keys[2 * t + 1], nd.heap[g], j, lo, hi);
     uint32_t l = 0, u = len - 1;  // x[l] <= thr < x[u]
     while (u - l > 1) {
       const uint32_t mid = (l + u) >> 1;
-      if (Xf[(size_t)L[mid] * b.p] <= thr) l = mid; else u = mid;
+      if (Xf[(size_t)(L[mid] & b.rowMask) * b.p] <= thr) l = mid; else u = mid;
     }
     bnd = l;
   }
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         sbW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W - lw;
         sbS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S - ls;
       }
-      const uint32_t r = L[c.listBase + c.i];
+      const uint32_t r = L[c.listBase + c.i] & b.rowMask;
       uint32_t wv;
       long long tv;
       if (b.wt) {  // (the chunk may span trees)
@@ -513,8 +517,10 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   unsigned long long rkey = 0ull, raux = ~0ull;
   int rg = c.g;
   const uint32_t* grank = b.grank;
+  // r: list entry of the current element; rk: its rank (packed: the entry's rank bits, the
+  // full rank gathered only when two neighbours' low rank bits agree)
   uint32_t r = L[c.listBase + c.i];
-  uint32_t rk = grank[(size_t)c.f * b.n + r];
+  uint32_t rk = b.packRank ? (r >> 17) : grank[(size_t)c.f * b.n + r];
   for (long long e = e0; e < e1; ++e) {
     const uint32_t wv = s_w[cbase + (int)(e - e0)];
     cW += wv;
@@ -526,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
       bool cand;
       if (b.extra) {
         cand = (uint32_t)c.i == c.xb;  // the segment's one candidate (R29)
+      } else if (b.packRank) {
+        rkn = rn >> 17;
+        cand = rkn != rk || grank[(size_t)c.f * b.n + (rn & 0x1FFFFu)] != grank[(size_t)c.f * b.n + (r & 0x1FFFFu)];
       } else {
         rkn = grank[(size_t)c.f * b.n + rn];
         cand = rkn != rk;
@@ -554,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
         segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
         rn = L[c.listBase];
-        rkn = grank[(size_t)c.f * b.n + rn];
+        rkn = b.packRank ? (rn >> 17) : grank[(size_t)c.f * b.n + rn];
       } else {
         ++c.i;
       }
@@ -581,9 +590,9 @@ __global__ void k_decide(Batch b, int cur, int NO) {
   const int j = (int)(bs.aux >> 32), i = (int)(bs.aux & 0xFFFFFFFFull);
   const int t = (int)nd.tree[g], f = b.feat[(size_t)g * b.m + j];
   const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
-  const uint32_t ra = L[i], rb = L[i + 1];
+  const uint32_t ra = L[i] & b.rowMask, rb = L[i + 1] & b.rowMask;
   if (b.extra) {  // the drawn threshold of slot j (R29)
-    const double lo = b.X[(size_t)L[0] * b.p + f], hi = b.X[(size_t)L[nd.len[g] - 1] * b.p + f];
+    const double lo = b.X[(size_t)(L[0] & b.rowMask) * b.p + f], hi = b.X[(size_t)(L[nd.len[g] - 1] & b.rowMask) * b.p + f];
     b.thr[g] = extra_thr(b.keys[2 * t], b.keys[2 * t + 1], nd.heap[g], j, lo, hi);
   } else {
     b.thr[g] = midpoint_thr(b.X[(size_t)ra * b.p + f], b.X[(size_t)rb * b.p + f]);
@@ -607,7 +616,7 @@ __global__ void k_mark(Batch b, int cur, int NP) {
       const int start = (int)nd.start[g];
       const int i = q - (int)b.tPos0[t] - start;
       const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + start;
-      const uint32_t r = L[i];
+      const uint32_t r = L[i] & b.rowMask;
       const bool left = i <= bi;
       if (b.sideBits) {
         if (left) atomicOr(&b.sideBits[(size_t)t * b.nbw + (r >> 5)], 1u << (r & 31u));
@@ -615,7 +624,7 @@ __global__ void k_mark(Batch b, int cur, int NP) {
         b.side[(size_t)t * b.n + r] = left ? 1 : 0;
       }
       const long long tv = b.tq[r];
-      const long long ref = b.tq[left ? L[0] : L[bi + 1]];
+      const long long ref = b.tq[(left ? L[0] : L[bi + 1]) & b.rowMask];
       if (tv != ref) b.nc[2 * g + (left ? 0 : 1)] = 1;
       if (left) {
         wl = b.w[(size_t)t * b.n + r];
@@ -1197,7 +1206,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(Batch b, int cur, c
 #pragma unroll
   for (int it = 0; it < kPartItems; ++it) {
     const uint32_t i = i0 + it;
-    if (i < N && b.best[posNode[pos0 + i]].key) c += side[L[i]];
+    if (i < N && b.best[posNode[pos0 + i]].key) c += side[L[i] & b.rowMask];
   }
   using BR = cub::BlockReduce<uint32_t, kPartThreads>;
   __shared__ typename BR::TempStorage tmp;
@@ -1234,7 +1243,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
       gg[it] = g;
       rr[it] = r;
       if (b.best[g].key) {
-        const uint32_t lf = side[r];
+        const uint32_t lf = side[r & b.rowMask];
         flags |= (1u | (lf << 1)) << (2 * it);
         c += lf;
       }
@@ -1266,11 +1275,11 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
         if (f == 0) posNode2[npos0 + dest] = child;
       } else if (debug_rows && f == 0) {
         const uint32_t cb = b.out[(size_t)t * b.cap + nd.bfs[g]].left;
-        b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)(cb + (left ? 0 : 1));
+        b.leaf_of_row[(size_t)t * b.n + (r & b.rowMask)] = (int32_t)(cb + (left ? 0 : 1));
       }
       leftBefore += left;
     } else if (debug_rows && f == 0) {
-      b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
+      b.leaf_of_row[(size_t)t * b.n + (r & b.rowMask)] = (int32_t)nd.bfs[g];
     }
   }
 }
@@ -1338,7 +1347,8 @@ __global__ void __launch_bounds__(32 * kPWWarps) k_part_lists_warp(Batch b, int 
     for (int k = 0; k < kPWSteps; ++k) {
       const uint32_t i = base + 32 * k + lane;
       const bool sp = (d[k].y >> 31) != 0u;
-      const bool left = sp && ((sbits[r[k] >> 5] >> (r[k] & 31u)) & 1u);
+      const uint32_t row = r[k] & b.rowMask;
+      const bool left = sp && ((sbits[row >> 5] >> (row & 31u)) & 1u);
       const unsigned bal = __ballot_sync(0xffffffffu, left);
       const uint32_t lb = carry + (uint32_t)__popc(bal & lt);  // left rows of this list before i
       if (sp) {
@@ -1369,7 +1379,7 @@ __global__ void k_part_debug_rows(Batch b, int cur, int NP) {
   const Nodes& nd = b.nd[cur];
   const uint32_t g = b.posNode[cur][q];
   const uint32_t t = nd.tree[g];
-  const uint32_t r = b.L[cur & 1][(size_t)t * b.nl * b.ntr + (q - b.tPos0[t])];
+  const uint32_t r = b.L[cur & 1][(size_t)t * b.nl * b.ntr + (q - b.tPos0[t])] & b.rowMask;
   if (!b.best[g].key) {
     b.leaf_of_row[(size_t)t * b.n + r] = (int32_t)nd.bfs[g];
     return;
@@ -1774,6 +1784,8 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.max_depth = prm->max_depth;
   b.X = d.X; b.tq = d.tq; b.grank = d.grank; b.err = d.err;
   b.nl = nlists;
+  b.packRank = (!hist && n <= (1 << 17)) ? 1 : 0;
+  b.rowMask = b.packRank ? 0x1FFFFu : 0xFFFFFFFFu;
   b.hist = hist ? 1 : 0;
   b.extra = extra ? 1 : 0;
   if (extra) LCK(sc.alloc(&b.xb, (size_t)pl.nmax * mtry));

@@ -669,3 +669,17 @@ def test_predict_threshold_ties():
             k = rnd.integers(0, len(feats))
             Q[r, feats[k]] = [thrs[k], np.nextafter(thrs[k], np.inf), np.nextafter(thrs[k], -np.inf)][r % 3]
     np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
+def test_large_packed_rank_collisions():
+    """The large path packs the low 15 bits of a row's x rank into its list entry (n <= 2^17)
+    and gathers full ranks only when two neighbours' low bits agree.  Here feature 1 pairs
+    rows i and i + 32768, so nodes end up holding such pairs whose x0 ranks differ by exactly
+    2^15 (equal low bits, different values): the split between them must still be found."""
+    n = 40_000
+    i = np.arange(n)
+    X = np.stack([i.astype(np.float64), (i % 32768).astype(np.float64)], 1)
+    y = np.random.default_rng(5).normal(size=n) * 3 + 10
+    of = oracle.fit(X, y, ntree=2, seed=1, mtry=2, bootstrap=False, leaf_rows=True)
+    gf = rfg.fit(X, y, ntree=2, seed=1, mtry=2, bootstrap=False, debug=True)
+    _compare_forest(gf, of, X)
