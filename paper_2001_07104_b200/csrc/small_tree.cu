@@ -816,6 +816,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         uint32_t wr = ws.w[r];
         int64_t tr = cs.tq[r];
         int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
+        uint32_t auxb = ((uint32_t)j << 8) | (uint32_t)st;  // candidate aux minus the index
         // reciprocal-table entries of the next element, loaded one iteration ahead
         double2 ylN = cs.rcp2[(cW + wr - segW) & 0xFFu], yrN = cs.rcp2[(Wk - (cW + wr - segW)) & 0xFFu];
         #pragma unroll 1
@@ -844,7 +845,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
                        : 0ull;
           else
             key = cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
-          const uint32_t aux = ((uint32_t)j << 8) | (uint32_t)(st + i);  // draw slot, position (R9)
+          const uint32_t aux = auxb + (uint32_t)i;  // draw slot << 8 | position (R9)
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
@@ -870,6 +871,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             f = ws.feat[k * p + j];
             if (extra) xbj = ws.xb[k * p + j];
             lbase = f * ntr_max;
+            auxb = ((uint32_t)j << 8) | (uint32_t)st;
             rn = L[lbase + st];
             rkn = cs.lrank[lbase + rn];
             wr = ws.w[rn];
