@@ -1,0 +1,58 @@
+"""run-to-run determinism of the CUDA path, and compute-sanitizer
+(memcheck, racecheck, synccheck) over a tiny end-to-end workload."""
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import datagen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2001_07104_b200 as rfg  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def test_determinism_run_to_run():
+    """Identical bytes from repeated calls: fold MAPEs and predictions of the CV study shape,
+    forests of the small, large (fused / tiled partition), histogram and ExtraTrees paths."""
+    X, y = datagen.paper_shaped(189, "V100", "time")
+    f = rfg.make_folds(y, 10, 3, seed=5, custom=True)
+    a = rfg.cross_validate_grid(X, y, 10, 3, [16, 32], [12, 3], fold_ids=f, target=1, seed=5, want_pred=True)
+    b = rfg.cross_validate_grid(X, y, 10, 3, [16, 32], [12, 3], fold_ids=f, target=1, seed=5, want_pred=True)
+    assert _same(a[0], b[0]) and _same(a[1], b[1])
+    Xl, yl = datagen.scaled(20_000, 64)
+    for kw in (dict(), dict(split_mode=rfg.SPLIT_EXTRA), dict(split_mode=rfg.SPLIT_HIST256, max_depth=10)):
+        e1 = rfg.fit(Xl, yl, ntree=4, mtry=21, target=1, seed=2, **kw).export()
+        e2 = rfg.fit(Xl, yl, ntree=4, mtry=21, target=1, seed=2, **kw).export()
+        for key in ("feature", "left", "value", "thr_index", "tree_off"):
+            assert _same(e1[key], e2[key]), (kw, key)
+    fs = rfg.fit(X, y, ntree=64, mtry=3, target=1, seed=2)
+    Q = X[np.random.default_rng(1).integers(0, 189, 5000)]
+    assert _same(rfg.predict(fs, Q), rfg.predict(fs, Q))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not available")
+    r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "97", "--target-processes", "all",
+                        sys.executable, os.path.join(ROOT, "tests", "sanitize_case.py")],
+                       capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "sanitize case ok" in r.stdout, tail
