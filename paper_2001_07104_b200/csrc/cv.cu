@@ -326,7 +326,7 @@ cudaError_t make_folds(const double* dy, int n, int k, int reps, uint64_t seed, 
     if (n > kFoldSmallMax) return cudaErrorNotSupported;
     size_t smem = (size_t)n * 18;
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_folds_custom_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      allow_max_dynamic_smem(k_folds_custom_small);
     k_folds_custom_small<<<reps, 256, smem, s>>>(dy, n, k, seed, dmask, dfold);
     note_launch();
     return cudaGetLastError();

@@ -23,6 +23,24 @@ inline void retain_pool() {
   done[dev] = true;
 }
 
+// Opt a kernel into the device's full dynamic shared memory (minus its static shared
+// memory).  Always the same value for a kernel, so host threads launching it concurrently
+// with different dynamic sizes cannot invalidate each other's launches (setting the exact
+// size per call raced: one thread lowered the limit under another's launch).
+template <typename K>
+inline cudaError_t allow_max_dynamic_smem(K kern) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
 // stream-ordered scratch allocations (cudaMallocAsync pool), freed at scope exit
 struct Scratch {
   cudaStream_t s;

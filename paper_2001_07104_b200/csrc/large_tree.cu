@@ -1821,7 +1821,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
       err = "histogram mode: mtry too large for the shared-memory staging of the drawn bins";
       return RF_E_UNSUPPORTED;
     }
-    LCK(cudaFuncSetAttribute(k_hist_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    LCK(allow_max_dynamic_smem(k_hist_build));
     list_src = tr_rows_in;  // one node-grouped list of training rows
   }
   int32_t hF = 0;
@@ -1886,7 +1886,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(cudaMemsetAsync(pbufs.flags, 0, ((size_t)pl.tiles_max + 1) * 4, s));
   if (fused_part) {
     LCK(sc.alloc(&pbufs.desc, (size_t)pl.npmax));
-    LCK(cudaFuncSetAttribute(k_part_lists_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)b.nbw * 4)));
+    LCK(allow_max_dynamic_smem(k_part_lists_warp));
   }
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));

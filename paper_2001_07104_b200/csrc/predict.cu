@@ -232,7 +232,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
   }
   if (p <= kSmemMaxP) {
     const size_t smem = (size_t)p * kSmemStrideF * 4;
-    cudaError_t e = cudaFuncSetAttribute(k_predict_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = allow_max_dynamic_smem(k_predict_smem);
     if (e != cudaSuccess) return e;
     k_predict_smem<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p,
                                                                                       mode, out);

@@ -205,7 +205,7 @@ cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (n <= kSmallSortMax) {
     size_t smem = (size_t)n * 8 + n;
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_presort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      allow_max_dynamic_smem(k_presort_small);
     k_presort_small<<<p, 256, smem, s>>>(d.X, n, p, d.order, d.grank);
     note_launch();
     return cudaGetLastError();

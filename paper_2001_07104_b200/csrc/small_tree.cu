@@ -888,6 +888,9 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           rkr = rkn;
         }
         if (cnt > 0 && rk == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
+        // every lane has read its start node's prefix bases (bW/bS) before any lane
+        // overwrites a border node's entries with its best below (racecheck)
+        __syncwarp();
         // nodes on chunk borders: segmented suffix reduction of the head partials
         unsigned long long vkey = hkey;
         uint32_t vaux = haux, vWL = hWL;
@@ -1143,6 +1146,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         }
       }
       PT_MARK(9);
+      __syncwarp();  // the routing above reads the thresholds in bkey, which desc aliases
 
       // ---------------- (g) stable partition of all p lists (feature-major), ping-pong.
       // One pass in 32-element chunks: a ballot of go-left flags gives every
@@ -1316,7 +1320,7 @@ int small_tree_ctas_per_sm(const SmallArgs& a) {
   const size_t smem = small_tree_smem_bytes(a, 0);
   if (smem > 227 * 1024) return 0;
   return with_variant(a, [&](void (*kern)(SmallArgs)) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (allow_max_dynamic_smem(kern) != cudaSuccess) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * a.wpb, smem) != cudaSuccess) return 0;
     return nb;
@@ -1347,7 +1351,7 @@ cudaError_t launch_small_tree(const SmallArgs& a, cudaStream_t s) {
   const long long grid = (long long)a.n_mtry * a.ntask * cta_per_mt;
   if (grid <= 0) return cudaSuccess;
   return with_variant(a, [&](void (*kern)(SmallArgs)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = allow_max_dynamic_smem(kern);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, 32 * a.wpb, smem, s>>>(a);
     note_launch();

@@ -56,3 +56,25 @@ def test_compute_sanitizer(tool):
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail
     assert "sanitize case ok" in r.stdout, tail
+
+
+def test_host_api_concurrent_threads():
+    """The host-pointer API from several threads at once (each thread's calls run on its own
+    CUDA stream; kernels' shared-memory limits are set to one value for every launch): the
+    results equal the same calls made one after another."""
+    import concurrent.futures as cf
+    ds = datagen.study(datagen.SEED)[:6]
+
+    def one(i):
+        d = ds[i]
+        custom = d["target"] == "time"
+        f = rfg.make_folds(d["y"], 10, 2, seed=11 + i, custom=custom)
+        return rfg.cross_validate_grid(d["X"], d["y"], 10, 2, [16, 32], [12, 3], fold_ids=f,
+                                       target=1 if custom else 0, seed=11 + i)
+
+    serial = [one(i) for i in range(len(ds))]
+    with cf.ThreadPoolExecutor(max_workers=len(ds)) as ex:
+        for _ in range(3):
+            par = list(ex.map(one, range(len(ds))))
+            for a, b in zip(serial, par):
+                assert _same(a, b)
