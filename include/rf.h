@@ -28,6 +28,10 @@
  *    stream).  Work is enqueued on that stream; a call may synchronise the
  *    stream internally when it needs a size on the host (documented per call).
  *    Results are complete when the stream is synchronised.
+ *  - Threads: every entry point may be called from several host threads at
+ *    once; host-pointer calls run on a per-thread, per-device CUDA stream, so
+ *    concurrent calls overlap on the GPU.  A forest handle may be read
+ *    (predict, export) concurrently; rf_forest_free must not race its users.
  *  - The library never calls NCCL: multi-GPU sharding is by tree range
  *    (tree_begin/end) and CV task range (task_begin/end); the Python driver
  *    performs the collectives.
