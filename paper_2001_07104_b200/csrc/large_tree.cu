@@ -223,14 +223,24 @@ __global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /
   }
 }
 
-// root node of every tree: W, S, distinct count, constancy
-__global__ void k_root(Batch b, uint32_t* rootInfo /*[B][4]: D, leaf flag*/) {
-  const int t = blockIdx.x;
+// Root node of every tree (W, S, distinct count, constancy) over many CTAs per tree (large n: one CTA per tree left the GPU idle at
+// C4 sizes).  acc[4 t..4 t+3] = (S, D, min t_q, max t_q), initialised by k_root_init.
+__global__ void k_root_init(int B, unsigned long long* acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B) return;
+  acc[4 * t] = 0ull;
+  acc[4 * t + 1] = 0ull;
+  acc[4 * t + 2] = (unsigned long long)LLONG_MAX;
+  acc[4 * t + 3] = (unsigned long long)LLONG_MIN;
+}
+
+__global__ void __launch_bounds__(256) k_root_partial(Batch b, unsigned long long* acc) {
+  const int t = blockIdx.y;
   const uint8_t* w = b.w + (size_t)t * b.n;
   long long S = 0;
   long long mn = LLONG_MAX, mx = LLONG_MIN;
   unsigned int D = 0;
-  for (int j = threadIdx.x; j < b.ntr; j += blockDim.x) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) {
     const uint32_t r = b.tr_rows[j];
     const uint32_t wv = w[r];
     if (wv) {
@@ -252,19 +262,87 @@ __global__ void k_root(Batch b, uint32_t* rootInfo /*[B][4]: D, leaf flag*/) {
   const long long mxr = BR(t1).Reduce(mx, cub::Max());
   __syncthreads();
   const unsigned int Dsum = BRu(t2).Sum(D);
-  if (threadIdx.x == 0) {
-    const bool leaf = (b.max_depth == 0) || ((int)Dsum < b.mss) || (mnr == mxr);
-    rootInfo[4 * t] = Dsum;
-    rootInfo[4 * t + 1] = leaf;
-    Node16 nd;
-    nd.feat = -1; nd.left = 0;
-    nd.v = scalbn(__ddiv_rn(__ll2double_rn(Ssum), __uint2double_rn((unsigned)b.ntr)), -b.F);
-    if (leaf) {
-      b.out[(size_t)t * b.cap] = nd;
-      b.outThr[(size_t)t * b.cap] = 0;
-      b.outCount[t] = 1;
+  if (threadIdx.x == 0 && Dsum) {
+    atomicAdd(&acc[4 * t], (unsigned long long)Ssum);  // modular: exact for the int64 sum
+    atomicAdd(&acc[4 * t + 1], (unsigned long long)Dsum);
+    atomicMin(reinterpret_cast<long long*>(&acc[4 * t + 2]), mnr);
+    atomicMax(reinterpret_cast<long long*>(&acc[4 * t + 3]), mxr);
+  }
+}
+
+__global__ void k_root_finish(Batch b, const unsigned long long* acc, uint32_t* rootInfo) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= b.B) return;
+  const long long Ssum = (long long)acc[4 * t];
+  const unsigned int Dsum = (unsigned int)acc[4 * t + 1];
+  const long long mnr = (long long)acc[4 * t + 2], mxr = (long long)acc[4 * t + 3];
+  const bool leaf = (b.max_depth == 0) || ((int)Dsum < b.mss) || (mnr == mxr);
+  rootInfo[4 * t] = Dsum;
+  rootInfo[4 * t + 1] = leaf;
+  Node16 nd;
+  nd.feat = -1; nd.left = 0;
+  nd.v = scalbn(__ddiv_rn(__ll2double_rn(Ssum), __uint2double_rn((unsigned)b.ntr)), -b.F);
+  if (leaf) {
+    b.out[(size_t)t * b.cap] = nd;
+    b.outThr[(size_t)t * b.cap] = 0;
+    b.outCount[t] = 1;
+  }
+  reinterpret_cast<long long*>(rootInfo)[2 * t + 1] = Ssum;  // words 2,3
+}
+
+// In-bag compaction of long lists in tiles (one CTA per list left the GPU idle at C4
+// sizes): per (tree, list, tile of kIbTile rows) the kept count, a device scan over all
+// tiles, then a block scan + tile prefix - the list's first tile prefix per tile.
+constexpr int kIbThreads = 256, kIbItems = 16, kIbTile = kIbThreads * kIbItems;
+
+__global__ void __launch_bounds__(kIbThreads) k_inbag_count(Batch b, const uint32_t* __restrict__ task_order,
+                                                            int tiles, uint32_t* cnt) {
+  const int lt = blockIdx.x, tile = lt % tiles, tl = lt / tiles;  // tl = t * nl + f
+  const int t = tl / b.nl, f = tl % b.nl;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  const uint32_t* src = task_order + (size_t)f * b.ntr;
+  uint32_t c = 0;
+  const int j0 = tile * kIbTile + threadIdx.x * kIbItems;
+#pragma unroll
+  for (int q = 0; q < kIbItems; ++q) {
+    const int j = j0 + q;
+    if (j < b.ntr) c += w[src[j]] != 0;
+  }
+  using BR = cub::BlockReduce<uint32_t, kIbThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint32_t tot = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) cnt[lt] = tot;
+}
+
+__global__ void __launch_bounds__(kIbThreads) k_inbag_scatter(Batch b, const uint32_t* __restrict__ task_order,
+                                                              int tiles, const uint32_t* __restrict__ pref) {
+  const int lt = blockIdx.x, tile = lt % tiles, tl = lt / tiles;
+  const int t = tl / b.nl, f = tl % b.nl;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  const uint32_t* src = task_order + (size_t)f * b.ntr;
+  uint32_t* dst = b.L[0] + ((size_t)t * b.nl + f) * b.ntr;
+  const int j0 = tile * kIbTile + threadIdx.x * kIbItems;
+  uint32_t rr[kIbItems];
+  uint32_t keep = 0, c = 0;
+#pragma unroll
+  for (int q = 0; q < kIbItems; ++q) {
+    const int j = j0 + q;
+    rr[q] = j < b.ntr ? src[j] : 0u;
+    const uint32_t k = (j < b.ntr && w[rr[q]] != 0) ? 1u : 0u;
+    keep |= k << q;
+    c += k;
+  }
+  using BS = cub::BlockScan<uint32_t, kIbThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  uint32_t ex;
+  BS(tmp).ExclusiveSum(c, ex);
+  uint32_t o = pref[lt] - pref[(size_t)tl * tiles] + ex;
+#pragma unroll
+  for (int q = 0; q < kIbItems; ++q) {
+    if ((keep >> q) & 1u) {
+      const uint32_t r = rr[q];
+      dst[o++] = b.packRank ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
     }
-    reinterpret_cast<long long*>(rootInfo)[2 * t + 1] = Ssum;  // words 2,3
   }
 }
 
@@ -1487,7 +1565,10 @@ struct HistBufs {  // histogram mode: per-chunk-of-nodes histograms and work-ite
   uint32_t* pref = nullptr; // [cap + 1]
 };
 
-struct PartBufs {  // per-level scratch: search look-back status, partition tiles
+struct PartBufs {  // per-level scratch: search look-back status, partition tiles, root / in-bag setup
+  unsigned long long* rootAcc = nullptr;  // [B][4] root statistics accumulators
+  uint32_t* ibCnt = nullptr;              // [B nl tiles] in-bag tile counts (long lists)
+  uint32_t* ibPref = nullptr;
   uint32_t* tileCtr = nullptr;  // search: next tile id
   TileStat* stat = nullptr;     // search: [tiles_max] published aggregates / prefixes
   uint32_t* flags = nullptr;    // search: [tiles_max] (epoch << 2) | state, zeroed once
@@ -1517,10 +1598,28 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       note_launch();
     }
   }
-  k_inbag_lists<<<b.B * b.nl, kThreads, 0, s>>>(b, task_order);
-  note_launch();
-  k_root<<<b.B, 256, 0, s>>>(b, rootInfo);
-  note_launch();
+  const int ibTiles = (b.ntr + kIbTile - 1) / kIbTile;
+  if (ibTiles > 1 && pb.ibCnt && (long long)b.B * b.nl < 4 * 148) {
+    // few long lists (histogram mode: one list per tree): tiled compaction over all
+    // (tree, list, tile); with many lists the one-CTA-per-list kernel fills the GPU already
+    // (and measured faster on the C3 shape)
+    const int items = b.B * b.nl * ibTiles;
+    k_inbag_count<<<items, kIbThreads, 0, s>>>(b, task_order, ibTiles, pb.ibCnt);
+    size_t tb = cub_bytes;
+    LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, pb.ibCnt, pb.ibPref, items, s));
+    k_inbag_scatter<<<items, kIbThreads, 0, s>>>(b, task_order, ibTiles, pb.ibPref);
+    note_launch(2);
+  } else {
+    k_inbag_lists<<<b.B * b.nl, kThreads, 0, s>>>(b, task_order);
+    note_launch();
+  }
+  {
+    k_root_init<<<nblk(b.B, 128), 128, 0, s>>>(b.B, pb.rootAcc);
+    const unsigned cpt = (unsigned)std::min<long long>(std::max<long long>(1, (b.ntr + 8191) / 8192), 256);
+    k_root_partial<<<dim3(cpt, (unsigned)b.B), 256, 0, s>>>(b, pb.rootAcc);
+    k_root_finish<<<nblk(b.B, 128), 128, 0, s>>>(b, pb.rootAcc, rootInfo);
+    note_launch(3);
+  }
   if (b.leaf_of_row) {
     k_root_rows<<<dim3(32, b.B), 256, 0, s>>>(b, rootInfo);
     note_launch();
@@ -1878,6 +1977,12 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   PartBufs pbufs;
   const long long max_tiles = (long long)nlists * (B + pl.npmax / kPartTile + 1) + 1;
   LCK(sc.alloc(&pbufs.tab, (size_t)2 * B));
+  LCK(sc.alloc(&pbufs.rootAcc, (size_t)4 * B));
+  const long long ibItems = (long long)B * nlists * ((ntr + kIbTile - 1) / kIbTile);
+  if ((ntr + kIbTile - 1) / kIbTile > 1 && (long long)B * nlists < 4 * 148) {
+    LCK(sc.alloc(&pbufs.ibCnt, (size_t)ibItems));
+    LCK(sc.alloc(&pbufs.ibPref, (size_t)ibItems));
+  }
   uint32_t search_epoch = 0;
   pbufs.epoch = &search_epoch;
   LCK(sc.alloc(&pbufs.tileCtr, 1));
@@ -1898,6 +2003,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   size_t cb1 = 0, cb2 = 0, cb3 = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, cb1, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)pl.nmax, s);
   cub::DeviceScan::ExclusiveScan(nullptr, cb3, b.chVal, b.chScan, U4Sum(), U4S{0u, 0u, 0u, 0u}, (int)pl.nmax, s);
+  if (pbufs.ibCnt) cub::DeviceScan::ExclusiveSum(nullptr, cb2, pbufs.ibCnt, pbufs.ibPref, (int)ibItems, s);
   size_t cb4 = 0, cb5 = 0;
   if (hist) cub::DeviceScan::ExclusiveSum(nullptr, cb4, hb.nch, hb.pref, (int)hb.cap + 1, s);
   cub::DeviceScan::ExclusiveSum(nullptr, cb5, pbufs.cnt, pbufs.pref, (int)max_tiles, s);
