@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--criterion", default="mse", choices=["mse", "mae"],
+                    help="mse (north_star, default) or mae (the criterion of the paper's best models, "
+                         "T4/T5 P:858-861; R32)")
     ap.add_argument("--streams", type=int, default=10,
                     help="CUDA streams the datasets of a step are spread over (1 = one after another)")
     ap.add_argument("--split", default="exact", choices=["exact", "extra"],
@@ -62,9 +65,10 @@ def parse():
 
 
 def split_kw(args):
-    if args.split == "extra":
-        return {"split_mode": 2, "bootstrap": False}
-    return {}
+    kw = {"split_mode": 2, "bootstrap": False} if args.split == "extra" else {}
+    if getattr(args, "criterion", "mse") == "mae":
+        kw["criterion"] = 1
+    return kw
 
 
 def dist_env():
@@ -141,6 +145,7 @@ def study_config(args, world):
             "l2": "flushed between timed steps (256 MB write)",
             "split": ("ExtraTrees, no bootstrap (P:468-469)" if args.split == "extra"
                       else "bootstrap + exact CART (north_star)"),
+            "criterion": getattr(args, "criterion", "mse"),
             "parallelism": f"task-sharded x{world}",
             "cuda_streams": getattr(args, "streams", 1)}
 
@@ -159,8 +164,9 @@ def run_reference(args):
     oracle.build()
     ds = study_inputs()[0]  # K20 / time
     folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
-    # bounded sample: repeat 0, tasks (folds) 0..3 of one dataset, full grid (~3 s per step)
-    sample_tasks = 4
+    # bounded sample: repeat 0, tasks (folds) 0..3 of one dataset, full grid (~3 s per step;
+    # one task under MAE, whose oracle is ~10x slower per tree)
+    sample_tasks = 1 if getattr(args, "criterion", "mse") == "mae" else 4
 
     def step():
         t0 = time.perf_counter()
@@ -192,7 +198,7 @@ def cpu_baseline_sample(skw):
     oracle.build()
     ds = study_inputs()[0]
     folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
-    tasks = 10  # one whole repeat of 10-fold CV: ~8 s on one host core
+    tasks = 1 if skw.get("criterion") else 10  # one repeat of 10-fold CV: ~8 s on one host core (MAE: one fold)
     t0 = time.perf_counter()
     oracle.cv_grid(ds["X"], ds["y"], K_FOLDS, 1, NTREES, [12, 3], fold_ids=folds, target=1, seed=SEED,
                    task_begin=0, task_end=tasks, **skw)

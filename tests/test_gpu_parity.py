@@ -683,3 +683,13 @@ def test_large_packed_rank_collisions():
     of = oracle.fit(X, y, ntree=2, seed=1, mtry=2, bootstrap=False, leaf_rows=True)
     gf = rfg.fit(X, y, ntree=2, seed=1, mtry=2, bootstrap=False, debug=True)
     _compare_forest(gf, of, X)
+
+
+def test_large_unpacked_rows_150k():
+    """Exact mode above 2^17 rows: list entries are plain row ids (no rank bits), ranks are
+    gathered for every boundary test; 150k rows, ExtraTrees and exact, vs the oracle."""
+    X, y = datagen.scaled(150_000, 16)
+    for kw in (dict(mtry=5), dict(mtry=8, split_mode=2, bootstrap=False)):
+        of = oracle.fit(X, y, ntree=1, seed=4, target=1, **kw)
+        gf = rfg.fit(X, y, ntree=1, seed=4, target=1, **kw)
+        _compare_forest(gf, of, X)
