@@ -119,9 +119,15 @@ struct WarpSmem {
                        // aliases bkey (free once the level's thresholds are used, (g))
   SA<int64_t> med2;    // MAE: [NM][2] doubled weighted medians of the children (or of the node)
   SA<uint64_t> bD;     // MAE fit: [NM] cost D of the chosen split (importance)
+  SA<ulonglong2> mq;   // MAE + ExtraTrees: [kMaeQ] ring of queued search candidates (mae_flush)
+  SA<unsigned long long> mkey;  // MAE: [NM] best queued candidate per open node (key, aux, WL, SL)
+  SA<uint32_t> maux;
+  SA<uint32_t> mWL;
+  SA<int64_t> mSL;
 };
 
 constexpr uint8_t kNone = 0xFF;
+constexpr int kMaeQ = 64;  // MAE candidate ring: <= 31 pending + one loop step's 32 appends
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
 // per-feature stride of the row lists: a multiple of 4 (32-bit list words in (g))
@@ -182,6 +188,11 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.desc = SA<uint32_t>{s.bkey.off};  // ntr_max * 4 <= NM * 8 bytes
   s.med2 = mae ? c.take<int64_t>((size_t)NM * 2, 8) : SA<int64_t>{0u};
   s.bD = (mae && fit) ? c.take<uint64_t>(NM, 8) : SA<uint64_t>{0u};
+  s.mq = (mae && extra) ? c.take<ulonglong2>(kMaeQ, 16) : SA<ulonglong2>{0u};
+  s.mkey = (mae && extra) ? c.take<unsigned long long>(NM, 8) : SA<unsigned long long>{0u};
+  s.mSL = (mae && extra) ? c.take<int64_t>(NM, 8) : SA<int64_t>{0u};
+  s.maux = (mae && extra) ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
+  s.mWL = (mae && extra) ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
 }
 
 // ---------------------------------------------------------------- warp ops --
@@ -308,9 +319,10 @@ __device__ __forceinline__ uint64_t med_sad2(const MedTrack& m, int64_t S) {
 // Search key of one MAE candidate: ~D with D = SAD2(left) + SAD2(right) < 2^63, so the
 // key is > 0 and "larger key = better" keeps the MSE path's reduction and tie-break (R9).
 // tl: the node's rows in t order (len ln); left rows are those with lrank_f <= thr.
-__device__ __noinline__ unsigned long long mae_key(SA<uint8_t> tl, int ln, SA<uint8_t> lr, uint32_t thr,
-                                                   SA<uint8_t> w, SA<int64_t> tq, uint32_t WL, int64_t SL,
-                                                   uint32_t WR, int64_t SR) {
+// m2L, m2R (if not null): the children's doubled medians (their leaf values if it wins).
+__device__ __forceinline__ unsigned long long mae_walk(SA<uint8_t> tl, int ln, SA<uint8_t> lr, uint32_t thr,
+                                                       SA<uint8_t> w, SA<int64_t> tq, uint32_t WL, int64_t SL,
+                                                       uint32_t WR, int64_t SR, int64_t& m2L, int64_t& m2R) {
   MedTrack mL, mR;
   med_init(mL, WL);
   med_init(mR, WR);
@@ -322,7 +334,15 @@ __device__ __noinline__ unsigned long long mae_key(SA<uint8_t> tl, int ln, SA<ui
     if ((uint32_t)lr[r] <= thr) med_push(mL, wv, t); else med_push(mR, wv, t);
     if (mL.state == 2 && mR.state == 2) break;
   }
+  m2L = mL.m2;
+  m2R = mR.m2;
   return ~(med_sad2(mL, SL) + med_sad2(mR, SR));
+}
+__device__ __noinline__ unsigned long long mae_key(SA<uint8_t> tl, int ln, SA<uint8_t> lr, uint32_t thr,
+                                                   SA<uint8_t> w, SA<int64_t> tq, uint32_t WL, int64_t SL,
+                                                   uint32_t WR, int64_t SR) {
+  int64_t a, b;
+  return mae_walk(tl, ln, lr, thr, w, tq, WL, SL, WR, SR, a, b);
 }
 
 // Doubled weighted median (and, if sad2 != null, the doubled SAD) of the rows of a t-ordered
@@ -342,6 +362,60 @@ __device__ __noinline__ int64_t seg_median2(SA<uint8_t> tl, int ln, SA<uint8_t> 
   }
   if (sad2) *sad2 = med_sad2(m, S);
   return m.m2;
+}
+
+// MAE candidate queue (R32).  The search loop appends its candidates to a per-warp ring
+// (ballot-compacted; entry = node k | feature f << 8 | boundary rank << 16 | aux << 24 |
+// WL << 40, and SL) and every 32 queued candidates are scored here one per lane, so each
+// lane walks one candidate's t-ordered rows instead of the warp waiting on the few lanes
+// that hold a candidate in a loop step (ExtraTrees: one candidate per segment).  The keys
+// merge into the per-node best (mkey ...) under the search's total order (R9), which does
+// not depend on the order in which candidates are merged.
+__device__ __noinline__ void mae_flush(SA<ulonglong2> q, uint32_t qh, int nq, NodeSet cur, SA<uint8_t> L, int p,
+                                       int ntr_max, SA<uint8_t> lrank, SA<uint8_t> w, SA<int64_t> tq,
+                                       SA<unsigned long long> mkey, SA<uint32_t> maux, SA<uint32_t> mWL,
+                                       SA<int64_t> mSL, SA<int64_t> med2) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();  // the entries written by every lane are visible
+  int k = -1 - lane;
+  unsigned long long key = 0ull;
+  uint32_t aux = 0u, WL = 0u;
+  int64_t SL = 0, m2L = 0, m2R = 0;
+  if (lane < nq) {
+    const ulonglong2 e = q[(qh + (uint32_t)lane) & (kMaeQ - 1)];
+    k = (int)(e.x & 0xFFu);
+    const int f = (int)((e.x >> 8) & 0xFFu);
+    const uint32_t thr = (uint32_t)((e.x >> 16) & 0xFFu);
+    aux = (uint32_t)((e.x >> 24) & 0xFFFFu);
+    WL = (uint32_t)((e.x >> 40) & 0xFFFFu);
+    SL = (int64_t)e.y;
+    const uint32_t Wk = cur.W[k];
+    const int64_t Sk = cur.S[k];
+    key = mae_walk(L + (p * ntr_max + cur.start[k]), cur.len[k], lrank + f * ntr_max, thr, w, tq, WL, SL,
+                   Wk - WL, Sk - SL, m2L, m2R);
+  }
+  __syncwarp();  // every entry is read before its ring slot is reused
+  // the lowest lane of each node's group merges the group's candidates, then the node best
+  bool lead = lane < nq;
+  #pragma unroll 1
+  for (int s = 0; s < nq; ++s) {
+    const int ok = __shfl_sync(0xffffffffu, k, s);
+    const unsigned long long okey = __shfl_sync(0xffffffffu, key, s);
+    const uint32_t oaux = __shfl_sync(0xffffffffu, aux, s);
+    const uint32_t oWL = __shfl_sync(0xffffffffu, WL, s);
+    const int64_t oSL = __shfl_sync(0xffffffffu, SL, s);
+    const int64_t om2L = __shfl_sync(0xffffffffu, m2L, s);
+    const int64_t om2R = __shfl_sync(0xffffffffu, m2R, s);
+    if (ok == k && s != lane) {
+      if (s < lane) lead = false;
+      else if (better(okey, oaux, key, aux)) { key = okey; aux = oaux; WL = oWL; SL = oSL; m2L = om2L; m2R = om2R; }
+    }
+  }
+  if (lead && better(key, aux, mkey[k], maux[k])) {
+    mkey[k] = key; maux[k] = aux; mWL[k] = WL; mSL[k] = SL;
+    med2[2 * k] = m2L; med2[2 * k + 1] = m2R;  // the children's medians of the node's best so far
+  }
+  __syncwarp();
 }
 
 __device__ __noinline__ double median_leaf(int64_t m2, int F) { return scalbn(__ll2double_rn(m2), -F - 1); }
@@ -817,6 +891,12 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         int64_t tr = cs.tq[r];
         int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
         uint32_t auxb = ((uint32_t)j << 8) | (uint32_t)st;  // candidate aux minus the index
+        uint32_t qh = 0u, qt = 0u;  // MAE candidate ring: head, tail
+        if (kMae && kExtra) {
+          #pragma unroll 1
+          for (int kk = lane; kk < nOpen; kk += 32) { ws.mkey[kk] = 0ull; ws.maux[kk] = 0x7FFFFFFFu; }
+          __syncwarp();
+        }
         // reciprocal-table entries of the next element, loaded one iteration ahead
         double2 ylN = cs.rcp2[(cW + wr - segW) & 0xFFu], yrN = cs.rcp2[(Wk - (cW + wr - segW)) & 0xFFu];
         #pragma unroll 1
@@ -840,12 +920,29 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
           const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
           unsigned long long key;
-          if (kMae)  // R32: left = rows of the node with rank <= the boundary's rank
+          const uint32_t aux = auxb + (uint32_t)i;  // draw slot << 8 | position (R9)
+          if (kMae && kExtra) {  // R32: queued, scored one per lane by mae_flush (left = rank <= rkr)
+            key = 0ull;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+            if (cand) {
+              const uint32_t slot = (qt + (uint32_t)__popc(bal & ((1u << lane) - 1u))) & (kMaeQ - 1);
+              ws.mq[slot] = make_ulonglong2((unsigned long long)k | ((unsigned long long)f << 8) |
+                                                ((unsigned long long)rkr << 16) |
+                                                ((unsigned long long)(aux & 0xFFFFu) << 24) |
+                                                ((unsigned long long)WL << 40),
+                                            (unsigned long long)SL);
+            }
+            qt += (uint32_t)__popc(bal);
+            if (qt - qh >= 32u) {  // warp-uniform
+              mae_flush(ws.mq, qh, 32, cur, L, p, ntr_max, cs.lrank, ws.w, cs.tq, ws.mkey, ws.maux, ws.mWL, ws.mSL, ws.med2);
+              qh += 32u;
+            }
+          } else if (kMae) {  // exact CART: nearly every element is a candidate, scored in place
             key = cand ? mae_key(L + (p * ntr_max + st), ln, cs.lrank + lbase, rkr, ws.w, cs.tq, WL, SL, WR, SR)
                        : 0ull;
-          else
+          } else {
             key = cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
-          const uint32_t aux = auxb + (uint32_t)i;  // draw slot << 8 | position (R9)
+          }
           ncand += cand;
           if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
@@ -888,6 +985,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           rkr = rkn;
         }
         if (cnt > 0 && rk == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
+        if (kMae && kExtra) {
+          #pragma unroll 1
+          while (qt != qh) {
+            const int nq = (int)min(qt - qh, 32u);
+            mae_flush(ws.mq, qh, nq, cur, L, p, ntr_max, cs.lrank, ws.w, cs.tq, ws.mkey, ws.maux, ws.mWL, ws.mSL, ws.med2);
+            qh += (uint32_t)nq;
+          }
+        }
         // every lane has read its start node's prefix bases (bW/bS) before any lane
         // overwrites a border node's entries with its best below (racecheck)
         __syncwarp();
@@ -928,6 +1033,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         }
       }
       __syncwarp();
+      if (kMae && kExtra) {  // the queued candidates' per-node bests replace the (empty) in-loop ones
+        #pragma unroll 1
+        for (int kk = lane; kk < nOpen; kk += 32) {
+          ws.bkey[kk] = ws.mkey[kk]; ws.baux[kk] = ws.maux[kk]; ws.bW[kk] = ws.mWL[kk];
+          ws.bS[kk] = (uint64_t)ws.mSL[kk];
+        }
+        __syncwarp();
+      }
       PT_MARK(5);
 
       // ---------------- (c) decisions and thresholds; first-row targets of the children
@@ -993,8 +1106,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           if (aux & 0x80000000u) {
             const uint32_t WLv = ws.bW[k];
             const int64_t SLv = (int64_t)ws.bS[k];
-            ws.med2[2 * k] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 1, WLv, SLv, nullptr);
-            ws.med2[2 * k + 1] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 2, cur.W[k] - WLv, cur.S[k] - SLv, nullptr);
+            if (!kExtra) {  // ExtraTrees: mae_flush stored the winning candidate's child medians
+              ws.med2[2 * k] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 1, WLv, SLv, nullptr);
+              ws.med2[2 * k + 1] = seg_median2(tl, ln, ws.w, cs.tq, ws.side, 2, cur.W[k] - WLv, cur.S[k] - SLv, nullptr);
+            }
             if (kFit && a.imp) {  // importance: (SAD2(node) - D) 2^(-F-1) (R30, R32)
               uint64_t sad = 0;
               seg_median2(tl, ln, ws.w, cs.tq, ws.side, 0, cur.W[k], cur.S[k], &sad);

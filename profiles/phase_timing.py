@@ -1,7 +1,7 @@
 """Per-phase cycle split of the warp-per-tree kernel on the full-study workload.
 
   RF_PHASE_TIMING=1 python -m paper_2001_07104_b200.build
-  RFGPU_LIB=$PWD/paper_2001_07104_b200/librfgpu_pt.so python profiles/phase_timing.py [exact|extra]
+  RFGPU_LIB=$PWD/paper_2001_07104_b200/librfgpu_pt.so python profiles/phase_timing.py [exact|extra|mae|extra_mae]
 
 Runs the K20/time dataset of the study (30 x 10-fold, ntree <= 1024, mtry {12,3})
 once for warm-up, then once measured; prints each phase's share of the summed
@@ -18,7 +18,9 @@ import datagen  # noqa: E402
 import paper_2001_07104_b200 as rfg  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "exact"
-kw = {"split_mode": rfg.SPLIT_EXTRA, "bootstrap": False} if mode == "extra" else {}
+kw = {"split_mode": rfg.SPLIT_EXTRA, "bootstrap": False} if mode.startswith("extra") else {}
+if mode.endswith("mae"):
+    kw["criterion"] = 1
 for ds in datagen.study(datagen.SEED)[:2]:
     X = torch.as_tensor(ds["X"], device="cuda")
     y = torch.as_tensor(ds["y"], device="cuda")
