@@ -57,23 +57,50 @@ def c3(rfg, torch, ntrees):
     rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7)  # warm-up (allocator pool, modules)
     torch.cuda.synchronize()
     rfg.set_profiling(True)
+    rfg.row_levels(reset=True)
     t0 = time.perf_counter()
     f = rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7)
     torch.cuda.synchronize()
     sec = time.perf_counter() - t0
+    rl = rfg.row_levels(reset=True)
     prof = rfg.last_profile()
     rfg.set_profiling(False)
     info = f.info()
+    kms = {k: v[0] for k, v in prof.items()}
+    # HBM roofline: algorithmic bytes per row-level =
+    # partition 8p (read + write a u32 entry in each of the p lists) + search 4m (the m drawn
+    # lists' entries); row-levels counted by the library (rf_debug_row_levels)
+    p, m = 64, 21
+    grow_ms = kms.get("large_search", 0.0) + kms.get("large_partition", 0.0)
+    peak, src = hbm_peak()
+    achieved = rl * (8 * p + 4 * m) / (grow_ms / 1e3) / 1e9 if grow_ms else None
+    part_gbs = rl * 8 * p / (kms["large_partition"] / 1e3) / 1e9 if kms.get("large_partition") else None
     return {"config": f"C3 rf_fit 100k x 64 exact, mtry 21, unbounded depth ({ntrees} of 500 trees)",
             "trees": ntrees, "seconds": sec, "trees_per_s": ntrees / sec,
-            "nodes_per_tree": info["total_nodes"] / ntrees, "kernels_ms": {k: v[0] for k, v in prof.items()}}
+            "nodes_per_tree": info["total_nodes"] / ntrees, "row_levels_per_tree": rl / ntrees,
+            "kernels_ms": kms,
+            "roofline": {"bound": "hbm", "unit": "GB/s", "bytes_per_row_level": 8 * p + 4 * m,
+                         "achieved": achieved, "peak": peak, "frac": achieved / peak if achieved else None,
+                         "partition_achieved": part_gbs,
+                         "partition_frac": part_gbs / peak if part_gbs else None,
+                         "kernels": "large_search + large_partition (CUDA events, rfg.last_profile)",
+                         "peak_source": src}}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
 
 
 def c4(rfg, torch, ntrees, nrows):
     X, y = datagen.scaled(nrows, 64)
     Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
     del X
-    rfg.fit(Xd, yd, ntree=2, mtry=21, target=1, seed=7, max_depth=12, split_mode=1)  # warm-up
+    # warm-up at the timed size (allocator pool and batch buffers sized as in the timed call)
+    rfg.fit(Xd, yd, ntree=ntrees, mtry=21, target=1, seed=7, max_depth=12, split_mode=1)
     torch.cuda.synchronize()
     rfg.set_profiling(True)
     t0 = time.perf_counter()

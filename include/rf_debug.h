@@ -19,6 +19,11 @@ RF_API rf_status rf_debug_philox_dev(const uint32_t* dctr_key, uint32_t* dout, u
    (host count) and candidate splits evaluated by the split-search kernels on
    the current device (device counter; this call synchronises the device). */
 RF_API rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates);
+/* Cumulative row-levels grown by the global level-synchronous (large-n) path of this
+   process: the sum over levels and trees of the live distinct in-bag rows N_l (SURVEY.md
+   8(a) a6/a7; the unit of the C3/C4 algorithmic-bytes figures).  Host
+   count, no synchronisation; reset != 0 zeroes it after reading.  out may be NULL. */
+RF_API rf_status rf_debug_row_levels(uint64_t* out, int reset);
 /* Per-phase SM cycles of the warp-per-tree kernel, summed over warps (lane 0
    of each warp adds clock64 deltas; out[16], phase names in DESIGN.md sec. 6).
    Only a library built with RF_PHASE_TIMING=1 (a profiling build) records

@@ -39,7 +39,7 @@ ABI_SYMBOLS = [
     "rf_cv_finalize_dev", "rf_predict_partial", "rf_cv_partial", "rf_cv_finalize", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
     "rf_last_profile", "rf_set_profiling",
-    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_phase_cycles", "rf_debug_set_option",
+    "rf_debug_ln_dev", "rf_debug_philox_dev", "rf_debug_counters", "rf_debug_row_levels", "rf_debug_phase_cycles", "rf_debug_set_option",
 ]
 
 
@@ -108,6 +108,7 @@ def lib():
             "rf_debug_ln_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_philox_dev": ([P, P, u64, P], C.c_int),
             "rf_debug_counters": ([P, P], C.c_int),
+            "rf_debug_row_levels": ([P, C.c_int], C.c_int),
             "rf_debug_phase_cycles": ([P, C.c_int], C.c_int),
             "rf_debug_set_option": ([C.c_char_p, C.c_int64], C.c_int),
         }
@@ -456,6 +457,13 @@ def counters():
     a, c = C.c_uint64(), C.c_uint64()
     _check(lib().rf_debug_counters(C.byref(a), C.byref(c)))
     return a.value, c.value
+
+
+def row_levels(reset=False):
+    """Row-levels (sum over levels and trees of live in-bag rows) grown by the large-n path."""
+    v = C.c_uint64()
+    _check(lib().rf_debug_row_levels(C.byref(v), 1 if reset else 0))
+    return v.value
 
 
 def launch_count():

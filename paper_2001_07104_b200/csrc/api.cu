@@ -518,6 +518,8 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
 namespace rf {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+static std::atomic<unsigned long long> g_row_levels{0};
+void note_row_levels(long long n) { g_row_levels.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 unsigned long long* candidate_counter() {
   static unsigned long long* ptrs[64] = {nullptr};
   int dev = 0;
@@ -1128,6 +1130,12 @@ rf_status rf_debug_counters(uint64_t* launches, uint64_t* candidates) {
     unsigned long long* c = rf::candidate_counter();
     if (c) CK(cudaMemcpy(candidates, c, 8, cudaMemcpyDeviceToHost), "counter");
   }
+  return RF_OK;
+}
+
+rf_status rf_debug_row_levels(uint64_t* out, int reset) {
+  const unsigned long long v = reset ? rf::g_row_levels.exchange(0ull) : rf::g_row_levels.load();
+  if (out) *out = v;
   return RF_OK;
 }
 

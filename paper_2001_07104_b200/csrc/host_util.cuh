@@ -66,6 +66,7 @@ struct Scratch {
 
 // count of this library's kernel launches (rf_debug_counters); defined in api.cu
 void note_launch(int n = 1);
+void note_row_levels(long long n);
 // device counter of evaluated candidate splits (algorithmic work of the split search)
 unsigned long long* candidate_counter();
 

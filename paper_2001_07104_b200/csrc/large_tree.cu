@@ -1530,6 +1530,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   }
   int cur = 0, depth = 0;
   while (NO > 0) {
+    note_row_levels(NP);
     k_node_prep<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
     note_launch();
     if (b.extra) {

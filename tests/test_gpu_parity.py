@@ -549,6 +549,11 @@ MAE_CASES = [
                                                                              split_mode=2)),
     ("extra_power_boot", lambda: datagen.paper_shaped(168, "GTX1650", "power"), dict(mtry=4, split_mode=2)),
     ("extra_ties", lambda: datagen.tiny(200, 5, 3, distinct=6), dict(mtry=2, split_mode=2, bootstrap=False)),
+    # ExtraTrees + MAE candidate ring (mae_flush): 12 candidates per node, several nodes and
+    # flushes per level, equal costs across candidates (ties in x and y) -> the R9 tie-break
+    ("extra_ring_ties", lambda: (datagen.tiny(240, 12, 4, distinct=4)[0],
+                                 np.round(datagen.tiny(240, 12, 4)[1], 0) + 1.0),
+     dict(mtry=12, split_mode=2)),
 ]
 
 
@@ -693,3 +698,26 @@ def test_large_unpacked_rows_150k():
         of = oracle.fit(X, y, ntree=1, seed=4, target=1, **kw)
         gf = rfg.fit(X, y, ntree=1, seed=4, target=1, **kw)
         _compare_forest(gf, of, X)
+
+
+@pytest.mark.gpu
+def test_large_path_row_level_counter():
+    """rf_debug_row_levels: the large-n path's unit of work equals
+    sum over rows of the depth of the row's leaf when every node with >= 2 distinct rows splits
+    (no bootstrap, mtry = p, continuous x and y) -- the figure bench_configs.py's C3 roofline uses."""
+    X, y = datagen.tiny(400, 3, 5)
+    rfg.row_levels(reset=True)
+    gf = rfg.fit(X, y, ntree=3, seed=4, mtry=3, bootstrap=False, debug=True)
+    got = rfg.row_levels(reset=True)
+    e = gf.export()
+    lr = gf.leaf_rows()
+    want = 0
+    for t in range(3):
+        a, b = int(e["tree_off"][t]), int(e["tree_off"][t + 1])
+        feat, left = e["feature"][a:b], e["left"][a:b]
+        depth = np.zeros(b - a, np.int64)
+        for i in range(b - a):  # BFS order: parents precede children
+            if feat[i] >= 0:
+                depth[left[i]] = depth[left[i] + 1] = depth[i] + 1
+        want += int(depth[lr[t]].sum())
+    assert got == want > 0
