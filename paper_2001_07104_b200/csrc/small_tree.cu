@@ -338,6 +338,8 @@ __device__ __forceinline__ unsigned long long mae_walk(SA<uint8_t> tl, int ln, S
   m2R = mR.m2;
   return ~(med_sad2(mL, SL) + med_sad2(mR, SR));
 }
+// (Issuing the next element's loads one step ahead in this walk measured 2.9x slower for
+// ExtraTrees + MAE -- profiles/r03k_mae_pf_ab.txt -- and is not used.)
 __device__ __noinline__ unsigned long long mae_key(SA<uint8_t> tl, int ln, SA<uint8_t> lr, uint32_t thr,
                                                    SA<uint8_t> w, SA<int64_t> tq, uint32_t WL, int64_t SL,
                                                    uint32_t WR, int64_t SR) {
