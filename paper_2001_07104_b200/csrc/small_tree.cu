@@ -1064,6 +1064,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             const double hi = cs.xs[fb + cs.lrank[fb + L[fb + st + cur.len[k] - 1]]];
             thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
           } else {
+            // (read-only-path loads (__ldg) here measured equal, profiles/r03n_x_ldg_ab.txt)
             thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
           }
           if (kMae && kFit) ws.bD[k] = ~key;  // cost D of the chosen split (importance)
