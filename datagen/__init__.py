@@ -134,3 +134,76 @@ def tiny(n: int, p: int, seed: int, distinct: int | None = None, pos: bool = Tru
         X = rng.normal(size=(n, p))
     y = rng.lognormal(0.0, 1.0, size=n) if pos else rng.normal(size=n)
     return np.ascontiguousarray(X), np.ascontiguousarray(y)
+
+
+# ------------------------------------------------------ on-device generator --
+# The C4 / C5 sets (10M / 100M rows x 64 features = 5.1 / 51 GB) are generated on the GPU with
+# the same recipe as scaled() ("For C4/C5 an on-device generator
+# may be used; the oracle then consumes the D2H copy of exactly those bytes").  torch's CUDA
+# Philox generator, one generator per block of DEV_BLOCK rows seeded by (seed, block), so the
+# rows of a block do not depend on n (a 10M-row set is the prefix of the 100M-row one) and the
+# output is identical run to run.  Like the rest of this module it holds none of the method's
+# arithmetic.
+DEV_BLOCK = 1 << 20
+
+
+def _features_torch(g, n, dev):
+    import torch
+    f64 = torch.float64
+    tpc_vals = torch.tensor([32, 64, 128, 192, 256, 512, 1024], dtype=f64, device=dev)
+    probs = torch.tensor([.05, .15, .30, .05, .30, .10, .05], dtype=f64, device=dev)
+    tpc = tpc_vals[torch.multinomial(probs, n, replacement=True, generator=g)]
+    U = lambda lo, hi: torch.rand(n, dtype=f64, device=dev, generator=g) * (hi - lo) + lo
+    ctas = torch.clamp(torch.round(10.0 ** U(0.0, 5.5)), min=1.0)
+    per_thread = 10.0 ** U(1.0, 4.5)
+    alpha = torch.tensor([4.0, 2.0, 2.0, 0.5, 0.5, 3.0], dtype=f64, device=dev).expand(n, 6)
+    gam = torch._standard_gamma(alpha.contiguous(), generator=g)
+    mix = gam / gam.sum(1, keepdim=True)
+    total = per_thread * tpc * ctas
+    cls = torch.round(mix * total[:, None])
+    arith, logic, control, special, sync, mem = (cls[:, i] for i in range(6))
+    vsz = torch.tensor([4.0, 8.0, 16.0], dtype=f64, device=dev)[torch.randint(0, 3, (n,), device=dev, generator=g)]
+    gvol = torch.round(mem * vsz * U(0.3, 1.0))
+    pvol = torch.round(10.0 ** U(1.0, 3.0) * tpc * ctas)
+    svol = torch.round(mem * 4.0 * U(0.0, 0.7))
+    ai = arith / torch.clamp(gvol, min=1.0)
+    tot = arith + logic + control + special + sync + mem
+    X = torch.stack([tpc, ctas, tot, special, logic, control, arith, sync, gvol, pvol, svol, ai], dim=1)
+    return X, dict(arith=arith, special=special, mem=mem, gvol=gvol, tpc=tpc, ctas=ctas, sync=sync, total=tot)
+
+
+def scaled_device(n: int, p: int = 64, seed: int = SEED, device="cuda", with_y: bool = True):
+    """scaled() on the GPU (torch tensors [n, p] fp64 and [n] fp64 > 0, K20 time target):
+    paper features, per-class sub-counts, 4 low-cardinality columns."""
+    import torch
+    assert p >= 16
+    dev = torch.device(device)
+    X = torch.empty((n, p), dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev) if with_y else None
+    g = torch.Generator(device=dev)
+    k20 = GPUS["K20"]
+    lanes = k20["sms"] * 64.0 * k20["clk"] * 1e6
+    nsub = p - 12 - 4
+    for b0 in range(0, n, DEV_BLOCK):
+        m = min(DEV_BLOCK, n - b0)
+        g.manual_seed((seed * 1000003 + 7 * p + b0 // DEV_BLOCK) & 0x7FFFFFFFFFFFFFFF)
+        X12, parts = _features_torch(g, m, dev)
+        blk = X[b0:b0 + m]
+        blk[:, :12] = X12
+        cls = torch.stack([X12[:, 6], X12[:, 4], X12[:, 5], X12[:, 3]], dim=1)
+        fr = torch.rand((m, nsub), dtype=torch.float64, device=dev, generator=g) * 0.45 + 0.05
+        idx = torch.arange(nsub, device=dev) % 4
+        blk[:, 12:12 + nsub] = torch.round(cls[:, idx] * fr)
+        blk[:, 12 + nsub:] = torch.randint(0, 8, (m, 4), device=dev, generator=g).to(torch.float64)
+        if with_y:
+            comp = (parts["arith"] + 4.0 * parts["special"] + parts["total"] * 0.25) / lanes * 1e6
+            memt = parts["gvol"] / (k20["bw"] * 1e9) * 1e6
+            sync = parts["sync"] / lanes * 1e6 * 8.0
+            t = 2.0 + comp + memt + sync
+            y[b0:b0 + m] = t * torch.exp(torch.randn(m, dtype=torch.float64, device=dev, generator=g) * k20["sigma"])
+    return (X, y) if with_y else X
+
+
+def queries_device(n: int, p: int = 64, seed: int = SEED, device="cuda"):
+    """Held-out query rows for inference on the GPU (seed + 1, as queries())."""
+    return scaled_device(n, p, seed + 1, device, with_y=False)

@@ -85,6 +85,15 @@ typedef enum { RF_TARGET_IDENTITY = 0, RF_TARGET_LOG = 1 } rf_target;
    (F = 62 - ceil(log2 n) - e - 2) so doubled medians and doubled absolute-
    deviation sums are exact integers below 2^63. */
 typedef enum { RF_CRITERION_MSE = 0, RF_CRITERION_MAE = 1 } rf_criterion;
+/* Tie-break among candidate splits with bitwise-equal scores (R9; the paper is
+   silent).  LOWEST_FEATURE (default): the lowest feature index, then the
+   lowest threshold -- BASELINE.json north_star's "deterministic tie-break of
+   lowest feature then lowest threshold".  DRAW_ORDER: the feature drawn first
+   at the node (the lowest slot of R4's partial Fisher-Yates), then the lowest
+   threshold -- scikit-learn's splitter (the paper's library) visits
+   the features in draw order and keeps the first best.  Both are total orders
+   over a node's candidates, so the GPU's reduction order cannot change them. */
+typedef enum { RF_TIE_LOWEST_FEATURE = 0, RF_TIE_DRAW_ORDER = 1 } rf_tie_break;
 
 /* Hyper-parameters and sharding. */
 typedef struct {
@@ -103,10 +112,12 @@ typedef struct {
   uint32_t task_begin;        /* CV tasks (task = rep*k + fold) [task_begin, task_end);  */
   uint32_t task_end;          /*   0,0 = all; outputs of other tasks are NaN             */
   uint32_t criterion;         /* rf_criterion: MSE (default) or MAE (R32)                */
+  uint32_t tie_break;         /* rf_tie_break: lowest feature (default) or draw order    */
 } rf_params;
 
 /* Fills the defaults: ntree 100, mtry 0, min_samples_split 2, max_depth -1,
-   bootstrap 1, exact, IDENTITY, seed 0, device 0, no sharding, MSE. */
+   bootstrap 1, exact, IDENTITY, seed 0, device 0, no sharding, MSE,
+   lowest-feature tie-break. */
 RF_API void rf_params_default(rf_params* prm);
 
 /* Opaque device-resident forest: flattened BFS nodes (16 B each:
@@ -186,10 +197,22 @@ RF_API rf_status rf_cross_validate_grid_dev(const double* dX, uint64_t n, uint32
                                      const int32_t* dfold_ids, const uint32_t* ntrees,
                                      uint32_t n_ntree, const uint32_t* mtrys, uint32_t n_mtry,
                                      double* dfold_mape, double* dpred, void* stream);
-/* Single grid point: prm->ntree trees, prm->mtry; fold_mape [repeats][k]. */
+/* rf_cross_validate: the problem statement's call:
+   repeated k-fold CV of ONE model -- prm->ntree trees, prm->mtry features per
+   split (0 => max(1, floor(p/3)), R5) -- returning per-fold MAPE
+   fold_mape [repeats][k] in percent (Eq. 1, raw y).  fold_ids as in
+   rf_cross_validate_grid ([repeats][n] in {-1, 0..k-1}; NULL => plain Philox
+   folds from prm->seed, R16).  Same as rf_cross_validate_grid with the grid
+   {prm->ntree} x {mtry}.  Errors: RF_E_NONPOSITIVE_Y (any y <= 0), RF_E_TOO_FEW
+   (k < 2, k > n, an empty test fold), RF_E_ARG (tree_begin/end set: a rank
+   cannot score a partial forest -- use rf_cv_partial), plus those of rf_fit.
+   The _dev twin takes device pointers and a stream (synchronised once). */
 RF_API rf_status rf_cross_validate(const double* X, uint64_t n, uint32_t p, const double* y,
                             const rf_params* prm, uint32_t k, uint32_t repeats,
                             const int32_t* fold_ids, double* fold_mape);
+RF_API rf_status rf_cross_validate_dev(const double* dX, uint64_t n, uint32_t p, const double* dy,
+                                       const rf_params* prm, uint32_t k, uint32_t repeats,
+                                       const int32_t* dfold_ids, double* dfold_mape, void* stream);
 
 /* Nested cross-validation ("First the scores of each hyperparameter
    combination are computed on all splits, then the best parameter combination

@@ -33,8 +33,11 @@ RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
 /* Test switches of this process (parity of alternative kernel paths):
    "large_tiled_partition" = 1 makes the large path use the tiled count ->
    scan -> scatter partition (otherwise only taken for the histogram mode and
-   n > 2^20) instead of the fused multi-list partition.  Unknown names return
-   RF_E_ARG. */
+   n > 2^20) instead of the fused multi-list partition.  "hist_node_chunk_cap"
+   = c > 0 caps the histogram mode's node chunk (nodes whose histograms are
+   built and searched per pass; otherwise sized by a 2 GB buffer) at c, so
+   small tests reach the multi-chunk loop; 0 restores the default.  Unknown
+   names and negative caps return RF_E_ARG. */
 RF_API rf_status rf_debug_set_option(const char* name, int64_t value);
 #ifdef __cplusplus
 }

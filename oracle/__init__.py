@@ -200,10 +200,12 @@ def importance(raw):
 
 
 def fit(X, y, ntree=1, mtry=None, min_samples_split=2, max_depth=-1, bootstrap=True,
-        split_mode=0, target=0, seed=0, tree_begin=0, tree_end=None, leaf_rows=False, criterion=0):
+        split_mode=0, target=0, seed=0, tree_begin=0, tree_end=None, leaf_rows=False, criterion=0,
+        tie_break=0):
     """Grow trees [tree_begin, tree_end) of task 0 (R2-R14).  criterion 0 = MSE
-    (P:215), 1 = MAE (P:489, R32)."""
-    split_mode = int(split_mode) | (int(criterion) << 8)
+    (P:215), 1 = MAE (R32).  tie_break 0 = lowest feature (north_star), 1 = first
+    drawn feature (R9)."""
+    split_mode = int(split_mode) | (int(criterion) << 8) | (int(tie_break) << 9)
     X = np.ascontiguousarray(X, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     n, p = X.shape
@@ -254,8 +256,9 @@ def mape(y, yhat):
 
 def cv_grid(X, y, k, reps, ntrees, mtrys, fold_ids=None, min_samples_split=2, max_depth=-1,
             bootstrap=True, split_mode=0, target=0, seed=0, task_begin=0, task_end=0,
-            want_pred=False, criterion=0):
-    """Repeated k-fold CV over an ntree x mtry grid; criterion 0 MSE, 1 MAE (R32).
+            want_pred=False, criterion=0, tie_break=0):
+    """Repeated k-fold CV over an ntree x mtry grid (P:473-491); criterion 0 MSE, 1 MAE (R32);
+    tie_break 0 lowest feature (north_star), 1 first drawn feature (R9).
 
     Returns fold_mape [n_mtry][n_ntree][reps][k] and optionally the per-row
     predictions [n_mtry][n_ntree][reps][n]."""
@@ -267,7 +270,7 @@ def cv_grid(X, y, k, reps, ntrees, mtrys, fold_ids=None, min_samples_split=2, ma
     fm = np.zeros((len(mt), len(nt), reps, k), dtype=np.float64)
     pr = np.zeros((len(mt), len(nt), reps, n), dtype=np.float64) if want_pred else None
     fid = None if fold_ids is None else np.ascontiguousarray(fold_ids, dtype=np.int32)
-    split_mode = int(split_mode) | (int(criterion) << 8)
+    split_mode = int(split_mode) | (int(criterion) << 8) | (int(tie_break) << 9)
     st = lib().or_cv_grid(_p(X), n, p, _p(y), min_samples_split, max_depth, int(bootstrap),
                           split_mode, target, seed, k, reps, _p(fid), _p(nt), len(nt), _p(mt),
                           len(mt), task_begin, task_end, _p(fm), _p(pr))

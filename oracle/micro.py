@@ -171,9 +171,12 @@ def sad(rows, w, tq):
     return sum(w[r] * abs(tq[r] - m) for r in rows)
 
 
-def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None, extra=False, mae=False):
+def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None, extra=False, mae=False,
+         tie_draw=False):
     """Depth-first recursive growth; returns the root Node.  mae: MAE criterion (R32) --
-    cost = SAD_L + SAD_R minimised (candidates as for MSE), leaves = weighted medians."""
+    cost = SAD_L + SAD_R minimised (candidates as for MSE), leaves = weighted medians.
+    tie_draw: ties go to the first drawn feature (R9) instead of the lowest feature index
+    (north_star's rule, the default)."""
     n, p = len(X), len(X[0])
     gvals = [sorted(set(X[i][f] for i in range(n))) for f in range(p)]
 
@@ -241,8 +244,9 @@ def grow(X, tq, F, w, key, mtry, min_split=2, max_depth=-1, hist_cuts_per_f=None
             v = wmedian(rows, w, tq) if mae else Fraction(nd.S, nd.W)  # R32 / R13
             nd.value = float(v * Fraction(2) ** (-F)) if F >= 0 else float(v / Fraction(2) ** F)
             return nd
-        # tie-break (R9): first drawn feature (slot j), then lowest threshold rank
-        best = min(cands, key=lambda c: (-c[0], c[6], c[2]))
+        # tie-break (R9): lowest feature index (north_star) or, with tie_draw, first drawn
+        # feature (slot j); then lowest threshold rank
+        best = min(cands, key=lambda c: (-c[0], c[6] if tie_draw else c[1], c[2]))
         nd.feature, nd.thr_index, nd.thr_value = best[1], best[2], best[3]
         nd.gain_exact_best = max(c[4] for c in cands)
         nd.gain_exact_chosen = best[4]
@@ -278,7 +282,7 @@ def to_bfs(root):
 
 
 def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=-1, hist=False,
-             task=0, train_rows=None, extra=False, mae=False):
+             task=0, train_rows=None, extra=False, mae=False, tie_draw=False):
     """Tree t of `task` over train_rows (default all rows).  extra=True grows an
     Extremely Randomized tree (split_mode 2)."""
     X = [[(0.0 if v == 0.0 else float(v)) for v in row] for row in X]
@@ -290,7 +294,7 @@ def fit_tree(X, y, t, mtry, seed=0, boot=True, target=0, min_split=2, max_depth=
     cuts = None
     if hist:
         cuts = [hist_cuts([X[r][f] for r in tr]) for f in range(len(X[0]))]
-    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra, mae)
+    root = grow(X, tq, F, w, key, mtry, min_split, max_depth, cuts, extra, mae, tie_draw)
     out = to_bfs(root)
     # MDI (NEXT-3): per feature, the exact SSE reductions of its splits (the definition
     # W imp(node) - WL imp(L) - WR imp(R), two-pass sums) in target units (x 2^-2F)

@@ -448,6 +448,10 @@ typedef struct {
     /* MAE criterion (R32): splits minimise the summed absolute deviations from the
        children's weighted medians; leaves hold the weighted median */
     int mae;
+    /* tie-break among bitwise-equal scores (R9): 0 = lowest feature index, then lowest
+       threshold (BASELINE.json north_star, the default); 1 = the feature drawn first at
+       the node (lowest draw slot), then lowest threshold (scikit-learn's visiting order) */
+    int tie_draw;
     double **cuts;
     uint32_t *ncuts;
     uint16_t *bins; /* [row*p + f] */
@@ -587,10 +591,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
         int found = 0;
         double bestG = 0.0;
         uint32_t bestF = 0;
-        /* tie-break (R9): among bitwise-equal G the feature drawn first (lowest
-           draw slot), then the lowest threshold rank -- scikit-learn's splitter
-           visits features in the random draw order and keeps the first best. */
-        uint32_t bestSlot = 0;
+        /* tie-break (R9): among bitwise-equal G the lowest tie key, then the lowest
+           threshold rank; tie key = the feature index (north_star: "lowest feature then
+           lowest threshold", default) or, with tie_draw, the draw slot (scikit-learn's
+           splitter visits features in the random draw order and keeps the first best). */
+        uint32_t bestTie = 0;
         uint64_t bestRank = 0; /* exact: rank_f(a) ; hist: cut index j */
         double bestA = 0.0, bestB = 0.0;
         if (!is_leaf) {
@@ -607,6 +612,7 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                    cost D = 2 (SAD_L + SAD_R), exact integers; best = lowest D, ties by
                    draw slot, then threshold rank (R9) */
                 uint32_t f = perm[jj];
+                uint32_t tk = c->tie_draw ? jj : f;
                 for (uint64_t i = 0; i < nd.nrows; ++i) {
                     xr[i].row = nd.rows[i];
                     xr[i].x = c->X[nd.rows[i] * p + f];
@@ -638,11 +644,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                     if (!found) better = 1;
                     else if (D < bestD) better = 1;
                     else if (D == bestD) {
-                        if (jj < bestSlot) better = 1;
-                        else if (jj == bestSlot && rk < bestRank) better = 1;
+                        if (tk < bestTie) better = 1;
+                        else if (tk == bestTie && rk < bestRank) better = 1;
                     }
                     if (better) {
-                        found = 1; bestD = D; bestF = f; bestSlot = jj; bestRank = rk;
+                        found = 1; bestD = D; bestF = f; bestTie = tk; bestRank = rk;
                         bestA = c->extra ? ethr : xr[i].x;
                         bestB = c->extra ? 0.0 : xr[i + 1].x;
                     }
@@ -650,6 +656,7 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
             }
             for (uint32_t jj = 0; jj < c->mtry && !c->mae; ++jj) {
                 uint32_t f = perm[jj];
+                uint32_t tk = c->tie_draw ? jj : f;
                 if (c->extra) {
                     /* Extremely Randomized Trees (R29):
                        thr uniform in [lo, hi) of the node's values of f,
@@ -683,9 +690,9 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                     int better = 0;
                     if (!found) better = 1;
                     else if (G > bestG) better = 1;
-                    else if (G == bestG && jj < bestSlot) better = 1;
+                    else if (G == bestG && tk < bestTie) better = 1;
                     if (better) {
-                        found = 1; bestG = G; bestF = f; bestSlot = jj;
+                        found = 1; bestG = G; bestF = f; bestTie = tk;
                         bestRank = find_index(c->gdist[f], c->gnd[f], a);
                         bestA = thr; bestB = 0.0;
                     }
@@ -707,11 +714,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                         if (!found) better = 1;
                         else if (G > bestG) better = 1;
                         else if (G == bestG) {
-                            if (jj < bestSlot) better = 1;
-                            else if (jj == bestSlot && rk < bestRank) better = 1;
+                            if (tk < bestTie) better = 1;
+                            else if (tk == bestTie && rk < bestRank) better = 1;
                         }
                         if (better) {
-                            found = 1; bestG = G; bestF = f; bestSlot = jj; bestRank = rk;
+                            found = 1; bestG = G; bestF = f; bestTie = tk; bestRank = rk;
                             bestA = xr[i].x; bestB = xr[i + 1].x;
                         }
                     }
@@ -735,11 +742,11 @@ static void grow_tree(const grow_ctx *c, const uint32_t *w, uint32_t k0, uint32_
                         if (!found) better = 1;
                         else if (G > bestG) better = 1;
                         else if (G == bestG) {
-                            if (jj < bestSlot) better = 1;
-                            else if (jj == bestSlot && j < bestRank) better = 1;
+                            if (tk < bestTie) better = 1;
+                            else if (tk == bestTie && j < bestRank) better = 1;
                         }
                         if (better) {
-                            found = 1; bestG = G; bestF = f; bestSlot = jj; bestRank = j;
+                            found = 1; bestG = G; bestF = f; bestTie = tk; bestRank = j;
                             bestA = c->cuts[f][j]; bestB = 0.0;
                         }
                     }
@@ -889,6 +896,17 @@ static double tree_predict(const or_tree *t, const double *x)
 /* Public oracle entry points                                          */
 /* ------------------------------------------------------------------ */
 
+/* split_mode word of or_fit / or_cv_grid: bits 0-7 the split rule (0 exact, 1 hist,
+   2 ExtraTrees), bit 8 the MAE criterion (R32; exact and ExtraTrees only), bit 9 the
+   draw-order tie-break (R9; clear = lowest feature index, north_star) */
+static int split_mode_ok(uint32_t split_mode)
+{
+    uint32_t rule = split_mode & 0xFFu, mae = (split_mode >> 8) & 1u;
+    if (rule > 2 || (split_mode >> 10) != 0) return 0;
+    if (rule == 1 && mae) return 0;
+    return 1;
+}
+
 /* Fit trees [tree_begin, tree_end) of task 0 (all rows train).
    Outputs per tree (index t - tree_begin) with capacity cap nodes:
    n_nodes[T], feature/thr_index/thr_value/left/leaf_value [T][cap],
@@ -904,17 +922,14 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
            double *imp_raw)
 {
     if (n == 0) return 2;
-    /* split_mode: bits 0-7 the split rule (0 exact, 1 hist, 2 ExtraTrees), bit 8 the MAE
-       criterion (R32; exact and ExtraTrees only) */
-    if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || (split_mode & 0xFFu) > 2 || (split_mode >> 8) > 1 ||
-        split_mode == 0x101u) return 1;
+    if (p == 0 || mtry == 0 || mtry > p || min_split < 2 || !split_mode_ok(split_mode)) return 1;
     double *Xc = (double *)malloc(sizeof(double) * n * p);
     int st = validate_X(X, n, p, Xc);
     if (st) { free(Xc); return st; }
     double *t = (double *)malloc(sizeof(double) * n);
     int64_t *tq = (int64_t *)malloc(sizeof(int64_t) * n);
     int32_t F;
-    st = quantize_g(y, n, (int)target, (split_mode >> 8) ? 2 : 0, t, tq, &F);
+    st = quantize_g(y, n, (int)target, ((split_mode >> 8) & 1u) ? 2 : 0, t, tq, &F);
     if (st) { free(Xc); free(t); free(tq); return st; }
     if (F_out) *F_out = F;
     uint64_t *tr = (uint64_t *)malloc(sizeof(uint64_t) * n);
@@ -925,7 +940,8 @@ int or_fit(const double *X, uint64_t n, uint32_t p, const double *y,
     g.mtry = mtry; g.min_split = min_split; g.max_depth = max_depth;
     g.hist = ((split_mode & 0xFFu) == 1);
     g.extra = ((split_mode & 0xFFu) == 2);
-    g.mae = (int)(split_mode >> 8);
+    g.mae = (int)((split_mode >> 8) & 1u);
+    g.tie_draw = (int)((split_mode >> 9) & 1u);
     if (g.hist) setup_hist(&g, Xc, n, p, tr, n); else setup_exact(&g, Xc, n, p);
     uint32_t *w = (uint32_t *)malloc(sizeof(uint32_t) * n);
     or_tree tree = { NULL, 0, 0 };
@@ -1004,7 +1020,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     if (n == 0) return 2;
     if (k < 2 || (uint64_t)k > n) return 6;
     if (p == 0 || min_split < 2 || n_ntree == 0 || n_mtry == 0 || (split_mode & 0xFFu) > 2 ||
-        (split_mode >> 8) > 1 || split_mode == 0x101u) return 1;
+        !split_mode_ok(split_mode)) return 1;
     for (uint32_t i = 0; i < n_mtry; ++i) if (mtrys[i] == 0 || mtrys[i] > p) return 1;
     for (uint32_t i = 0; i < n_ntree; ++i) if (ntrees[i] == 0) return 1;
     for (uint64_t i = 0; i < n; ++i) {
@@ -1017,7 +1033,7 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     double *t = (double *)malloc(sizeof(double) * n);
     int64_t *tq = (int64_t *)malloc(sizeof(int64_t) * n);
     int32_t F;
-    st = quantize_g(y, n, (int)target, (split_mode >> 8) ? 2 : 0, t, tq, &F);
+    st = quantize_g(y, n, (int)target, ((split_mode >> 8) & 1u) ? 2 : 0, t, tq, &F);
     if (st) { free(Xc); free(t); free(tq); return st; }
     int32_t *fid = (int32_t *)malloc(sizeof(int32_t) * n * reps);
     if (fold_ids_in) memcpy(fid, fold_ids_in, sizeof(int32_t) * n * reps);
@@ -1046,7 +1062,8 @@ int or_cv_grid(const double *X, uint64_t n, uint32_t p, const double *y,
     g.min_split = min_split; g.max_depth = max_depth;
     g.hist = ((split_mode & 0xFFu) == 1);
     g.extra = ((split_mode & 0xFFu) == 2);
-    g.mae = (int)(split_mode >> 8);
+    g.mae = (int)((split_mode >> 8) & 1u);
+    g.tie_draw = (int)((split_mode >> 9) & 1u);
     if (!g.hist) setup_exact(&g, Xc, n, p);
     uint64_t *tr = (uint64_t *)malloc(sizeof(uint64_t) * n);
     uint64_t *te = (uint64_t *)malloc(sizeof(uint64_t) * n);

@@ -29,13 +29,15 @@ STATUS_NAMES = ["OK", "ARG", "EMPTY", "NONFINITE", "NONPOSITIVE_Y", "ARITY", "TO
 SPLIT_EXACT, SPLIT_HIST256, SPLIT_EXTRA = 0, 1, 2
 TARGET_IDENTITY, TARGET_LOG = 0, 1
 CRITERION_MSE, CRITERION_MAE = 0, 1
+TIE_LOWEST_FEATURE, TIE_DRAW_ORDER = 0, 1  # rf_tie_break (R9): north_star's rule is the default
 
 # every entry point declared in include/rf.h and include/rf_debug.h
 ABI_SYMBOLS = [
     "rf_params_default", "rf_fit", "rf_fit_dev", "rf_fit_debug", "rf_predict", "rf_predict_dev",
     "rf_predict_partial_dev", "rf_predict_finalize_dev", "rf_make_folds", "rf_make_folds_dev",
     "rf_make_folds_masked_dev", "rf_nested_cv", "rf_nested_cv_dev", "rf_error_buckets", "rf_error_buckets_dev",
-    "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cv_partial_dev",
+    "rf_cross_validate_grid", "rf_cross_validate_grid_dev", "rf_cross_validate", "rf_cross_validate_dev",
+    "rf_cv_partial_dev",
     "rf_cv_finalize_dev", "rf_predict_partial", "rf_cv_partial", "rf_cv_finalize", "rf_forest_free", "rf_last_error", "rf_forest_info", "rf_forest_export",
     "rf_forest_export_leaf_rows", "rf_forest_import", "rf_forest_importance", "rf_importance_dev",
     "rf_last_profile", "rf_set_profiling",
@@ -54,7 +56,8 @@ class Params(C.Structure):
                 ("min_samples_split", C.c_uint32), ("max_depth", C.c_int32), ("bootstrap", C.c_uint32),
                 ("split_mode", C.c_uint32), ("target", C.c_uint32), ("seed", C.c_uint64),
                 ("device", C.c_int32), ("tree_begin", C.c_uint32), ("tree_end", C.c_uint32),
-                ("task_begin", C.c_uint32), ("task_end", C.c_uint32), ("criterion", C.c_uint32)]
+                ("task_begin", C.c_uint32), ("task_end", C.c_uint32), ("criterion", C.c_uint32),
+                ("tie_break", C.c_uint32)]
 
 
 _lib = None
@@ -93,6 +96,7 @@ def lib():
             "rf_cross_validate_grid_dev": ([P, u64, u32, P, pp, u32, u32, P, P, u32, P, u32, P, P, P],
                                            C.c_int),
             "rf_cross_validate": ([P, u64, u32, P, pp, u32, u32, P, P], C.c_int),
+            "rf_cross_validate_dev": ([P, u64, u32, P, pp, u32, u32, P, P, P], C.c_int),
             "rf_cv_partial_dev": ([P, u64, u32, P, pp, u32, u32, P, P, u32, P, u32, P, P], C.c_int),
             "rf_cv_finalize_dev": ([P, u64, u32, u32, u32, P, P, u32, u32, P, P, P, P], C.c_int),
             "rf_forest_free": ([P], None),
@@ -149,6 +153,32 @@ def _torch():
 
 def _stream():
     return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _dev(t, dtype, ref=None, name="argument"):
+    """A CUDA tensor argument of a *_dev entry point: must be a CUDA tensor of the expected dtype
+    ("float64", "int32", "uint8") on ref's device; returned contiguous -- the caller keeps the
+    returned tensor alive until the call returns.  Wrong inputs raise TypeError instead of being
+    read as fp64 row-major device memory."""
+    if t is None:
+        return None
+    torch = _torch()
+    if not _is_torch(t) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor (device path), got {type(t).__name__}")
+    want = getattr(torch, dtype)
+    if t.dtype != want:
+        raise TypeError(f"{name}: expected dtype {want}, got {t.dtype}")
+    if ref is not None and t.device != ref.device:
+        raise TypeError(f"{name}: on {t.device}, expected {ref.device}")
+    return t.contiguous()
+
+
+def _dev_out(t, dtype, ref, name="out"):
+    """An output tensor of a *_dev entry point: CUDA, dtype, ref's device, and contiguous (a
+    contiguous copy would not receive the results)."""
+    if _dev(t, dtype, ref, name) is not t:
+        raise TypeError(f"{name}: expected a contiguous CUDA {dtype} tensor")
+    return t
 
 
 def _host(a, dtype):
@@ -233,16 +263,19 @@ def forest_import(feature, left, value, thr_index, tree_off, p, F, target, devic
 # ------------------------------------------------------------------- API --
 def fit(X, y, *, ntree=100, mtry=0, min_samples_split=2, max_depth=-1, bootstrap=True,
         split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0, tree_begin=0, tree_end=0,
-        debug=False, criterion=CRITERION_MSE) -> Forest:
+        debug=False, criterion=CRITERION_MSE, tie_break=TIE_LOWEST_FEATURE) -> Forest:
     """Grow a forest (rf_fit).  X: [n, p] fp64, y: [n] fp64 (numpy or CUDA tensors).
-    criterion: CRITERION_MSE (P:215) or CRITERION_MAE (P:489, R32)."""
+    criterion: CRITERION_MSE (P:215) or CRITERION_MAE (P:489, R32); tie_break:
+    TIE_LOWEST_FEATURE (north_star) or TIE_DRAW_ORDER (R9)."""
     prm = params(ntree=ntree, mtry=mtry, min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
-                 tree_begin=tree_begin, tree_end=tree_end, criterion=criterion)
+                 tree_begin=tree_begin, tree_end=tree_end, criterion=criterion, tie_break=tie_break)
     h = C.c_void_p()
     if _is_torch(X):
         if debug:
             raise ValueError("debug fits take host arrays")
+        X = _dev(X, "float64", None, "X")
+        y = _dev(y, "float64", X, "y")
         n, p = X.shape
         _check(lib().rf_fit_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), _stream(), C.byref(h)))
     else:
@@ -257,8 +290,9 @@ def predict(forest: Forest, X, out=None):
     """Mean of the trees' leaf values (exp for LOG forests)."""
     if _is_torch(X):
         torch = _torch()
+        X = _dev(X, "float64", None, "X")
         n, p = X.shape
-        out = torch.empty(n, dtype=torch.float64, device=X.device) if out is None else out
+        out = torch.empty(n, dtype=torch.float64, device=X.device) if out is None else _dev_out(out, "float64", X)
         _check(lib().rf_predict_dev(forest.handle, _ptr(X), n, p, _ptr(out), _stream()))
         return out
     X = _host(X, np.float64)
@@ -278,15 +312,17 @@ def predict_partial(forest: Forest, X, out=None):
         _check(lib().rf_predict_partial(forest.handle, _ptr(X), n, p, _ptr(out)))
         return out
     torch = _torch()
+    X = _dev(X, "float64", None, "X")
     n, p = X.shape
-    out = torch.empty(n, dtype=torch.float64, device=X.device) if out is None else out
+    out = torch.empty(n, dtype=torch.float64, device=X.device) if out is None else _dev_out(out, "float64", X)
     _check(lib().rf_predict_partial_dev(forest.handle, _ptr(X), n, p, _ptr(out), _stream()))
     return out
 
 
 def predict_finalize(partial, ntree_total, target, out=None):
     torch = _torch()
-    out = torch.empty_like(partial) if out is None else out
+    partial = _dev(partial, "float64", None, "partial")
+    out = torch.empty_like(partial) if out is None else _dev_out(out, "float64", partial)
     _check(lib().rf_predict_finalize_dev(_ptr(partial), partial.shape[0], ntree_total, target, _ptr(out),
                                          _stream()))
     return out
@@ -296,8 +332,10 @@ def make_folds(y, k, repeats=1, seed=0, custom=False, out=None):
     """Fold ids [repeats, n] (rf_make_folds)."""
     if _is_torch(y):
         torch = _torch()
+        y = _dev(y, "float64", None, "y")
         n = y.shape[0]
-        out = torch.empty((repeats, n), dtype=torch.int32, device=y.device) if out is None else out
+        out = torch.empty((repeats, n), dtype=torch.int32, device=y.device) if out is None else \
+            _dev_out(out, "int32", y)
         _check(lib().rf_make_folds_dev(_ptr(y), n, k, repeats, seed, int(custom), _ptr(out), _stream()))
         return out
     y = _host(y, np.float64)
@@ -309,24 +347,28 @@ def make_folds(y, k, repeats=1, seed=0, custom=False, out=None):
 def make_folds_masked(y, k, mask, seed=0, custom=False, out=None):
     """Device fold ids [reps, n] of the row subsets mask [reps, n] != 0 (others -2), R31."""
     torch = _torch()
+    y = _dev(y, "float64", None, "y")
+    mask = _dev(mask.to(torch.uint8), "uint8", y, "mask")
     reps, n = mask.shape
-    out = torch.empty((reps, n), dtype=torch.int32, device=y.device) if out is None else out
-    _check(lib().rf_make_folds_masked_dev(_ptr(y), n, k, reps, seed, int(custom), _ptr(mask.to(torch.uint8)),
+    out = torch.empty((reps, n), dtype=torch.int32, device=y.device) if out is None else _dev_out(out, "int32", y)
+    _check(lib().rf_make_folds_masked_dev(_ptr(y), n, k, reps, seed, int(custom), _ptr(mask),
                                           _ptr(out), _stream()))
     return out
 
 
 def nested_cv(X, y, k_outer, k_inner, iterations, ntrees, mtrys, *, custom=False, min_samples_split=2,
               max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0,
-              criterion=CRITERION_MSE):
+              criterion=CRITERION_MSE, tie_break=TIE_LOWEST_FEATURE):
     """Nested CV (rf_nested_cv, R31): (best [it, k_outer] grid index mi*n_ntree+ti,
     outer_mape [it, k_outer], inner_score [it, k_outer, n_mtry, n_ntree])."""
     prm = params(ntree=max(ntrees), mtry=0, min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
-                 criterion=criterion)
+                 criterion=criterion, tie_break=tie_break)
     nt, mt = _u32(ntrees), _u32(mtrys)
     if _is_torch(X):
         torch = _torch()
+        X = _dev(X, "float64", None, "X")
+        y = _dev(y, "float64", X, "y")
         n, p = X.shape
         best = torch.empty((iterations, k_outer), dtype=torch.int32, device=X.device)
         om = torch.empty((iterations, k_outer), dtype=torch.float64, device=X.device)
@@ -349,6 +391,8 @@ def error_buckets(y, yhat):
     """LOO error buckets (rf_error_buckets): counts of APE in [0,10) [10,25) [25,50) [50,100) [100,inf) %."""
     if _is_torch(y):
         torch = _torch()
+        y = _dev(y, "float64", None, "y")
+        yhat = _dev(yhat, "float64", y, "yhat")
         out = torch.zeros(5, dtype=torch.int64, device=y.device)
         _check(lib().rf_error_buckets_dev(_ptr(y), _ptr(yhat), y.shape[0], _ptr(out), _stream()))
         return out
@@ -361,17 +405,20 @@ def error_buckets(y, yhat):
 def cross_validate_grid(X, y, k, repeats, ntrees, mtrys, fold_ids=None, *, want_pred=False,
                         min_samples_split=2, max_depth=-1, bootstrap=True, split_mode=SPLIT_EXACT,
                         target=TARGET_IDENTITY, seed=0, device=0, task_begin=0, task_end=0, out=None,
-                        criterion=CRITERION_MSE):
+                        criterion=CRITERION_MSE, tie_break=TIE_LOWEST_FEATURE):
     """fold_mape [n_mtry, n_ntree, repeats, k] (+ pred [n_mtry, n_ntree, repeats, n])."""
     prm = params(ntree=max(ntrees), mtry=0, min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
-                 task_begin=task_begin, task_end=task_end, criterion=criterion)
+                 task_begin=task_begin, task_end=task_end, criterion=criterion, tie_break=tie_break)
     nt, mt = _u32(ntrees), _u32(mtrys)
     shape = (len(mt), len(nt), repeats, k)
     if _is_torch(X):
         torch = _torch()
+        X = _dev(X, "float64", None, "X")
+        y = _dev(y, "float64", X, "y")
+        fold_ids = _dev(fold_ids, "int32", X, "fold_ids")
         n, p = X.shape
-        fm = torch.empty(shape, dtype=torch.float64, device=X.device) if out is None else out
+        fm = torch.empty(shape, dtype=torch.float64, device=X.device) if out is None else _dev_out(out, "float64", X)
         pr = torch.empty((len(mt), len(nt), repeats, n), dtype=torch.float64, device=X.device) \
             if want_pred else None
         _check(lib().rf_cross_validate_grid_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats,
@@ -388,21 +435,43 @@ def cross_validate_grid(X, y, k, repeats, ntrees, mtrys, fold_ids=None, *, want_
     return (fm, pr) if want_pred else fm
 
 
-def cross_validate(X, y, k, repeats=1, fold_ids=None, *, ntree=100, mtry=0, **kw):
-    """Single grid point (rf_cross_validate semantics): fold_mape [repeats, k]."""
-    p = X.shape[1]
-    m = mtry if mtry else max(1, p // 3)
-    return cross_validate_grid(X, y, k, repeats, [ntree], [m], fold_ids, **kw)[0, 0]
+def cross_validate(X, y, k, repeats=1, fold_ids=None, *, ntree=100, mtry=0, min_samples_split=2, max_depth=-1,
+                   bootstrap=True, split_mode=SPLIT_EXACT, target=TARGET_IDENTITY, seed=0, device=0, tree_begin=0,
+                   tree_end=0, task_begin=0, task_end=0, criterion=CRITERION_MSE, tie_break=TIE_LOWEST_FEATURE,
+                   out=None):
+    """One model under repeated k-fold CV (rf_cross_validate / rf_cross_validate_dev):
+    fold_mape [repeats, k] in percent.  mtry 0 = the library default (R5)."""
+    prm = params(ntree=ntree, mtry=mtry, min_samples_split=min_samples_split, max_depth=max_depth,
+                 bootstrap=int(bootstrap), split_mode=split_mode, target=target, seed=seed, device=device,
+                 tree_begin=tree_begin, tree_end=tree_end, task_begin=task_begin, task_end=task_end,
+                 criterion=criterion, tie_break=tie_break)
+    if _is_torch(X):
+        torch = _torch()
+        X = _dev(X, "float64", None, "X")
+        y = _dev(y, "float64", X, "y")
+        fold_ids = _dev(fold_ids, "int32", X, "fold_ids")
+        n, p = X.shape
+        fm = torch.empty((repeats, k), dtype=torch.float64, device=X.device) if out is None else \
+            _dev_out(out, "float64", X)
+        _check(lib().rf_cross_validate_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats, _ptr(fold_ids),
+                                           _ptr(fm), _stream()))
+        return fm
+    X, y = _host(X, np.float64), _host(y, np.float64)
+    n, p = X.shape
+    fm = np.zeros((repeats, k), np.float64)
+    fid = None if fold_ids is None else _host(fold_ids, np.int32)
+    _check(lib().rf_cross_validate(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats, _ptr(fid), _ptr(fm)))
+    return fm
 
 
 def cv_partial(X, y, k, repeats, fold_ids, ntrees, mtrys, *, tree_begin, tree_end, min_samples_split=2,
                max_depth=-1, bootstrap=True, target=TARGET_IDENTITY, seed=0, out=None, split_mode=SPLIT_EXACT,
-               criterion=CRITERION_MSE):
+               criterion=CRITERION_MSE, tie_break=TIE_LOWEST_FEATURE):
     """Tree-sharded CV partial sums [n_mtry, n_ntree, repeats, n] (device tensors, or host arrays
     through rf_cv_partial)."""
     prm = params(ntree=max(ntrees), min_samples_split=min_samples_split, max_depth=max_depth,
                  bootstrap=int(bootstrap), target=target, seed=seed, tree_begin=tree_begin, tree_end=tree_end,
-                 split_mode=split_mode, criterion=criterion)
+                 split_mode=split_mode, criterion=criterion, tie_break=tie_break)
     nt, mt = _u32(ntrees), _u32(mtrys)
     n, p = X.shape
     if not _is_torch(X):
@@ -412,7 +481,11 @@ def cv_partial(X, y, k, repeats, fold_ids, ntrees, mtrys, *, tree_begin, tree_en
                                    _ptr(mt), len(mt), _ptr(out)))
         return out
     torch = _torch()
-    out = torch.empty((len(mt), len(nt), repeats, n), dtype=torch.float64, device=X.device) if out is None else out
+    X = _dev(X, "float64", None, "X")
+    y = _dev(y, "float64", X, "y")
+    fold_ids = _dev(fold_ids, "int32", X, "fold_ids")
+    out = torch.empty((len(mt), len(nt), repeats, n), dtype=torch.float64, device=X.device) if out is None else \
+        _dev_out(out, "float64", X)
     _check(lib().rf_cv_partial_dev(_ptr(X), n, p, _ptr(y), C.byref(prm), k, repeats, _ptr(fold_ids), _ptr(nt),
                                    len(nt), _ptr(mt), len(mt), _ptr(out), _stream()))
     return out
@@ -431,6 +504,9 @@ def cv_finalize(y, k, repeats, fold_ids, ntrees, n_mtry, reduced, *, target=TARG
                                     _ptr(fm), _ptr(pr), device))
         return (fm, pr) if want_pred else fm
     torch = _torch()
+    y = _dev(y, "float64", None, "y")
+    fold_ids = _dev(fold_ids, "int32", y, "fold_ids")
+    reduced = _dev(reduced, "float64", y, "reduced")
     fm = torch.empty((n_mtry, len(nt), repeats, k), dtype=torch.float64, device=y.device)
     pr = torch.empty((n_mtry, len(nt), repeats, n), dtype=torch.float64, device=y.device) if want_pred else None
     _check(lib().rf_cv_finalize_dev(_ptr(y), n, target, k, repeats, _ptr(fold_ids), _ptr(nt), len(nt), n_mtry,
@@ -515,6 +591,7 @@ def importance_dev(raw, out=None):
     """Device: importance [p] from per-tree split-decrease sums raw [ntree][p]
     (torch float64 CUDA tensor; e.g. all-gathered tree shards), rf_importance_dev."""
     import torch
+    raw = _dev(raw, "float64", None, "raw")
     T, p = raw.shape
     if out is None:
         out = torch.empty(p, dtype=torch.float64, device=raw.device)

@@ -3,6 +3,7 @@
 // Every compute step runs in this library's CUDA kernels; there is no CPU
 // fallback (without a device every call returns RF_E_CUDA).
 #include <algorithm>
+#include <mutex>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -87,6 +88,7 @@ rf_status check_params(const rf_params* prm, uint32_t p, uint32_t* mtry_out) {
   if (prm->max_depth < -1) return fail(RF_E_ARG, "max_depth must be >= -1");
   if (prm->split_mode > RF_SPLIT_EXTRA || prm->target > 1) return fail(RF_E_ARG, "bad split_mode/target");
   if (prm->criterion > RF_CRITERION_MAE) return fail(RF_E_ARG, "bad criterion");
+  if (prm->tie_break > RF_TIE_DRAW_ORDER) return fail(RF_E_ARG, "bad tie_break");
   if (prm->criterion == RF_CRITERION_MAE && prm->split_mode == RF_SPLIT_HIST256)
     return fail(RF_E_UNSUPPORTED, "MAE criterion: exact and ExtraTrees split modes only (R32)");
   uint32_t m = prm->mtry ? prm->mtry : std::max<uint32_t>(1, p / 3);
@@ -265,6 +267,7 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
   a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
   a.extra = prm->split_mode == RF_SPLIT_EXTRA;
   a.mae = prm->criterion == RF_CRITERION_MAE;
+  a.tie_draw = prm->tie_break == RF_TIE_DRAW_ORDER;
   a.max_depth = prm->max_depth; a.n_mtry = nmd;
   for (int i = 0; i < nmd; ++i) a.mtrys[i] = gp.mtry_distinct[i];
   a.tree_lo = tree_lo; a.tree_hi = tree_hi;
@@ -415,17 +418,19 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   rf::Node16* nodes_w = nullptr;
   uint32_t* tidx_w = nullptr;
   uint32_t* nn_d = nullptr;
-  int32_t* lor = nullptr;
+  // leaf rows (debug) and per-tree MDI decreases [T][p] (feature importance, NEXT-3) end up owned
+  // by the forest; until then this guard frees them on every early return (CK included)
+  struct OwnedBufs {
+    int32_t* lor = nullptr;
+    double* imp = nullptr;
+    ~OwnedBufs() { cudaFree(lor); cudaFree(imp); }
+  } own;
+  int32_t*& lor = own.lor;
+  double*& imp = own.imp;
   uint64_t cap = 0;
   if (debug) CK(cudaMalloc(&lor, (size_t)T * n * sizeof(int32_t)), "alloc leaf_of_row");
-  // per-tree MDI decreases [T][p] (feature importance, NEXT-3), owned by the forest
-  double* imp = nullptr;
-  {
-    cudaError_t e = cudaMalloc(&imp, (size_t)T * p * sizeof(double));
-    if (e == cudaSuccess) e = cudaMemsetAsync(imp, 0, (size_t)T * p * sizeof(double), s);
-    if (e != cudaSuccess) { cudaFree(lor); cudaFree(imp); return cuda_fail(e, "alloc importance"); }
-  }
-  auto drop = [&]() { cudaFree(lor); cudaFree(imp); };
+  CK(cudaMalloc(&imp, (size_t)T * p * sizeof(double)), "alloc importance");
+  CK(cudaMemsetAsync(imp, 0, (size_t)T * p * sizeof(double), s), "alloc importance");
   if (small) {
     rf::TaskData td;
     td.ntask = 1; td.task0 = 0; td.n = (int)n; td.p = (int)p; td.ntr_stride = (int)n;
@@ -451,6 +456,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     a.seed = prm->seed; a.bootstrap = (int)prm->bootstrap; a.min_split = (int)prm->min_samples_split;
     a.extra = prm->split_mode == RF_SPLIT_EXTRA;
     a.mae = prm->criterion == RF_CRITERION_MAE;
+    a.tie_draw = prm->tie_break == RF_TIE_DRAW_ORDER;
     a.max_depth = prm->max_depth; a.n_mtry = 1; a.mtrys[0] = (int)mtry;
     a.tree_lo = tree_lo; a.tree_hi = tree_hi; a.Cw = 1; a.nsub = T; a.wpb = 4;
     a.fit_mode = 1; a.nodes = nodes_w; a.thr_index = tidx_w; a.tree_nnodes = nn_d;
@@ -466,32 +472,33 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     } else {
       ProfScope ps("small_tree_fit", s);
       cudaError_t e = rf::launch_small_tree(a, s);
-      if (e != cudaSuccess) { drop(); return cuda_fail(e, "small_tree fit"); }
+      if (e != cudaSuccess) return cuda_fail(e, "small_tree fit");
     }
   }
   if (!small && prm->criterion == RF_CRITERION_MAE) {
-    drop();
     return fail(RF_E_UNSUPPORTED, "MAE criterion: training sets of <= 255 rows and p <= 64 only (R32)");
   }
   if (!small) {
     rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,
                                  &cap, lor, imp, g_err);
-    if (ls) { drop(); return ls; }
+    if (ls) return ls;
   }
   std::vector<uint32_t> hnn(T);
   CK(cudaMemcpyAsync(hnn.data(), nn_d, T * 4, cudaMemcpyDeviceToHost, s), "d2h");
   int32_t hF = 0;
   CK(cudaMemcpyAsync(&hF, d.F, 4, cudaMemcpyDeviceToHost, s), "d2h");
   st = read_err(d.err, s);
-  if (st) { drop(); return st; }
+  if (st) return st;
   rf_forest* f = new rf_forest();
   f->imp = imp;
+  own.imp = nullptr;  // owned by the forest from here on (rf_forest_free)
   f->device = dev; f->ntree = (uint32_t)T; f->p = p; f->target = prm->target; f->F = hF;
   f->h_tree_off.resize(T + 1);
   f->h_tree_off[0] = 0;
   for (int t = 0; t < T; ++t) f->h_tree_off[t + 1] = f->h_tree_off[t] + hnn[t];
   f->total_nodes = f->h_tree_off[T];
-  f->leaf_of_row = lor;
+  f->leaf_of_row = own.lor;
+  own.lor = nullptr;
   f->n_rows = n;
   cudaError_t e = cudaMalloc(&f->nodes, f->total_nodes * sizeof(rf::Node16));
   if (e == cudaSuccess) e = cudaMalloc(&f->thr_index, f->total_nodes * sizeof(uint32_t));
@@ -520,11 +527,14 @@ static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 static std::atomic<unsigned long long> g_row_levels{0};
 void note_row_levels(long long n) { g_row_levels.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+// per-device counter, created once under a mutex (entry points may run on several host threads)
 unsigned long long* candidate_counter() {
   static unsigned long long* ptrs[64] = {nullptr};
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
   if (!ptrs[dev]) {
     if (cudaMalloc(&ptrs[dev], sizeof(unsigned long long)) != cudaSuccess) return nullptr;
     cudaMemset(ptrs[dev], 0, sizeof(unsigned long long));
@@ -810,6 +820,7 @@ rf_status rf_error_buckets_dev(const double* dy, const double* dyhat, uint64_t n
 rf_status rf_error_buckets(const double* y, const double* yhat, uint64_t n, uint64_t* counts) {
   if (rf_status st = check_device()) return st;
   if (!counts || (n && (!y || !yhat))) return fail(RF_E_ARG, "NULL argument");
+  CK(cudaSetDevice(0), "set device");  // host twin: device 0 (documented in rf.h)
   cudaStream_t s = host_stream(0);
   Scratch sc(s);
   double *dy, *dh;
@@ -830,6 +841,7 @@ rf_status rf_error_buckets(const double* y, const double* yhat, uint64_t n, uint
 rf_status rf_make_folds(const double* y, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
                         uint32_t custom, int32_t* fold_ids) {
   if (rf_status st = check_device()) return st;
+  CK(cudaSetDevice(0), "set device");  // host twin: device 0 (documented in rf.h)
   cudaStream_t s = host_stream(0);
   Scratch sc(s);
   double* dy;
@@ -898,6 +910,17 @@ rf_status rf_cross_validate(const double* X, uint64_t n, uint32_t p, const doubl
   if (rf_status st = check_params(prm, p, &m)) return st;
   uint32_t nt = prm->ntree;
   return rf_cross_validate_grid(X, n, p, y, prm, k, repeats, fold_ids, &nt, 1, &m, 1, fold_mape, nullptr);
+}
+
+rf_status rf_cross_validate_dev(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
+                                uint32_t k, uint32_t repeats, const int32_t* dfold_ids, double* dfold_mape,
+                                void* stream) {
+  if (!prm) return fail(RF_E_ARG, "params is NULL");
+  uint32_t m = 0;
+  if (rf_status st = check_params(prm, p, &m)) return st;
+  uint32_t nt = prm->ntree;
+  return rf_cross_validate_grid_dev(dX, n, p, dy, prm, k, repeats, dfold_ids, &nt, 1, &m, 1, dfold_mape, nullptr,
+                                    stream);
 }
 
 rf_status rf_cv_partial_dev(const double* dX, uint64_t n, uint32_t p, const double* dy, const rf_params* prm,
@@ -1068,6 +1091,23 @@ rf_status rf_forest_import(const int32_t* feature, const uint32_t* left, const d
   *out = nullptr;
   if (rf_status st = check_device()) return st;
   if (ntree == 0 || !tree_off || !feature || !left || !value) return fail(RF_E_ARG, "bad arrays");
+  if (p == 0 || target > RF_TARGET_LOG) return fail(RF_E_ARG, "p must be >= 1 and target 0 or 1");
+  // structure check before upload: a malformed forest (e.g. a mis-gathered shard) must not make
+  // the predict kernels read out of bounds or loop on a cyclic child index.  Per tree (nodes
+  // tree_off[t] .. tree_off[t+1], child ids tree-local): at least one node; an internal node i
+  // has 0 <= feature < p and i < left, left + 1 < node count (children follow their parent in
+  // BFS order, so every walk ends); leaves have feature -1.
+  if (tree_off[0] != 0) return fail(RF_E_ARG, "tree_off[0] must be 0");
+  for (uint32_t t = 0; t < ntree; ++t) {
+    const uint64_t a = tree_off[t], b = tree_off[t + 1];
+    if (b <= a) return fail(RF_E_ARG, "tree_off must be strictly increasing (every tree has a node)");
+    for (uint64_t i = a; i < b; ++i) {
+      const int32_t ft = feature[i];
+      if (ft < -1 || ft >= (int32_t)p) return fail(RF_E_ARG, "node feature out of range");
+      if (ft >= 0 && (left[i] <= i - a || (uint64_t)left[i] + 1 >= b - a))
+        return fail(RF_E_ARG, "child index out of range or not after its parent");
+    }
+  }
   CK(cudaSetDevice(device), "set device");
   rf_forest* f = new rf_forest();
   f->device = device; f->ntree = ntree; f->p = p; f->F = F; f->target = target;
@@ -1152,6 +1192,11 @@ rf_status rf_debug_set_option(const char* name, int64_t value) {
   if (!name) return fail(RF_E_ARG, "name is NULL");
   if (!strcmp(name, "large_tiled_partition")) {
     rf::g_opt_tiled_partition = value != 0;
+    return RF_OK;
+  }
+  if (!strcmp(name, "hist_node_chunk_cap")) {
+    if (value < 0) return fail(RF_E_ARG, "hist_node_chunk_cap must be >= 0");
+    rf::g_opt_hist_node_cap = value;
     return RF_OK;
   }
   return fail(RF_E_ARG, "unknown option");

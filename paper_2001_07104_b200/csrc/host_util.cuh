@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 namespace rf {
@@ -11,16 +13,20 @@ namespace rf {
 // with the default threshold 0 the pool returns its memory to the driver at every
 // synchronisation, and the next call maps it again (a 128-tree large-path batch
 // allocates ~5 GB: re-mapping it cost ~1.5 s per rf_fit call).  Once per device.
+// Per-device flags behind a mutex: entry points may be called from several host threads.
 inline void retain_pool() {
-  static bool done[64] = {};
+  static std::atomic<bool> done[64] = {};
+  static std::mutex mu;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev].load(std::memory_order_acquire)) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev].load(std::memory_order_relaxed)) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done[dev] = true;
+  done[dev].store(true, std::memory_order_release);
 }
 
 // Opt a kernel into the device's full dynamic shared memory (minus its static shared

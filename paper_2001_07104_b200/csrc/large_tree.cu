@@ -53,7 +53,9 @@ constexpr int kTile = kThreads * kKC;
 
 struct __align__(16) Best {
   unsigned long long key;  // G bits + 1 (0 = no candidate)
-  unsigned long long aux;  // feature << 32 | position in node (ascending = preferred)
+  // search: tie key << 56 | draw slot << 48 | position (ascending = preferred; tie key = feature
+  // index (north_star) or draw slot (R9)); after decide: feature << 32 | position
+  unsigned long long aux;
 };
 
 __device__ __forceinline__ bool better(unsigned long long k1, unsigned long long a1, unsigned long long k2,
@@ -109,6 +111,7 @@ struct Batch {
   int nl;                   // row lists per tree: p (exact, one per feature) or 1 (histogram)
   int hist;                 // 256-bin histogram split mode (R23)
   int extra;                // ExtraTrees split mode (R29)
+  int tie_draw;             // tie-break (R9): 0 lowest feature index (north_star), 1 first drawn
   uint32_t* xb;             // [NMAX][m] ExtraTrees: boundary index in the (node, slot) segment or ~0
   const uint8_t* bins;      // [n][p] bin of every row (histogram mode)
   const double* cuts;       // [p][256] cut values (histogram mode)
@@ -158,6 +161,13 @@ struct Batch {
   int tree0;             // global tree index of batch slot 0
   int* err;
 };
+
+// candidate aux (search order among bitwise-equal keys, R9): tie key << 56 | draw slot << 48 |
+// position; the tie key is the feature index (north_star: lowest feature, then lowest
+// threshold) or the draw slot (first drawn feature); f, j < 256 (p <= 255)
+__device__ __forceinline__ unsigned long long cand_aux(const Batch& b, int j, int f, unsigned pos) {
+  return ((unsigned long long)(b.tie_draw ? j : f) << 56) | ((unsigned long long)j << 48) | pos;
+}
 
 // ---------------------------------------------------------------- setup ------
 __global__ void k_keys_boot(Batch b, uint64_t seed, int task, int bootstrap) {
@@ -358,7 +368,8 @@ __global__ void k_node_prep(Batch b, int cur, int NO) {
   b.accS[g] = 0ull;
   b.nc[2 * g] = 0;
   b.nc[2 * g + 1] = 0;
-  // the draw order matters even for m = p: ties go to the first drawn feature (R9)
+  // the draw order matters even for m = p under the draw-order tie-break (R9) and for the
+  // ExtraTrees thresholds (keyed by draw slot, R29)
   uint8_t* fp = b.feat + (size_t)g * b.m;
   uint8_t perm[256];
   for (int f = 0; f < b.p; ++f) perm[f] = (uint8_t)f;
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         const long long SR = c.S - SL;
         const double G = split_gain((long long)WL, SL, (long long)WR, SR);
         const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
-        const unsigned long long aux = ((unsigned long long)c.j << 32) | (unsigned long long)c.i;  // R9
+        const unsigned long long aux = cand_aux(b, c.j, c.f, (unsigned)c.i);  // R9
         ++nc;
         if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; }
       }
@@ -667,7 +678,7 @@ __global__ void k_decide(Batch b, int cur, int NO) {
   const Nodes& nd = b.nd[cur];
   const Best bs = b.best[g];
   if (!bs.key) return;
-  const int j = (int)(bs.aux >> 32), i = (int)(bs.aux & 0xFFFFFFFFull);
+  const int j = (int)((bs.aux >> 48) & 0xFFull), i = (int)(bs.aux & 0xFFFFFFFFull);
   const int t = (int)nd.tree[g], f = b.feat[(size_t)g * b.m + j];
   const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
   const uint32_t ra = L[i] & b.rowMask, rb = L[i + 1] & b.rowMask;
@@ -738,7 +749,7 @@ __global__ void k_mark(Batch b, int cur, int NP) {
 // drawn feature the (W, S) sums per bin are exact integers (order-free atomics);
 // the candidate after cut c is valid iff WL > 0 and WR > 0; threshold = cut
 // value, threshold index = c; ties -> first drawn feature (R9), then lowest c.
-constexpr int kHistThreads = 256;
+constexpr int kHistThreads = 512;
 constexpr int kHistChunk = 8192;  // rows per histogram work item
 
 // one CTA per feature: cuts from the task's training rows sorted by x_f
@@ -821,17 +832,31 @@ __global__ void k_hist_zero(Batch b, int cur, int g0, int g1, uint32_t* hW, unsi
   for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) { hW[base + i] = 0u; hS[base + i] = 0ull; }
 }
 
-// work item = (node, chunk of <= kHistChunk rows): shared-memory histograms of the drawn features
-// (A warp-private variant -- 32 rows per step aggregated by a warp bitonic sort on the
-// bin and a segmented sum, one plain read-modify-write per distinct bin -- measured
-// 1.8x slower on the C4 shape: the shuffle work exceeds the atomics it saves.)
+// work item = (node, chunk of <= kHistChunk rows): shared-memory histograms of the drawn
+// features.  A warp takes 32 rows of the chunk at a time (coalesced row ids, gathered weights
+// and targets) and then walks them one by one with the lanes over the drawn features: lane j
+// reads byte sF[j] of the row's 64-byte bin row (one coalesced access per row) and updates
+// feature j's histogram, so the lanes of a warp never hit the same counter (no same-address
+// serialisation on low-cardinality features, where a row-per-lane layout made whole warps
+// collide).  The sums are kept in 32-bit shared counters only: W, and S = w t_q as a (lo, hi)
+// pair whose carry is taken from the returned old lo (exact modular 64-bit arithmetic, order
+// free).  Measured (profiles/micro, rd2_02): one 64-bit shared atomicAdd compiles to a
+// compare-and-swap loop at 1.3 pair-updates/clk/SM, three 32-bit atomics run 3.0/clk/SM.
+// Feature histograms are kHistStride = 257 words apart so equal low bins of different
+// features fall in different banks.  (Earlier variants: row per lane with u32 + u64 CAS
+// atomics, 18 ms per C4 tree; a warp bitonic sort + segmented sums, 1.8x slower still.)
+constexpr int kHistStride = 257;
+constexpr int kHistRowsAhead = 8;  // bin-row gathers issued before their atomics
+
 __global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, int g0, int g1,
                                                              const uint32_t* itemPref, uint32_t* hW,
                                                              unsigned long long* hS) {
-  extern __shared__ __align__(16) char sm[];
-  unsigned long long* sS = reinterpret_cast<unsigned long long*>(sm);  // [m][256]
-  uint32_t* sW = reinterpret_cast<uint32_t*>(sS + (size_t)b.m * 256);    // [m][256]
-  int* sF = reinterpret_cast<int*>(sW + (size_t)b.m * 256);              // [m]
+  extern __shared__ __align__(16) uint32_t hsm[];
+  const int m = b.m;
+  uint32_t* sW = hsm;                                     // [m][kHistStride]
+  uint32_t* sLo = sW + (size_t)m * kHistStride;           // low words of S
+  uint32_t* sHi = sLo + (size_t)m * kHistStride;          // high words of S
+  int* sF = reinterpret_cast<int*>(sHi + (size_t)m * kHistStride);  // [m] drawn features
   const int item = blockIdx.x;
   int lo = g0, hi = g1;  // node: last g with itemPref[g - g0] <= item
   while (hi - lo > 1) {
@@ -844,37 +869,71 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, i
   const int t = (int)nd.tree[g];
   const uint32_t start = nd.start[g], len = nd.len[g];
   const uint32_t i0 = c * kHistChunk, i1 = min(len, i0 + (uint32_t)kHistChunk);
-  for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) { sW[i] = 0u; sS[i] = 0ull; }
-  for (int j = threadIdx.x; j < b.m; j += blockDim.x) sF[j] = b.feat[(size_t)g * b.m + j];
+  for (int i = threadIdx.x; i < 3 * m * kHistStride; i += blockDim.x) hsm[i] = 0u;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) sF[j] = b.feat[(size_t)g * m + j];
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr + start;
   const uint8_t* w = b.w + (size_t)t * b.n;
-  for (uint32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const uint32_t r = L[i];
-    const uint32_t wv = w[r];
-    const unsigned long long sv = (unsigned long long)((long long)wv * b.tq[r]);
-    const uint8_t* br = b.bins + (size_t)r * b.p;
-    for (int j = 0; j < b.m; ++j) {
-      const int bin = br[sF[j]];
-      atomicAdd(&sW[j * 256 + bin], wv);
-      atomicAdd(&sS[j * 256 + bin], sv);
+  const int ngrp = (m + 31) >> 5;  // feature groups of 32 lanes (m <= 73 by the smem limit)
+  for (uint32_t base = i0 + 32u * warp; base < i1; base += 32u * nwarp) {
+    const uint32_t i = base + lane;
+    uint32_t r = 0, wv = 0;
+    unsigned long long v = 0;
+    if (i < i1) {
+      r = L[i];
+      wv = w[r];
+      v = (unsigned long long)((long long)wv * b.tq[r]);
+    }
+    const int nk = (int)min(32u, i1 - base);
+    for (int gq = 0; gq < ngrp; ++gq) {
+      const int j = gq * 32 + lane;
+      const bool act = j < m;
+      const int f = act ? sF[j] : 0;
+      uint32_t* cW = sW + (size_t)j * kHistStride;
+      uint32_t* cLo = sLo + (size_t)j * kHistStride;
+      uint32_t* cHi = sHi + (size_t)j * kHistStride;
+      for (int k0 = 0; k0 < nk; k0 += kHistRowsAhead) {
+        uint32_t bn[kHistRowsAhead];
+#pragma unroll
+        for (int q = 0; q < kHistRowsAhead; ++q) {
+          const uint32_t rq = __shfl_sync(0xffffffffu, r, k0 + q);
+          bn[q] = (act && k0 + q < nk) ? (uint32_t)b.bins[(size_t)rq * b.p + f] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kHistRowsAhead; ++q) {
+          const uint32_t wq = __shfl_sync(0xffffffffu, wv, k0 + q);
+          const unsigned long long vq = __shfl_sync(0xffffffffu, v, k0 + q);
+          if (act && k0 + q < nk) {
+            const uint32_t vlo = (uint32_t)vq, vhi = (uint32_t)(vq >> 32);
+            atomicAdd(&cW[bn[q]], wq);
+            const uint32_t old = atomicAdd(&cLo[bn[q]], vlo);
+            const uint32_t add = vhi + (old > ~vlo ? 1u : 0u);  // carry out of the low word
+            if (add) atomicAdd(&cHi[bn[q]], add);
+          }
+        }
+      }
     }
   }
   __syncthreads();
-  const size_t base = (size_t)(g - g0) * b.m * 256;
+  const size_t base = (size_t)(g - g0) * m * 256;
   const bool single = len <= (uint32_t)kHistChunk;
-  for (int i = threadIdx.x; i < b.m * 256; i += blockDim.x) {
+  for (int idx = threadIdx.x; idx < m * 256; idx += blockDim.x) {
+    const int j = idx >> 8, bin = idx & 255;
+    const uint32_t Wv = sW[j * kHistStride + bin];
+    const unsigned long long Sv =
+        ((unsigned long long)sHi[j * kHistStride + bin] << 32) | sLo[j * kHistStride + bin];
     if (single) {
-      hW[base + i] = sW[i];
-      hS[base + i] = sS[i];
-    } else if (sW[i]) {
-      atomicAdd(&hW[base + i], sW[i]);
-      atomicAdd(&hS[base + i], sS[i]);
+      hW[base + idx] = Wv;
+      hS[base + idx] = Sv;
+    } else if (Wv) {
+      atomicAdd(&hW[base + idx], Wv);
+      atomicAdd(&hS[base + idx], Sv);
     }
   }
 }
 
-size_t hist_build_smem(int m) { return (size_t)m * 256 * 12 + (size_t)m * 4 + 16; }
+size_t hist_build_smem(int m) { return (size_t)3 * m * kHistStride * 4 + (size_t)m * 4 + 16; }
 
 // one CTA per node: best cut over the drawn features (warp per feature, 8 bins per lane)
 __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int g1, const uint32_t* hW,
@@ -920,7 +979,7 @@ __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int
         const long long SL = (long long)cs;
         const double G = split_gain((long long)cw, SL, (long long)(Wt - cw), St - SL);
         const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
-        const unsigned long long aux = ((unsigned long long)j << 32) | (unsigned long long)cidx;  // R9
+        const unsigned long long aux = cand_aux(b, j, f, (unsigned)cidx);  // R9
         ++nc;
         if (better(key, aux, bk, ba)) { bk = key; ba = aux; }
       }
@@ -952,7 +1011,7 @@ __global__ void k_decide_hist(Batch b, int NO) {
   if (g >= NO) return;
   const Best bs = b.best[g];
   if (!bs.key) return;
-  const int j = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
+  const int j = (int)((bs.aux >> 48) & 0xFFull), c = (int)(bs.aux & 0xFFFFFFFFull);
   const int f = b.feat[(size_t)g * b.m + j];
   b.thr[g] = b.cuts[(size_t)f * 256 + c];
   b.thrIdx[g] = (uint32_t)c;
@@ -1688,6 +1747,7 @@ __global__ void k_chunk_predict(const Node16* __restrict__ nodes, uint64_t cap, 
 }  // namespace
 
 int g_opt_tiled_partition = 0;
+long long g_opt_hist_node_cap = 0;
 
 static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, int tree_lo, int tree_hi,
                              int task, const uint32_t* tr_rows_in, int ntr, const uint32_t* task_order,
@@ -1780,6 +1840,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.rowMask = b.packRank ? 0x1FFFFu : 0xFFFFFFFFu;
   b.hist = hist ? 1 : 0;
   b.extra = extra ? 1 : 0;
+  b.tie_draw = prm->tie_break == RF_TIE_DRAW_ORDER ? 1 : 0;
   if (extra) LCK(sc.alloc(&b.xb, (size_t)pl.nmax * mtry));
   HistBufs hb;
   const uint32_t* list_src = task_order;
@@ -1803,6 +1864,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&b.accN, (size_t)pl.nmax));
     LCK(sc.alloc(&b.cmm, (size_t)pl.nmax * 4));
     hb.cap = std::max<long long>(1, std::min<long long>(pl.nmax, ((long long)2 << 30) / ((long long)mtry * 256 * 12)));
+    if (g_opt_hist_node_cap > 0) hb.cap = std::min<long long>(hb.cap, g_opt_hist_node_cap);  // test switch
     LCK(sc.alloc(&hb.W, (size_t)hb.cap * mtry * 256));
     LCK(sc.alloc(&hb.S, (size_t)hb.cap * mtry * 256));
     LCK(sc.alloc(&hb.nch, (size_t)hb.cap + 1));

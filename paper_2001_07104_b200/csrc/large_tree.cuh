@@ -13,6 +13,7 @@ namespace rf {
 
 // test switch (rf_debug_set_option "large_tiled_partition"): force the tiled partition
 extern int g_opt_tiled_partition;
+extern long long g_opt_hist_node_cap;  // test switch: histogram node-chunk cap (0 = by memory)
 
 // Grows trees [tree_lo, tree_hi) of task 0 over all rows.  Outputs (scratch
 // owned by `sc`): per-tree BFS node blocks of capacity *cap, node counts.

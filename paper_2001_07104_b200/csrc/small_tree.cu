@@ -10,7 +10,7 @@
 //   drawn feature scan the node's rows in x order, exact int64 prefix sums
 //   WL = sum w, SL = sum w t_q (R7), score G = SL^2/WL + SR^2/WR in canonical
 //   fp64 (R6, R28) at every boundary between distinct values (R8); best by
-//   (G desc, draw slot asc, threshold rank asc) (R9); threshold midway (R8);
+//   (G desc, feature or draw slot asc, threshold rank asc) (R9); threshold midway (R8);
 //   leaf if depth cap, < min_split distinct rows, constant t_q or no
 //   candidate (R11); leaf value fl(S/W) 2^-F (R13).
 //   ExtraTrees (split_mode 2, R29): the only candidate of a
@@ -269,7 +269,8 @@ __device__ __noinline__ void philox_pair_ool(uint32_t k0, uint32_t k1, uint32_t 
   philox_pair(k0, k1, b, c1, c2, c3, d0, d1);
 }
 
-// total order of candidates: key (G bits + 1) descending, aux (draw slot, position) ascending (R9)
+// total order of candidates: key (G bits + 1) descending, aux (tie key, draw slot, position)
+// ascending; tie key = feature index (north_star, default) or draw slot (R9)
 __device__ __forceinline__ bool better(unsigned long long k1, uint32_t a1, unsigned long long k2, uint32_t a2) {
   return k1 > k2 || (k1 == k2 && a1 < a2);
 }
@@ -368,7 +369,7 @@ __device__ __noinline__ int64_t seg_median2(SA<uint8_t> tl, int ln, SA<uint8_t> 
 
 // MAE candidate queue (R32).  The search loop appends its candidates to a per-warp ring
 // (ballot-compacted; entry = node k | feature f << 8 | boundary rank << 16 | aux << 24 |
-// WL << 40, and SL) and every 32 queued candidates are scored here one per lane, so each
+// WL << 48, and SL) and every 32 queued candidates are scored here one per lane, so each
 // lane walks one candidate's t-ordered rows instead of the warp waiting on the few lanes
 // that hold a candidate in a loop step (ExtraTrees: one candidate per segment).  The keys
 // merge into the per-node best (mkey ...) under the search's total order (R9), which does
@@ -388,8 +389,8 @@ __device__ __noinline__ void mae_flush(SA<ulonglong2> q, uint32_t qh, int nq, No
     k = (int)(e.x & 0xFFu);
     const int f = (int)((e.x >> 8) & 0xFFu);
     const uint32_t thr = (uint32_t)((e.x >> 16) & 0xFFu);
-    aux = (uint32_t)((e.x >> 24) & 0xFFFFu);
-    WL = (uint32_t)((e.x >> 40) & 0xFFFFu);
+    aux = (uint32_t)((e.x >> 24) & 0xFFFFFFu);
+    WL = (uint32_t)((e.x >> 48) & 0xFFFFu);
     SL = (int64_t)e.y;
     const uint32_t Wk = cur.W[k];
     const int64_t Sk = cur.S[k];
@@ -892,7 +893,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         uint32_t wr = ws.w[r];
         int64_t tr = cs.tq[r];
         int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
-        uint32_t auxb = ((uint32_t)j << 8) | (uint32_t)st;  // candidate aux minus the index
+        // candidate aux minus the index: tie key << 16 | draw slot << 8 | node start, tie key =
+        // the feature (north_star) or the draw slot (R9); ascending aux = preferred among equal keys
+        const bool tie_draw = a.tie_draw != 0;
+        uint32_t auxb = ((uint32_t)(tie_draw ? j : f) << 16) | ((uint32_t)j << 8) | (uint32_t)st;
         uint32_t qh = 0u, qt = 0u;  // MAE candidate ring: head, tail
         if (kMae && kExtra) {
           #pragma unroll 1
@@ -922,7 +926,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const double gr = div_small(__dmul_rn(dSR, dSR), yr.x, yr.y);
           const bool cand = act && hasNext && (extra ? (rkr <= (uint32_t)xbj && rkn > (uint32_t)xbj) : rkr != rkn);
           unsigned long long key;
-          const uint32_t aux = auxb + (uint32_t)i;  // draw slot << 8 | position (R9)
+          const uint32_t aux = auxb + (uint32_t)i;  // tie key << 16 | draw slot << 8 | position (R9)
           if (kMae && kExtra) {  // R32: queued, scored one per lane by mae_flush (left = rank <= rkr)
             key = 0ull;
             const uint32_t bal = __ballot_sync(0xffffffffu, cand);
@@ -930,8 +934,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               const uint32_t slot = (qt + (uint32_t)__popc(bal & ((1u << lane) - 1u))) & (kMaeQ - 1);
               ws.mq[slot] = make_ulonglong2((unsigned long long)k | ((unsigned long long)f << 8) |
                                                 ((unsigned long long)rkr << 16) |
-                                                ((unsigned long long)(aux & 0xFFFFu) << 24) |
-                                                ((unsigned long long)WL << 40),
+                                                ((unsigned long long)(aux & 0xFFFFFFu) << 24) |
+                                                ((unsigned long long)WL << 48),
                                             (unsigned long long)SL);
             }
             qt += (uint32_t)__popc(bal);
@@ -970,7 +974,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             f = ws.feat[k * p + j];
             if (extra) xbj = ws.xb[k * p + j];
             lbase = f * ntr_max;
-            auxb = ((uint32_t)j << 8) | (uint32_t)st;
+            auxb = ((uint32_t)(tie_draw ? j : f) << 16) | ((uint32_t)j << 8) | (uint32_t)st;
             rn = L[lbase + st];
             rkn = cs.lrank[lbase + rn];
             wr = ws.w[rn];
@@ -1053,7 +1057,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         ws.ncb[2 * k + 1] = 0;
         if (key) {
           const uint32_t aux = ws.baux[k];
-          const int j = (int)(aux >> 8), bp = (int)(aux & 0xFFu);
+          const int j = (int)((aux >> 8) & 0xFFu), bp = (int)(aux & 0xFFu);
           const int f = ws.feat[k * p + j];
           const uint8_t ra = L[f * ntr_max + bp], rb = L[f * ntr_max + bp + 1];
           const uint32_t ga = cs.trr[ra], gb = cs.trr[rb];

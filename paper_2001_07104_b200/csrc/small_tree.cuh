@@ -42,6 +42,7 @@ struct SmallArgs {
   int bootstrap, min_split, max_depth;
   int extra;                // ExtraTrees split mode (R29): one random threshold per drawn feature
   int mae;                  // MAE criterion (R32): absolute deviations from weighted medians
+  int tie_draw;             // tie-break (R9): 0 lowest feature index (north_star), 1 first drawn
   int n_mtry;
   int mtrys[kMaxMtry];
   int tree_lo, tree_hi;     // trees [tree_lo, tree_hi)

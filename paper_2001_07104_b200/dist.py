@@ -35,6 +35,12 @@ def _world(group=None):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
+def _host_staged(t, group=None):
+    """gloo process groups (CPU tests, and several ranks sharing one GPU in the GPU tests)
+    exchange host tensors: True if t is a CUDA tensor and the group's backend is gloo."""
+    return isinstance(t, torch.Tensor) and t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 # ------------------------------------------------------------ exchanges ----
 def gather_task_tables(local: torch.Tensor, task_axis_len: int, group=None) -> torch.Tensor:
     """local: [..., T_local] slice of a table whose last axis is the flat task index
@@ -43,6 +49,8 @@ def gather_task_tables(local: torch.Tensor, task_axis_len: int, group=None) -> t
     rank, world = _world(group)
     if world == 1:
         return local
+    if _host_staged(local, group):
+        return gather_task_tables(local.cpu(), task_axis_len, group).to(local.device)
     local = local.contiguous()
     flat = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(flat, local, group=group)  # concatenated along dim 0 (all backends)
@@ -56,7 +64,12 @@ def reduce_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
     """In-place all_reduce(SUM) of per-row partial sums (fp64)."""
     rank, world = _world(group)
     if world > 1:
-        dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+        if _host_staged(partial, group):
+            h = partial.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            partial.copy_(h)
+        else:
+            dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
     return partial
 
 
@@ -66,6 +79,10 @@ def allgather_forest_arrays(feature, left, value, thr_index, tree_off, group=Non
     rank, world = _world(group)
     if world == 1:
         return feature, left, value, thr_index, tree_off
+    if _host_staged(feature, group):
+        arrs = allgather_forest_arrays(feature.cpu(), left.cpu(), value.cpu(), thr_index.cpu(), tree_off.cpu(),
+                                       group)
+        return tuple(a.to(feature.device) for a in arrs)
     dev = feature.device
     counts = torch.tensor([feature.shape[0], tree_off.shape[0] - 1], dtype=torch.int64, device=dev)
     allc = torch.empty((world * 2,), dtype=torch.int64, device=dev)
@@ -102,6 +119,8 @@ def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
     rank, world = _world(group)
     if world == 1:
         return local
+    if _host_staged(local, group):
+        return gather_rows(local.cpu(), group).to(local.device)
     dev = local.device
     n = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
     alln = torch.empty((world,), dtype=torch.int64, device=dev)
@@ -166,6 +185,21 @@ def predict_tree_sharded(local_forest, X, ntree_total, target, group=None):
     return predict_finalize(part, ntree_total, target)
 
 
+def study_units(sizes, rank, world):
+    """Strong-scaling split of a fixed CV study (SURVEY 8(e) "shard whole (dataset, rep, fold)
+    tasks"): sizes[d] = tasks of dataset d; the flattened (dataset, task) list is cut into
+    `world` contiguous ranges.  Returns this rank's [(d, task_lo, task_hi)] (non-empty only)."""
+    total = sum(sizes)
+    lo, hi = shard(total, rank, world)
+    out, base = [], 0
+    for d, n in enumerate(sizes):
+        a, b = max(lo, base), min(hi, base + n)
+        if b > a:
+            out.append((d, a - base, b - base))
+        base += n
+    return out
+
+
 def cv_task_sharded(X, y, k, repeats_per_rank, ntrees, mtrys, *, custom=False, seed=0,
                     target=TARGET_IDENTITY, group=None, **kw):
     """Weak-scaling CV study: rank r runs repeats [r R, (r+1) R) of an R*world-repeat study.
@@ -188,7 +222,67 @@ def cv_tree_sharded(X, y, k, repeats, folds, ntrees, mtrys, *, target=TARGET_IDE
     trees, all_reduce(SUM), finalize (divide, exp, MAPE) on every rank."""
     rank, world = _world(group)
     lo, hi = shard(max(ntrees), rank, world)
-    part = cv_partial(X, y, k, repeats, folds, ntrees, mtrys, tree_begin=lo, tree_end=hi, target=target,
-                      seed=seed, **kw)
+    if hi > lo:
+        part = cv_partial(X, y, k, repeats, folds, ntrees, mtrys, tree_begin=lo, tree_end=hi, target=target,
+                          seed=seed, **kw)
+    else:
+        # empty shard (fewer trees than ranks): contribute zeros -- (0, 0) would mean "all trees"
+        # to the C ABI and double-count the forest in the all_reduce
+        n = y.shape[0]
+        shape = (len(mtrys), len(ntrees), repeats, n)
+        part = torch.zeros(shape, dtype=torch.float64, device=X.device) if isinstance(X, torch.Tensor) \
+            else np.zeros(shape, np.float64)
+    host = not isinstance(part, torch.Tensor)
+    if host:
+        part = torch.from_numpy(part)
     reduce_partials(part, group)
+    if host:
+        part = part.numpy()
     return cv_finalize(y, k, repeats, folds, ntrees, len(mtrys), part, target=target, want_pred=want_pred)
+
+
+def cv_study_sharded(datasets, k, repeats, ntrees, mtrys, *, folds, outs, group=None, streams=None, **kw):
+    """Strong-scaling CV study (BASELINE.json configs[1], SURVEY 8(e) CV C2): the fixed study's
+    (dataset, task) units are cut into contiguous rank ranges (study_units); each rank runs
+    rf_cross_validate_grid with task_begin/task_end on its units only, then the owned task
+    columns of every table are all-gathered in unit order (gather_rows) and written back, so
+    every rank ends with the full tables -- bit-identical for any number of ranks (no
+    floating-point reduction).
+
+    datasets: [dict(X, y, target, seed)] device tensors; folds[d]: int32 [repeats, n] device
+    fold ids; outs[d]: fp64 [n_mtry, n_ntree, repeats, k] device tables (filled in place).
+    streams: optional CUDA streams, one per dataset (the launches of different datasets overlap).
+    Returns this rank's units [(d, lo, hi)]."""
+    rank, world = _world(group)
+    T = repeats * k
+    units = study_units([T] * len(datasets), rank, world)
+    main = torch.cuda.current_stream() if streams else None
+    for d, lo, hi in units:
+        ds = datasets[d]
+        st = streams[d % len(streams)] if streams else None
+        if st is not None:
+            st.wait_stream(main)
+        with torch.cuda.stream(st) if st is not None else _nullctx():
+            cross_validate_grid(ds["X"], ds["y"], k, repeats, ntrees, mtrys, fold_ids=folds[d], target=ds["target"],
+                                seed=ds["seed"], task_begin=lo, task_end=hi, out=outs[d], **kw)
+    if streams:
+        for st in streams:
+            main.wait_stream(st)
+    if world > 1:
+        G = len(mtrys) * len(ntrees)
+        mine = [outs[d].reshape(G, T)[:, lo:hi].t() for d, lo, hi in units]
+        local = torch.cat(mine) if mine else torch.empty((0, G), dtype=torch.float64, device=outs[0].device)
+        full = gather_rows(local.contiguous(), group)  # [sum of all units, G] in unit order
+        o = 0
+        for d in range(len(datasets)):
+            outs[d].reshape(G, T).copy_(full[o:o + T].t())
+            o += T
+    return units
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
