@@ -1,23 +1,26 @@
-"""Benchmark: the paper-shaped full CV study (BASELINE.json configs[1]).
+"""Benchmark of the hot path (BASELINE.json metric: trees/s and predictions/s; CV-study wall
+time vs the CPU oracle), one JSON line.
 
-Workload of one step ("full study"): 10 datasets = 5 GPUs
-of Table 3 x {time (n=189, LOG, paper custom split), power (n=168, plain
-k-fold)}, 30 repeats x 10-fold CV, grid ntree {128,256,512,1024} (prefixes of
-1024-tree forests) x mtry {12 (max), 3 (sqrt), 3 (log2)}.  Distinct trees
-grown per step per rank: 10 x 300 tasks x 2 distinct mtry x 1024 = 6,144,000.
-Every step runs the whole hot path: validation + quantisation + presort
-(a1, a3), folds (a2), bootstrap / feature draws / split search / partition /
-leaves (a4-a8) in the small-tree kernel, CV scoring (a10); N>1 adds the
+Headline (top-level value): the full paper-shaped CV study, configs[1]:
+10 datasets = 5 GPUs of Table 3 x {time (n=189, LOG, paper custom split), power (n=168, plain
+k-fold)}, 30 repeats x 10-fold CV, grid ntree {128,256,512,1024} (prefixes of 1024-tree
+forests) x mtry {12 (max), 3 (sqrt), 3 (log2)}: 6,144,000 distinct trees per step.  Every step
+runs the whole hot path: validation + quantisation + presort (a1, a3), folds (a2), bootstrap /
+feature draws / split search / partition / leaves (a4-a8), CV scoring (a10); N > 1 adds the
 cross-rank gather of the fold-MAPE tables (a11).
 
-Multi-GPU (weak scaling): rank r runs repeats [30 r, 30 r + 30) of a
-30 N-repeat study (task sharding, no data-path collective besides the final
-all_gather of MAPE tables).  value = trees grown by all ranks / max over
-ranks of the device time.  Within a rank the ten datasets run on ten CUDA
-streams (--streams 1: one after another).
+Multi-GPU (--scaling strong, the default): the FIXED study's 3,000 (dataset, rep, fold) tasks
+are cut into contiguous rank ranges (SURVEY 8(e) "shard whole (dataset, rep, fold) tasks"),
+so its wall time drops with N; --scaling weak: every rank runs its own 30-repeat study.  value
+= trees grown by all ranks / max over ranks of the device time.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--split exact|extra]
-                  [--streams S] [--no-cpu-baseline] [--no-e2e]
+Per-config objects ("configs": C1, C3, C4, C5 of BASELINE.json, measured on rank 0 at N = 1):
+value / unit / ms, roofline of the dominant kernel, cpu_baseline (oracle, 1 core and N pinned
+cores), e2e through the host-pointer C ABI, clocks during the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--scaling strong|weak]
+                  [--configs c1,c3,c4,c5 | --no-configs] [--no-cpu-baseline] [--no-e2e]
+                  [--split exact|extra] [--criterion mse|mae] [--streams S]
 """
 from __future__ import annotations
 
@@ -44,6 +47,13 @@ MTRYS = [12, 3, 3]
 SEED = 7104
 DISTINCT_MTRY = 2
 
+# fp64 arithmetic per evaluated candidate split: 2 squares + 2 divisions + 1 add
+FLOPS_PER_CANDIDATE = 5
+# measured on the B200 (profiles/micro/microbench.cu, profiles/rd2_02_micro.txt): DFMA 17.12 T
+# ops/s = 34.2 TFLOP/s counting 2 flops per FMA (DMUL 17.2 T, DADD 18.6 T ops/s)
+FP64_PEAK_TFLOPS = 34.23
+FP64_PEAK_SOURCE = "measured: profiles/rd2_02_micro.txt (DFMA 17.12 Tops/s x 2 flops, 148 SMs, 1965 MHz)"
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -51,6 +61,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--configs", default="c1,c3,c4,c5")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--criterion", default="mse", choices=["mse", "mae"],
@@ -76,6 +89,15 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
 
 
 # ------------------------------------------------------------ clocks -------
@@ -134,35 +156,118 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# -------------------------------------------------------------- data -------
+# ------------------------------------------------- CPU oracle baselines -----
+def host_info():
+    model, gov = None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        gov = open("/sys/devices/system/cpu/cpu0/cpufreq/scaling_governor").read().strip()
+    except OSError:
+        gov = "n/a (no cpufreq interface)"
+    return {"cpu_model": model, "governor": gov}
+
+
+def _pinned_worker(core, fn, arg, q):
+    try:
+        os.sched_setaffinity(0, {core})
+    except OSError:
+        pass
+    t0 = time.perf_counter()
+    units = fn(arg)
+    q.put((core, units, time.perf_counter() - t0))
+
+
+def run_on_cores(fn, args_per_core):
+    """SURVEY 8(d) protocol (ii): one oracle process pinned per host core over disjoint
+    units; returns (units done, wall seconds, cores)."""
+    import multiprocessing as mp
+    cores = sorted(os.sched_getaffinity(0))[:len(args_per_core)]
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    t0 = time.perf_counter()
+    ps = [ctx.Process(target=_pinned_worker, args=(c, fn, a, q)) for c, a in zip(cores, args_per_core)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    wall = time.perf_counter() - t0
+    return sum(r[1] for r in res), wall, len(ps)
+
+
+def ncores():
+    return len(os.sched_getaffinity(0))
+
+
+def _oracle():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def _cv_trees(a):
+    """Oracle CV of dataset a['ds'] over tasks [lo, hi) of repeat block a['reps']: trees grown."""
+    oracle = _oracle()
+    d = datagen.study(datagen.SEED)[a["ds"]]
+    custom = d["target"] == "time"
+    folds = oracle.make_folds(d["y"], K_FOLDS, a["reps"], seed=SEED + a["ds"], custom=custom)
+    oracle.cv_grid(d["X"], d["y"], K_FOLDS, a["reps"], a.get("ntrees", NTREES), a.get("mtrys", [12, 3]),
+                   fold_ids=folds, target=1 if custom else 0, seed=SEED + a["ds"], task_begin=a["lo"],
+                   task_end=a["hi"], **a.get("skw", {}))
+    return (a["hi"] - a["lo"]) * len(a.get("mtrys", [12, 3])) * max(a.get("ntrees", NTREES))
+
+
+def cpu_baseline_c2(skw):
+    """1 core: K20/time repeat 0, 10 folds, mtry {12, 3} x 1024 trees (20,480 trees); N cores:
+    every core runs the same block of a different (dataset, repeat)."""
+    tasks = 1 if skw.get("criterion") else 10
+    t0 = time.perf_counter()
+    trees = _cv_trees(dict(ds=0, reps=1, lo=0, hi=tasks, skw=skw))
+    one = trees / (time.perf_counter() - t0)
+    n = ncores()
+    args = [dict(ds=i % 10, reps=1 + i // 10, lo=(i // 10) * K_FOLDS, hi=(i // 10) * K_FOLDS + tasks, skw=skw)
+            for i in range(n)]
+    tot, wall, used = run_on_cores(_cv_trees, args)
+    return {"value": one, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{trees} trees: K20/time dataset, repeat 0 (folds 0-{tasks - 1}), ntree<=1024 x mtry {{12,3}}",
+            "n_cores": {"value": tot / wall, "unit": UNIT, "cores": used,
+                        "sample": f"{used} processes pinned one per core, each {trees} trees of a different "
+                                  f"(dataset, repeat) block; {tot} trees in {wall:.1f} s wall"},
+            **host_info()}
+
+
+# ------------------------------------------------------- reference arm ------
 def study_config(args, world):
     """The workload both arms report (the reference arm times a bounded sample of it)."""
+    strong = getattr(args, "scaling", "strong") == "strong"
+    reps = REPS if strong else REPS * world
     return {"workload": "full study (configs[1]): 5 GPUs x {time n=189, power n=168} x 12 features, "
-                        "30x10-fold CV per rank, ntree {128,256,512,1024} x mtry {12,3,3}",
-            "trees_per_step": len(datagen.GPU_NAMES) * 2 * REPS * K_FOLDS * DISTINCT_MTRY * max(NTREES) * world,
-            "nominal_grid_trees_per_step": len(datagen.GPU_NAMES) * 2 * REPS * K_FOLDS * len(MTRYS) * sum(NTREES)
-            * world,
+                        f"{reps}x10-fold CV, ntree {{128,256,512,1024}} x mtry {{12,3,3}}",
+            "trees_per_step": len(datagen.GPU_NAMES) * 2 * reps * K_FOLDS * DISTINCT_MTRY * max(NTREES),
+            "nominal_grid_trees_per_step": len(datagen.GPU_NAMES) * 2 * reps * K_FOLDS * len(MTRYS) * sum(NTREES),
             "l2": "flushed between timed steps (256 MB write)",
             "split": ("ExtraTrees, no bootstrap (P:468-469)" if args.split == "extra"
                       else "bootstrap + exact CART (north_star)"),
             "criterion": getattr(args, "criterion", "mse"),
-            "parallelism": f"task-sharded x{world}",
+            "tie_break": "lowest feature, then lowest threshold (north_star; R9)",
+            "parallelism": f"{'task' if strong else 'repeat'}-sharded x{world} "
+                           f"({'strong: one fixed study' if strong else 'weak: a study per rank'})",
             "cuda_streams": getattr(args, "streams", 1)}
 
 
-def study_inputs():
-    return datagen.study(datagen.SEED)
-
-
-# ------------------------------------------------------- reference arm ------
 def run_reference(args):
     """The oracle (plain single-threaded C), timed as it stands on the host."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import oracle
-    oracle.build()
-    ds = study_inputs()[0]  # K20 / time
+    oracle = _oracle()
+    ds = datagen.study(datagen.SEED)[0]  # K20 / time
     folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
     # bounded sample: repeat 0, tasks (folds) 0..3 of one dataset, full grid (~3 s per step;
     # one task under MAE, whose oracle is ~10x slower per tree)
@@ -182,8 +287,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if args.scaling == "strong" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(study_config(args, 1), reference_sample=f"per step: K20/time, repeat 0, folds "
                        f"0-{sample_tasks - 1}, ntree {{128..1024}} x mtry {{12,3}} = {trees} trees"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -193,29 +298,13 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def cpu_baseline_sample(skw):
-    import oracle
-    oracle.build()
-    ds = study_inputs()[0]
-    folds = oracle.make_folds(ds["y"], K_FOLDS, 1, seed=SEED, custom=True)
-    tasks = 1 if skw.get("criterion") else 10  # one repeat of 10-fold CV: ~8 s on one host core (MAE: one fold)
-    t0 = time.perf_counter()
-    oracle.cv_grid(ds["X"], ds["y"], K_FOLDS, 1, NTREES, [12, 3], fold_ids=folds, target=1, seed=SEED,
-                   task_begin=0, task_end=tasks, **skw)
-    dt = time.perf_counter() - t0
-    trees = tasks * DISTINCT_MTRY * max(NTREES)
-    return {"value": trees / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{trees} trees: K20/time dataset, repeat 0 (folds 0-{tasks - 1}), ntree<=1024 x mtry {{12,3}} "
-                      f"({dt:.1f} s on 1 host core)"}
-
-
 # --------------------------------------------------------------- our arm ----
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2001_07104_b200 as rfg
-    from paper_2001_07104_b200.dist import gather_task_tables
+    from paper_2001_07104_b200.dist import cv_study_sharded, gather_task_tables
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -224,41 +313,40 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     rfg.lib()
     stream = torch.cuda.current_stream()
-    ds = study_inputs()
-    reps_total = REPS * world
-    task_lo, task_hi = rank * REPS * K_FOLDS, (rank + 1) * REPS * K_FOLDS
+    ds = datagen.study(datagen.SEED)
+    strong = args.scaling == "strong"
+    reps_total = REPS if strong else REPS * world
     dX = [torch.as_tensor(d["X"], device=dev) for d in ds]
     dy = [torch.as_tensor(d["y"], device=dev) for d in ds]
     folds = [torch.empty((reps_total, d["X"].shape[0]), dtype=torch.int32, device=dev) for d in ds]
     out = [torch.empty((len(MTRYS), len(NTREES), reps_total, K_FOLDS), dtype=torch.float64, device=dev) for _ in ds]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
     skw = split_kw(args)
-
-    # one CUDA stream per dataset: the ten CV launches of a step overlap, so each launch's
-    # last partial wave of CTAs is filled by the next dataset's work (--streams 1: serial)
+    datasets = [dict(X=dX[i], y=dy[i], target=1 if d["target"] == "time" else 0, seed=SEED + i)
+                for i, d in enumerate(ds)]
+    # one CUDA stream per dataset: the launches of a step overlap, so each launch's last partial
+    # wave of CTAs is filled by the next dataset's work (--streams 1: serial)
     streams = [torch.cuda.Stream(device=dev) for _ in ds] if args.streams > 1 else None
-
-    def one(i, d):
-        custom = d["target"] == "time"
-        rfg.make_folds(dy[i], K_FOLDS, reps_total, seed=SEED + i, custom=custom, out=folds[i])
-        rfg.cross_validate_grid(dX[i], dy[i], K_FOLDS, reps_total, NTREES, MTRYS, fold_ids=folds[i],
-                                target=1 if custom else 0, seed=SEED + i, task_begin=task_lo,
-                                task_end=task_hi, out=out[i], **skw)
+    task_lo, task_hi = rank * REPS * K_FOLDS, (rank + 1) * REPS * K_FOLDS  # weak scaling
 
     def step():
-        if streams is None:
-            for i, d in enumerate(ds):
-                one(i, d)
-        else:
-            main = torch.cuda.current_stream()
-            for i, d in enumerate(ds):
-                st = streams[i % len(streams)]
-                st.wait_stream(main)
-                with torch.cuda.stream(st):
-                    one(i, d)
-            for st in streams:
-                main.wait_stream(st)
-        if world > 1:  # a11: fold-MAPE tables of all ranks, in task order (NCCL all_gather)
+        for i, d in enumerate(ds):
+            rfg.make_folds(dy[i], K_FOLDS, reps_total, seed=SEED + i, custom=d["target"] == "time", out=folds[i])
+        if strong:
+            cv_study_sharded(datasets, K_FOLDS, reps_total, NTREES, MTRYS, folds=folds, outs=out, streams=streams,
+                             **skw)
+            return
+        main = torch.cuda.current_stream()
+        for i, d in enumerate(ds):
+            st = streams[i % len(streams)] if streams else main
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                rfg.cross_validate_grid(dX[i], dy[i], K_FOLDS, reps_total, NTREES, MTRYS, fold_ids=folds[i],
+                                        target=datasets[i]["target"], seed=SEED + i, task_begin=task_lo,
+                                        task_end=task_hi, out=out[i], **skw)
+        for st in streams or []:
+            main.wait_stream(st)
+        if world > 1:  # a11: fold-MAPE tables of all ranks, in task order
             for i in range(len(ds)):
                 mine = out[i].reshape(len(MTRYS), len(NTREES), -1)[:, :, task_lo:task_hi]
                 out[i].copy_(gather_task_tables(mine, reps_total * K_FOLDS).reshape(out[i].shape))
@@ -266,8 +354,6 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # profile pass (per-kernel events) outside the timed loop is not used for the roofline;
-    # the roofline uses events recorded inside the timed steps.
     rfg.set_profiling(True)
     start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stop = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -295,56 +381,63 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    trees_per_step_rank = len(ds) * REPS * K_FOLDS * DISTINCT_MTRY * max(NTREES)
-    value = trees_per_step_rank * world / (ms_per_step / 1e3)
+    trees_per_step = len(ds) * reps_total * K_FOLDS * DISTINCT_MTRY * max(NTREES)
+    value = trees_per_step / (ms_per_step / 1e3)
+    # candidates of all ranks (each rank counts its own)
+    ct = torch.tensor([float(cands)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ct)
+    cands_all = float(ct.item())
 
-    # dominant kernel roofline: the small-tree kernel is ALU (fp64 + integer/SMEM issue) bound
+    # dominant kernel: the small-tree kernel, plain fp64/integer ALU bound
     kern_ms, kern_n = prof.get("small_tree", (0.0, 0))
     roofline = None
     if kern_n:
-        ops_per_cand = FP64_OPS_PER_CANDIDATE
-        # with overlapping per-dataset streams the per-launch event spans overlap, so the kernel's
-        # busy time is bounded by the step's device time
+        # overlapping per-dataset streams: the kernel's busy time is bounded by the step's device time
         kern_busy_ms = min(kern_ms, dev_ms)
-        achieved = cands * ops_per_cand / (kern_busy_ms / 1e3) / 1e12
-        peak = FP64_PEAK_TOPS
-        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (fp64 pipe ops)",
-                    "frac": achieved / peak, "traffic": SMALL_TREE_DRAM_BYTES_PER_LAUNCH,
-                    "traffic_source": "ncu --set full, one launch (one dataset, 614,400 trees): dram read + write "
-                                      "bytes (profiles/r02i_small_tree_ncu.txt); the working set is on chip",
+        achieved = cands * FLOPS_PER_CANDIDATE / (kern_busy_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": SMALL_TREE_DRAM_BYTES_PER_LAUNCH,
+                    "traffic_source": "ncu --set full of one launch (one dataset): dram read + write bytes; the "
+                                      "working set is on chip (profiles/README.md)",
                     "kernel": "small_tree_kernel",
-                    "ncu_context": {"ipc": 2.55, "issue_slots_busy_pct": 63.8, "warps_per_sm": 16,
-                                    "top_stalls": "wait 37 %, short_scoreboard 17 %",
-                                    "source": "profiles/r02i_small_tree_ncu.txt (latency-bound: the fp64 "
-                                              "pipe fraction is low because each candidate also costs "
-                                              "shared-memory scans and per-level node work)"},
+                    "flops_per_candidate": FLOPS_PER_CANDIDATE,
+                    "flops_definition": "SURVEY 8(d) C2: per evaluated candidate split 2 fp64 divisions + 2 squares "
+                                        "+ 1 add (algorithmic, not the kernel's instruction count)",
+                    "candidates_per_step": cands / args.steps,
                     "kernel_ms_per_step": kern_busy_ms / args.steps, "launches_per_step": kern_n / args.steps,
                     "kernel_share_of_step": kern_busy_ms / max(dev_ms, 1e-9),
-                    "kernel_launch_spans_ms_per_step": kern_ms / args.steps,
-                    "streams": args.streams,
-                    "candidates_per_step": cands / args.steps, "fp64_ops_per_candidate": ops_per_cand,
-                    "peak_source": "DESIGN.md sec. 6: 148 SM x 64 fp64 lanes x 1965 MHz (guide unit counts)"}
+                    "peak_source": FP64_PEAK_SOURCE,
+                    "bound_context": "issue/latency bound, not fp64 bound: ncu shows ~12 warp instructions per "
+                                     "candidate (profiles/README.md); the fraction is low by construction"}
 
     e2e = None
     if not args.no_e2e and rank == 0 and world == 1:
         e2e = measure_e2e(rfg, ds, args, skw)
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = run_configs(rfg, torch, args, dev, flush)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": study_config(args, world),
+            "study_wall_s": ms_per_step / 1e3,
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "wall_s_timed": wall,
+            "candidates_per_step_all_ranks": cands_all / args.steps,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
         }
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline_sample(skw)
-        print(json.dumps(line))
+            line["cpu_baseline"] = cpu_baseline_c2(skw)
+        if configs:
+            line["configs"] = configs
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -396,13 +489,11 @@ def measure_e2e(rfg, ds, args, skw):
             "api": "rf_make_folds + rf_cross_validate_grid (host pointers, pinned inputs)"}
 
 
-# fp64 arithmetic per evaluated candidate split: 2 squares (DMUL),
-# 2 correctly rounded divisions by W <= 255 as DMUL + 2 DFMA each (Markstein), 1 DADD
-FP64_OPS_PER_CANDIDATE = 9
-# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (1.75 MB + 0.50 MB),
-# from the round-1 final ncu --set full capture (profiles/r02i_small_tree_ncu.txt)
+# dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (one dataset of the
+# study), ncu --set full (profiles/README.md)
 SMALL_TREE_DRAM_BYTES_PER_LAUNCH = 2.25e6
-FP64_PEAK_TOPS = 148 * 64 * 1.965e9 / 1e12
+
+from bench_configs import run_configs  # noqa: E402  (C1, C3, C4, C5 objects)
 
 
 def main():

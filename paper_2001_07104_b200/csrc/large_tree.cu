@@ -33,6 +33,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "large_tree.cuh"
@@ -371,6 +372,10 @@ __global__ void k_node_prep(Batch b, int cur, int NO) {
   // the draw order matters even for m = p under the draw-order tie-break (R9) and for the
   // ExtraTrees thresholds (keyed by draw slot, R29)
   uint8_t* fp = b.feat + (size_t)g * b.m;
+  if (b.m == b.p && !b.tie_draw && !b.extra) {  // all features, order irrelevant (as small_tree.cu)
+    for (int f = 0; f < b.p; ++f) fp[f] = (uint8_t)f;
+    return;
+  }
   uint8_t perm[256];
   for (int f = 0; f < b.p; ++f) perm[f] = (uint8_t)f;
   const uint32_t t = nd.tree[g];
@@ -833,30 +838,34 @@ __global__ void k_hist_zero(Batch b, int cur, int g0, int g1, uint32_t* hW, unsi
 }
 
 // work item = (node, chunk of <= kHistChunk rows): shared-memory histograms of the drawn
-// features.  A warp takes 32 rows of the chunk at a time (coalesced row ids, gathered weights
-// and targets) and then walks them one by one with the lanes over the drawn features: lane j
-// reads byte sF[j] of the row's 64-byte bin row (one coalesced access per row) and updates
-// feature j's histogram, so the lanes of a warp never hit the same counter (no same-address
-// serialisation on low-cardinality features, where a row-per-lane layout made whole warps
-// collide).  The sums are kept in 32-bit shared counters only: W, and S = w t_q as a (lo, hi)
-// pair whose carry is taken from the returned old lo (exact modular 64-bit arithmetic, order
-// free).  Measured (profiles/micro, rd2_02): one 64-bit shared atomicAdd compiles to a
-// compare-and-swap loop at 1.3 pair-updates/clk/SM, three 32-bit atomics run 3.0/clk/SM.
-// Feature histograms are kHistStride = 257 words apart so equal low bins of different
-// features fall in different banks.  (Earlier variants: row per lane with u32 + u64 CAS
-// atomics, 18 ms per C4 tree; a warp bitonic sort + segmented sums, 1.8x slower still.)
-constexpr int kHistStride = 257;
-constexpr int kHistRowsAhead = 8;  // bin-row gathers issued before their atomics
+// features.  A warp takes 32 rows of the chunk at a time: the lanes load the rows' ids,
+// weights and targets (coalesced ids, gathered w and t_q) and stage (byte offset of the bin
+// row, w, S low word, S high word) in a per-warp shared buffer; then the warp walks the 32 rows
+// one by one with the lanes over the drawn features: each step reads the row's record with one
+// broadcast 16-byte shared load, lane j reads byte sF[j] of the row's 64-byte bin row (one
+// coalesced access per row) and updates feature j's histogram -- the lanes of a warp never hit
+// the same counter (no same-address serialisation on low-cardinality features, where a
+// row-per-lane layout made whole warps collide).  The sums are kept in 32-bit shared counters
+// only: W, and S = w t_q as a (lo, hi) pair whose carry is taken from the returned old lo
+// (exact modular 64-bit arithmetic, order free).  A bin's three counters are adjacent, so one
+// address serves all three atomics (immediate offsets); 257 bins per feature spread equal low
+// bins of different features over different banks.  Measured (profiles/micro, rd2_02): one
+// 64-bit shared atomicAdd compiles to a compare-and-swap loop (1.3 pair-updates/clk/SM),
+// three 32-bit atomics run 3.0/clk/SM.  (Earlier variants: row per lane with u32 + u64 CAS
+// atomics, 18 ms per C4 tree; a warp bitonic sort + segmented sums, 1.8x slower still; the
+// per-row shuffles of the record instead of the staged broadcast, 41 instructions per row.)
+constexpr int kHistBins = 257;       // bins per feature histogram in shared memory (256 + pad)
+constexpr int kHistRowsAhead = 8;    // bin-row gathers issued before their atomics
 
-__global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, int g0, int g1,
-                                                             const uint32_t* itemPref, uint32_t* hW,
-                                                             unsigned long long* hS) {
-  extern __shared__ __align__(16) uint32_t hsm[];
+__global__ void __launch_bounds__(kHistThreads, 2) k_hist_build(Batch b, int cur, int g0, int g1,
+                                                                const uint32_t* itemPref, uint32_t* hW,
+                                                                unsigned long long* hS) {
+  extern __shared__ __align__(16) uint4 hst[];
   const int m = b.m;
-  uint32_t* sW = hsm;                                     // [m][kHistStride]
-  uint32_t* sLo = sW + (size_t)m * kHistStride;           // low words of S
-  uint32_t* sHi = sLo + (size_t)m * kHistStride;          // high words of S
-  int* sF = reinterpret_cast<int*>(sHi + (size_t)m * kHistStride);  // [m] drawn features
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  uint4* stage = hst + warp * 32;                                               // [nwarp][32] row records
+  uint32_t* hist = reinterpret_cast<uint32_t*>(hst + nwarp * 32);                // [m][kHistBins][3]
+  int* sF = reinterpret_cast<int*>(hist + (size_t)m * kHistBins * 3);           // [m] drawn features
   const int item = blockIdx.x;
   int lo = g0, hi = g1;  // node: last g with itemPref[g - g0] <= item
   while (hi - lo > 1) {
@@ -869,71 +878,69 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_build(Batch b, int cur, i
   const int t = (int)nd.tree[g];
   const uint32_t start = nd.start[g], len = nd.len[g];
   const uint32_t i0 = c * kHistChunk, i1 = min(len, i0 + (uint32_t)kHistChunk);
-  for (int i = threadIdx.x; i < 3 * m * kHistStride; i += blockDim.x) hsm[i] = 0u;
+  for (int i = threadIdx.x; i < 3 * m * kHistBins; i += blockDim.x) hist[i] = 0u;
   for (int j = threadIdx.x; j < m; j += blockDim.x) sF[j] = b.feat[(size_t)g * m + j];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr + start;
   const uint8_t* w = b.w + (size_t)t * b.n;
-  const int ngrp = (m + 31) >> 5;  // feature groups of 32 lanes (m <= 73 by the smem limit)
+  const uint32_t p = (uint32_t)b.p;  // host guarantees n * p < 2^32 (32-bit bin-row offsets)
+  const int ngrp = (m + 31) >> 5;    // feature groups of 32 lanes (m <= 73 by the smem limit)
   for (uint32_t base = i0 + 32u * warp; base < i1; base += 32u * nwarp) {
     const uint32_t i = base + lane;
-    uint32_t r = 0, wv = 0;
-    unsigned long long v = 0;
     if (i < i1) {
-      r = L[i];
-      wv = w[r];
-      v = (unsigned long long)((long long)wv * b.tq[r]);
+      const uint32_t r = L[i];
+      const uint32_t wv = w[r];
+      const unsigned long long v = (unsigned long long)((long long)wv * b.tq[r]);
+      stage[lane] = make_uint4(r * p, wv, (uint32_t)v, (uint32_t)(v >> 32));
     }
+    __syncwarp();
     const int nk = (int)min(32u, i1 - base);
     for (int gq = 0; gq < ngrp; ++gq) {
       const int j = gq * 32 + lane;
       const bool act = j < m;
-      const int f = act ? sF[j] : 0;
-      uint32_t* cW = sW + (size_t)j * kHistStride;
-      uint32_t* cLo = sLo + (size_t)j * kHistStride;
-      uint32_t* cHi = sHi + (size_t)j * kHistStride;
+      const uint8_t* bcol = b.bins + (act ? sF[j] : 0);
+      uint32_t* hj = hist + (size_t)(act ? j : 0) * kHistBins * 3;
       for (int k0 = 0; k0 < nk; k0 += kHistRowsAhead) {
         uint32_t bn[kHistRowsAhead];
 #pragma unroll
-        for (int q = 0; q < kHistRowsAhead; ++q) {
-          const uint32_t rq = __shfl_sync(0xffffffffu, r, k0 + q);
-          bn[q] = (act && k0 + q < nk) ? (uint32_t)b.bins[(size_t)rq * b.p + f] : 0u;
-        }
+        for (int q = 0; q < kHistRowsAhead; ++q)
+          bn[q] = (act && k0 + q < nk) ? (uint32_t)bcol[stage[k0 + q].x] : 0u;
 #pragma unroll
         for (int q = 0; q < kHistRowsAhead; ++q) {
-          const uint32_t wq = __shfl_sync(0xffffffffu, wv, k0 + q);
-          const unsigned long long vq = __shfl_sync(0xffffffffu, v, k0 + q);
           if (act && k0 + q < nk) {
-            const uint32_t vlo = (uint32_t)vq, vhi = (uint32_t)(vq >> 32);
-            atomicAdd(&cW[bn[q]], wq);
-            const uint32_t old = atomicAdd(&cLo[bn[q]], vlo);
-            const uint32_t add = vhi + (old > ~vlo ? 1u : 0u);  // carry out of the low word
-            if (add) atomicAdd(&cHi[bn[q]], add);
+            const uint4 e = stage[k0 + q];
+            uint32_t* cb = hj + 3 * bn[q];
+            atomicAdd(cb, e.y);
+            const uint32_t old = atomicAdd(cb + 1, e.z);
+            const uint32_t add = e.w + (old > ~e.z ? 1u : 0u);  // carry out of the low word
+            if (add) atomicAdd(cb + 2, add);
           }
         }
       }
     }
+    __syncwarp();  // the records are read before the next batch overwrites them
   }
   __syncthreads();
-  const size_t base = (size_t)(g - g0) * m * 256;
+  const size_t obase = (size_t)(g - g0) * m * 256;
   const bool single = len <= (uint32_t)kHistChunk;
   for (int idx = threadIdx.x; idx < m * 256; idx += blockDim.x) {
     const int j = idx >> 8, bin = idx & 255;
-    const uint32_t Wv = sW[j * kHistStride + bin];
-    const unsigned long long Sv =
-        ((unsigned long long)sHi[j * kHistStride + bin] << 32) | sLo[j * kHistStride + bin];
+    const uint32_t* cb = hist + ((size_t)j * kHistBins + bin) * 3;
+    const uint32_t Wv = cb[0];
+    const unsigned long long Sv = ((unsigned long long)cb[2] << 32) | cb[1];
     if (single) {
-      hW[base + idx] = Wv;
-      hS[base + idx] = Sv;
+      hW[obase + idx] = Wv;
+      hS[obase + idx] = Sv;
     } else if (Wv) {
-      atomicAdd(&hW[base + idx], Wv);
-      atomicAdd(&hS[base + idx], Sv);
+      atomicAdd(&hW[obase + idx], Wv);
+      atomicAdd(&hS[obase + idx], Sv);
     }
   }
 }
 
-size_t hist_build_smem(int m) { return (size_t)3 * m * kHistStride * 4 + (size_t)m * 4 + 16; }
+size_t hist_build_smem(int m) {
+  return (size_t)(kHistThreads / 32) * 32 * 16 + (size_t)3 * m * kHistBins * 4 + (size_t)m * 4 + 16;
+}
 
 // one CTA per node: best cut over the drawn features (warp per feature, 8 bins per lane)
 __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int g1, const uint32_t* hW,
@@ -1537,6 +1544,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
                      uint32_t* nextNode0, uint32_t* nextPos0, uint32_t* nlBase, WS2* wsTmp, const HistBufs& hb,
                      const PartBufs& pb, unsigned long long* ncand, cudaStream_t s, std::string& err) {
   const size_t plSmem = (size_t)b.nbw * 4;
+  std::unique_ptr<ProfScope> setup_scope(new ProfScope("large_tree_setup", s));  // bootstrap, in-bag lists, root statistics
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
   LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
   if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
@@ -1577,6 +1585,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   }
   k_init_level0<<<1, 1, 0, s>>>(b, rootInfo, counters);
   note_launch();
+  setup_scope.reset();
   LCK(cudaMemcpyAsync(hcounters, counters, 8, cudaMemcpyDeviceToHost, s));
   uint32_t* htPos0 = hcounters + 4;            // [B + 1] per-tree first positions (host)
   uint32_t* htab = htPos0 + (b.B + 1);         // [2 B] partition tile table (host)
@@ -1618,26 +1627,30 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       k_hist_reset<<<nblk(NO, 256), 256, 0, s>>>(b, (int)NO);
       note_launch();
       const size_t hsm = hist_build_smem(b.m);
-      ProfScope ps("hist_search", s);
-      for (long long g0 = 0; g0 < NO; g0 += hb.cap) {
-        const long long g1 = std::min<long long>(NO, g0 + hb.cap);
-        const int cnt = (int)(g1 - g0);
-        k_hist_nchunks<<<nblk(cnt, 256), 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.nch);
-        note_launch();
-        tb = cub_bytes;
-        LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, hb.nch, hb.pref, cnt + 1, s));
-        uint32_t items = 0;
-        LCK(cudaMemcpyAsync(&items, hb.pref + cnt, 4, cudaMemcpyDeviceToHost, s));
-        LCK(cudaStreamSynchronize(s));
-        k_hist_zero<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S);
-        k_hist_build<<<items, kHistThreads, hsm, s>>>(b, cur, (int)g0, (int)g1, hb.pref, hb.W, hb.S);
-        k_hist_best<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S, ncand);
-        note_launch(3);
+      {
+        ProfScope ps("hist_search", s);
+        for (long long g0 = 0; g0 < NO; g0 += hb.cap) {
+          const long long g1 = std::min<long long>(NO, g0 + hb.cap);
+          const int cnt = (int)(g1 - g0);
+          k_hist_nchunks<<<nblk(cnt, 256), 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.nch);
+          note_launch();
+          tb = cub_bytes;
+          LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, hb.nch, hb.pref, cnt + 1, s));
+          uint32_t items = 0;
+          LCK(cudaMemcpyAsync(&items, hb.pref + cnt, 4, cudaMemcpyDeviceToHost, s));
+          LCK(cudaStreamSynchronize(s));
+          k_hist_zero<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S);
+          k_hist_build<<<items, kHistThreads, hsm, s>>>(b, cur, (int)g0, (int)g1, hb.pref, hb.W, hb.S);
+          k_hist_best<<<cnt, 256, 0, s>>>(b, cur, (int)g0, (int)g1, hb.W, hb.S, ncand);
+          note_launch(3);
+        }
       }
+      ProfScope pm("hist_mark", s);
       k_decide_hist<<<nblk(NO, 128), 128, 0, s>>>(b, (int)NO);
       k_mark_hist<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
       note_launch(2);
     }
+    std::unique_ptr<ProfScope> ch_scope(new ProfScope("large_children", s));
     k_children_count<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, depth);
     note_launch();
     tb = cub_bytes;
@@ -1645,6 +1658,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     k_tree_update<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, (int)NO, nextNode0, nextPos0, nlBase);
     k_children_write<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, nextNode0, nextPos0, nlBase, depth);
     note_launch(2);
+    ch_scope.reset();
     if (b.sideBits) {
       ProfScope ps("large_partition", s);
       k_part_desc<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP, nextPos0, nlBase, pb.desc);
@@ -1871,6 +1885,10 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&hb.pref, (size_t)hb.cap + 1));
     LCK(cudaMemsetAsync(hb.nch, 0, ((size_t)hb.cap + 1) * 4, s));
     const size_t hsm = hist_build_smem(mtry);
+    if ((uint64_t)n * (uint64_t)p >= (1ull << 32)) {
+      err = "histogram mode: n * p must be < 2^32 (32-bit bin-row offsets)";
+      return RF_E_UNSUPPORTED;
+    }
     if (hsm > 227 * 1024) {
       err = "histogram mode: mtry too large for the shared-memory staging of the drawn bins";
       return RF_E_UNSUPPORTED;

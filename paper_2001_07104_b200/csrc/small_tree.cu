@@ -694,7 +694,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
       // feature draws (R4): partial Fisher-Yates; the draw order matters even for m = p
       // (ties go to the first drawn feature, R9).
       const int nblk = (m + 1) >> 1;
-      if (p <= 16) {
+      // m = p under the lowest-feature tie-break (north_star; exact mode): the drawn set is all
+      // features and the winner does not depend on the draw order, so the draws are skipped and
+      // slot j holds feature j (same trees as the oracle's Fisher-Yates; ExtraTrees keeps its
+      // draws: its thresholds are keyed by draw slot, R29)
+      if (m == p && !a.tie_draw && !extra) {
+        #pragma unroll 1
+        for (int q = lane; q < nOpen * p; q += 32) ws.feat[q] = (uint8_t)(q % p);
+      } else if (p <= 16) {
         // L lanes per node share its Philox blocks; the swap indices (4 bits per slot) are
         // OR-combined across the group, then one lane applies the swaps to a nibble-packed
         // permutation in a register

@@ -158,7 +158,8 @@ def fit_sharded(X, y, *, ntree, group=None, **kw):
         raise ValueError("fewer trees than ranks")
     e = local.export()
     dev = X.device if isinstance(X, torch.Tensor) else torch.device("cpu")
-    t = lambda a: torch.as_tensor(a.astype(np.int64) if a.dtype == np.uint64 else a, device=dev)
+    # unsigned arrays travel as int64 (gloo has no unsigned types); converted back below
+    t = lambda a: torch.as_tensor(a.astype(np.int64) if a.dtype in (np.uint64, np.uint32) else a, device=dev)
     arrs = allgather_forest_arrays(t(e["feature"]), t(e["left"]), t(e["value"]), t(e["thr_index"]),
                                    t(e["tree_off"]), group)
     feature, left, value, thr_index, off = (a.cpu().numpy() for a in arrs)

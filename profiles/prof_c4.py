@@ -1,8 +1,8 @@
-"""C4 shape at reduced rows (scaled(N, 64), histogram mode, mtry 21, max_depth 12), a few
-trees, for ncu launch lists:
+"""C4 shape (device-generated scaled(N, 64), histogram mode, mtry 21, max_depth 12), T trees,
+for ncu launch lists and per-kernel profiles:
 
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c4.csv \
-      python profiles/prof_c4.py 2000000 4
+      python profiles/prof_c4.py 10000000 89
 """
 import os
 import sys
@@ -16,7 +16,7 @@ import paper_2001_07104_b200 as rfg  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-X, y = datagen.scaled(N, 64)
-Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
+Xd, yd = datagen.scaled_device(N, 64)
+torch.cuda.synchronize()
 rfg.fit(Xd, yd, ntree=T, mtry=21, target=1, seed=7, max_depth=12, split_mode=rfg.SPLIT_HIST256)
 torch.cuda.synchronize()
