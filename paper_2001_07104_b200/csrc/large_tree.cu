@@ -755,49 +755,79 @@ __global__ void k_mark(Batch b, int cur, int NP) {
 // the candidate after cut c is valid iff WL > 0 and WR > 0; threshold = cut
 // value, threshold index = c; ties -> first drawn feature (R9), then lowest c.
 constexpr int kHistThreads = 512;
-constexpr int kHistChunk = 8192;  // rows per histogram work item
+// rows per histogram work item: nodes longer than one chunk add their chunk histograms with
+// global atomics (m x 256 x 2 per chunk), so chunks are long (8192 rows measured 35 % slower per
+// row at the top levels of C4, rd2_06)
+#ifndef RF_HIST_CHUNK
+#define RF_HIST_CHUNK 32768
+#endif
+constexpr int kHistChunk = RF_HIST_CHUNK;
 
-// one CTA per feature: cuts from the task's training rows sorted by x_f
-__global__ void k_cuts(const double* __restrict__ X, int p, const uint32_t* __restrict__ order, int ntr,
-                       double* cuts, int32_t* ncuts) {
+// Cuts from the task's training rows sorted by x_f (R23), in three kernels over (chunk of
+// kCutChunk sorted positions, feature) so the value gathers X[order[j]] use the whole GPU (one
+// CTA per feature gathered 640M values with 64 CTAs on C4: 107 ms, rd2_06):
+//   k_cut_count    distinct-run starts per chunk
+//   k_cut_finish   one CTA per feature: D = number of distinct values; D > 256: the distinct
+//                  values among s_{ceil(j ntr / 256) - 1}, j = 1..255, minus the maximum
+//   k_cut_collect  D <= 256: all distinct values but the largest, in order, at their offsets
+constexpr int kCutChunk = 4096;
+
+__device__ __forceinline__ double sorted_x(const double* __restrict__ X, int p, const uint32_t* __restrict__ o,
+                                           int f, long long j) {
+  return X[(size_t)o[j] * p + f];
+}
+
+__global__ void __launch_bounds__(256) k_cut_count(const double* __restrict__ X, int p,
+                                                   const uint32_t* __restrict__ order, int ntr, uint32_t* cnt) {
+  const int f = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
+  const uint32_t* o = order + (size_t)f * ntr;
+  uint32_t c = 0;
+  for (long long j = (long long)ch * kCutChunk + threadIdx.x; j < min((long long)ntr, (long long)(ch + 1) * kCutChunk);
+       j += blockDim.x)
+    c += (j == 0 || sorted_x(X, p, o, f, j) != sorted_x(X, p, o, f, j - 1)) ? 1u : 0u;
+  using BR = cub::BlockReduce<uint32_t, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint32_t tot = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) cnt[(size_t)f * nch + ch] = tot;
+}
+
+__global__ void __launch_bounds__(256) k_cut_finish(const double* __restrict__ X, int p,
+                                                    const uint32_t* __restrict__ order, int ntr, uint32_t* cnt,
+                                                    int nch, double* cuts, int32_t* ncuts) {
   const int f = blockIdx.x;
   const uint32_t* o = order + (size_t)f * ntr;
-  auto s = [&](int j) { return X[(size_t)o[j] * p + f]; };
-  using BR = cub::BlockReduce<int, 256>;
-  using BS = cub::BlockScan<int, 256>;
-  __shared__ typename BR::TempStorage tr;
-  __shared__ typename BS::TempStorage ts;
-  __shared__ int Dsh, carry;
-  int cnt = 0;
-  for (int j = threadIdx.x; j < ntr; j += blockDim.x) cnt += (j == 0 || s(j) != s(j - 1));
-  const int D = BR(tr).Sum(cnt);
-  if (threadIdx.x == 0) { Dsh = D; carry = 0; }
+  uint32_t* cf = cnt + (size_t)f * nch;
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  __shared__ double q[256];
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  const double vmax = ntr > 0 ? s(ntr - 1) : 0.0;
-  if (Dsh <= 256) {
-    // all distinct values but the largest, in order
-    for (int base = 0; base < ntr; base += blockDim.x) {
-      const int j = base + threadIdx.x;
-      int keep = 0;
-      double v = 0.0;
-      if (j < ntr) {
-        v = s(j);
-        keep = (j == 0 || v != s(j - 1)) && v != vmax;
-      }
-      int ex, tot;
-      BS(ts).ExclusiveSum(keep, ex, tot);
-      if (keep) cuts[(size_t)f * 256 + carry + ex] = v;
-      __syncthreads();
-      if (threadIdx.x == 0) carry += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) ncuts[f] = Dsh - 1;
-  } else if (threadIdx.x == 0) {
+  for (int base = 0; base < nch; base += 256) {  // exclusive offsets of the chunks' distinct starts
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < nch ? cf[i] : 0u;
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(v, ex, tot);
+    if (i < nch) cf[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  const uint32_t D = carry;
+  if (threadIdx.x == 0) cnt[(size_t)p * nch + f] = D;  // read by k_cut_collect
+  if (D <= 256) {  // k_cut_collect writes the values
+    if (threadIdx.x == 0) ncuts[f] = (int)D - 1;
+    return;
+  }
+  const double vmax = sorted_x(X, p, o, f, ntr - 1);
+  const int jq = threadIdx.x + 1;  // 1..255
+  if (jq <= 255) q[jq] = sorted_x(X, p, o, f, ((long long)jq * ntr + 255) / 256 - 1);  // ceil(jq ntr / 256) - 1
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int c = 0;
     double last = 0.0;
-    for (int jq = 1; jq <= 255; ++jq) {
-      const long long q = ((long long)jq * ntr + 255) / 256 - 1;  // ceil(jq ntr / 256) - 1
-      const double v = s((int)q);
+    for (int j = 1; j <= 255; ++j) {
+      const double v = q[j];
       if (v == vmax || (c > 0 && v == last)) continue;
       cuts[(size_t)f * 256 + c++] = v;
       last = v;
@@ -806,20 +836,63 @@ __global__ void k_cuts(const double* __restrict__ X, int p, const uint32_t* __re
   }
 }
 
-// bin(x) = #{cuts < x} for every row and feature (row-major [n][p] u8)
-__global__ void k_bins(const double* __restrict__ X, int n, int p, const double* __restrict__ cuts,
-                       const int32_t* __restrict__ ncuts, uint8_t* bins) {
-  const size_t total = (size_t)n * p;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int f = (int)(i % p);
-    const double x = X[i];
-    const double* c = cuts + (size_t)f * 256;
-    int lo = 0, hi = ncuts[f];  // first index with c[idx] >= x
+__global__ void __launch_bounds__(256) k_cut_collect(const double* __restrict__ X, int p,
+                                                     const uint32_t* __restrict__ order, int ntr,
+                                                     const uint32_t* __restrict__ off, const int32_t* __restrict__ ncuts,
+                                                     double* cuts) {
+  const int f = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
+  if (off[(size_t)gridDim.y * nch + f] > 256u) return;  // D > 256: quantile cuts (k_cut_finish)
+  const int nc = ncuts[f];
+  const uint32_t* o = order + (size_t)f * ntr;
+  const long long j0 = (long long)ch * kCutChunk, j1 = min((long long)ntr, j0 + kCutChunk);
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = off[(size_t)f * nch + ch];
+  __syncthreads();
+  for (long long base = j0; base < j1; base += 256) {
+    const long long j = base + threadIdx.x;
+    uint32_t keep = 0;
+    double v = 0.0;
+    if (j < j1) {
+      v = sorted_x(X, p, o, f, j);
+      keep = (j == 0 || v != sorted_x(X, p, o, f, j - 1)) ? 1u : 0u;
+    }
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(keep, ex, tot);
+    if (keep && carry + ex < (uint32_t)nc) cuts[(size_t)f * 256 + carry + ex] = v;  // all but the largest
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// bin(x) = #{cuts < x} for every row and feature (row-major [n][p] u8).  The cut tables of a
+// group of features are staged in shared memory (8 dependent loads per element from L1/L2 made
+// the binary search latency-bound: 120 ms for C4's 640M elements, rd2_07); grid-stride over
+// rows, the group's columns per thread.
+constexpr int kBinFeat = 16;  // features per shared-memory cut group (16 x 256 x 8 B = 32 KB)
+
+__global__ void __launch_bounds__(256) k_bins(const double* __restrict__ X, int n, int p,
+                                              const double* __restrict__ cuts, const int32_t* __restrict__ ncuts,
+                                              uint8_t* bins) {
+  __shared__ double sc[kBinFeat][256];
+  __shared__ int snc[kBinFeat];
+  const int f0 = blockIdx.y * kBinFeat, nf = min(kBinFeat, p - f0);
+  for (int i = threadIdx.x; i < nf * 256; i += blockDim.x) sc[i >> 8][i & 255] = cuts[(size_t)(f0 + (i >> 8)) * 256 + (i & 255)];
+  if (threadIdx.x < nf) snc[threadIdx.x] = ncuts[f0 + threadIdx.x];
+  __syncthreads();
+  const size_t total = (size_t)n * nf;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = e / nf;
+    const int fl = (int)(e - r * nf);
+    const double x = X[r * p + f0 + fl];
+    int lo = 0, hi = snc[fl];  // first index with c[idx] >= x
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (c[mid] < x) lo = mid + 1; else hi = mid;
+      if (sc[fl][mid] < x) lo = mid + 1; else hi = mid;
     }
-    bins[i] = (uint8_t)lo;
+    bins[r * p + f0 + fl] = (uint8_t)lo;
   }
 }
 
@@ -855,7 +928,10 @@ __global__ void k_hist_zero(Batch b, int cur, int g0, int g1, uint32_t* hW, unsi
 // atomics, 18 ms per C4 tree; a warp bitonic sort + segmented sums, 1.8x slower still; the
 // per-row shuffles of the record instead of the staged broadcast, 41 instructions per row.)
 constexpr int kHistBins = 257;       // bins per feature histogram in shared memory (256 + pad)
-constexpr int kHistRowsAhead = 8;    // bin-row gathers issued before their atomics
+#ifndef RF_HIST_AHEAD
+#define RF_HIST_AHEAD 16
+#endif
+constexpr int kHistRowsAhead = RF_HIST_AHEAD;  // bin-row gathers issued before their atomics
 
 __global__ void __launch_bounds__(kHistThreads, 2) k_hist_build(Batch b, int cur, int g0, int g1,
                                                                 const uint32_t* itemPref, uint32_t* hW,
@@ -878,20 +954,35 @@ __global__ void __launch_bounds__(kHistThreads, 2) k_hist_build(Batch b, int cur
   const int t = (int)nd.tree[g];
   const uint32_t start = nd.start[g], len = nd.len[g];
   const uint32_t i0 = c * kHistChunk, i1 = min(len, i0 + (uint32_t)kHistChunk);
+  __shared__ long long sTmin, sTmax;  // t_q range of the chunk's rows (node constancy, R11)
   for (int i = threadIdx.x; i < 3 * m * kHistBins; i += blockDim.x) hist[i] = 0u;
   for (int j = threadIdx.x; j < m; j += blockDim.x) sF[j] = b.feat[(size_t)g * m + j];
+  if (threadIdx.x == 0) { sTmin = LLONG_MAX; sTmax = LLONG_MIN; }
   __syncthreads();
+  long long tmin = LLONG_MAX, tmax = LLONG_MIN;
   const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr + start;
   const uint8_t* w = b.w + (size_t)t * b.n;
+  const long long* wt = b.wt ? b.wt + (size_t)t * b.n : nullptr;
   const uint32_t p = (uint32_t)b.p;  // host guarantees n * p < 2^32 (32-bit bin-row offsets)
   const int ngrp = (m + 31) >> 5;    // feature groups of 32 lanes (m <= 73 by the smem limit)
   for (uint32_t base = i0 + 32u * warp; base < i1; base += 32u * nwarp) {
     const uint32_t i = base + lane;
     if (i < i1) {
       const uint32_t r = L[i];
-      const uint32_t wv = w[r];
-      const unsigned long long v = (unsigned long long)((long long)wv * b.tq[r]);
+      uint32_t wv;
+      long long tv;
+      if (wt) {  // one 8-byte gather: (t_q << 8) | w
+        const long long pk = wt[r];
+        wv = (uint32_t)(pk & 0xFF);
+        tv = pk >> 8;
+      } else {
+        wv = w[r];
+        tv = b.tq[r];
+      }
+      const unsigned long long v = (unsigned long long)((long long)wv * tv);
       stage[lane] = make_uint4(r * p, wv, (uint32_t)v, (uint32_t)(v >> 32));
+      tmin = min(tmin, tv);
+      tmax = max(tmax, tv);
     }
     __syncwarp();
     const int nk = (int)min(32u, i1 - base);
@@ -901,15 +992,17 @@ __global__ void __launch_bounds__(kHistThreads, 2) k_hist_build(Batch b, int cur
       const uint8_t* bcol = b.bins + (act ? sF[j] : 0);
       uint32_t* hj = hist + (size_t)(act ? j : 0) * kHistBins * 3;
       for (int k0 = 0; k0 < nk; k0 += kHistRowsAhead) {
-        uint32_t bn[kHistRowsAhead];
+        uint32_t bn[kHistRowsAhead / 4];  // the gathered bins, four per register
+#pragma unroll
+        for (int q = 0; q < kHistRowsAhead / 4; ++q) bn[q] = 0u;
 #pragma unroll
         for (int q = 0; q < kHistRowsAhead; ++q)
-          bn[q] = (act && k0 + q < nk) ? (uint32_t)bcol[stage[k0 + q].x] : 0u;
+          if (act && k0 + q < nk) bn[q >> 2] |= (uint32_t)bcol[stage[k0 + q].x] << (8 * (q & 3));
 #pragma unroll
         for (int q = 0; q < kHistRowsAhead; ++q) {
           if (act && k0 + q < nk) {
             const uint4 e = stage[k0 + q];
-            uint32_t* cb = hj + 3 * bn[q];
+            uint32_t* cb = hj + 3 * ((bn[q >> 2] >> (8 * (q & 3))) & 0xFFu);
             atomicAdd(cb, e.y);
             const uint32_t old = atomicAdd(cb + 1, e.z);
             const uint32_t add = e.w + (old > ~e.z ? 1u : 0u);  // carry out of the low word
@@ -920,7 +1013,20 @@ __global__ void __launch_bounds__(kHistThreads, 2) k_hist_build(Batch b, int cur
     }
     __syncwarp();  // the records are read before the next batch overwrites them
   }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, d));
+    tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+  }
+  if (lane == 0 && tmin != LLONG_MAX) {
+    atomicMin(&sTmin, tmin);
+    atomicMax(&sTmax, tmax);
+  }
   __syncthreads();
+  if (threadIdx.x == 0 && sTmin != LLONG_MAX) {
+    atomicMin(&b.cmm[4 * g], sTmin);
+    atomicMax(&b.cmm[4 * g + 1], sTmax);
+  }
   const size_t obase = (size_t)(g - g0) * m * 256;
   const bool single = len <= (uint32_t)kHistChunk;
   for (int idx = threadIdx.x; idx < m * 256; idx += blockDim.x) {
@@ -951,9 +1057,13 @@ __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int
   const Nodes& nd = b.nd[cur];
   const unsigned long long Wt = nd.W[g];
   const long long St = nd.S[g];
-  unsigned long long bk = 0ull, ba = ~0ull;
+  unsigned long long bk = 0ull, ba = ~0ull, bw = 0ull, bs = 0ull;  // best key, aux, left W, left S
   unsigned int nc = 0;
-  for (int j = warp; j < b.m; j += 8) {
+  // constant target (R11; t_q range from k_hist_build): a leaf, no candidate is searched.  The
+  // children of a split are opened without a constancy pass (that needed a t_q gather per row);
+  // a constant child is recognised here, one level later, with the same leaf value and BFS slot
+  const bool constant = b.cmm[4 * g] == b.cmm[4 * g + 1];
+  for (int j = constant ? b.m : warp; j < b.m; j += 8) {
     const int f = b.feat[(size_t)g * b.m + j];
     const int ncut = b.ncuts[f];
     const size_t base = ((size_t)(g - g0) * b.m + j) * 256 + 8 * lane;
@@ -988,7 +1098,7 @@ __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int
         const unsigned long long key = (unsigned long long)__double_as_longlong(G) + 1ull;
         const unsigned long long aux = cand_aux(b, j, f, (unsigned)cidx);  // R9
         ++nc;
-        if (better(key, aux, bk, ba)) { bk = key; ba = aux; }
+        if (better(key, aux, bk, ba)) { bk = key; ba = aux; bw = cw; bs = cs; }
       }
     }
   }
@@ -996,15 +1106,21 @@ __global__ void __launch_bounds__(256) k_hist_best(Batch b, int cur, int g0, int
   for (int d = 16; d > 0; d >>= 1) {
     const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, d);
     const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ba, d);
-    if (better(ok, oa, bk, ba)) { bk = ok; ba = oa; }
+    const unsigned long long ow = __shfl_xor_sync(0xffffffffu, bw, d);
+    const unsigned long long os = __shfl_xor_sync(0xffffffffu, bs, d);
+    if (better(ok, oa, bk, ba)) { bk = ok; ba = oa; bw = ow; bs = os; }
   }
-  __shared__ unsigned long long sk[8], sa[8];
-  if (lane == 0) { sk[warp] = bk; sa[warp] = ba; }
+  __shared__ unsigned long long sk[8], sa[8], sw[8], ss[8];
+  if (lane == 0) { sk[warp] = bk; sa[warp] = ba; sw[warp] = bw; ss[warp] = bs; }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w2 = 1; w2 < 8; ++w2)
-      if (better(sk[w2], sa[w2], bk, ba)) { bk = sk[w2]; ba = sa[w2]; }
+      if (better(sk[w2], sa[w2], bk, ba)) { bk = sk[w2]; ba = sa[w2]; bw = sw[w2]; bs = ss[w2]; }
     b.best[g] = Best{bk, bk ? ba : ~0ull};
+    if (bk) {  // the winner's left child sums straight from its histogram prefix (no row pass)
+      b.accW[g] = (uint32_t)bw;
+      b.accS[g] = bs;
+    }
   }
   if (ncand) {
     unsigned long long v = nc;
@@ -1023,67 +1139,6 @@ __global__ void k_decide_hist(Batch b, int NO) {
   b.thr[g] = b.cuts[(size_t)f * 256 + c];
   b.thrIdx[g] = (uint32_t)c;
   b.best[g].aux = ((unsigned long long)f << 32) | (unsigned long long)c;  // slot -> feature
-}
-
-// positions: go-left flags (bin <= cut), left count and sums, child t_q min / max
-__global__ void k_mark_hist(Batch b, int cur, int NP) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  const Nodes& nd = b.nd[cur];
-  int g = -1;
-  unsigned int cnt = 0, wl = 0;
-  unsigned long long sl = 0;
-  long long mnL = LLONG_MAX, mxL = LLONG_MIN, mnR = LLONG_MAX, mxR = LLONG_MIN;
-  if (q < NP) {
-    g = (int)b.posNode[cur][q];
-    const Best bs = b.best[g];
-    if (bs.key) {
-      const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), c = (int)(bs.aux & 0xFFFFFFFFull);
-      const int start = (int)nd.start[g];
-      const int i = q - (int)b.tPos0[t] - start;
-      const uint32_t r = b.L[cur & 1][(size_t)t * b.ntr + start + i];
-      const bool left = b.bins[(size_t)r * b.p + f] <= c;
-      b.side[(size_t)t * b.n + r] = left ? 1 : 0;
-      const long long tv = b.tq[r];
-      if (left) {
-        cnt = 1;
-        wl = b.w[(size_t)t * b.n + r];
-        sl = (unsigned long long)((long long)wl * tv);
-        mnL = mxL = tv;
-      } else {
-        mnR = mxR = tv;
-      }
-    } else {
-      g = -1;
-    }
-  }
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int og = __shfl_down_sync(0xffffffffu, g, d);
-    const unsigned int oc = __shfl_down_sync(0xffffffffu, cnt, d);
-    const unsigned int ow = __shfl_down_sync(0xffffffffu, wl, d);
-    const unsigned long long os = __shfl_down_sync(0xffffffffu, sl, d);
-    const long long a0 = __shfl_down_sync(0xffffffffu, mnL, d), a1 = __shfl_down_sync(0xffffffffu, mxL, d);
-    const long long a2 = __shfl_down_sync(0xffffffffu, mnR, d), a3 = __shfl_down_sync(0xffffffffu, mxR, d);
-    if (lane + d < 32 && og == g) {
-      cnt += oc; wl += ow; sl += os;
-      mnL = min(mnL, a0); mxL = max(mxL, a1); mnR = min(mnR, a2); mxR = max(mxR, a3);
-    }
-  }
-  const int pg = __shfl_up_sync(0xffffffffu, g, 1);
-  if (g >= 0 && (lane == 0 || pg != g)) {
-    if (cnt) {
-      atomicAdd(&b.accN[g], cnt);
-      atomicAdd(&b.accW[g], wl);
-      atomicAdd(&b.accS[g], sl);
-      atomicMin(&b.cmm[4 * g], mnL);
-      atomicMax(&b.cmm[4 * g + 1], mxL);
-    }
-    if (mnR != LLONG_MAX) {
-      atomicMin(&b.cmm[4 * g + 2], mnR);
-      atomicMax(&b.cmm[4 * g + 3], mxR);
-    }
-  }
 }
 
 __global__ void k_hist_reset(Batch b, int NO) {
@@ -1107,8 +1162,9 @@ __global__ void k_children_count(Batch b, int cur, int NO, int depth) {
     const uint32_t nl = b.hist ? b.accN[g] : (uint32_t)(bs.aux & 0xFFFFFFFFull) + 1u;
     const uint32_t lenL = nl, lenR = nd.len[g] - nl;
     const bool capd = (b.max_depth >= 0) && (depth + 1 >= b.max_depth);
-    const bool ncL = b.hist ? (b.cmm[4 * g] != b.cmm[4 * g + 1]) : (b.nc[2 * g] != 0);
-    const bool ncR = b.hist ? (b.cmm[4 * g + 2] != b.cmm[4 * g + 3]) : (b.nc[2 * g + 1] != 0);
+    // histogram mode: constancy of a child is found at the next level (k_hist_best)
+    const bool ncL = b.hist ? true : (b.nc[2 * g] != 0);
+    const bool ncR = b.hist ? true : (b.nc[2 * g + 1] != 0);
     const bool oL = !capd && (int)lenL >= b.mss && ncL;
     const bool oR = !capd && (int)lenR >= b.mss && ncR;
     v.sp = 1u;
@@ -1250,9 +1306,97 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(Batch b, int cur, c
   if (threadIdx.x == 0) tileCnt[blockIdx.x] = tot;
 }
 
+// histogram mode, fused into the partition's count pass (a separate go-left pass with per-warp
+// global atomics and t_q gathers for the children's constancy was 41 % of a C4 fit, rd2_06:
+// every warp of a top-level node hit the same few counters): per tile of kPartTile positions
+// of the single row list, the go-left decision bin(x_f) <= cut from the row's bins, the
+// decisions as one byte per thread for the scatter, the tile's left count for the scatter's
+// scan, and per split node its distinct left rows (per-thread runs, a warp segmented sum, a CTA
+// table of the tile's first 32 nodes, one global atomic per node and CTA).  The children's
+// (W, S) come from k_hist_best's histogram prefix; their constancy from the next level's build.
+__global__ void __launch_bounds__(kPartThreads) k_part_count_hist(Batch b, int cur, const uint32_t* tileTab,
+                                                                  uint32_t* tileCnt, uint8_t* leftBits) {
+  int t, f, k;
+  part_locate(b, tileTab, blockIdx.x, t, f, k);
+  const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
+  const uint32_t* L = b.L[cur & 1] + (size_t)t * b.ntr;
+  const uint32_t* posNode = b.posNode[cur];
+  __shared__ unsigned int sN[32];
+  __shared__ int sG0;
+  if (threadIdx.x < 32) sN[threadIdx.x] = 0u;
+  const uint32_t tile0 = (uint32_t)k * kPartTile;
+  if (threadIdx.x == 0) sG0 = tile0 < N ? (int)posNode[pos0 + tile0] : 0;
+  __syncthreads();
+  const int g0 = sG0;
+  int rg = -1;  // this thread's current run (node) and its left rows
+  unsigned int rc = 0;
+  auto flush = [&](int g) {  // into the CTA table, or global for nodes beyond it
+    if (g < 0 || !rc) return;
+    const int sl = g - g0;
+    if (sl >= 0 && sl < 32) atomicAdd(&sN[sl], rc);
+    else atomicAdd(&b.accN[g], rc);
+  };
+  uint32_t c = 0, bits = 0;
+  const uint32_t i0 = tile0 + threadIdx.x * kPartItems;
+  // the thread's loads in three independent rounds (node ids and rows, split rules, bins) so
+  // kPartItems gathers of each round are in flight at once
+  int gg[kPartItems];
+  uint32_t rr[kPartItems], fc[kPartItems];
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    const uint32_t i = i0 + it;
+    gg[it] = i < N ? (int)posNode[pos0 + i] : -1;
+    rr[it] = i < N ? L[i] : 0u;
+  }
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    fc[it] = 0xFFFFFFFFu;  // feature << 16 | cut, or none (unsplit node / past the end)
+    if (gg[it] >= 0) {
+      const Best bs = b.best[gg[it]];
+      if (bs.key) fc[it] = (uint32_t)((bs.aux >> 32) << 16) | (uint32_t)(bs.aux & 0xFFFFull);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it)
+    if (fc[it] != 0xFFFFFFFFu)
+      bits |= ((uint32_t)b.bins[(size_t)rr[it] * b.p + (fc[it] >> 16)] <= (fc[it] & 0xFFFFu) ? 1u : 0u) << it;
+#pragma unroll
+  for (int it = 0; it < kPartItems; ++it) {
+    if (fc[it] == 0xFFFFFFFFu) continue;
+    const int g = gg[it];
+    const bool left = (bits >> it) & 1u;
+    if (g != rg) {
+      flush(rg);
+      rg = g;
+      rc = 0;
+    }
+    rc += left ? 1u : 0u;
+    c += left ? 1u : 0u;
+  }
+  // the threads' last runs: warp segmented sum over equal nodes (positions of a node are
+  // contiguous, so equal-node lanes are adjacent), run heads flush
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int og = __shfl_down_sync(0xffffffffu, rg, d);
+    const unsigned int oc = __shfl_down_sync(0xffffffffu, rc, d);
+    if (lane + d < 32 && og == rg) rc += oc;
+  }
+  const int pg = __shfl_up_sync(0xffffffffu, rg, 1);
+  if (rg >= 0 && (lane == 0 || pg != rg)) flush(rg);
+  leftBits[(size_t)blockIdx.x * kPartThreads + threadIdx.x] = (uint8_t)bits;  // read by the scatter
+  using BR = cub::BlockReduce<uint32_t, kPartThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint32_t tot = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) tileCnt[blockIdx.x] = tot;
+  __syncthreads();
+  if (threadIdx.x < 32 && sN[threadIdx.x]) atomicAdd(&b.accN[g0 + (int)threadIdx.x], sN[threadIdx.x]);
+}
+
 __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur, const uint32_t* tileTab,
                                                                const uint32_t* tilePref, const uint32_t* nextPos0,
-                                                               const uint32_t* nlBase, int debug_rows) {
+                                                               const uint32_t* nlBase, int debug_rows,
+                                                               const uint8_t* leftBits) {
   int t, f, k;
   part_locate(b, tileTab, blockIdx.x, t, f, k);
   const Nodes& nd = b.nd[cur];
@@ -1268,6 +1412,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
   const uint32_t i0 = (uint32_t)k * kPartTile + threadIdx.x * kPartItems;
   uint32_t rr[kPartItems], gg[kPartItems];
   uint32_t flags = 0, c = 0;  // bit 2it: split node, bit 2it+1: left
+  // histogram mode: the go-left bits of this thread's positions from the count pass
+  const uint32_t lb8 = leftBits ? leftBits[(size_t)blockIdx.x * kPartThreads + threadIdx.x] : 0u;
 #pragma unroll
   for (int it = 0; it < kPartItems; ++it) {
     const uint32_t i = i0 + it;
@@ -1278,8 +1424,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(Batch b, int cur,
       const uint32_t r = L[i];
       gg[it] = g;
       rr[it] = r;
-      if (b.best[g].key) {
-        const uint32_t lf = side[r & b.rowMask];
+      const Best bs = b.best[g];
+      if (bs.key) {
+        const uint32_t lf = leftBits ? ((lb8 >> it) & 1u) : side[r & b.rowMask];
         flags |= (1u | (lf << 1)) << (2 * it);
         c += lf;
       }
@@ -1534,6 +1681,7 @@ struct PartBufs {  // per-level scratch: search look-back status, partition tile
   uint4* desc = nullptr;     // [npmax] per-position split descriptors (fused path)
   uint32_t* tab = nullptr;   // [2 B]
   uint32_t* cnt = nullptr;   // [max tiles]
+  uint8_t* leftBits = nullptr;  // histogram mode: [max tiles][kPartThreads] go-left bits of 8 positions
   uint32_t* pref = nullptr;  // [max tiles]
 };
 
@@ -1546,7 +1694,7 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   const size_t plSmem = (size_t)b.nbw * 4;
   std::unique_ptr<ProfScope> setup_scope(new ProfScope("large_tree_setup", s));  // bootstrap, in-bag lists, root statistics
   LCK(cudaMemsetAsync(b.w, 0, (size_t)b.B * b.n, s));
-  LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
+  if (b.side) LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
   if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
   {
     dim3 g(nblk((b.ntr + 1) / 2, 256) > 64 ? 64 : nblk((b.ntr + 1) / 2, 256), b.B);
@@ -1599,6 +1747,17 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   int cur = 0, depth = 0;
   while (NO > 0) {
     note_row_levels(NP);
+    // tile table of the tiled partition (per-tree position counts read back at the level start)
+    uint32_t tiles = 0;
+    if (!b.sideBits) {
+      for (int t = 0; t < b.B; ++t) {
+        const uint32_t Nt = htPos0[t + 1] - htPos0[t];
+        const uint32_t per = (Nt + kPartTile - 1) / kPartTile;
+        htab[2 * t] = tiles;
+        htab[2 * t + 1] = per ? per : 1u;
+        tiles += per * (uint32_t)b.nl;
+      }
+    }
     k_node_prep<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO);
     note_launch();
     if (b.extra) {
@@ -1645,10 +1804,15 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
           note_launch(3);
         }
       }
-      ProfScope pm("hist_mark", s);
       k_decide_hist<<<nblk(NO, 128), 128, 0, s>>>(b, (int)NO);
-      k_mark_hist<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
-      note_launch(2);
+      note_launch();
+      // partition count pass, fused with the children's row counts and constancy (k_part_count_hist)
+      ProfScope pm("hist_count", s);
+      if (tiles > 0) {
+        LCK(cudaMemcpyAsync(pb.tab, htab, (size_t)2 * b.B * 4, cudaMemcpyHostToDevice, s));
+        k_part_count_hist<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.cnt, pb.leftBits);
+        note_launch();
+      }
     }
     std::unique_ptr<ProfScope> ch_scope(new ProfScope("large_children", s));
     k_children_count<<<nblk(NO, 128), 128, 0, s>>>(b, cur, (int)NO, depth);
@@ -1672,23 +1836,17 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       note_launch();
     } else {
       ProfScope ps("large_partition", s);
-      // tile table of the current level (per-tree position counts read back at the level start)
-      uint32_t tiles = 0;
-      for (int t = 0; t < b.B; ++t) {
-        const uint32_t Nt = htPos0[t + 1] - htPos0[t];
-        const uint32_t per = (Nt + kPartTile - 1) / kPartTile;
-        htab[2 * t] = tiles;
-        htab[2 * t + 1] = per ? per : 1u;
-        tiles += per * (uint32_t)b.nl;
-      }
       if (tiles > 0) {
-        LCK(cudaMemcpyAsync(pb.tab, htab, (size_t)2 * b.B * 4, cudaMemcpyHostToDevice, s));
-        k_part_count<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.cnt);
+        if (!b.hist) {  // (histogram mode: counted above, k_part_count_hist)
+          LCK(cudaMemcpyAsync(pb.tab, htab, (size_t)2 * b.B * 4, cudaMemcpyHostToDevice, s));
+          k_part_count<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.cnt);
+          note_launch();
+        }
         tb = cub_bytes;
         LCK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, pb.cnt, pb.pref, (int)tiles, s));
         k_part_scatter<<<tiles, kPartThreads, 0, s>>>(b, cur, pb.tab, pb.pref, nextPos0, nlBase,
-                                                       b.leaf_of_row ? 1 : 0);
-        note_launch(2);
+                                                       b.leaf_of_row ? 1 : 0, b.hist ? pb.leftBits : nullptr);
+        note_launch();
       }
     }
     k_set_next_tree_tables<<<nblk(b.B + 1, 64), 64, 0, s>>>(b, nextNode0, nextPos0, counters);
@@ -1868,8 +2026,15 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&bins, (size_t)n * p));
     {
       ProfScope ps("hist_binning", s);
-      k_cuts<<<p, 256, 0, s>>>(d.X, p, task_order, ntr, cuts, ncuts);
-      k_bins<<<std::min<unsigned>(nblk((long long)n * p, 256), 148 * 32), 256, 0, s>>>(d.X, n, p, cuts, ncuts, bins);
+      const int nch = (ntr + kCutChunk - 1) / kCutChunk;
+      uint32_t* ccnt;
+      LCK(sc.alloc(&ccnt, (size_t)nch * p + p));  // chunk counts -> offsets, then D per feature
+      k_cut_count<<<dim3((unsigned)nch, (unsigned)p), 256, 0, s>>>(d.X, p, task_order, ntr, ccnt);
+      k_cut_finish<<<p, 256, 0, s>>>(d.X, p, task_order, ntr, ccnt, nch, cuts, ncuts);
+      k_cut_collect<<<dim3((unsigned)nch, (unsigned)p), 256, 0, s>>>(d.X, p, task_order, ntr, ccnt, ncuts, cuts);
+      note_launch(2);
+      k_bins<<<dim3(std::min<unsigned>(nblk((long long)n * kBinFeat, 256), 148 * 8), (unsigned)((p + kBinFeat - 1) / kBinFeat)),
+               256, 0, s>>>(d.X, n, p, cuts, ncuts, bins);
       note_launch(2);
     }
     b.cuts = cuts;
@@ -1903,8 +2068,8 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.tr_rows = tr_rows_in;
   LCK(sc.alloc(&b.keys, (size_t)2 * B));
   LCK(sc.alloc(&b.w, (size_t)B * n + 4));
-  if (!hist && n > 256) LCK(sc.alloc(&b.wt, (size_t)B * n));
-  LCK(sc.alloc(&b.side, (size_t)B * n));
+  if (n > 256) LCK(sc.alloc(&b.wt, (size_t)B * n));  // packed (t_q << 8) | w gathers
+  if (!hist) LCK(sc.alloc(&b.side, (size_t)B * n));  // histogram mode decides from the bins
   // fused partition path (exact / ExtraTrees): go-left bits per row, staged per tree in
   // shared memory by the partition CTAs (n <= 2^20 rows: <= 128 KB)
   b.nbw = (n + 31) / 32;
@@ -1967,6 +2132,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(allow_max_dynamic_smem(k_part_lists_warp));
   }
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
+  if (hist) LCK(sc.alloc(&pbufs.leftBits, (size_t)max_tiles * kPartThreads));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
   struct HostFree {
     uint32_t* p;
