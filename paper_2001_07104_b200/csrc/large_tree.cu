@@ -1770,11 +1770,11 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       note_launch();
       LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)NO, s));
       const long long E = (long long)b.m * NP;
-      const long long tiles = (E + kTile - 1) / kTile;
       {
         ProfScope ps("large_search", s);
         const uint32_t epoch = ++*pb.epoch;
         LCK(cudaMemsetAsync(pb.tileCtr, 0, 4, s));
+        const long long tiles = (E + kTile - 1) / kTile;
         k_search_fused<<<(unsigned)tiles, kThreads, 0, s>>>(b, cur, E, ncand, pb.tileCtr, pb.stat, pb.flags, epoch);
         note_launch();
       }

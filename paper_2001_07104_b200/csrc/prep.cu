@@ -7,7 +7,9 @@
 //     of x over all n rows (threshold index, R10).  Small n: one CTA per
 //     feature ranks by counting in shared memory; large n: CUB segmented
 //     radix sort of order-preserving u64 keys + a per-feature rank scan.
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include "common.cuh"
 #include "host_util.cuh"
 #include "ddlog.cuh"
@@ -185,11 +187,23 @@ cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int t
 size_t presort_ws_bytes(int n, int p) {
   if (n <= kSmallSortMax) return 0;
   const size_t total = (size_t)n * p;
-  size_t temp = 0;
+  size_t temp = 0, temp2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, temp, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, n);
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp2, (const unsigned long long*)nullptr,
+                                           (unsigned long long*)nullptr, (const uint32_t*)nullptr,
+                                           (uint32_t*)nullptr, (int64_t)total, p, (const int64_t*)nullptr,
+                                           (const int64_t*)nullptr);
+  temp = std::max(temp, temp2);
   return total * (8 + 8 + 4) + (size_t)(p + 1) * 8 + temp + 256;  // keys x2, values, offsets, CUB temp
 }
+
+namespace {
+__global__ void k_seg_offsets(int64_t* off, int p, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= p) off[i] = (int64_t)i * n;
+}
+}  // namespace
 
 cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int n = d.n, p = d.p;
@@ -211,13 +225,22 @@ cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
   size_t temp_bytes = ws_bytes - (size_t)(temp - w);
   k_make_keys<<<148 * 8, 256, 0, s>>>(d.X, n, p, kin, vin);
   note_launch();
-  // one device-wide radix sort per feature (each column is long: CUB's segmented sort gives a
-  // segment to one CTA, which left the GPU idle -- 190 ms for C4's 64 x 10M keys, rd2_06)
-  for (int f = 0; f < p; ++f) {
-    size_t tb = temp_bytes;
-    const size_t o = (size_t)f * n;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, tb, kin + o, kout + o, vin + o, d.order + o, n, 0, 64, s);
+  k_seg_offsets<<<(p + 1 + 127) / 128, 128, 0, s>>>(offs, p, n);
+  note_launch();
+  // long columns: one device-wide radix sort per feature (CUB's segmented sort gives a segment
+  // to one CTA, which left the GPU idle -- 190 ms for C4's 64 x 10M keys, rd2_06); short ones:
+  // the segmented sort (64 separate sorts of 100k keys took 8 ms against its 2 ms)
+  if (n < (1 << 20)) {
+    cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, d.order,
+                                                             (int64_t)total, p, offs, offs + 1, 0, 64, s);
     if (e != cudaSuccess) return e;
+  } else {
+    for (int f = 0; f < p; ++f) {
+      size_t tb = temp_bytes;
+      const size_t o = (size_t)f * n;
+      cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, tb, kin + o, kout + o, vin + o, d.order + o, n, 0, 64, s);
+      if (e != cudaSuccess) return e;
+    }
   }
   k_rank_sorted<<<p, 1024, 0, s>>>(kout, d.order, n, d.grank);
   note_launch();
