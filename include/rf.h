@@ -79,8 +79,10 @@ typedef enum { RF_TARGET_IDENTITY = 0, RF_TARGET_LOG = 1 } rf_target;
    in Tables 4/5): a split minimises the summed weighted absolute
    deviations of the children from their weighted medians, leaves hold the
    weighted median (R32).  MAE is implemented for the exact and ExtraTrees
-   split modes on the CTA-resident path (training sets of <= 255 rows, p <= 64;
-   the paper's datasets have 189 / 168 rows); other shapes return
+   split modes on both paths: the CTA-resident kernel (training sets of <= 255
+   rows, p <= 64; the paper's datasets have 189 / 168 rows) and the
+   level-synchronous one up to 12,288 training rows (the paper's n = 4,096
+   sensitivity variant); histogram mode and larger training sets return
    RF_E_UNSUPPORTED.  Under MAE the targets are quantised with 2 guard bits
    (F = 62 - ceil(log2 n) - e - 2) so doubled medians and doubled absolute-
    deviation sums are exact integers below 2^63. */

@@ -284,8 +284,6 @@ rf_status cv_core(const double* dX, uint64_t n, uint32_t p, const double* dy, co
     }
     if (best_wpb == 0) large = true;
   }
-  if (large && a.mae)
-    return fail(RF_E_UNSUPPORTED, "MAE criterion: training sets of <= 255 rows and p <= 64 only (R32)");
   if (large) {
     for (int c = 32; c >= 1; --c)
       if (g % c == 0) { Cw = c; break; }
@@ -474,9 +472,6 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
       cudaError_t e = rf::launch_small_tree(a, s);
       if (e != cudaSuccess) return cuda_fail(e, "small_tree fit");
     }
-  }
-  if (!small && prm->criterion == RF_CRITERION_MAE) {
-    return fail(RF_E_UNSUPPORTED, "MAE criterion: training sets of <= 255 rows and p <= 64 only (R32)");
   }
   if (!small) {
     rf_status ls = rf::fit_large(d, prm, (int)mtry, tree_lo, tree_hi, s, sc, &nodes_w, &tidx_w, &nn_d,

@@ -30,6 +30,7 @@
 // Per-level sizes are read back once per round (one small D2H).
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -113,6 +114,8 @@ struct Batch {
   int hist;                 // 256-bin histogram split mode (R23)
   int extra;                // ExtraTrees split mode (R29)
   int tie_draw;             // tie-break (R9): 0 lowest feature index (north_star), 1 first drawn
+  int mae;                  // MAE criterion (R32): list p holds the in-bag rows in t_q order
+  int64_t* med2;            // [NMAX][2] MAE: doubled weighted medians of the children (or the node)
   uint32_t* xb;             // [NMAX][m] ExtraTrees: boundary index in the (node, slot) segment or ~0
   const uint8_t* bins;      // [n][p] bin of every row (histogram mode)
   const double* cuts;       // [p][256] cut values (histogram mode)
@@ -229,7 +232,7 @@ __global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /
     if (j < b.ntr) { r = src[j]; keep = w[r] != 0; }
     uint32_t ex, tot;
     BS(tmp).ExclusiveSum(keep, ex, tot);
-    if (keep) dst[carry + ex] = b.packRank ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
+    if (keep) dst[carry + ex] = (b.packRank && f < b.p) ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(kIbThreads) k_inbag_scatter(Batch b, const uin
   for (int q = 0; q < kIbItems; ++q) {
     if ((keep >> q) & 1u) {
       const uint32_t r = rr[q];
-      dst[o++] = b.packRank ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
+      dst[o++] = (b.packRank && f < b.p) ? r | ((b.grank[(size_t)f * b.n + r] & 0x7FFFu) << 17) : r;
     }
   }
 }
@@ -403,7 +406,7 @@ __global__ void k_extra_bounds(Batch b, int cur, long long NQ) {
   const Nodes& nd = b.nd[cur];
   const int t = (int)nd.tree[g], f = b.feat[q];
   const uint32_t len = nd.len[g];
-  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr + nd.start[g];
   const double* Xf = b.X + f;
   const double lo = Xf[(size_t)(L[0] & b.rowMask) * b.p], hi = Xf[(size_t)(L[len - 1] & b.rowMask) * b.p];
   uint32_t bnd = ~0u;
@@ -444,7 +447,7 @@ __device__ __forceinline__ void cursor_load(const Batch& b, const Nodes& nd, Cur
 }
 __device__ __forceinline__ void cursor_feat(const Batch& b, Cursor& c) {
   c.f = b.feat[(size_t)c.g * b.m + c.j];
-  c.listBase = ((long long)c.t * b.p + c.f) * b.ntr + c.start;
+  c.listBase = ((long long)c.t * b.nl + c.f) * b.ntr + c.start;
   if (b.extra) c.xb = b.xb[(size_t)c.g * b.m + c.j];
 }
 // element e = m * gpos0(g) + j * len + i, gpos0 = concatenated first position of g
@@ -677,6 +680,237 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   }
 }
 
+// ------------------------------------------------------- MAE criterion (R32) ----
+// Level-synchronous MAE (SURVEY 8(f) NEXT-4 on training sets beyond the CTA-resident kernel:
+// the paper's n = 4,096 sensitivity variant).  Same candidates, tie-break, thresholds and
+// stopping as the MSE path (R8, R9, R29, R11); a candidate's cost is D = 2 (SAD_L + SAD_R), the
+// doubled weighted absolute deviations of the children from their weighted medians (exact in
+// uint64 under the 2 guard bits of quantisation), key = ~D so "larger key = better" and the
+// 128-bit node-best CAS apply unchanged.  Each tree carries one more row list (list p): its
+// in-bag rows in (t_q, row) order, partitioned with the feature lists.  A candidate's D is one
+// walk of the node's t-ordered rows that routes every row to the left or right tracker by
+// rank_f(row) <= rank_f(boundary row) and stops at both weighted medians (the small kernel's
+// MedTrack, scikit-learn's median rule).  One CTA per (node, draw slot): the node's t-ordered
+// (rank_f, w, t_q) are staged in shared memory once (nodes up to kMaeMaxLen distinct rows), the
+// candidates' (W_L, S_L) come from a chunked prefix of the feature-ordered segment, and each warp
+// walks the staged list for 32 candidates in lock step (broadcast shared loads).
+constexpr int kMaeMaxLen = 12288;
+constexpr int kMaeThreads = 256;
+
+struct LMed {  // weighted-median tracker (as small_tree.cu MedTrack)
+  uint32_t W, cum, Wk;
+  int64_t sum, Sk, m2;
+  int state;  // 0 searching, 1 waiting for t_k+1, 2 done
+};
+__device__ __forceinline__ void lmed_init(LMed& m, uint32_t W) {
+  m.W = W; m.cum = 0; m.Wk = 0; m.sum = 0; m.Sk = 0; m.m2 = 0; m.state = W ? 0 : 2;
+}
+__device__ __forceinline__ void lmed_push(LMed& m, uint32_t wv, int64_t t) {
+  if (m.state == 0) {
+    m.cum += wv;
+    m.sum += (int64_t)wv * t;
+    if (2u * m.cum >= m.W) {
+      m.Wk = m.cum; m.Sk = m.sum;
+      if (2u * m.cum == m.W) { m.m2 = t; m.state = 1; }
+      else { m.m2 = 2 * t; m.state = 2; }
+    }
+  } else if (m.state == 1) {
+    m.m2 += t;
+    m.state = 2;
+  }
+}
+__device__ __forceinline__ uint64_t lmed_sad2(const LMed& m, int64_t S) {  // sum w |2t - m2|
+  return (uint64_t)m.m2 * (uint64_t)(2u * m.Wk - m.W) + 2ull * (uint64_t)(S - 2 * m.Sk);
+}
+
+__device__ __forceinline__ void mae_row(const Batch& b, int t, uint32_t r, uint32_t& wv, long long& tv) {
+  if (b.wt) {
+    const long long v = b.wt[(size_t)t * b.n + r];
+    wv = (uint32_t)(v & 0xFF);
+    tv = v >> 8;
+  } else {
+    wv = b.w[(size_t)t * b.n + r];
+    tv = b.tq[r];
+  }
+}
+
+size_t mae_search_smem(int) { return (size_t)kMaeMaxLen * 13 + (size_t)(kMaeMaxLen / 32 + 1) * 16 + 64; }
+
+__global__ void __launch_bounds__(kMaeThreads) k_mae_search(Batch b, int cur, unsigned long long* ncand) {
+  extern __shared__ __align__(16) char msm[];
+  long long* tt = reinterpret_cast<long long*>(msm);                          // [len] t_q, t order
+  uint32_t* trk = reinterpret_cast<uint32_t*>(tt + kMaeMaxLen);               // [len] rank_f, t order
+  WS2* cpref = reinterpret_cast<WS2*>(trk + kMaeMaxLen);                       // [chunks] exclusive prefix
+  uint8_t* tw = reinterpret_cast<uint8_t*>(cpref + kMaeMaxLen / 32 + 1);       // [len] w, t order
+  __shared__ unsigned long long sk[kMaeThreads / 32], sa[kMaeThreads / 32];
+  const int g = blockIdx.x / b.m, j = blockIdx.x % b.m;
+  const Nodes& nd = b.nd[cur];
+  const int t = (int)nd.tree[g], len = (int)nd.len[g];
+  const int f = b.feat[(size_t)g * b.m + j];
+  const uint32_t W = nd.W[g];
+  const long long S = nd.S[g];
+  const uint32_t* Lf = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr + nd.start[g];
+  const uint32_t* Lt = b.L[cur & 1] + ((size_t)t * b.nl + b.p) * b.ntr + nd.start[g];
+  const uint32_t* rk = b.grank + (size_t)f * b.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kMaeThreads / 32;
+  const uint32_t xb = b.extra ? b.xb[(size_t)g * b.m + j] : 0u;
+  // stage the node's rows in t order; chunk totals of the feature-ordered segment
+  for (int s = threadIdx.x; s < len; s += kMaeThreads) {
+    const uint32_t r = Lt[s] & b.rowMask;
+    uint32_t wv;
+    long long tv;
+    mae_row(b, t, r, wv, tv);
+    tt[s] = tv;
+    tw[s] = (uint8_t)wv;
+    trk[s] = rk[r];
+  }
+  const int nch = (len + 31) >> 5;
+  for (int c = warp; c < nch; c += nw) {
+    const int i = c * 32 + lane;
+    uint32_t wv = 0;
+    long long tv = 0;
+    if (i < len) mae_row(b, t, Lf[i] & b.rowMask, wv, tv);
+    unsigned long long sw = wv, ss = (unsigned long long)((long long)wv * tv);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      sw += __shfl_xor_sync(0xffffffffu, sw, d);
+      ss += __shfl_xor_sync(0xffffffffu, ss, d);
+    }
+    if (lane == 0) cpref[c] = WS2{sw, ss};
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix over the chunks (<= 384)
+    unsigned long long aw = 0, as = 0;
+    for (int c = 0; c < nch; ++c) {
+      const WS2 v = cpref[c];
+      cpref[c] = WS2{aw, as};
+      aw += v.w;
+      as += v.s;
+    }
+  }
+  __syncthreads();
+  unsigned long long bk = 0ull, ba = ~0ull;
+  unsigned int nc = 0;
+  for (int c = warp; c < nch; c += nw) {
+    const int i = c * 32 + lane;
+    uint32_t r = 0, wv = 0, rki = 0;
+    long long tv = 0;
+    if (i < len) {
+      r = Lf[i] & b.rowMask;
+      mae_row(b, t, r, wv, tv);
+      rki = rk[r];
+    }
+    unsigned long long iw = wv, is = (unsigned long long)((long long)wv * tv);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long yw = __shfl_up_sync(0xffffffffu, iw, d);
+      const unsigned long long ys = __shfl_up_sync(0xffffffffu, is, d);
+      if (lane >= d) { iw += yw; is += ys; }
+    }
+    const WS2 cp = cpref[c];
+    const uint32_t WL = (uint32_t)(cp.w + iw);
+    const long long SL = (long long)(cp.s + is);
+    uint32_t rkn = __shfl_down_sync(0xffffffffu, rki, 1);
+    if (lane == 31 && i + 1 < len) rkn = rk[Lf[i + 1] & b.rowMask];
+    const bool cand = i + 1 < len && (b.extra ? (uint32_t)i == xb : rki != rkn);
+    nc += cand ? 1u : 0u;
+    // lock-step walk of the staged t-ordered rows for every candidate of the chunk
+    LMed mL, mR;
+    lmed_init(mL, cand ? WL : 0u);
+    lmed_init(mR, cand ? W - WL : 0u);
+    for (int s = 0; s < len; ++s) {
+      if (((s & 7) == 0) && !__any_sync(0xffffffffu, mL.state != 2 || mR.state != 2)) break;
+      const uint32_t rs = trk[s];
+      const uint32_t ws = tw[s];
+      const long long ts = tt[s];
+      if (rs <= rki) lmed_push(mL, ws, ts); else lmed_push(mR, ws, ts);
+    }
+    if (cand) {
+      const uint64_t D = lmed_sad2(mL, SL) + lmed_sad2(mR, S - SL);
+      const unsigned long long key = ~D, aux = cand_aux(b, j, f, (unsigned)i);
+      if (better(key, aux, bk, ba)) { bk = key; ba = aux; }
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, d);
+    const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ba, d);
+    if (better(ok, oa, bk, ba)) { bk = ok; ba = oa; }
+  }
+  if (lane == 0) { sk[warp] = bk; sa[warp] = ba; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < nw; ++w2)
+      if (better(sk[w2], sa[w2], bk, ba)) { bk = sk[w2]; ba = sa[w2]; }
+    if (bk) cas128(&b.best[g], bk, ba);
+  }
+  if (ncand) {
+    unsigned long long v = nc;
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0 && v) atomicAdd(ncand, v);
+  }
+}
+
+// After the mark pass: per open node, one walk of its t-ordered rows.  Split node: the weighted
+// medians of both children (their leaf values if they are not opened) and, in fit mode with
+// importance, SAD2(node) for the decrease (SAD2 - D) 2^(-F-1) (R30, R32); unsplit node: its own
+// median (leaf value).
+__global__ void k_mae_nodes(Batch b, int cur, int NO) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NO) return;
+  const Nodes& nd = b.nd[cur];
+  const int t = (int)nd.tree[g], len = (int)nd.len[g];
+  const uint32_t* Lt = b.L[cur & 1] + ((size_t)t * b.nl + b.p) * b.ntr + nd.start[g];
+  const Best bs = b.best[g];
+  const bool split = bs.key != 0ull;
+  LMed mL, mR, mA;
+  const uint32_t WL = split ? b.accW[g] : 0u;
+  lmed_init(mL, split ? WL : 0u);
+  lmed_init(mR, split ? nd.W[g] - WL : 0u);
+  lmed_init(mA, (!split || b.imp) ? nd.W[g] : 0u);
+  for (int s = 0; s < len; ++s) {
+    if (mL.state == 2 && mR.state == 2 && mA.state == 2) break;
+    const uint32_t r = Lt[s] & b.rowMask;
+    uint32_t wv;
+    long long tv;
+    mae_row(b, t, r, wv, tv);
+    if (split) {
+      const bool left = b.sideBits ? ((b.sideBits[(size_t)t * b.nbw + (r >> 5)] >> (r & 31u)) & 1u)
+                                   : (b.side[(size_t)t * b.n + r] != 0);
+      if (left) lmed_push(mL, wv, tv); else lmed_push(mR, wv, tv);
+    }
+    lmed_push(mA, wv, tv);
+  }
+  if (split) {
+    b.med2[2 * g] = mL.m2;
+    b.med2[2 * g + 1] = mR.m2;
+    if (b.imp) {
+      const uint64_t D = ~bs.key;
+      const int f = (int)(bs.aux >> 32);  // after k_decide: feature << 32 | position
+      atomicAdd(&b.imp[(size_t)t * b.p + f], scalbn(__ull2double_rn(lmed_sad2(mA, nd.S[g]) - D), -b.F - 1));
+    }
+  } else {
+    b.med2[2 * g] = mA.m2;
+  }
+}
+
+// trees whose root is a leaf: the weighted median of all in-bag rows (list p of the root level)
+__global__ void k_mae_root(Batch b, const uint32_t* rootInfo) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= b.B || !rootInfo[4 * t + 1]) return;
+  const uint32_t* Lt = b.L[0] + ((size_t)t * b.nl + b.p) * b.ntr;
+  const uint32_t D = rootInfo[4 * t];
+  LMed m;
+  lmed_init(m, (uint32_t)b.ntr);
+  for (uint32_t s = 0; s < D && m.state != 2; ++s) {
+    uint32_t wv;
+    long long tv;
+    mae_row(b, t, Lt[s] & b.rowMask, wv, tv);
+    lmed_push(m, wv, tv);
+  }
+  b.out[(size_t)t * b.cap].v = scalbn(__ll2double_rn(m.m2), -b.F - 1);
+}
+
 __global__ void k_decide(Batch b, int cur, int NO) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= NO) return;
@@ -685,7 +919,7 @@ __global__ void k_decide(Batch b, int cur, int NO) {
   if (!bs.key) return;
   const int j = (int)((bs.aux >> 48) & 0xFFull), i = (int)(bs.aux & 0xFFFFFFFFull);
   const int t = (int)nd.tree[g], f = b.feat[(size_t)g * b.m + j];
-  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + nd.start[g];
+  const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr + nd.start[g];
   const uint32_t ra = L[i] & b.rowMask, rb = L[i + 1] & b.rowMask;
   if (b.extra) {  // the drawn threshold of slot j (R29)
     const double lo = b.X[(size_t)(L[0] & b.rowMask) * b.p + f], hi = b.X[(size_t)(L[nd.len[g] - 1] & b.rowMask) * b.p + f];
@@ -711,7 +945,7 @@ __global__ void k_mark(Batch b, int cur, int NP) {
       const int t = (int)nd.tree[g], f = (int)(bs.aux >> 32), bi = (int)(bs.aux & 0xFFFFFFFFull);
       const int start = (int)nd.start[g];
       const int i = q - (int)b.tPos0[t] - start;
-      const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.p + f) * b.ntr + start;
+      const uint32_t* L = b.L[cur & 1] + ((size_t)t * b.nl + f) * b.ntr + start;
       const uint32_t r = L[i] & b.rowMask;
       const bool left = i <= bi;
       if (b.sideBits) {
@@ -1219,7 +1453,8 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
   if (!bs.key) {  // open node without any candidate split: leaf (R11)
     Node16 l;
     l.feat = -1; l.left = 0;
-    l.v = scalbn(__ddiv_rn(__ll2double_rn(nd.S[g]), __uint2double_rn(nd.W[g])), -b.F);
+    l.v = b.mae ? scalbn(__ll2double_rn(b.med2[2 * g]), -b.F - 1)  // weighted median (R32)
+                : scalbn(__ddiv_rn(__ll2double_rn(nd.S[g]), __uint2double_rn(nd.W[g])), -b.F);
     out[me] = l;
     outThr[me] = 0;
     return;
@@ -1241,7 +1476,7 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
   me_n.v = b.thr[g];
   out[me] = me_n;
   outThr[me] = b.thrIdx[g];
-  if (b.imp)  // feature importance (MDI, NEXT-3)
+  if (b.imp && !b.mae)  // feature importance (MDI, NEXT-3; MAE: k_mae_nodes)
     atomicAdd(&b.imp[(size_t)t * b.p + me_n.feat], mdi_decrease(WLv, SLv, WRv, SRv, b.F));
   uint32_t oi = sc.op;                             // global open index of the first child
   uint32_t ps = sc.pos - nextPos0[t];              // tree-local position of the first child
@@ -1251,7 +1486,8 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
     ++oi; ps += nl;
   } else {
     Node16 l; l.feat = -1; l.left = 0;
-    l.v = scalbn(__ddiv_rn(__ll2double_rn(SLv), __uint2double_rn(WLv)), -b.F);
+    l.v = b.mae ? scalbn(__ll2double_rn(b.med2[2 * g]), -b.F - 1)
+                : scalbn(__ddiv_rn(__ll2double_rn(SLv), __uint2double_rn(WLv)), -b.F);
     out[childBase] = l; outThr[childBase] = 0;
   }
   if (oR) {
@@ -1259,7 +1495,8 @@ __global__ void k_children_write(Batch b, int cur, int NO, const uint32_t* nextN
     nx.heap[oi] = 2ull * nd.heap[g] + 1ull; nx.bfs[oi] = childBase + 1;
   } else {
     Node16 l; l.feat = -1; l.left = 0;
-    l.v = scalbn(__ddiv_rn(__ll2double_rn(SRv), __uint2double_rn(WRv)), -b.F);
+    l.v = b.mae ? scalbn(__ll2double_rn(b.med2[2 * g + 1]), -b.F - 1)
+                : scalbn(__ddiv_rn(__ll2double_rn(SRv), __uint2double_rn(WRv)), -b.F);
     out[childBase + 1] = l; outThr[childBase + 1] = 0;
   }
   (void)nlBase;
@@ -1632,6 +1869,13 @@ __global__ void k_set_next_tree_tables(Batch b, const uint32_t* nextNode0, const
 // ============================================================ host driver ====
 namespace {
 
+// ordered keys of the training rows' t_q (MAE t-order list): signed -> unsigned order
+__global__ void k_tq_keys(const uint32_t* __restrict__ rows, const int64_t* __restrict__ tq, int ntr,
+                          unsigned long long* keys) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < ntr) keys[j] = (unsigned long long)tq[rows[j]] ^ 0x8000000000000000ull;
+}
+
 __global__ void k_iota(uint32_t* a, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = (uint32_t)i;
 }
@@ -1726,6 +1970,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     k_root_partial<<<dim3(cpt, (unsigned)b.B), 256, 0, s>>>(b, pb.rootAcc);
     k_root_finish<<<nblk(b.B, 128), 128, 0, s>>>(b, pb.rootAcc, rootInfo);
     note_launch(3);
+    if (b.mae) {  // root leaves hold the weighted median (R32)
+      k_mae_root<<<nblk(b.B, 64), 64, 0, s>>>(b, rootInfo);
+      note_launch();
+    }
   }
   if (b.leaf_of_row) {
     k_root_rows<<<dim3(32, b.B), 256, 0, s>>>(b, rootInfo);
@@ -1770,7 +2018,11 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       note_launch();
       LCK(cub::DeviceScan::ExclusiveScan(cub_tmp, tb, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)NO, s));
       const long long E = (long long)b.m * NP;
-      {
+      if (b.mae) {
+        ProfScope ps("large_mae_search", s);
+        k_mae_search<<<(unsigned)(NO * b.m), kMaeThreads, mae_search_smem(0), s>>>(b, cur, ncand);
+        note_launch();
+      } else {
         ProfScope ps("large_search", s);
         const uint32_t epoch = ++*pb.epoch;
         LCK(cudaMemsetAsync(pb.tileCtr, 0, 4, s));
@@ -1782,6 +2034,10 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
       if (b.sideBits) LCK(cudaMemsetAsync(b.sideBits, 0, (size_t)b.B * b.nbw * 4, s));
       k_mark<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
       note_launch(2);
+      if (b.mae) {  // children's medians / own median, MAE importance
+        k_mae_nodes<<<nblk(NO, 64), 64, 0, s>>>(b, cur, (int)NO);
+        note_launch();
+      }
     } else {
       k_hist_reset<<<nblk(NO, 256), 256, 0, s>>>(b, (int)NO);
       note_launch();
@@ -1982,8 +2238,13 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   }
   const bool hist = prm->split_mode == RF_SPLIT_HIST256;
   const bool extra = prm->split_mode == RF_SPLIT_EXTRA;
+  const bool mae = prm->criterion == RF_CRITERION_MAE;
   const int n = d.n, p = d.p, T = tree_hi - tree_lo;
-  const int nlists = hist ? 1 : p;
+  if (mae && (hist || ntr > kMaeMaxLen)) {
+    err = "MAE criterion on the level-synchronous path: exact and ExtraTrees modes, training sets of <= 12288 rows (R32)";
+    return RF_E_UNSUPPORTED;
+  }
+  const int nlists = hist ? 1 : p + (mae ? 1 : 0);  // MAE: list p = in-bag rows in t_q order
   uint64_t cap = 2ull * (uint64_t)ntr - 1ull;
   if (prm->max_depth >= 0 && prm->max_depth < 40) cap = std::min<uint64_t>(cap, (2ull << prm->max_depth) - 1ull);
   // open nodes per level per tree <= min(ntr / 2, 2^(max_depth - 1))
@@ -2013,9 +2274,29 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.hist = hist ? 1 : 0;
   b.extra = extra ? 1 : 0;
   b.tie_draw = prm->tie_break == RF_TIE_DRAW_ORDER ? 1 : 0;
+  b.mae = mae ? 1 : 0;
   if (extra) LCK(sc.alloc(&b.xb, (size_t)pl.nmax * mtry));
   HistBufs hb;
   const uint32_t* list_src = task_order;
+  if (mae) {
+    // per-task list sources [p + 1][ntr]: the p feature orders and the training rows in
+    // (t_q, row) order (a stable radix sort of the ascending rows by their ordered t_q)
+    uint32_t* src;
+    unsigned long long *kin, *kout;
+    LCK(sc.alloc(&src, (size_t)(p + 1) * ntr));
+    LCK(sc.alloc(&kin, (size_t)ntr));
+    LCK(sc.alloc(&kout, (size_t)ntr));
+    LCK(cudaMemcpyAsync(src, task_order, (size_t)p * ntr * 4, cudaMemcpyDeviceToDevice, s));
+    k_tq_keys<<<nblk(ntr, 256), 256, 0, s>>>(tr_rows_in, d.tq, ntr, kin);
+    note_launch();
+    size_t tb = 0;
+    LCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, tr_rows_in, src + (size_t)p * ntr, ntr, 0, 64, s));
+    char* tmp;
+    LCK(sc.alloc(&tmp, tb + 16));
+    LCK(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, tr_rows_in, src + (size_t)p * ntr, ntr, 0, 64, s));
+    list_src = src;
+    LCK(allow_max_dynamic_smem(k_mae_search));
+  }
   if (hist) {
     // cuts of this task's training rows (R23) and the bins of every row
     double* cuts;
@@ -2088,6 +2369,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&nd.bfs, (size_t)pl.nmax));
   }
   LCK(sc.alloc(&b.feat, (size_t)pl.nmax * mtry));
+  if (mae) LCK(sc.alloc(&b.med2, (size_t)pl.nmax * 2));
   LCK(sc.alloc(&b.best, (size_t)pl.nmax));
   LCK(sc.alloc(&b.accW, (size_t)pl.nmax));
   LCK(sc.alloc(&b.accS, (size_t)pl.nmax));

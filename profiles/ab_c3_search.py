@@ -1,5 +1,6 @@
 """A/B of the large-path split search on C3 (100k x 64, exact, mtry 21): the warp-striped kernel
-per library build (RF_SEARCH_UNROLL variants) and the thread-serial one ("large_thread_search").
+per library build (round 2: RF_SEARCH_UNROLL variants of a warp-striped kernel against the
+thread-serial one via a test switch -- removed after this A/B; then RF_SEARCH_PF 0/1).
 
   python profiles/ab_c3_search.py librfgpu.so librfgpu_su1.so ...
 """
@@ -16,8 +17,7 @@ import datagen, paper_2001_07104_b200 as rfg
 X, y = datagen.scaled(100_000, 64)
 Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
 out = {}
-for thread in (0, 1):
-    rfg.debug_set_option("large_thread_search", thread)
+for thread in (0,):
     rfg.fit(Xd, yd, ntree=128, mtry=21, target=1, seed=7)
     torch.cuda.synchronize()
     rfg.set_profiling(True)
@@ -27,7 +27,7 @@ for thread in (0, 1):
     sec = time.perf_counter() - t0
     prof = rfg.last_profile()
     rfg.set_profiling(False)
-    out["thread" if thread else "striped"] = {"trees_per_s": 500 / sec, "search_ms": prof["large_search"][0],
+    out["search"] = {"trees_per_s": 500 / sec, "search_ms": prof["large_search"][0],
                                               "partition_ms": prof["large_partition"][0]}
 print(json.dumps(out))
 ''' % ROOT

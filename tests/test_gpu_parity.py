@@ -608,16 +608,44 @@ def test_mae_importance_parity(split_mode):
 
 
 def test_mae_unsupported_shapes():
-    X, y = datagen.paper_shaped(600, "K20", "time")
-    with pytest.raises(rfg.RFError) as e:  # n_tr > 255: no CTA-resident MAE path
+    X, y = datagen.scaled(13_000, 16)
+    with pytest.raises(rfg.RFError) as e:  # beyond the level-synchronous MAE path (12,288 rows)
         rfg.fit(X, y, ntree=2, mtry=3, target=1, criterion=1)
     assert e.value.code == rfg.E_UNSUPPORTED
     with pytest.raises(rfg.RFError) as e:  # histogram mode has no MAE variant (R32)
         rfg.fit(X[:100], y[:100], ntree=2, mtry=3, target=1, split_mode=rfg.SPLIT_HIST256, criterion=1)
     assert e.value.code == rfg.E_UNSUPPORTED
-    with pytest.raises(rfg.RFError) as e:
-        rfg.cross_validate_grid(X, y, 2, 1, [2], [3], target=1, criterion=1)
-    assert e.value.code == rfg.E_UNSUPPORTED
+
+
+MAE_LARGE_CASES = [
+    # n_tr > 255: the level-synchronous MAE path (R32), exact and ExtraTrees, ties, no bootstrap
+    ("paper600", lambda: datagen.paper_shaped(600, "K20", "time"), dict(mtry=4, target=1)),
+    ("ties", lambda: datagen.tiny(700, 5, 51, distinct=7), dict(mtry=3)),
+    ("extra_noboot", lambda: datagen.paper_shaped(500, "V100", "power"), dict(mtry=6, split_mode=2, bootstrap=False)),
+    ("depth_mss", lambda: datagen.tiny(900, 6, 52, distinct=40), dict(mtry=6, max_depth=7, min_samples_split=4)),
+    ("scaled_p64", lambda: datagen.scaled(1500, 64), dict(mtry=21, target=1, max_depth=10)),
+    ("tie_draw", lambda: datagen.tiny(400, 4, 53, distinct=5), dict(mtry=4, tie_break=1)),
+]
+
+
+@pytest.mark.parametrize("name,data,kw", MAE_LARGE_CASES, ids=[c[0] for c in MAE_LARGE_CASES])
+def test_mae_large_fit_bit_exact(name, data, kw):
+    """MAE on the level-synchronous path: structures, medians and leaf row sets bit-exact; MAE
+    importance (SAD2(node) - D) within 1e-12."""
+    X, y = data()
+    of = oracle.fit(X, y, ntree=4, seed=61, leaf_rows=True, criterion=1, **kw)
+    gf = rfg.fit(X, y, ntree=4, seed=61, debug=True, criterion=1, **kw)
+    _compare_forest(gf, of, X)
+    imp, raw = gf.importance(raw=True)
+    np.testing.assert_allclose(raw, np.stack([t.imp_raw for t in of.trees]), rtol=1e-12, atol=0)
+
+
+def test_mae_large_cv_parity():
+    X, y = datagen.paper_shaped(700, "P100", "time")
+    fm_o, pr_o = oracle.cv_grid(X, y, 3, 1, [3, 6], [4], target=1, seed=8, criterion=1, want_pred=True)
+    fm_g, pr_g = rfg.cross_validate_grid(X, y, 3, 1, [3, 6], [4], target=1, seed=8, criterion=1, want_pred=True)
+    np.testing.assert_allclose(fm_g, fm_o, rtol=RTOL, atol=0)
+    np.testing.assert_allclose(pr_g, pr_o, rtol=RTOL, atol=0)
 
 
 # ------------------------------------------- alternative large-path kernels ---
