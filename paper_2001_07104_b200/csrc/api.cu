@@ -109,7 +109,8 @@ rf_status read_err(const int* derr, cudaStream_t s) {
 
 // dataset on device: canonical X, t_q, F, presort
 rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, int target,
-                  int require_pos, bool need_sort, rf::DevData& d, Scratch& sc, cudaStream_t s, int guard = 0) {
+                  int require_pos, bool need_sort, rf::DevData& d, Scratch& sc, cudaStream_t s, int guard = 0,
+                  bool need_rank = true) {
   d.n = (int)n;
   d.p = (int)p;
   CK(sc.alloc(&d.X, n * p), "alloc X");
@@ -130,7 +131,7 @@ rf_status prepare(const double* dX, const double* dy, uint64_t n, uint32_t p, in
     void* ws = nullptr;
     if (wsb) CK(sc.alloc(reinterpret_cast<char**>(&ws), wsb), "alloc presort ws");
     ProfScope ps("presort", s);
-    CK(rf::presort(d, ws, wsb, s), "presort");
+    CK(rf::presort(d, ws, wsb, s, need_rank), "presort");
   }
   return RF_OK;
 }
@@ -406,7 +407,9 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   const int T = tree_hi - tree_lo;
   Scratch sc(s);
   rf::DevData d;
-  st = prepare(dX, dy, n, p, prm->target, prm->target == RF_TARGET_LOG, true, d, sc, s, mae_guard(prm));
+  // histogram fits beyond the CTA-resident sizes need the orders (cuts) but no dense ranks
+  const bool hist_large = prm->split_mode == RF_SPLIT_HIST256 && n > 4096;
+  st = prepare(dX, dy, n, p, prm->target, prm->target == RF_TARGET_LOG, true, d, sc, s, mae_guard(prm), !hist_large);
   if (st) return st;
   int dev = 0;
   cudaGetDevice(&dev);

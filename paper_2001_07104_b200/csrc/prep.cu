@@ -205,7 +205,7 @@ __global__ void k_seg_offsets(int64_t* off, int p, int n) {
 }
 }  // namespace
 
-cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
+cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s, bool ranks) {
   const int n = d.n, p = d.p;
   if (n <= kSmallSortMax) {
     size_t smem = (size_t)n * 8 + n;
@@ -242,8 +242,10 @@ cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s) {
       if (e != cudaSuccess) return e;
     }
   }
-  k_rank_sorted<<<p, 1024, 0, s>>>(kout, d.order, n, d.grank);
-  note_launch();
+  if (ranks) {
+    k_rank_sorted<<<p, 1024, 0, s>>>(kout, d.order, n, d.grank);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

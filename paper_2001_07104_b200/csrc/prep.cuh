@@ -25,7 +25,8 @@ struct DevData {
 cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int target,
                          int require_pos, int guard, DevData& d, double* scratch_t, cudaStream_t s);
 // stable per-feature order + dense ranks (needs workspace for large n)
-cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s);
+// ranks = false: orders only (the histogram mode needs no dense ranks; large n only)
+cudaError_t presort(DevData& d, void* ws, size_t ws_bytes, cudaStream_t s, bool ranks = true);
 size_t presort_ws_bytes(int n, int p);
 
 // device ln correctly rounded (exposed for tests via the API)
