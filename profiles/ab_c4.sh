@@ -1,7 +1,8 @@
 #!/bin/bash
-# A/B of large-path builds on the C4 shape (2M rows, 16 trees): bash profiles/ab_c4.sh tag1 tag2 ...
-for tag in "$@"; do
-  if [ "$tag" = base ]; then lib=$PWD/paper_2001_07104_b200/librfgpu.so; else lib=$PWD/paper_2001_07104_b200/librfgpu_$tag.so; fi
-  echo "== $tag"
-  RFGPU_LIB=$lib timeout 600 python bench_configs.py --configs c4 --c4-rows 2000000 --c4-trees 16
+# A/B of C4 variants: LIBS="librfgpu.so librfgpu_<tag>.so ..." (round 2: RF_HIST_CHUNK 32768/65536/131072; RF_HIST_LW 1/0)
+cd "$(dirname "$0")/.."
+for lib in ${LIBS:-librfgpu.so}; do
+  echo "== $lib"
+  RFGPU_LIB=$PWD/paper_2001_07104_b200/$lib python bench_configs.py --configs c4 --no-cpu-baseline --no-e2e | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read())['C4']; print(d['value'], json.dumps(d['kernels_ms_per_fit']))"
 done
