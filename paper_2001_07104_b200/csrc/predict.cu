@@ -95,11 +95,21 @@ __device__ __forceinline__ bool le_exact(float xf, double thr, const double* xro
   return __ldg(xrow + f) <= thr;
 }
 
+// The first kStage nodes (BFS order) of the group's kGs trees are staged in shared memory for
+// every group -- the top levels, which every row visits (a prefix of the BFS order holds all
+// nodes above the first level that has a node at index >= kStage) -- so most of a walk's dependent
+// node loads hit shared memory; deeper nodes come from L1/L2 as before.
+#ifndef RF_PRED_STAGE
+#define RF_PRED_STAGE 63
+#endif
+constexpr int kStage = RF_PRED_STAGE;
+
 __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __restrict__ nodes,
                                                            const uint64_t* __restrict__ tree_off, int T,
                                                            const double* __restrict__ X, long long n, int p,
                                                            int mode, double* __restrict__ out) {
-  extern __shared__ float xsf[];  // [p][kSmemStrideF]
+  extern __shared__ __align__(16) float xsf[];  // [p][kSmemStrideF] rows, then [kGs][kStage] nodes
+  Node16* sn = reinterpret_cast<Node16*>(xsf + ((p * kSmemStrideF + 3) & ~3));
   const long long r0 = (long long)blockIdx.x * kSmemRows;
   const int nr = (int)min((long long)kSmemRows, n - r0);
   const double* Xb = X + r0 * p;
@@ -109,27 +119,37 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
   }
   __syncthreads();
   const int i = threadIdx.x;
-  if (i >= nr) return;
-  const float* x = xsf + i;  // feature f at x[f * kSmemStrideF]
-  const double* xrow = Xb + (size_t)i * p;
+  const bool live = i < nr;  // (no early exit: every thread takes part in the node staging)
+  const float* x = xsf + min(i, nr - 1);  // feature f at x[f * kSmemStrideF]
+  const double* xrow = Xb + (size_t)min(i, nr - 1) * p;
   double s = 0.0;
   int t = 0;
   for (; t + kGs <= T; t += kGs) {
+    if (kStage > 0) {
+      __syncthreads();  // the previous group's nodes are no longer read
+      for (int q = threadIdx.x; q < kGs * kStage; q += kSmemRows) {
+        const int g = q / kStage, k = q - g * kStage;
+        const uint64_t o0 = __ldg(tree_off + t + g), o1 = __ldg(tree_off + t + g + 1);
+        if (o0 + k < o1) reinterpret_cast<uint4*>(sn)[q] = __ldg(reinterpret_cast<const uint4*>(nodes + o0 + k));
+      }
+      __syncthreads();
+    }
     const Node16* tn[kGs];
     Node16 nd[kGs];
 #pragma unroll
     for (int g = 0; g < kGs; ++g) {
       tn[g] = nodes + __ldg(tree_off + t + g);
-      nd[g] = tn[g][0];
+      nd[g] = kStage > 0 ? sn[g * kStage] : tn[g][0];
     }
-    bool open = true;
+    bool open = live;
     while (open) {
       open = false;
 #pragma unroll
       for (int g = 0; g < kGs; ++g) {
         if (nd[g].feat >= 0) {
           const int f = nd[g].feat;
-          nd[g] = tn[g][nd[g].left + (le_exact(x[f * kSmemStrideF], nd[g].v, xrow, f) ? 0u : 1u)];
+          const uint32_t c = nd[g].left + (le_exact(x[f * kSmemStrideF], nd[g].v, xrow, f) ? 0u : 1u);
+          nd[g] = (kStage > 0 && c < (uint32_t)kStage) ? sn[g * kStage + c] : tn[g][c];
           open = true;
         }
       }
@@ -137,6 +157,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
 #pragma unroll
     for (int g = 0; g < kGs; ++g) s += nd[g].v;
   }
+  if (!live) return;
   for (; t < T; ++t) {
     const Node16* tn = nodes + tree_off[t];
     Node16 nd = tn[0];
@@ -231,7 +252,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     return cudaGetLastError();
   }
   if (p <= kSmemMaxP) {
-    const size_t smem = (size_t)p * kSmemStrideF * 4;
+    const size_t smem = (size_t)((p * kSmemStrideF + 3) & ~3) * 4 + (size_t)kGs * kStage * sizeof(Node16);
     cudaError_t e = allow_max_dynamic_smem(k_predict_smem);
     if (e != cudaSuccess) return e;
     k_predict_smem<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p,

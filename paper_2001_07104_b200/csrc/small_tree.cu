@@ -1075,7 +1075,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             const double hi = cs.xs[fb + cs.lrank[fb + L[fb + st + cur.len[k] - 1]]];
             thr = extra_thr(k0, k1, cur.heap[k], j, lo, hi);
           } else {
-            // (read-only-path loads (__ldg) here measured equal, profiles/r03n_x_ldg_ab.txt)
+            // (read-only-path loads (__ldg) here measured equal, profiles/r03n_x_ldg_ab.txt;
+            // deferring these loads past the mark pass 0.5 % slower, rd2_19_ab_defer_thr.txt)
             thr = midpoint_thr(a.X[(size_t)ga * p + f], a.X[(size_t)gb * p + f]);
           }
           if (kMae && kFit) ws.bD[k] = ~key;  // cost D of the chosen split (importance)
@@ -1333,7 +1334,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         // lists 1..p-1, flattened feature-major in chunks of 4 positions (one 32-bit word of
         // a list, one 16-byte load of descriptors): chunk c -> list 1 + c / nc4, positions
         // 4 (c % nc4) .. +3 (c / nc4 exactly via a float reciprocal: c < 2^16).  Four
-        // ballots give each element its rank among the left rows before it.
+        // ballots give each element its rank among the left rows before it.  (Issuing the next
+        // step's loads one step ahead measured 0.9 % slower, profiles/rd2_20_ab_part_pf.txt.)
         const int nc4 = (N + 3) >> 2;
         const int C = (nlists_of(p, kMae) - 1) * nc4;
         const float inv4 = 1.0f / (float)nc4;
