@@ -632,7 +632,7 @@ static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, 
   {
     ProfScope ps("predict", s);
     CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s,
-                          few ? err : nullptr),
+                          few ? err : nullptr, f->total_nodes),
        "predict");
   }
   if (host_out) {  // one synchronisation for result and error flag

@@ -2393,7 +2393,21 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(sc.alloc(&nextPos0, (size_t)B + 1));
   LCK(sc.alloc(&nlBase, (size_t)B + 1));
   uint32_t* hcounters = nullptr;
-  LCK(cudaMallocHost(&hcounters, (size_t)(4 + 3 * (B + 1)) * 4));
+  // pinned level counters: one grow-only buffer per host thread (cudaMallocHost / cudaFreeHost
+  // per fit stalled the host for up to hundreds of ms, rd2_24_c3wall.txt)
+  {
+    static thread_local uint32_t* tl_buf = nullptr;
+    static thread_local size_t tl_words = 0;
+    const size_t need = (size_t)(4 + 3 * (B + 1));
+    if (tl_words < need) {
+      if (tl_buf) cudaFreeHost(tl_buf);
+      tl_buf = nullptr;
+      tl_words = 0;
+      LCK(cudaMallocHost(&tl_buf, need * 4));
+      tl_words = need;
+    }
+    hcounters = tl_buf;
+  }
   PartBufs pbufs;
   const long long max_tiles = (long long)nlists * (B + pl.npmax / kPartTile + 1) + 1;
   LCK(sc.alloc(&pbufs.tab, (size_t)2 * B));
@@ -2416,10 +2430,6 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   LCK(sc.alloc(&pbufs.cnt, (size_t)max_tiles));
   if (hist) LCK(sc.alloc(&pbufs.leftBits, (size_t)max_tiles * kPartThreads));
   LCK(sc.alloc(&pbufs.pref, (size_t)max_tiles));
-  struct HostFree {
-    uint32_t* p;
-    ~HostFree() { cudaFreeHost(p); }
-  } hf{hcounters};
   // CUB temp storage for the largest scan
   size_t cb1 = 0, cb2 = 0, cb3 = 0;
   cub::DeviceScan::ExclusiveScan(nullptr, cb1, wsTmp, b.nodePref, WS2Sum(), WS2{0ull, 0ull}, (int)pl.nmax, s);

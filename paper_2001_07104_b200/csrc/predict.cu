@@ -95,15 +95,17 @@ __device__ __forceinline__ bool le_exact(float xf, double thr, const double* xro
   return __ldg(xrow + f) <= thr;
 }
 
-// The first kStage nodes (BFS order) of the group's kGs trees are staged in shared memory for
-// every group -- the top levels, which every row visits (a prefix of the BFS order holds all
-// nodes above the first level that has a node at index >= kStage) -- so most of a walk's dependent
-// node loads hit shared memory; deeper nodes come from L1/L2 as before.
+// kStage > 0: the first kStage nodes (BFS order) of the group's kGs trees are staged in shared
+// memory for every group -- the top levels, which every row visits (a prefix of the BFS order
+// holds all nodes above the first level that has a node at index >= kStage) -- so the first
+// levels' dependent node loads hit shared memory; deeper nodes come from L1/L2.  Taken for
+// shallow forests (C5: depth 12, +46 %, profiles/rd2_22_ab_c5_stage.txt); deep unbounded trees
+// (C3: ~49 levels) lose, because the per-group barrier waits for the longest walk of the CTA.
 #ifndef RF_PRED_STAGE
 #define RF_PRED_STAGE 63
 #endif
-constexpr int kStage = RF_PRED_STAGE;
 
+template <int kStage>
 __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __restrict__ nodes,
                                                            const uint64_t* __restrict__ tree_off, int T,
                                                            const double* __restrict__ X, long long n, int p,
@@ -244,7 +246,8 @@ __global__ void k_check_finite(const double* X, size_t total, int* err) {
 }  // namespace
 
 cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
-                           long long n, int p, int mode, double* out, cudaStream_t s, int* err_few) {
+                           long long n, int p, int mode, double* out, cudaStream_t s, int* err_few,
+                           uint64_t total_nodes) {
   if (n <= 0) return cudaSuccess;
   if (err_few && n <= kFewRows) {  // latency path: rows checked for finiteness in-kernel
     k_predict_few<<<(unsigned)n, kFewThreads, 0, s>>>(nodes, tree_off, T, X, p, mode, out, err_few);
@@ -252,11 +255,12 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     return cudaGetLastError();
   }
   if (p <= kSmemMaxP) {
-    const size_t smem = (size_t)((p * kSmemStrideF + 3) & ~3) * 4 + (size_t)kGs * kStage * sizeof(Node16);
-    cudaError_t e = allow_max_dynamic_smem(k_predict_smem);
+    const bool stage = RF_PRED_STAGE > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * 16384u;
+    const size_t smem = (size_t)((p * kSmemStrideF + 3) & ~3) * 4 + (stage ? (size_t)kGs * RF_PRED_STAGE * sizeof(Node16) : 0);
+    auto kern = stage ? k_predict_smem<RF_PRED_STAGE> : k_predict_smem<0>;
+    cudaError_t e = allow_max_dynamic_smem(kern);
     if (e != cudaSuccess) return e;
-    k_predict_smem<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p,
-                                                                                      mode, out);
+    kern<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(nodes, tree_off, T, X, n, p, mode, out);
     note_launch();
     return cudaGetLastError();
   }

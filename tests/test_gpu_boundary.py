@@ -186,3 +186,26 @@ def test_forest_import_rejects_malformed():
         with pytest.raises(rfg.RFError) as ex:
             rfg.forest_import(**a)
         assert ex.value.code == rfg.E_ARG
+
+
+def test_ln_device_bit_exact_wide():
+    """The device ln (double-double evaluation, R20) against the oracle's binary128 logq on 4M+
+    values: uniform in the exponent over the whole normal range, the paper-shaped span (µs to
+    seconds), dense neighbourhoods of 1 (tiny results, the hardest relative rounding), of powers of
+    two and of e^k, and subnormals.  One disagreement would flip t_q and every tree on a LOG target."""
+    rnd = np.random.default_rng(12)
+    parts = [
+        np.exp2(rnd.uniform(-1021, 1023, 1_500_000)),
+        10 ** rnd.uniform(-3, 9, 1_000_000),
+        1.0 + rnd.uniform(-2 ** -20, 2 ** -20, 500_000),
+        np.nextafter(1.0, 2.0) ** 0 + np.arange(1, 200_001) * np.finfo(np.float64).eps,
+        np.ldexp(1.0, rnd.integers(-1020, 1020, 400_000)) * (1.0 + rnd.integers(-64, 65, 400_000) * 2.0 ** -52),
+        np.exp(rnd.integers(-700, 700, 300_000).astype(np.float64)) * (1.0 + rnd.normal(0, 1e-15, 300_000)),
+        rnd.uniform(1e-310, 2.2e-308, 100_000),
+    ]
+    y = np.concatenate(parts)
+    y = y[(y > 0) & np.isfinite(y)]
+    got = rfg.debug_ln(_cuda(y)).cpu().numpy()
+    want = oracle.quantize(y, 1)[0]
+    bad = np.nonzero(got.view(np.int64) != want.view(np.int64))[0]
+    assert bad.size == 0, (bad.size, y[bad[:5]], got[bad[:5]], want[bad[:5]])
