@@ -34,6 +34,7 @@ struct rf_forest {
   int32_t* leaf_of_row = nullptr;  // device [ntree][n_rows] (debug fits)
   double* imp = nullptr;           // device [ntree][p] MDI decreases (rf_fit), null if imported
   uint64_t n_rows = 0;
+  bool pooled = false;  // nodes / thr_index / tree_off from the device's stream-ordered pool
 };
 
 namespace {
@@ -498,9 +499,12 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
   f->leaf_of_row = own.lor;
   own.lor = nullptr;
   f->n_rows = n;
-  cudaError_t e = cudaMalloc(&f->nodes, f->total_nodes * sizeof(rf::Node16));
-  if (e == cudaSuccess) e = cudaMalloc(&f->thr_index, f->total_nodes * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&f->tree_off, (T + 1) * sizeof(uint64_t));
+  // the forest's arrays come from the stream-ordered pool (retained): a fresh cudaMalloc of the
+  // ~1 GB C3 forest per fit stalled the fit for 0.1-1 s (profiles/rd2_27_c3wall.txt)
+  f->pooled = true;
+  cudaError_t e = cudaMallocAsync(&f->nodes, std::max<uint64_t>(1, f->total_nodes) * sizeof(rf::Node16), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&f->thr_index, std::max<uint64_t>(1, f->total_nodes) * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&f->tree_off, (T + 1) * sizeof(uint64_t), s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(f->tree_off, f->h_tree_off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) {
@@ -565,9 +569,20 @@ const char* rf_last_error(void) { return g_err.c_str(); }
 
 void rf_forest_free(rf_forest* f) {
   if (!f) return;
-  cudaFree(f->nodes);
-  cudaFree(f->thr_index);
-  cudaFree(f->tree_off);
+  if (f->pooled) {  // back to the pool (kept mapped): the next fit reuses it without a cudaMalloc
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(f->device);
+    cudaStream_t s = host_stream(f->device);
+    cudaFreeAsync(f->nodes, s);
+    cudaFreeAsync(f->thr_index, s);
+    cudaFreeAsync(f->tree_off, s);
+    cudaSetDevice(cur);
+  } else {
+    cudaFree(f->nodes);
+    cudaFree(f->thr_index);
+    cudaFree(f->tree_off);
+  }
   cudaFree(f->leaf_of_row);
   cudaFree(f->imp);
   delete f;

@@ -184,13 +184,14 @@ __global__ void k_keys_boot(Batch b, uint64_t seed, int task, int bootstrap) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) w[b.tr_rows[j]] = 1;
     return;
   }
-  // byte counters updated by 32-bit atomics on the aligned word holding them; the word
-  // is located from the absolute byte offset (tree slots of n bytes need not be 4-aligned)
+  // byte counters updated by 32-bit reductions (no return value) on the aligned word holding
+  // them; the word is located from the absolute byte offset (tree slots of n bytes need not be
+  // 4-aligned).  A count passing 255 would carry into the next byte (or out of the word) and
+  // lower the sum of the bytes, so k_root_finish flags overflow when sum(w) != n_tr.
   const auto count = [&](uint32_t r) {
     const size_t idx = (size_t)t * b.n + r;
     const uint32_t sh = (uint32_t)(idx & 3u) * 8u;
-    const unsigned int old = atomicAdd(reinterpret_cast<unsigned int*>(b.w + (idx & ~(size_t)3)), 1u << sh);
-    if (((old >> sh) & 0xFFu) == 0xFFu) atomicOr(b.err, kErrOverflow);
+    atomicAdd(reinterpret_cast<unsigned int*>(b.w + (idx & ~(size_t)3)), 1u << sh);
   };
   const int nblk = (b.ntr + 1) >> 1;
   for (int blk = blockIdx.x * blockDim.x + threadIdx.x; blk < nblk; blk += gridDim.x * blockDim.x) {
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(256) k_root_partial(Batch b, unsigned long lon
   const uint8_t* w = b.w + (size_t)t * b.n;
   long long S = 0;
   long long mn = LLONG_MAX, mx = LLONG_MIN;
-  unsigned int D = 0;
+  unsigned long long D = 0;  // distinct rows (low 32 bits) and sum of multiplicities (high 32 bits)
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < b.ntr; j += gridDim.x * blockDim.x) {
     const uint32_t r = b.tr_rows[j];
     const uint32_t wv = w[r];
@@ -264,11 +265,11 @@ __global__ void __launch_bounds__(256) k_root_partial(Batch b, unsigned long lon
       S += (long long)wv * v;
       mn = min(mn, v);
       mx = max(mx, v);
-      ++D;
+      D += 1ull + ((unsigned long long)wv << 32);
     }
   }
   using BR = cub::BlockReduce<long long, 256>;
-  using BRu = cub::BlockReduce<unsigned int, 256>;
+  using BRu = cub::BlockReduce<unsigned long long, 256>;
   __shared__ typename BR::TempStorage t1;
   __shared__ typename BRu::TempStorage t2;
   const long long Ssum = BR(t1).Sum(S);
@@ -277,10 +278,10 @@ __global__ void __launch_bounds__(256) k_root_partial(Batch b, unsigned long lon
   __syncthreads();
   const long long mxr = BR(t1).Reduce(mx, cub::Max());
   __syncthreads();
-  const unsigned int Dsum = BRu(t2).Sum(D);
+  const unsigned long long Dsum = BRu(t2).Sum(D);
   if (threadIdx.x == 0 && Dsum) {
     atomicAdd(&acc[4 * t], (unsigned long long)Ssum);  // modular: exact for the int64 sum
-    atomicAdd(&acc[4 * t + 1], (unsigned long long)Dsum);
+    atomicAdd(&acc[4 * t + 1], Dsum);
     atomicMin(reinterpret_cast<long long*>(&acc[4 * t + 2]), mnr);
     atomicMax(reinterpret_cast<long long*>(&acc[4 * t + 3]), mxr);
   }
@@ -290,7 +291,8 @@ __global__ void k_root_finish(Batch b, const unsigned long long* acc, uint32_t* 
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= b.B) return;
   const long long Ssum = (long long)acc[4 * t];
-  const unsigned int Dsum = (unsigned int)acc[4 * t + 1];
+  const unsigned int Dsum = (unsigned int)(acc[4 * t + 1] & 0xFFFFFFFFull);
+  if ((acc[4 * t + 1] >> 32) != (unsigned long long)b.ntr) atomicOr(b.err, kErrOverflow);  // a count wrapped
   const long long mnr = (long long)acc[4 * t + 2], mxr = (long long)acc[4 * t + 3];
   const bool leaf = (b.max_depth == 0) || ((int)Dsum < b.mss) || (mnr == mxr);
   rootInfo[4 * t] = Dsum;

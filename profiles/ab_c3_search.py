@@ -19,7 +19,8 @@ X, y = datagen.scaled(100_000, 64)
 Xd, yd = torch.as_tensor(X, device="cuda"), torch.as_tensor(y, device="cuda")
 out = {}
 for k in KS:
-    rfg.debug_set_option("node_search_min", k)
+    if k:
+        rfg.debug_set_option("node_search_min", k)
     rfg.fit(Xd, yd, ntree=128, mtry=21, target=1, seed=7)
     torch.cuda.synchronize()
     rfg.set_profiling(True)
@@ -33,7 +34,7 @@ for k in KS:
                                               "partition_ms": prof["large_partition"][0]}
 print(json.dumps(out))
 ''' % ROOT
-KS = [int(v) for v in os.environ.get('KS', '2048').split(',')]
+KS = [int(v) for v in os.environ.get('KS', '0').split(',')]  # 0: no switch (the option existed only for rd2_22)
 CODE = CODE.replace('for k in KS:', 'for k in %r:' % KS)
 for lib in sys.argv[1:]:
     env = dict(os.environ, RFGPU_LIB=os.path.join(ROOT, "paper_2001_07104_b200", lib))
