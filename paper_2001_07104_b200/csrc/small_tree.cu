@@ -104,15 +104,18 @@ struct WarpSmem {
   SA<uint8_t> pnB;
   SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
   NodeSet cur, nxt;
-  SA<uint8_t> feat;    // [NM][p] drawn features (partial Fisher-Yates), in draw order
-  SA<uint8_t> xb;      // ExtraTrees: [NM][p] rank threshold per draw slot (last rank with x <= thr) or kNone
+  SA<uint8_t> feat;    // [NM][fs] drawn features (partial Fisher-Yates), in draw order
+  SA<uint8_t> xb;      // ExtraTrees: [NM][fs] rank threshold per draw slot (last rank with x <= thr) or kNone
   SA<unsigned long long> bkey;  // best key (G bits + 1; 0 = none); after decide: threshold bits
   SA<uint32_t> baux;   // best (feature << 8 | position); bit 31 = split
   SA<uint32_t> bW;     // search: prefix base of W; then the best's left W
   SA<uint64_t> bS;     // search: prefix base of S; then the best's left S; then the partition record
-  SA<uint8_t> ncb;     // [NM][2] child non-constant flags
+  SA<uint8_t> ncb;     // [NM][2] child non-constant flags (decide, mark); aliases chOpen, which (e)
+                       // writes for node k after its lane has read them
   SA<uint8_t> chOpen;  // [NM][2] open index of the children or kNone
-  SA<double> chVal;    // [NM][2] leaf value of a leaf child (or of the node itself)
+  // leaf values of a split node's leaf children (or of an unsplit node itself) for the test-row
+  // routing (f) live in cur.S[k] (left / the node) and cur.heap[k] (right) as fp64 bits: (e) has
+  // read both for node k (its lane only) and nothing reads them before the level advance
   SA<uint16_t> chBase; // BFS id of the left child
   SA<uint32_t> thrIdx; // fit mode: threshold rank
   SA<uint32_t> desc;   // [ntr_max] partition descriptor per position (shared by all lists);
@@ -130,6 +133,17 @@ constexpr uint8_t kNone = 0xFF;
 constexpr int kMaeQ = 64;  // MAE candidate ring: <= 31 pending + one loop step's 32 appends
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
+// m = p under the lowest-feature tie-break (north_star; exact mode): the drawn set is all features and
+// the winner does not depend on the draw order, so no draws are made and slot j is feature j
+__host__ __device__ inline bool no_draws(int m, int p, int tie_draw, bool extra) { return m == p && !tie_draw && !extra; }
+// per-node stride of the drawn-feature table: the largest m that draws (p > 16: the whole in-place
+// permutation), 0 when no grid point draws (saves shared memory: more resident warps)
+__host__ __device__ inline int feat_stride_of(const SmallArgs& a) {
+  int fs = 0;
+  for (int i = 0; i < a.n_mtry; ++i)
+    if (!no_draws(a.mtrys[i], a.p, a.tie_draw, a.extra != 0)) fs = max(fs, a.p > 16 ? a.p : a.mtrys[i]);
+  return fs;
+}
 // per-feature stride of the row lists: a multiple of 4 (32-bit list words in (g))
 __host__ __device__ inline int stride_of(int ntr_max) { return (ntr_max + 3) & ~3; }
 
@@ -162,7 +176,7 @@ __host__ __device__ inline void carve_nodeset(Carve& c, NodeSet& s, int NM, bool
 // row lists per tree: the p feature lists, plus the t_q-ordered list under MAE (list p)
 __host__ __device__ inline int nlists_of(int p, bool mae) { return p + (mae ? 1 : 0); }
 
-__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, bool extra,
+__host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr_max, int fs, bool extra,
                                            bool fit, bool mae) {
   const int NM = nmax_of(ntr_max);
   const int P = nlists_of(p, mae);
@@ -174,15 +188,14 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.side = c.take<uint8_t>(ntr_max, 4);
   carve_nodeset(c, s.cur, NM, fit);
   carve_nodeset(c, s.nxt, NM, fit);
-  s.feat = c.take<uint8_t>((size_t)NM * p, 4);
-  s.xb = extra ? c.take<uint8_t>((size_t)NM * p, 4) : SA<uint8_t>{0u};
+  s.feat = c.take<uint8_t>((size_t)NM * fs, 4);
+  s.xb = extra ? c.take<uint8_t>((size_t)NM * fs, 4) : SA<uint8_t>{0u};
   s.bkey = c.take<unsigned long long>(NM, 16);  // 16-aligned: desc aliases it (uint4 loads)
   s.baux = c.take<uint32_t>(NM, 4);
   s.bW = c.take<uint32_t>(NM, 4);
   s.bS = c.take<uint64_t>(NM, 8);
-  s.ncb = c.take<uint8_t>((size_t)NM * 2, 4);
   s.chOpen = c.take<uint8_t>((size_t)NM * 2, 4);
-  s.chVal = c.take<double>((size_t)NM * 2, 8);
+  s.ncb = s.chOpen;
   s.chBase = fit ? c.take<uint16_t>(NM, 4) : SA<uint16_t>{0u};
   s.thrIdx = fit ? c.take<uint32_t>(NM, 4) : SA<uint32_t>{0u};
   s.desc = SA<uint32_t>{s.bkey.off};  // ntr_max * 4 <= NM * 8 bytes
@@ -461,6 +474,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
   const int mi = bid / a.ntask;
   const int m = a.mtrys[mi];
   constexpr bool extra = kExtra;
+  const int fs = feat_stride_of(a);
+  const bool nodraw = no_draws(m, p, a.tie_draw, extra);
 
   Carve cv;
   CtaSmem cs;
@@ -470,10 +485,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
     const size_t cta_bytes = (cv.off + 15) / 16 * 16;
     Carve cw;
     WarpSmem dummy;
-    carve_warp(cw, dummy, p, ntr_max, extra, kFit, kMae);
+    carve_warp(cw, dummy, p, ntr_max, fs, extra, kFit, kMae);
     const size_t per_warp = (cw.off + 15) / 16 * 16;
     Carve mine(cta_bytes + per_warp * warp);
-    carve_warp(mine, ws, p, ntr_max, extra, kFit, kMae);
+    carve_warp(mine, ws, p, ntr_max, fs, extra, kFit, kMae);
   }
 
   const int ntr = a.ntr[tl];
@@ -698,9 +713,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
       // features and the winner does not depend on the draw order, so the draws are skipped and
       // slot j holds feature j (same trees as the oracle's Fisher-Yates; ExtraTrees keeps its
       // draws: its thresholds are keyed by draw slot, R29)
-      if (m == p && !a.tie_draw && !extra) {
-        #pragma unroll 1
-        for (int q = lane; q < nOpen * p; q += 32) ws.feat[q] = (uint8_t)(q % p);
+      if (nodraw) {
+        // nothing to draw: slot j is feature j (feat_of)
       } else if (p <= 16) {
         // L lanes per node share its Philox blocks; the swap indices (4 bits per slot) are
         // OR-combined across the group, then one lane applies the swaps to a nibble-packed
@@ -726,7 +740,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           #pragma unroll 1
           for (int d = 1; d < Lg; d <<= 1) sw |= __shfl_xor_sync(0xffffffffu, sw, d);
           if (k < nOpen && sub == 0) {
-            const SA<uint8_t> fp = ws.feat + k * p;
+            const SA<uint8_t> fp = ws.feat + k * fs;
             uint64_t perm = 0xFEDCBA9876543210ull;
             #pragma unroll 1
             for (int j = 0; j < m; ++j) {
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
       } else {
       #pragma unroll 1
       for (int k = lane; k < nOpen; k += 32) {
-        const SA<uint8_t> fp = ws.feat + k * p;
+        const SA<uint8_t> fp = ws.feat + k * fs;
         const uint64_t h = cur.heap[k];
         {
           #pragma unroll 1
@@ -775,7 +789,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           #pragma unroll 1
           for (int s = 0; s < 2 && 2 * b + s < m; ++s) {
             const int j = 2 * b + s;
-            const int f = ws.feat[k * p + j];
+            const int f = ws.feat[k * fs + j];
             const int fb = f * ntr_max;
             const int rlo = cs.lrank[fb + L[fb + st]], rhi = cs.lrank[fb + L[fb + st + ln - 1]];
             uint8_t bnd = kNone;
@@ -788,7 +802,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               }
               bnd = (uint8_t)l;
             }
-            ws.xb[k * p + j] = bnd;
+            ws.xb[k * fs + j] = bnd;
           }
         }
         __syncwarp();
@@ -815,7 +829,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           const int off = e - m * st;
           j = off / ln;
           i = off - j * ln;
-          f = ws.feat[k * p + j];
+          f = nodraw ? j : ws.feat[k * fs + j];
           lbase = f * ntr_max;
         }
         const int k_init = k, j_init = j, i_init = i, st_init = st, ln_init = ln, f_init = f;
@@ -868,7 +882,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
                 st = cur.start[k];
                 ln = cur.len[k];
               }
-              f = ws.feat[k * p + j];
+              f = nodraw ? j : ws.feat[k * fs + j];
               lbase = f * ntr_max;
             }
             r1 = L[lbase + st + min(i, ln - 1)];
@@ -899,7 +913,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         // critical path of the prefix sums -> reciprocal table -> fp64 score chain)
         uint32_t wr = ws.w[r];
         int64_t tr = cs.tq[r];
-        int xbj = extra ? (int)ws.xb[k * p + j] : (int)kNone;  // ExtraTrees boundary of the segment
+        int xbj = extra ? (int)ws.xb[k * fs + j] : (int)kNone;  // ExtraTrees boundary of the segment
         // candidate aux minus the index: tie key << 16 | draw slot << 8 | node start, tie key =
         // the feature (north_star) or the draw slot (R9); ascending aux = preferred among equal keys
         const bool tie_draw = a.tie_draw != 0;
@@ -978,8 +992,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               Wk = cur.W[k];
               Sk = cur.S[k];
             }
-            f = ws.feat[k * p + j];
-            if (extra) xbj = ws.xb[k * p + j];
+            f = nodraw ? j : ws.feat[k * fs + j];
+            if (extra) xbj = ws.xb[k * fs + j];
             lbase = f * ntr_max;
             auxb = ((uint32_t)(tie_draw ? j : f) << 16) | ((uint32_t)j << 8) | (uint32_t)st;
             rn = L[lbase + st];
@@ -1065,7 +1079,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         if (key) {
           const uint32_t aux = ws.baux[k];
           const int j = (int)((aux >> 8) & 0xFFu), bp = (int)(aux & 0xFFu);
-          const int f = ws.feat[k * p + j];
+          const int f = nodraw ? j : ws.feat[k * fs + j];
           const uint8_t ra = L[f * ntr_max + bp], rb = L[f * ntr_max + bp + 1];
           const uint32_t ga = cs.trr[ra], gb = cs.trr[rb];
           double thr;
@@ -1083,9 +1097,10 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           ws.bkey[k] = (unsigned long long)__double_as_longlong(thr);
           ws.baux[k] = ((uint32_t)f << 8) | (uint32_t)bp | 0x80000000u;  // feature, boundary, split flag
           if (kFit) ws.thrIdx[k] = a.grank[(size_t)f * a.n + ga];
-          const SA<int64_t> tqf{ws.chVal.off};  // child first-row targets (chVal is free here)
-          tqf[2 * k] = cs.tq[L[f * ntr_max + cur.start[k]]];
-          tqf[2 * k + 1] = cs.tq[rb];
+          // child first-row targets for the constancy test in (d): in the next level's node table,
+          // which (e) fills only after (d)
+          nxt.S[k] = cs.tq[L[f * ntr_max + cur.start[k]]];
+          nxt.heap[k] = (uint64_t)cs.tq[rb];
         }
       }
       __syncwarp();
@@ -1103,7 +1118,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             const uint8_t r = L[f * ntr_max + pos];
             const int sd = pos <= (int)(aux & 0xFFu) ? 0 : 1;
             ws.side[r] = (uint8_t)(1 - sd);
-            if (cs.tq[r] != SA<int64_t>{ws.chVal.off}[2 * k + sd]) ws.ncb[2 * k + sd] = 1;
+            if (cs.tq[r] != (sd ? (int64_t)nxt.heap[k] : nxt.S[k])) ws.ncb[2 * k + sd] = 1;
           }
         }
       }
@@ -1200,8 +1215,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               vR = kMae ? median_leaf(ws.med2[2 * k + 1], F) : leaf_value(SRv, cs.rcp2[WRv], F);
               ws.chOpen[2 * k + 1] = kNone;
             }
-            ws.chVal[2 * k] = vL;
-            ws.chVal[2 * k + 1] = vR;
+            cur.S[k] = __double_as_longlong(vL);  // routing leaf values (cur.S / cur.heap are read above)
+            cur.heap[k] = (uint64_t)__double_as_longlong(vR);
             {
               // packed partition record: start | baseL | dstL | dstR | openL | openR | split
               const uint64_t dL = openL ? nxt.start[ws.chOpen[2 * k]] : kNone;
@@ -1229,7 +1244,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           } else if (act) {
             // open node without any candidate split: leaf (R11)
             const double v = kMae ? median_leaf(ws.med2[2 * k], F) : leaf_value(cur.S[k], cs.rcp2[cur.W[k]], F);
-            ws.chVal[2 * k] = v;
+            cur.S[k] = __double_as_longlong(v);
             ws.bS[k] = 0ull;  // partition record: not split
             if (kFit) {
               Node16 nd;
@@ -1262,14 +1277,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             const uint32_t aux = ws.baux[k];
             uint32_t nc_;
             if (!(aux & 0x80000000u)) {
-              acc[s] += ws.chVal[2 * k];
+              acc[s] += __longlong_as_double(cur.S[k]);
               nc_ = kNone;
             } else {
               const int f = (int)((aux >> 8) & 0xFFu);
               const double thr = __longlong_as_double((long long)ws.bkey[k]);
               const int sd = (cs.xte[(size_t)r * p + f] <= thr) ? 0 : 1;
               nc_ = ws.chOpen[2 * k + sd];
-              if (nc_ == kNone) acc[s] += ws.chVal[2 * k + sd];
+              if (nc_ == kNone) acc[s] += __longlong_as_double(sd ? (long long)cur.heap[k] : cur.S[k]);
             }
             tcur = (tcur & ~(0xFFu << (8 * s))) | (nc_ << (8 * s));
           }
@@ -1424,7 +1439,7 @@ size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   const size_t cta = (c.off + 15) / 16 * 16;
   Carve w;
   WarpSmem ws;
-  carve_warp(w, ws, a.p, stride_of(a.ntr_max), a.extra != 0, a.fit_mode != 0, a.mae != 0);
+  carve_warp(w, ws, a.p, stride_of(a.ntr_max), feat_stride_of(a), a.extra != 0, a.fit_mode != 0, a.mae != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
   return cta + per_warp * a.wpb;
 }
