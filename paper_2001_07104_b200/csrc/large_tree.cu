@@ -15,7 +15,10 @@
 //               bests merged into the node best with a 128-bit compare-and-swap on
 //               (G key, draw slot|position) -- a total order, so the result does not
 //               depend on timing.  (Gathering a thread's 16 elements at once instead
-//               of one by one measured 20 % slower: 80 registers, fewer warps.)
+//               of one by one measured 20 % slower: 80 registers, fewer warps; staging
+//               list indices first and loading entries and (w, t_q) lane-strided --
+//               coalesced list reads, 8 gathers in flight per lane -- 3.5 % slower,
+//               profiles/rd2_34_ab_c3.txt.)
 //   (ExtraTrees, R29: extra_bounds locates each (node, slot) segment's random
 //   threshold first; the search then scores only that boundary)
 //   decide      split flag, threshold, first-row targets for the constancy test
@@ -133,6 +136,7 @@ struct Batch {
   // ExtraTrees modes), else the row; every reader masks with rowMask
   int packRank;
   uint32_t rowMask;
+  const uint8_t* rfit;      // [p] 1: all dense ranks of feature f < 2^15 (packed bits decide) or null
   uint8_t* side;            // [B][n]
   uint32_t* sideBits;       // [B][nbw] go-left bit per row (fused partition path) or null
   int nbw;                  // words per tree in sideBits = ceil(n / 32)
@@ -483,6 +487,16 @@ __device__ __forceinline__ void cursor_next_segment(const Batch& b, const Nodes&
 // aggregate before it waits, so the look-back cannot deadlock.  Flags carry a per-level
 // epoch ((epoch << 2) | state; state 1 = aggregate, 2 = inclusive), so the status
 // array is never reset.
+// Shared staging of a thread's kKC = 16 elements: slot k of thread tid at tid * 16 + (k ^ (tid & 15)).
+// Thread-serial walks (all threads at the same k) then spread over the banks instead of all 32
+// threads hitting one bank (stride 16 x 8 B = 128 B); lane-strided walks (16 lanes over one
+// thread's slots) stay conflict-free.
+#ifdef RF_SEARCH_NOSWZ
+#define SWZ(tid, k) ((tid) * kKC + (k))
+#else
+#define SWZ(tid, k) ((tid) * kKC + ((k) ^ ((tid) & (kKC - 1))))
+#endif
+
 struct TileStat {
   unsigned long long aw, as, iw, is;  // aggregate (W, S), inclusive prefix (W, S)
 };
@@ -506,7 +520,6 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   const uint32_t* L = b.L[cur & 1];
   const long long e0 = tile * kTile + (long long)threadIdx.x * kKC;
   const long long e1 = min(e0 + kKC, E);
-  const int cbase = threadIdx.x * kKC;
   // pass 1: thread totals (weights and targets cached).  The absolute prefix at every
   // segment start is known from the node prefixes (m bW[g] + j W[g]), so a tile that
   // contains a segment start derives its own prefix and skips the look-back.
@@ -534,8 +547,8 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         wv = b.w[(size_t)c.t * b.n + r];
         tv = b.tq[r];
       }
-      s_w[cbase + (int)(e - e0)] = (uint8_t)wv;
-      s_t[cbase + (int)(e - e0)] = tv;
+      s_w[SWZ(threadIdx.x, (int)(e - e0))] = (uint8_t)wv;
+      s_t[SWZ(threadIdx.x, (int)(e - e0))] = tv;
       lw += wv;
       ls += (unsigned long long)((long long)wv * tv);
       if (++c.i == c.len && e + 1 < e1) cursor_next_segment(b, nd, c);
@@ -618,14 +631,15 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
   unsigned long long rkey = 0ull, raux = ~0ull;
   int rg = c.g;
   const uint32_t* grank = b.grank;
+  bool fits = b.rfit && b.rfit[c.f];  // packed rank bits decide alone (all ranks of f < 2^15)
   // r: list entry of the current element; rk: its rank (packed: the entry's rank bits, the
   // full rank gathered only when two neighbours' low rank bits agree)
   uint32_t r = L[c.listBase + c.i];
   uint32_t rk = b.packRank ? (r >> 17) : grank[(size_t)c.f * b.n + r];
   for (long long e = e0; e < e1; ++e) {
-    const uint32_t wv = s_w[cbase + (int)(e - e0)];
+    const uint32_t wv = s_w[SWZ(threadIdx.x, (int)(e - e0))];
     cW += wv;
-    cS += (unsigned long long)((long long)wv * s_t[cbase + (int)(e - e0)]);
+    cS += (unsigned long long)((long long)wv * s_t[SWZ(threadIdx.x, (int)(e - e0))]);
     const bool hasNext = c.i + 1 < c.len;
     uint32_t rn = r, rkn = rk;
     if (hasNext) {
@@ -635,7 +649,8 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
         cand = (uint32_t)c.i == c.xb;  // the segment's one candidate (R29)
       } else if (b.packRank) {
         rkn = rn >> 17;
-        cand = rkn != rk || grank[(size_t)c.f * b.n + (rn & 0x1FFFFu)] != grank[(size_t)c.f * b.n + (r & 0x1FFFFu)];
+        cand = rkn != rk ||
+               (!fits && grank[(size_t)c.f * b.n + (rn & 0x1FFFFu)] != grank[(size_t)c.f * b.n + (r & 0x1FFFFu)]);
       } else {
         rkn = grank[(size_t)c.f * b.n + rn];
         cand = rkn != rk;
@@ -661,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
           rkey = 0ull; raux = ~0ull;
           rg = c.g;
         }
+        fits = b.rfit && b.rfit[c.f];
         segW = (unsigned long long)b.m * b.nodePref[c.g].w + (unsigned long long)c.j * c.W;
         segS = (unsigned long long)b.m * b.nodePref[c.g].s + (unsigned long long)c.j * (unsigned long long)c.S;
         rn = L[c.listBase];
@@ -680,6 +696,21 @@ __global__ void __launch_bounds__(kThreads, RF_SEARCH_MINB) k_search_fused(Batch
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(ncand, v);
   }
+}
+
+// per feature: 1 if every dense rank fits the 15 packed rank bits of a list entry (rfit)
+__global__ void k_rank_fit(const uint32_t* __restrict__ grank, int n, int p, uint32_t* maxr, uint8_t* rfit,
+                           int finish) {
+  const int f = blockIdx.y;
+  if (finish) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) rfit[f] = maxr[f] < 0x8000u ? 1 : 0;
+    return;
+  }
+  uint32_t mx = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    mx = max(mx, grank[(size_t)f * n + i]);
+  for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  if ((threadIdx.x & 31) == 0) atomicMax(&maxr[f], mx);
 }
 
 // ------------------------------------------------------- MAE criterion (R32) ----
@@ -1738,13 +1769,25 @@ __global__ void k_part_desc(Batch b, int cur, int NP, const uint32_t* __restrict
 // streams one list through the position space 32 x kPWSteps positions at a time (all
 // loads of a step issued before use); a ballot gives every element its rank among the
 // left rows before it -- no block scans, no barriers after the bitmap load.  (A/B against
-// a CTA-per-list-group version with 64-bit block scans over four lists: -22 % time.)
-constexpr int kPWWarps = 8, kPWSteps = 4;
+// a CTA-per-list-group version with 64-bit block scans over four lists: -22 % time.  Steps of
+// 32 positions in flight per warp: 8 beat 4 by 22 % and 16 (C3 partition 88.8 / 113.4 / 139.1 ms,
+// profiles/rd2_33_ab_c3.txt, rd2_34_ab_c3.txt); tree-major CTA order measured neutral.)
+#ifndef RF_PW_STEPS
+#define RF_PW_STEPS 8
+#endif
+constexpr int kPWWarps = 8, kPWSteps = RF_PW_STEPS;
 
 __global__ void __launch_bounds__(32 * kPWWarps) k_part_lists_warp(Batch b, int cur, const uint4* __restrict__ desc) {
   extern __shared__ uint32_t sbits[];
+#ifdef RF_PART_TREE_X
   const int t = blockIdx.x;
   const int f = blockIdx.y * kPWWarps + (threadIdx.x >> 5);
+#else
+  // the list groups of one tree are adjacent CTAs: they read the tree's descriptors while
+  // they are in L2
+  const int t = blockIdx.y;
+  const int f = blockIdx.x * kPWWarps + (threadIdx.x >> 5);
+#endif
   const int lane = threadIdx.x & 31;
   const uint32_t pos0 = b.tPos0[t], N = b.tPos0[t + 1] - pos0;
   if (N == 0) return;
@@ -2089,8 +2132,13 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
         k_part_debug_rows<<<nblk(NP, 256), 256, 0, s>>>(b, cur, (int)NP);
         note_launch();
       }
+#ifdef RF_PART_TREE_X
       k_part_lists_warp<<<dim3((unsigned)b.B, (unsigned)((b.nl + kPWWarps - 1) / kPWWarps)), 32 * kPWWarps, plSmem, s>>>(
           b, cur, pb.desc);
+#else
+      k_part_lists_warp<<<dim3((unsigned)((b.nl + kPWWarps - 1) / kPWWarps), (unsigned)b.B), 32 * kPWWarps, plSmem, s>>>(
+          b, cur, pb.desc);
+#endif
       note_launch();
     } else {
       ProfScope ps("large_partition", s);
@@ -2256,8 +2304,16 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   const size_t per_tree = (size_t)2 * nlists * ntr * 4 + (size_t)ntr * 8 + (size_t)n * 2 +
                           (size_t)open_max * (128 + (extra ? 4 * (size_t)mtry : 0));
   // trees per batch: per-level launch and sync costs are shared by the batch, so batches are
-  // as large as a 16 GB working-set budget allows (of the 180 GB HBM), up to 128 trees
-  int B = (int)std::max<size_t>(1, std::min<size_t>(128, ((size_t)16 << 30) / std::max<size_t>(per_tree, 1)));
+  // as large as the working-set budget allows (of the 180 GB HBM)
+#ifndef RF_LARGE_BMAX
+#define RF_LARGE_BMAX 128
+#endif
+#ifndef RF_LARGE_BUDGET_GB
+#define RF_LARGE_BUDGET_GB 16
+#endif
+  int B = (int)std::max<size_t>(
+      1, std::min<size_t>(RF_LARGE_BMAX, ((size_t)RF_LARGE_BUDGET_GB << 30) / std::max<size_t>(per_tree, 1)));
+  B = std::min(B, (int)std::min<long long>(INT_MAX, (long long)INT_MAX / std::max(ntr, 1)));  // positions: int
   B = std::min(B, T);
   LargePlan pl;
   pl.B = B;
@@ -2273,6 +2329,17 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.nl = nlists;
   b.packRank = (!hist && n <= (1 << 17)) ? 1 : 0;
   b.rowMask = b.packRank ? 0x1FFFFu : 0xFFFFFFFFu;
+  if (b.packRank) {
+    uint32_t* maxr;
+    uint8_t* rfit;
+    LCK(sc.alloc(&maxr, (size_t)p));
+    LCK(sc.alloc(&rfit, (size_t)p));
+    LCK(cudaMemsetAsync(maxr, 0, (size_t)p * 4, s));
+    k_rank_fit<<<dim3(std::min<unsigned>(nblk(n, 256), 64), (unsigned)p), 256, 0, s>>>(d.grank, n, p, maxr, rfit, 0);
+    k_rank_fit<<<dim3(1, (unsigned)p), 32, 0, s>>>(d.grank, n, p, maxr, rfit, 1);
+    note_launch(2);
+    b.rfit = rfit;
+  }
   b.hist = hist ? 1 : 0;
   b.extra = extra ? 1 : 0;
   b.tie_draw = prm->tie_break == RF_TIE_DRAW_ORDER ? 1 : 0;

@@ -103,6 +103,7 @@ struct WarpSmem {
   SA<uint8_t> pnA;     // [ntr_max] position -> open node
   SA<uint8_t> pnB;
   SA<uint8_t> side;    // [ntr_max] by local row: 1 = goes left
+  SA<uint8_t> trash;   // [32] target of the partition's discarded entries, one byte per lane
   NodeSet cur, nxt;
   SA<uint8_t> feat;    // [NM][fs] drawn features (partial Fisher-Yates), in draw order
   SA<uint8_t> xb;      // ExtraTrees: [NM][fs] rank threshold per draw slot (last rank with x <= thr) or kNone
@@ -130,6 +131,11 @@ struct WarpSmem {
 };
 
 constexpr uint8_t kNone = 0xFF;
+// The search reads the list entry after a segment's last one and the tables indexed by it (row id
+// < 256: lrank, w, tq) without a bounds select; the value is never used, and this much shared
+// memory past the last region keeps every such read inside the allocation (tq[255] is 2040 B past
+// the table's start).
+constexpr size_t kReadSlack = 2048;
 constexpr int kMaeQ = 64;  // MAE candidate ring: <= 31 pending + one loop step's 32 appends
 
 __host__ __device__ inline int nmax_of(int ntr_max) { return ntr_max / 2 + 1; }
@@ -186,6 +192,7 @@ __host__ __device__ inline void carve_warp(Carve& c, WarpSmem& s, int p, int ntr
   s.pnA = c.take<uint8_t>(ntr_max, 4);
   s.pnB = c.take<uint8_t>(ntr_max, 4);
   s.side = c.take<uint8_t>(ntr_max, 4);
+  s.trash = c.take<uint8_t>(32, 4);
   carve_nodeset(c, s.cur, NM, fit);
   carve_nodeset(c, s.nxt, NM, fit);
   s.feat = c.take<uint8_t>((size_t)NM * fs, 4);
@@ -905,8 +912,13 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         uint32_t haux = 0x7FFFFFFFu, raux = 0x7FFFFFFFu;
         uint32_t hWL = 0, rWL = 0;   // left sums of the best candidate (children sums)
         int64_t hSL = 0, rSL = 0;
-        uint32_t segW = (uint32_t)m * ws.bW[k] + (uint32_t)j * Wk;
-        uint64_t segS = (uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk;
+        // left sums of the current segment up to the element (relative to the segment start: they
+        // restart at 0 at every segment start, the previous segment's sums having reached (W_k, S_k))
+        uint32_t WLr = cW - ((uint32_t)m * ws.bW[k] + (uint32_t)j * Wk);
+        int64_t SLr = (int64_t)(cS - ((uint64_t)m * ws.bS[k] + (uint64_t)j * (uint64_t)Sk));
+        // MSE: the run best's key minus one, signed (-1 = none): G >= 0, so its bits compare as
+        // signed integers and no "+ 1" is formed per candidate (exported as key = rkm1 + 1)
+        long long rkm1 = -1;
         uint8_t r = L[lbase + st + i];
         uint32_t rkr = cs.lrank[lbase + r];
         // the element's weight and target are loaded one iteration ahead (off the
@@ -925,20 +937,22 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           __syncwarp();
         }
         // reciprocal-table entries of the next element, loaded one iteration ahead
-        double2 ylN = cs.rcp2[(cW + wr - segW) & 0xFFu], yrN = cs.rcp2[(Wk - (cW + wr - segW)) & 0xFFu];
+        double2 ylN = cs.rcp2[(WLr + wr) & 0xFFu], yrN = cs.rcp2[(Wk - (WLr + wr)) & 0xFFu];
         #pragma unroll 1
         for (int c = 0; c < Kc; ++c) {
           const bool act = c < cnt;
           const uint32_t wv = act ? wr : 0u;
-          cW += wv;
-          cS += (uint64_t)((int64_t)wv * tr);
+          WLr += wv;
+          SLr += (int64_t)wv * tr;
           const bool hasNext = i + 1 < ln;
-          uint8_t rn = L[lbase + st + (hasNext ? i + 1 : i)];
+          // the entry after the segment's last one is read but not used (a row id < 256: every
+          // load below stays inside the CTA's shared memory)
+          uint8_t rn = L[lbase + st + i + 1];
           uint32_t rkn = cs.lrank[lbase + rn];
           wr = ws.w[rn];
           tr = cs.tq[rn];
-          const uint32_t WL = cW - segW;
-          const int64_t SL = (int64_t)(cS - segS);
+          const uint32_t WL = WLr;
+          const int64_t SL = SLr;
           const uint32_t WR = Wk - WL;
           const int64_t SR = Sk - SL;
           const double dSL = __ll2double_rn(SL), dSR = __ll2double_rn(SR);
@@ -968,23 +982,27 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             key = cand ? mae_key(L + (p * ntr_max + st), ln, cs.lrank + lbase, rkr, ws.w, cs.tq, WL, SL, WR, SR)
                        : 0ull;
           } else {
-            key = cand ? (unsigned long long)__double_as_longlong(__dadd_rn(gl, gr)) + 1ull : 0ull;
+            key = 0ull;
+            const long long kb = __double_as_longlong(__dadd_rn(gl, gr));
+            if (cand && (kb > rkm1 || (kb == rkm1 && aux < raux))) { rkm1 = kb; raux = aux; rWL = WL; rSL = SL; }
           }
           ncand += cand;
-          if (better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
+          if (kMae && better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
           if (!hasNext && c + 1 < cnt) {
             // end of segment: next feature slot or next node.  Segments are contiguous in the
-            // flattened order and each holds all rows of its node, so the next segment's base
-            // is this one's plus the node's sums (W_k, S_k)
+            // flattened order and each holds all rows of its node: the next segment's left sums
+            // start at 0
             i = 0;
-            segW += Wk;
-            segS += (uint64_t)Sk;
+            WLr = 0u;
+            SLr = 0;
             if (++j == m) {
               j = 0;
+              if (!kMae) rkey = (unsigned long long)(rkm1 + 1);
               // node k complete inside this lane (no other lane reads its bW/bS any more)
               if (k == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
               else { ws.bkey[k] = rkey; ws.baux[k] = raux; ws.bW[k] = rWL; ws.bS[k] = (uint64_t)rSL; }
               rkey = 0ull; raux = 0x7FFFFFFFu;
+              rkm1 = -1;
               ++k;
               rk = k;
               st = cur.start[k];
@@ -1004,13 +1022,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
             ++i;
           }
           {
-            const uint32_t WLn = cW + wr - segW;
+            const uint32_t WLn = WLr + wr;
             ylN = cs.rcp2[WLn & 0xFFu];
             yrN = cs.rcp2[(Wk - WLn) & 0xFFu];
           }
           r = rn;
           rkr = rkn;
         }
+        if (!kMae) rkey = (unsigned long long)(rkm1 + 1);
         if (cnt > 0 && rk == hk) { hkey = rkey; haux = raux; hWL = rWL; hSL = rSL; }
         if (kMae && kExtra) {
           #pragma unroll 1
@@ -1344,6 +1363,8 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           }
           carry += __popc(bal);
         }
+        // descriptors of the padding positions N .. 4 ceil(N / 4) - 1 (read by the four-wide pass)
+        if (lane < ((4 - (N & 3)) & 3)) ws.desc[N + lane] = 0xFFFFFFFFu;
         __syncwarp();
         PT_MARK(10);
         // lists 1..p-1, flattened feature-major in chunks of 4 positions (one 32-bit word of
@@ -1353,16 +1374,14 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         // step's loads one step ahead measured 0.9 % slower, profiles/rd2_20_ab_part_pf.txt.)
         const int nc4 = (N + 3) >> 2;
         const int C = (nlists_of(p, kMae) - 1) * nc4;
-        const float inv4 = 1.0f / (float)nc4;
+        // the lane's chunk (list fi + 1, word q) advances by 32 chunks per step
+        const int dfi = 32 / nc4, dq = 32 - dfi * nc4;
+        int fi = lane / nc4, q = lane - fi * nc4;
         carry = 0;
         #pragma unroll 1
         for (int base = 0; base < C; base += 32) {
-          const int c = base + lane;
-          const bool valid = c < C;
-          int fi = (int)((float)c * inv4);
-          fi += (c - fi * nc4 >= nc4) ? 1 : 0;
-          fi -= (c - fi * nc4 < 0) ? 1 : 0;
-          const int q4 = (c - fi * nc4) * 4;
+          const bool valid = base + lane < C;
+          const int q4 = q * 4;
           const int f = fi + 1;
           uint32_t rows4 = 0;
           uint4 d4 = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -1376,7 +1395,7 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           uint32_t before = carry;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            if (q4 + i >= N) dsc[i] = 0xFFFFFFFFu;  // padding positions (stale descriptors)
+            // (padding positions N .. 4 nc4 - 1 hold ~0 descriptors, written by the list-0 pass)
             left[i] = dsc[i] != 0xFFFFFFFFu && ws.side[(rows4 >> (8 * i)) & 0xFFu];
             bal[i] = __ballot_sync(0xffffffffu, left[i]);
             before += __popc(bal[i] & lt);
@@ -1385,14 +1404,18 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t d = left[i] ? (dsc[i] & 0xFFu) : ((dsc[i] >> 8) & 0xFFu);
-            if (d != kNone) {  // also false for padding and unsplit positions
-              const uint32_t leftBefore = before - ((dsc[i] >> 16) & 0xFFu);
-              const uint32_t dest = d + (left[i] ? leftBefore : ((uint32_t)(q4 + i) - (dsc[i] >> 24)) - leftBefore);
-              L2[f * ntr_max + dest] = (uint8_t)(rows4 >> (8 * i));
-            }
+            const uint32_t leftBefore = before - ((dsc[i] >> 16) & 0xFFu);
+            const uint32_t dest = d + (left[i] ? leftBefore : ((uint32_t)(q4 + i) - (dsc[i] >> 24)) - leftBefore);
+            // entries of leaf children, unsplit nodes and padding (d = kNone) go to a trash byte:
+            // an unconditional store instead of a branch per entry
+            const uint32_t at = d != kNone ? L2.off + (uint32_t)(f * ntr_max) + dest : ws.trash.off + (uint32_t)lane;
+            SA<uint8_t>{at}[0] = (uint8_t)(rows4 >> (8 * i));
             before += left[i] ? 1u : 0u;
           }
           carry += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
+          q += dq;
+          fi += dfi;
+          if (q >= nc4) { q -= nc4; ++fi; }
         }
       }
       PT_MARK(11);
@@ -1441,7 +1464,7 @@ size_t small_tree_smem_bytes(const SmallArgs& a, int /*mmax*/) {
   WarpSmem ws;
   carve_warp(w, ws, a.p, stride_of(a.ntr_max), feat_stride_of(a), a.extra != 0, a.fit_mode != 0, a.mae != 0);
   const size_t per_warp = (w.off + 15) / 16 * 16;
-  return cta + per_warp * a.wpb;
+  return cta + per_warp * a.wpb + kReadSlack;
 }
 
 // calls fn(kernel) with the variant for (fit mode, test rows per lane, split mode, criterion)
