@@ -53,7 +53,10 @@ constexpr int kThreads = 128;
 #ifndef RF_SEARCH_MINB
 #define RF_SEARCH_MINB 8
 #endif
-constexpr int kKC = 16;  // elements per thread in the search tiles
+#ifndef RF_SEARCH_KC
+#define RF_SEARCH_KC 16
+#endif
+constexpr int kKC = RF_SEARCH_KC;  // elements per thread in the search tiles
 constexpr int kTile = kThreads * kKC;
 
 struct __align__(16) Best {
@@ -241,6 +244,41 @@ __global__ void k_inbag_lists(Batch b, const uint32_t* __restrict__ task_order /
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
+  }
+}
+
+// Warp per (tree, list): the same stable compaction streamed by one warp with ballot ranks and a
+// running carry (the partition kernel's pattern: 8 x 32 entries in flight per step, no block
+// scans or barriers); a CTA's 8 warps take 8 lists of one tree.
+constexpr int kIbwWarps = 8, kIbwSteps = 8;
+__global__ void __launch_bounds__(32 * kIbwWarps) k_inbag_lists_warp(Batch b, const uint32_t* __restrict__ task_order) {
+  const int t = blockIdx.y;
+  const int f = blockIdx.x * kIbwWarps + (threadIdx.x >> 5);
+  if (f >= b.nl) return;
+  const int lane = threadIdx.x & 31;
+  const uint8_t* w = b.w + (size_t)t * b.n;
+  const uint32_t* src = task_order + (size_t)f * b.ntr;
+  uint32_t* dst = b.L[0] + ((size_t)t * b.nl + f) * b.ntr;
+  const bool pack = b.packRank && f < b.p;
+  const uint32_t* gr = b.grank + (size_t)f * b.n;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t carry = 0;
+  for (int base = 0; base < b.ntr; base += 32 * kIbwSteps) {
+    uint32_t r[kIbwSteps];
+#pragma unroll
+    for (int k = 0; k < kIbwSteps; ++k) {
+      const int j = base + 32 * k + lane;
+      r[k] = j < b.ntr ? src[j] : 0u;
+    }
+    bool keep[kIbwSteps];
+#pragma unroll
+    for (int k = 0; k < kIbwSteps; ++k) keep[k] = base + 32 * k + lane < b.ntr && w[r[k]] != 0;
+#pragma unroll
+    for (int k = 0; k < kIbwSteps; ++k) {
+      const unsigned bal = __ballot_sync(0xffffffffu, keep[k]);
+      if (keep[k]) dst[carry + __popc(bal & lt)] = pack ? r[k] | ((gr[r[k]] & 0x7FFFu) << 17) : r[k];
+      carry += __popc(bal);
+    }
   }
 }
 
@@ -2006,7 +2044,12 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
     k_inbag_scatter<<<items, kIbThreads, 0, s>>>(b, task_order, ibTiles, pb.ibPref);
     note_launch(2);
   } else {
+#ifdef RF_INBAG_CTA
     k_inbag_lists<<<b.B * b.nl, kThreads, 0, s>>>(b, task_order);
+#else
+    k_inbag_lists_warp<<<dim3((unsigned)((b.nl + kIbwWarps - 1) / kIbwWarps), (unsigned)b.B), 32 * kIbwWarps, 0, s>>>(
+        b, task_order);
+#endif
     note_launch();
   }
   {
@@ -2306,15 +2349,16 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   // trees per batch: per-level launch and sync costs are shared by the batch, so batches are
   // as large as the working-set budget allows (of the 180 GB HBM)
 #ifndef RF_LARGE_BMAX
-#define RF_LARGE_BMAX 128
+#define RF_LARGE_BMAX 512
 #endif
 #ifndef RF_LARGE_BUDGET_GB
-#define RF_LARGE_BUDGET_GB 16
+#define RF_LARGE_BUDGET_GB 32
 #endif
   int B = (int)std::max<size_t>(
       1, std::min<size_t>(RF_LARGE_BMAX, ((size_t)RF_LARGE_BUDGET_GB << 30) / std::max<size_t>(per_tree, 1)));
   B = std::min(B, (int)std::min<long long>(INT_MAX, (long long)INT_MAX / std::max(ntr, 1)));  // positions: int
   B = std::min(B, T);
+  B = (T + (T + B - 1) / B - 1) / ((T + B - 1) / B);  // equal batches (the same count of batches)
   LargePlan pl;
   pl.B = B;
   pl.nmax = (long long)B * open_max;

@@ -479,7 +479,9 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
   bid /= cta_per_mt;
   const int tl = bid % a.ntask;
   const int mi = bid / a.ntask;
-  const int m = a.mtrys[mi];
+  // (through a shuffle: the compiler keeps it in a register instead of re-reading the parameter bank
+  // with a dynamic index inside the search loop's divergent segment ends; A/B -2 %, rd2_38)
+  const int m = __shfl_sync(0xffffffffu, a.mtrys[mi], 0);
   constexpr bool extra = kExtra;
   const int fs = feat_stride_of(a);
   const bool nodraw = no_draws(m, p, a.tie_draw, extra);
@@ -930,6 +932,16 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
         // the feature (north_star) or the draw slot (R9); ascending aux = preferred among equal keys
         const bool tie_draw = a.tie_draw != 0;
         uint32_t auxb = ((uint32_t)(tie_draw ? j : f) << 16) | ((uint32_t)j << 8) | (uint32_t)st;
+        // the following segment (next draw slot of node k, or slot 0 of node k + 1): its feature
+        // and start, fetched one segment ahead so that the element loop reads the next segment's
+        // first entry on its main path (a select of the address) and a segment end only moves
+        // registers -- segment ends are divergent (lanes reach them at different steps) and, with
+        // ~10-element segments, fall in most lock-step iterations of the warp.  (Reads for a node
+        // past the last open one return stale bytes that are never used; the feature is clamped
+        // to < p so that the addresses formed from it stay inside shared memory.)
+        int nf, nst;
+        if (j + 1 < m) { nf = nodraw ? j + 1 : ws.feat[k * fs + j + 1]; nst = st; }
+        else { nf = nodraw ? 0 : min((int)ws.feat[(k + 1) * fs], p - 1); nst = cur.start[k + 1]; }
         uint32_t qh = 0u, qt = 0u;  // MAE candidate ring: head, tail
         if (kMae && kExtra) {
           #pragma unroll 1
@@ -945,10 +957,12 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           WLr += wv;
           SLr += (int64_t)wv * tr;
           const bool hasNext = i + 1 < ln;
-          // the entry after the segment's last one is read but not used (a row id < 256: every
-          // load below stays inside the CTA's shared memory)
-          uint8_t rn = L[lbase + st + i + 1];
-          uint32_t rkn = cs.lrank[lbase + rn];
+          // next element: this segment's next entry or the following segment's first (after the
+          // lane's last element a stale row id < 256 is read and not used: every load below stays
+          // inside the CTA's shared memory)
+          const int nfb = nf * ntr_max;
+          uint8_t rn = L[hasNext ? lbase + st + i + 1 : nfb + nst];
+          uint32_t rkn = cs.lrank[(hasNext ? lbase : nfb) + rn];
           wr = ws.w[rn];
           tr = cs.tq[rn];
           const uint32_t WL = WLr;
@@ -1005,19 +1019,17 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
               rkm1 = -1;
               ++k;
               rk = k;
-              st = cur.start[k];
               ln = cur.len[k];
               Wk = cur.W[k];
               Sk = cur.S[k];
             }
-            f = nodraw ? j : ws.feat[k * fs + j];
+            f = nf;
+            st = nst;
+            lbase = nfb;
             if (extra) xbj = ws.xb[k * fs + j];
-            lbase = f * ntr_max;
             auxb = ((uint32_t)(tie_draw ? j : f) << 16) | ((uint32_t)j << 8) | (uint32_t)st;
-            rn = L[lbase + st];
-            rkn = cs.lrank[lbase + rn];
-            wr = ws.w[rn];
-            tr = cs.tq[rn];
+            if (j + 1 < m) { nf = nodraw ? j + 1 : ws.feat[k * fs + j + 1]; }
+            else { nf = nodraw ? 0 : min((int)ws.feat[(k + 1) * fs], p - 1); nst = cur.start[k + 1]; }
           } else if (act) {
             ++i;
           }
