@@ -47,7 +47,10 @@ namespace rf {
 namespace {
 
 constexpr int kThreads = 128;
-// resident-CTA hint of the split search (A/B via RF_DEFS: 8 per SM beat 1, 10, 12; gathering the
+// resident-CTA hint of the split search (A/B via RF_DEFS: 8 per SM beat 1, 10, 12; caching the
+// list entries of pass 1 in shared memory for pass 2 (+8 KB per CTA) made the search 22 % slower
+// -- the shared carve-out costs L1 capacity the gathers need -- and two gathers (t_q shared, w per
+// tree) instead of the packed word 44 % slower, profiles/rd2_41_ab.txt; gathering the
 // ranks in pass 1 with the weights instead of in pass 2 measured 39 % slower, and walking the
 // cursor first to issue a thread's 16 weight/target gathers back to back 18 % slower)
 #ifndef RF_SEARCH_MINB
@@ -2462,7 +2465,9 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
   b.tr_rows = tr_rows_in;
   LCK(sc.alloc(&b.keys, (size_t)2 * B));
   LCK(sc.alloc(&b.w, (size_t)B * n + 4));
+#ifndef RF_NO_WT
   if (n > 256) LCK(sc.alloc(&b.wt, (size_t)B * n));  // packed (t_q << 8) | w gathers
+#endif
   if (!hist) LCK(sc.alloc(&b.side, (size_t)B * n));  // histogram mode decides from the bins
   // fused partition path (exact / ExtraTrees): go-left bits per row, staged per tree in
   // shared memory by the partition CTAs (n <= 2^20 rows: <= 128 KB)
