@@ -35,7 +35,28 @@ struct rf_forest {
   double* imp = nullptr;           // device [ntree][p] MDI decreases (rf_fit), null if imported
   uint64_t n_rows = 0;
   bool pooled = false;  // nodes / thr_index / tree_off from the device's stream-ordered pool
+  rf::Node8* n8 = nullptr;  // compact copy for batch inference (null if a tree has >= 2^24 nodes)
+  double* val = nullptr;    // [total_nodes] fp64 threshold / leaf value beside n8
 };
+
+namespace {
+// compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream
+cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
+#ifdef RF_NO_NODE8
+  return cudaSuccess;
+#endif
+  if (f->p >= 255 || f->total_nodes == 0) return cudaSuccess;
+  for (uint32_t t = 0; t < f->ntree; ++t)
+    if (f->h_tree_off[t + 1] - f->h_tree_off[t] >= (1ull << 24)) return cudaSuccess;
+  cudaError_t e = f->pooled ? cudaMallocAsync(&f->n8, f->total_nodes * sizeof(rf::Node8), s)
+                            : cudaMalloc(&f->n8, f->total_nodes * sizeof(rf::Node8));
+  if (e == cudaSuccess)
+    e = f->pooled ? cudaMallocAsync(&f->val, f->total_nodes * sizeof(double), s)
+                  : cudaMalloc(&f->val, f->total_nodes * sizeof(double));
+  if (e == cudaSuccess) e = rf::build_node8(f->nodes, f->total_nodes, f->n8, f->val, s);
+  return e;
+}
+}  // namespace
 
 namespace {
 
@@ -513,6 +534,7 @@ rf_status fit_core(const double* dX, uint64_t n, uint32_t p, const double* dy, c
     rf::note_launch();
     e = cudaGetLastError();
   }
+  if (e == cudaSuccess) e = attach_node8(f, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     rf_forest_free(f);
@@ -577,11 +599,15 @@ void rf_forest_free(rf_forest* f) {
     cudaFreeAsync(f->nodes, s);
     cudaFreeAsync(f->thr_index, s);
     cudaFreeAsync(f->tree_off, s);
+    if (f->n8) cudaFreeAsync(f->n8, s);
+    if (f->val) cudaFreeAsync(f->val, s);
     cudaSetDevice(cur);
   } else {
     cudaFree(f->nodes);
     cudaFree(f->thr_index);
     cudaFree(f->tree_off);
+    cudaFree(f->n8);
+    cudaFree(f->val);
   }
   cudaFree(f->leaf_of_row);
   cudaFree(f->imp);
@@ -647,7 +673,7 @@ static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, 
   {
     ProfScope ps("predict", s);
     CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s,
-                          few ? err : nullptr, f->total_nodes),
+                          few ? err : nullptr, f->total_nodes, f->n8, f->val),
        "predict");
   }
   if (host_out) {  // one synchronisation for result and error flag
@@ -1134,6 +1160,8 @@ rf_status rf_forest_import(const int32_t* feature, const uint32_t* left, const d
   if (e == cudaSuccess) e = cudaMemcpy(f->nodes, h.data(), f->total_nodes * sizeof(rf::Node16), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && thr_index) e = cudaMemcpy(f->thr_index, thr_index, f->total_nodes * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(f->tree_off, tree_off, (ntree + 1) * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = attach_node8(f, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { rf_forest_free(f); return cuda_fail(e, "import"); }
   *out = f;
   return RF_OK;

@@ -127,6 +127,8 @@ struct Batch {
   int64_t* med2;            // [NMAX][2] MAE: doubled weighted medians of the children (or the node)
   uint32_t* xb;             // [NMAX][m] ExtraTrees: boundary index in the (node, slot) segment or ~0
   const uint8_t* bins;      // [n][p] bin of every row (histogram mode)
+  const uint8_t* binsT;     // [p][n] the same, feature-major (the count pass's one-byte reads: a node's
+                            // rows are ascending in its list, so the top levels read dense runs)
   const double* cuts;       // [p][256] cut values (histogram mode)
   const int32_t* ncuts;     // [p]
   uint32_t* accN;           // [NMAX] rows going left (histogram mode)
@@ -1204,6 +1206,22 @@ __global__ void __launch_bounds__(256) k_bins(const double* __restrict__ X, int 
   }
 }
 
+// bins [n][p] -> binsT [p][n] through 64 x 64 shared tiles (both sides coalesced)
+__global__ void __launch_bounds__(256) k_bins_T(const uint8_t* __restrict__ bins, int n, int p, uint8_t* __restrict__ binsT) {
+  __shared__ uint8_t tile[64][65];
+  const long long r0 = (long long)blockIdx.x * 64;
+  const int f0 = blockIdx.y * 64;
+  for (int q = threadIdx.x; q < 64 * 64; q += blockDim.x) {
+    const int rr = q >> 6, ff = q & 63;
+    if (r0 + rr < n && f0 + ff < p) tile[rr][ff] = bins[(size_t)(r0 + rr) * p + f0 + ff];
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 64 * 64; q += blockDim.x) {
+    const int ff = q >> 6, rr = q & 63;
+    if (r0 + rr < n && f0 + ff < p) binsT[(size_t)(f0 + ff) * n + r0 + rr] = tile[rr][ff];
+  }
+}
+
 __global__ void k_hist_nchunks(Batch b, int cur, int g0, int g1, uint32_t* nch) {
   const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= g1) return;
@@ -1670,7 +1688,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count_hist(Batch b, int c
 #pragma unroll
   for (int it = 0; it < kPartItems; ++it)
     if (fc[it] != 0xFFFFFFFFu)
-      bits |= ((uint32_t)b.bins[(size_t)rr[it] * b.p + (fc[it] >> 16)] <= (fc[it] & 0xFFFFu) ? 1u : 0u) << it;
+      bits |= ((uint32_t)(b.binsT ? b.binsT[(size_t)(fc[it] >> 16) * b.n + rr[it]] : b.bins[(size_t)rr[it] * b.p + (fc[it] >> 16)]) <=
+                       (fc[it] & 0xFFFFu) ? 1u : 0u) << it;
 #pragma unroll
   for (int it = 0; it < kPartItems; ++it) {
     if (fc[it] == 0xFFFFFFFFu) continue;
@@ -2421,6 +2440,7 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
     LCK(sc.alloc(&cuts, (size_t)p * 256));
     LCK(sc.alloc(&ncuts, (size_t)p));
     LCK(sc.alloc(&bins, (size_t)n * p));
+    uint8_t* binsT = nullptr;
     {
       ProfScope ps("hist_binning", s);
       const int nch = (ntr + kCutChunk - 1) / kCutChunk;
@@ -2433,10 +2453,16 @@ static rf_status grow_forest(const DevData& d, const rf_params* prm, int mtry, i
       k_bins<<<dim3(std::min<unsigned>(nblk((long long)n * kBinFeat, 256), 148 * 8), (unsigned)((p + kBinFeat - 1) / kBinFeat)),
                256, 0, s>>>(d.X, n, p, cuts, ncuts, bins);
       note_launch(2);
+#ifndef RF_NO_BINST
+      LCK(sc.alloc(&binsT, (size_t)n * p));
+      k_bins_T<<<dim3((unsigned)((n + 63) / 64), (unsigned)((p + 63) / 64)), 256, 0, s>>>(bins, n, p, binsT);
+      note_launch();
+#endif
     }
     b.cuts = cuts;
     b.ncuts = ncuts;
     b.bins = bins;
+    b.binsT = binsT;
     LCK(sc.alloc(&b.accN, (size_t)pl.nmax));
     LCK(sc.alloc(&b.cmm, (size_t)pl.nmax * 4));
     hb.cap = std::max<long long>(1, std::min<long long>(pl.nmax, ((long long)2 << 30) / ((long long)mtry * 256 * 12)));

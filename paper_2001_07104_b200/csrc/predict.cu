@@ -8,6 +8,8 @@
 // forest (C5: 64 MB) stays L2-resident; the rows' features come from shared memory
 // (p <= 192, fp32 with an exact fp64 fallback) or from a feature-major copy of the row block (wider rows).  Few rows
 // (single-query latency) take a CTA per row with threads over trees.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "host_util.cuh"
 #include "predict.cuh"
@@ -173,6 +175,129 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
   if (mode == 2) s = exp(s / (double)T);
   out[r0 + i] = s;
 }
+// Compact-node variant (Node8, forests built with a compact copy): rows staged quantised (below),
+// the same tree groups, interleaving and tree-order sums; a walk carries the node index and reads
+// 8-byte nodes, the exact threshold (on an fp32 tie) and the leaf value from val[].  The staged
+// BFS prefix holds kStage8 nodes per tree for the same shared memory as the 16-byte layout's
+// kStage (one more tree level in shared memory): 19.2 -> 21.3 M predictions/s on C5 with fp32
+// staging (127 staged nodes beat 63 and 255, 12 trees per thread beat 10 and 16; rd2_43/44).
+#ifndef RF_PRED_STAGE8
+#define RF_PRED_STAGE8 127
+#endif
+#ifndef RF_PRED_G8
+#define RF_PRED_G8 12
+#endif
+constexpr int kG8 = RF_PRED_G8;
+// staged row values and node thresholds quantised by q = RN_bf16 o RN_fp32 (RF_PRED_FP32: RN_fp32):
+// q is monotonic, so q(x) < q(thr) implies x <= thr and q(x) > q(thr) implies x > thr; only
+// q(x) = q(thr) reads the fp64 values.  bf16 halves the staged rows (128 x 64 features: 16 KB) --
+// more resident CTAs -- for a few more fp64 tie reads: 21.3 -> 26.2 M predictions/s on C5
+// (profiles/rd2_44_ab_c5.txt)
+#ifndef RF_PRED_FP32
+typedef __nv_bfloat16 XStage;
+__device__ __forceinline__ float q_thr(double v) { return __bfloat162float(__float2bfloat16_rn(__double2float_rn(v))); }
+__device__ __forceinline__ XStage q_stage(double v) { return __float2bfloat16_rn(__double2float_rn(v)); }
+__device__ __forceinline__ float x_of(XStage v) { return __bfloat162float(v); }
+#else
+typedef float XStage;
+__device__ __forceinline__ float q_thr(double v) { return __double2float_rn(v); }
+__device__ __forceinline__ XStage q_stage(double v) { return __double2float_rn(v); }
+__device__ __forceinline__ float x_of(XStage v) { return v; }
+#endif
+__host__ __device__ constexpr size_t xstage_bytes(int p) { return ((size_t)p * kSmemStrideF * sizeof(XStage) + 15) / 16 * 16; }
+
+template <int kStage>
+__global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __restrict__ nodes,
+                                                            const double* __restrict__ val,
+                                                            const uint64_t* __restrict__ tree_off, int T,
+                                                            const double* __restrict__ X, long long n, int p,
+                                                            int mode, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char sm8[];  // [p][kSmemStrideF] rows, then [kG8][kStage] nodes
+  XStage* xsf8 = reinterpret_cast<XStage*>(sm8);
+  Node8* sn = reinterpret_cast<Node8*>(sm8 + xstage_bytes(p));
+  const long long r0 = (long long)blockIdx.x * kSmemRows;
+  const int nr = (int)min((long long)kSmemRows, n - r0);
+  const double* Xb = X + r0 * p;
+  for (int q = threadIdx.x; q < nr * p; q += kSmemRows) {
+    const int i = q / p, f = q - i * p;
+    xsf8[f * kSmemStrideF + i] = q_stage(Xb[q]);
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  const bool live = i < nr;  // (no early exit: every thread takes part in the node staging)
+  const XStage* x = xsf8 + min(i, nr - 1);
+  const double* xrow = Xb + (size_t)min(i, nr - 1) * p;
+  double s = 0.0;
+  int t = 0;
+  for (; t + kG8 <= T; t += kG8) {
+    if (kStage > 0) {
+      __syncthreads();  // the previous group's nodes are no longer read
+      for (int q = threadIdx.x; q < kG8 * kStage; q += kSmemRows) {
+        const int g = q / kStage, k = q - g * kStage;
+        const uint64_t o0 = __ldg(tree_off + t + g), o1 = __ldg(tree_off + t + g + 1);
+        if (o0 + k < o1) reinterpret_cast<uint2*>(sn)[q] = __ldg(reinterpret_cast<const uint2*>(nodes + o0 + k));
+      }
+      __syncthreads();
+    }
+    uint64_t base[kG8];
+    Node8 nd[kG8];
+    uint32_t idx[kG8];
+#pragma unroll
+    for (int g = 0; g < kG8; ++g) {
+      base[g] = __ldg(tree_off + t + g);
+      idx[g] = 0u;
+      nd[g] = kStage > 0 ? sn[g * kStage] : nodes[base[g]];
+    }
+    bool open = live;
+    while (open) {
+      open = false;
+#pragma unroll
+      for (int g = 0; g < kG8; ++g) {
+        const uint32_t f = nd[g].fl & 0xFFu;
+        if (f != 0xFFu) {
+          const float xf = x_of(x[f * kSmemStrideF]);
+          // q decides unless q(x) = q(thr) (monotonic rounding), then the fp64 values do
+          const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
+          idx[g] = (nd[g].fl >> 8) + (le ? 0u : 1u);
+          nd[g] = (kStage > 0 && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
+          open = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kG8; ++g) s += __ldg(val + base[g] + idx[g]);
+  }
+  if (!live) return;
+  for (; t < T; ++t) {
+    const uint64_t b0 = tree_off[t];
+    uint32_t id = 0;
+    Node8 nd = nodes[b0];
+    while ((nd.fl & 0xFFu) != 0xFFu) {
+      const uint32_t f = nd.fl & 0xFFu;
+      const float xf = x_of(x[f * kSmemStrideF]);
+      const bool le = xf < nd.tf || (xf == nd.tf && xrow[f] <= val[b0 + id]);
+      id = (nd.fl >> 8) + (le ? 0u : 1u);
+      nd = nodes[b0 + id];
+    }
+    s += val[b0 + id];
+  }
+  if (mode == 1) s = s / (double)T;
+  if (mode == 2) s = exp(s / (double)T);
+  out[r0 + i] = s;
+}
+
+__global__ void k_build_node8(const Node16* __restrict__ nodes, uint64_t total, Node8* __restrict__ n8,
+                              double* __restrict__ val) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total; q += (uint64_t)gridDim.x * blockDim.x) {
+    const Node16 nd = nodes[q];
+    Node8 c;
+    c.fl = nd.feat < 0 ? 0xFFu : ((uint32_t)nd.feat | (nd.left << 8));
+    c.tf = nd.feat < 0 ? 0.0f : q_thr(nd.v);
+    n8[q] = c;
+    val[q] = nd.v;
+  }
+}
+
 // rows [r0, r0 + cn) of X (row-major, n x p) -> XT (p x cn, feature-major), 32 x 32 tiles
 __global__ void k_transpose(const double* __restrict__ X, long long r0, long long cn, int p, double* __restrict__ XT) {
   __shared__ double tile[32][33];
@@ -245,12 +370,30 @@ __global__ void k_check_finite(const double* X, size_t total, int* err) {
 
 }  // namespace
 
+cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* val, cudaStream_t s) {
+  if (!total) return cudaSuccess;
+  const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148 * 16);
+  k_build_node8<<<(unsigned)blocks, 256, 0, s>>>(nodes, total, n8, val);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
                            long long n, int p, int mode, double* out, cudaStream_t s, int* err_few,
-                           uint64_t total_nodes) {
+                           uint64_t total_nodes, const Node8* n8, const double* val) {
   if (n <= 0) return cudaSuccess;
   if (err_few && n <= kFewRows) {  // latency path: rows checked for finiteness in-kernel
     k_predict_few<<<(unsigned)n, kFewThreads, 0, s>>>(nodes, tree_off, T, X, p, mode, out, err_few);
+    note_launch();
+    return cudaGetLastError();
+  }
+  if (n8 && val && p <= kSmemMaxP) {
+    const bool stage = RF_PRED_STAGE8 > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * 16384u;
+    const size_t smem = xstage_bytes(p) + (stage ? (size_t)kG8 * RF_PRED_STAGE8 * sizeof(Node8) : 0);
+    auto kern = stage ? k_predict_smem8<RF_PRED_STAGE8> : k_predict_smem8<0>;
+    cudaError_t e = allow_max_dynamic_smem(kern);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(n8, val, tree_off, T, X, n, p, mode, out);
     note_launch();
     return cudaGetLastError();
   }

@@ -12,9 +12,19 @@ constexpr long long kFewRows = 256;
 // for non-finite values (flag bit 0); otherwise the caller checks separately.
 // total_nodes (if known): forests of shallow trees (<= 16384 nodes per tree on average) have
 // the top BFS nodes of each tree group staged in shared memory (see k_predict_smem).
+// Compact copy of a forest for batch inference: 8-byte nodes (feature | left child << 8, the
+// feature 0xFF marking a leaf; the threshold rounded to fp32) and the exact fp64 value of every
+// node (threshold or leaf value) beside them.  Trees of < 2^24 nodes, p < 255.
+struct __align__(8) Node8 {
+  uint32_t fl;  // feature (0xFF: leaf) | tree-local left child << 8
+  float tf;     // fp32(threshold), round to nearest (exact decisions: see k_predict_smem8)
+};
+cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* val, cudaStream_t s);
+// n8 / val (optional): the compact copy; batches then walk 8-byte nodes (twice the nodes per
+// staged byte and per cache line).
 cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
                            long long n, int p, int mode, double* out, cudaStream_t s, int* err_few = nullptr,
-                           uint64_t total_nodes = 0);
+                           uint64_t total_nodes = 0, const Node8* n8 = nullptr, const double* val = nullptr);
 cudaError_t predict_finalize(const double* partial, long long n, int T, int target, double* out,
                              cudaStream_t s);
 cudaError_t check_finite(const double* X, size_t total, int* err, cudaStream_t s);
