@@ -15,8 +15,9 @@ constexpr int kMaxMtry = 16;        // grid points per launch
 #endif
 // warps per CTA (launch bound 32 x kSmallMaxWpb threads); the host picks the count with the most
 // resident warps (A/B on the full study, round 1: up to 16 warps in one CTA per SM beat 2 CTAs x 7
-// warps by 5 %; round 2, after the search's segment-end prefetch: 14 warps beat 16 by 3 % and 12
-// (158 registers) lost 16 %, 20 (96 registers) 14 %: profiles/rd2_32_ab_occ.txt, rd2_36/38_ab_c2.txt)
+// warps by 5 %; round 2, after the search's segment-end prefetch: the 14-warp bound -- on the C2
+// shapes the host then runs two CTAs of 8 warps per SM -- beat one CTA of 16 by 3 %; 12 (158
+// registers) lost 16 %, 20 (96 registers) 14 %: profiles/rd2_32_ab_occ.txt, rd2_36/38_ab_c2.txt)
 constexpr int kSmallMaxWpb = RF_SMALL_MAXWPB;
 
 struct SmallArgs {
