@@ -36,8 +36,11 @@ RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
    n > 2^20) instead of the fused multi-list partition.  "hist_node_chunk_cap"
    = c > 0 caps the histogram mode's node chunk (nodes whose histograms are
    built and searched per pass; otherwise sized by a 2 GB buffer) at c, so
-   small tests reach the multi-chunk loop; 0 restores the default.  Unknown
-   names and negative caps return RF_E_ARG. */
+   small tests reach the multi-chunk loop; 0 restores the default.
+   "predict_node16" = 1 makes batched inference walk the forest's 16-byte nodes
+   with fp32 staging instead of its compact 8-byte copy with bf16 staging (both
+   exact; tests run each); 0 restores the default.  Unknown names and negative
+   caps return RF_E_ARG. */
 RF_API rf_status rf_debug_set_option(const char* name, int64_t value);
 #ifdef __cplusplus
 }

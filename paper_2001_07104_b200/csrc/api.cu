@@ -40,6 +40,8 @@ struct rf_forest {
 };
 
 namespace {
+std::atomic<bool> g_opt_predict_node16{false};  // test switch (rf_debug_set_option "predict_node16")
+
 // compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream
 cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
 #ifdef RF_NO_NODE8
@@ -673,7 +675,8 @@ static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, 
   {
     ProfScope ps("predict", s);
     CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s,
-                          few ? err : nullptr, f->total_nodes, f->n8, f->val),
+                          few ? err : nullptr, f->total_nodes, g_opt_predict_node16 ? nullptr : f->n8,
+                          g_opt_predict_node16 ? nullptr : f->val),
        "predict");
   }
   if (host_out) {  // one synchronisation for result and error flag
@@ -1233,6 +1236,10 @@ rf_status rf_debug_set_option(const char* name, int64_t value) {
   if (!name) return fail(RF_E_ARG, "name is NULL");
   if (!strcmp(name, "large_tiled_partition")) {
     rf::g_opt_tiled_partition = value != 0;
+    return RF_OK;
+  }
+  if (!strcmp(name, "predict_node16")) {  // batches walk the 16-byte nodes (the compact copy is ignored)
+    g_opt_predict_node16 = value != 0;
     return RF_OK;
   }
   if (!strcmp(name, "hist_node_chunk_cap")) {

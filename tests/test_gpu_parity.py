@@ -141,8 +141,17 @@ def test_fit_device_path_matches_host():
 
 
 # ------------------------------------------------------------ predict ---
+@pytest.fixture(params=[0, 1], ids=["node8_bf16", "node16_fp32"])
+def node_layout(request):
+    """Batched inference through the compact 8-byte nodes with bf16 staging (default) and through
+    the 16-byte nodes with fp32 staging (rf_debug_set_option "predict_node16")."""
+    rfg.debug_set_option("predict_node16", request.param)
+    yield request.param
+    rfg.debug_set_option("predict_node16", 0)
+
+
 @pytest.mark.parametrize("target", [0, 1])
-def test_predict_parity(target):
+def test_predict_parity(target, node_layout):
     X, y = datagen.paper_shaped(189, "P100", "time")
     Q = datagen.paper_shaped(500, "P100", "time", seed=123)[0]
     of = oracle.fit(X, y, ntree=50, seed=3, mtry=4, target=target)
@@ -671,7 +680,7 @@ def test_large_partition_paths_agree():
         rfg.debug_set_option("no_such_option", 1)
 
 
-def test_predict_c5_shape():
+def test_predict_c5_shape(node_layout):
     """Config 5 shape: forest grown on scaled(20k, 64) with max_depth 12 (30 trees: two
     12-tree groups of the batched kernel plus a remainder), 200k query rows through the
     batched kernel (device and host entry points) vs the oracle, <= 1e-9 relative."""
@@ -685,7 +694,7 @@ def test_predict_c5_shape():
     np.testing.assert_allclose(rfg.predict(gf, Q[:777]), want[:777], rtol=RTOL, atol=0)
 
 
-def test_predict_threshold_ties():
+def test_predict_threshold_ties(node_layout):
     """Batched inference on query values at and next to the split thresholds (x == thr goes
     left; neighbours one ulp away, which share the threshold's fp32 rounding, must be decided
     in fp64) -- thresholds taken from the oracle's forest."""
@@ -701,6 +710,26 @@ def test_predict_threshold_ties():
         for _ in range(6):
             k = rnd.integers(0, len(feats))
             Q[r, feats[k]] = [thrs[k], np.nextafter(thrs[k], np.inf), np.nextafter(thrs[k], -np.inf)][r % 3]
+    np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), oracle.predict(of, Q), rtol=RTOL, atol=0)
+
+
+def test_predict_quantised_ties(node_layout):
+    """Query values that round to the threshold's bf16 (and, some, fp32) value but differ from it
+    in fp64 -- thr * (1 +- 2^-k) for k = 9 .. 30 -- so the staged comparison ties and the decision
+    must come from the fp64 row and threshold; every internal node's threshold is hit."""
+    X, y = datagen.scaled(3_000, 16)
+    of = oracle.fit(X, y, ntree=24, seed=5, mtry=5, target=1, max_depth=10)
+    gf = rfg.fit(X, y, ntree=24, seed=5, mtry=5, target=1, max_depth=10)
+    _compare_forest(gf, of, X)
+    rnd = np.random.default_rng(1)
+    feats = np.concatenate([t.feature[t.feature >= 0] for t in of.trees])
+    thrs = np.concatenate([t.thr_value[t.feature >= 0] for t in of.trees])
+    Q = X[rnd.integers(0, len(X), 3000)].copy()
+    for r in range(len(Q)):
+        for _ in range(8):
+            k = rnd.integers(0, len(feats))
+            e = int(rnd.integers(9, 31))
+            Q[r, feats[k]] = thrs[k] * (1.0 + (1 if r % 2 else -1) * 2.0 ** -e)
     np.testing.assert_allclose(rfg.predict(gf, _cuda(Q)).cpu().numpy(), oracle.predict(of, Q), rtol=RTOL, atol=0)
 
 
