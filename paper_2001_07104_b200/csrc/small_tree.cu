@@ -998,7 +998,11 @@ __global__ void __launch_bounds__(32 * kSmallMaxWpb, (kSmallMaxWpb <= 8 ? 2 : 1)
           } else {
             key = 0ull;
             const long long kb = __double_as_longlong(__dadd_rn(gl, gr));
-            if (cand && (kb > rkm1 || (kb == rkm1 && aux < raux))) { rkm1 = kb; raux = aux; rWL = WL; rSL = SL; }
+            // a lane's running best improves O(log n) times over a segment: the update is a rare
+            // branch rather than selects on every candidate
+            if (__builtin_expect(cand && kb >= rkm1, 0)) {
+              if (kb > rkm1 || aux < raux) { rkm1 = kb; raux = aux; rWL = WL; rSL = SL; }
+            }
           }
           ncand += cand;
           if (kMae && better(key, aux, rkey, raux)) { rkey = key; raux = aux; rWL = WL; rSL = SL; }
