@@ -50,7 +50,9 @@ constexpr int kThreads = 128;
 // resident-CTA hint of the split search (A/B via RF_DEFS: 8 per SM beat 1, 10, 12; caching the
 // list entries of pass 1 in shared memory for pass 2 (+8 KB per CTA) made the search 22 % slower
 // -- the shared carve-out costs L1 capacity the gathers need -- and two gathers (t_q shared, w per
-// tree) instead of the packed word 44 % slower, profiles/rd2_41_ab.txt; gathering the
+// tree) instead of the packed word 44 % slower, profiles/rd2_41_ab.txt; deciding the candidate
+// flags in pass 1 (bit 0 of the staged t_q) so that pass 2 reads no list entries: neutral,
+// rd2_49_ab_c3.txt; gathering the
 // ranks in pass 1 with the weights instead of in pass 2 measured 39 % slower, and walking the
 // cursor first to issue a thread's 16 weight/target gathers back to back 18 % slower)
 #ifndef RF_SEARCH_MINB
