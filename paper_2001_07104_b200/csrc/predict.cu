@@ -82,13 +82,16 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
 #ifndef RF_PRED_SMEM_G
 #define RF_PRED_SMEM_G 12
 #endif
-constexpr int kSmemRows = 128, kSmemMaxP = 192, kGs = RF_PRED_SMEM_G;
+#ifndef RF_PRED_ROWS
+#define RF_PRED_ROWS 128
+#endif
+constexpr int kSmemRows = RF_PRED_ROWS, kSmemMaxP = 192, kGs = RF_PRED_SMEM_G;
 
 // Features staged as fp32 (half the shared memory per row -> more resident warps).  The
 // comparison stays exact: rounding to nearest is monotonic, so float(x) < float(thr)
 // implies x <= thr and float(x) > float(thr) implies x > thr; only float(x) ==
 // float(thr) is undecided, and then the fp64 value is read from X.
-constexpr int kSmemStrideF = 129;
+constexpr int kSmemStrideF = kSmemRows + 1;
 
 __device__ __forceinline__ bool le_exact(float xf, double thr, const double* xrow, int f) {
   const float tf = __double2float_rn(thr);
