@@ -64,7 +64,11 @@ typedef enum {
   RF_E_CUDA = 7,           /* CUDA runtime error (incl. no device)                */
   RF_E_OOM = 8,            /* device allocation failed                            */
   RF_E_OVERFLOW = 9,       /* size limits of a kernel variant exceeded           */
-  RF_E_UNSUPPORTED = 10    /* valid request outside what this build implements    */
+  RF_E_UNSUPPORTED = 10,   /* valid request outside what this build implements    */
+  RF_E_INEXACT = 11        /* LOG target: ln(y) of some y could not be certified  */
+                           /* correctly rounded (within ~2^-94 relative of a      */
+                           /* rounding boundary; R20) -- no result is   */
+                           /* produced rather than a possibly misrounded t_q      */
 } rf_status;
 
 /* Split rule.  EXACT: every boundary between consecutive distinct in-node
@@ -132,7 +136,8 @@ typedef struct rf_forest rf_forest;
    n rows (task 0).  Tree t uses Philox key k_t = f(seed, task 0, t) (R15), so
    a forest of T trees is the prefix of any larger one and a tree shard is
    identical to the same trees of the full forest.
-   Errors: RF_E_EMPTY, RF_E_NONFINITE, RF_E_NONPOSITIVE_Y (LOG), RF_E_ARG. */
+   Errors: RF_E_EMPTY, RF_E_NONFINITE, RF_E_NONPOSITIVE_Y (LOG), RF_E_INEXACT
+   (LOG), RF_E_ARG. */
 RF_API rf_status rf_fit(const double* X, uint64_t n, uint32_t p, const double* y, const rf_params* prm,
                  rf_forest** out);
 /* Device twin.  Synchronises `stream` once (forest size). */
@@ -185,7 +190,7 @@ RF_API rf_status rf_make_folds_masked_dev(const double* dy, uint64_t n, uint32_t
    [n_mtry][n_ntree][repeats][k] in percent (Eq. 1, on raw y).  Optional
    pred [n_mtry][n_ntree][repeats][n]: each row's prediction by the forest of
    its test fold (NaN for rows with fold -1); pass NULL to skip.
-   Errors: RF_E_NONPOSITIVE_Y (any y <= 0), RF_E_TOO_FEW, RF_E_ARG
+   Errors: RF_E_NONPOSITIVE_Y (any y <= 0), RF_E_INEXACT (LOG), RF_E_TOO_FEW, RF_E_ARG
    (tree_begin/end set: use rf_cv_partial), RF_E_UNSUPPORTED (n_tr > 255 in
    this build's exact small-tree kernel without the large path).
    The _dev twin synchronises `stream` once (per-task sizes). */

@@ -39,8 +39,11 @@ RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
    small tests reach the multi-chunk loop; 0 restores the default.
    "predict_node16" = 1 makes batched inference walk the forest's 16-byte nodes
    with fp32 staging instead of its compact 8-byte copy with bf16 staging (both
-   exact; tests run each); 0 restores the default.  Unknown names and negative
-   caps return RF_E_ARG. */
+   exact; tests run each); 0 restores the default.  "ln_cert_margin_log2" = e
+   in [-200, -2] sets the margin of ln's rounding test (ddlog.cuh) to 2^e
+   instead of 2^-94, so a wide margin reaches the RF_E_INEXACT path; 0
+   restores the default.  Unknown names, negative caps and margins outside
+   that range return RF_E_ARG. */
 RF_API rf_status rf_debug_set_option(const char* name, int64_t value);
 #ifdef __cplusplus
 }

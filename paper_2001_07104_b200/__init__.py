@@ -23,9 +23,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RFGPU_LIB") or os.path.join(_HERE, "librfgpu.so")
 
 OK, E_ARG, E_EMPTY, E_NONFINITE, E_NONPOSITIVE_Y, E_ARITY, E_TOO_FEW, E_CUDA, E_OOM, E_OVERFLOW, \
-    E_UNSUPPORTED = range(11)
+    E_UNSUPPORTED, E_INEXACT = range(12)
 STATUS_NAMES = ["OK", "ARG", "EMPTY", "NONFINITE", "NONPOSITIVE_Y", "ARITY", "TOO_FEW", "CUDA", "OOM",
-                "OVERFLOW", "UNSUPPORTED"]
+                "OVERFLOW", "UNSUPPORTED", "INEXACT"]
 SPLIT_EXACT, SPLIT_HIST256, SPLIT_EXTRA = 0, 1, 2
 TARGET_IDENTITY, TARGET_LOG = 0, 1
 CRITERION_MSE, CRITERION_MAE = 0, 1

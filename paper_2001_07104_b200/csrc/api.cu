@@ -128,6 +128,7 @@ rf_status read_err(const int* derr, cudaStream_t s) {
   if (h & rf::kErrNonFinite) return fail(RF_E_NONFINITE, "non-finite value in X or y");
   if (h & rf::kErrNonPositive) return fail(RF_E_NONPOSITIVE_Y, "y <= 0 (LOG target or CV / MAPE)");
   if (h & rf::kErrOverflow) return fail(RF_E_OVERFLOW, "kernel size limit exceeded");
+  if (h & rf::kErrInexact) return fail(RF_E_INEXACT, "ln(y) not certified correctly rounded (LOG target)");
   return RF_OK;
 }
 
@@ -1240,6 +1241,11 @@ rf_status rf_debug_set_option(const char* name, int64_t value) {
   }
   if (!strcmp(name, "predict_node16")) {  // batches walk the 16-byte nodes (the compact copy is ignored)
     g_opt_predict_node16 = value != 0;
+    return RF_OK;
+  }
+  if (!strcmp(name, "ln_cert_margin_log2")) {  // widened margin: reaches the RF_E_INEXACT path
+    if (value != 0 && (value > -2 || value < -200)) return fail(RF_E_ARG, "ln_cert_margin_log2 must be in [-200, -2] or 0");
+    rf::g_opt_ln_margin_log2 = (int)value;
     return RF_OK;
   }
   if (!strcmp(name, "hist_node_chunk_cap")) {

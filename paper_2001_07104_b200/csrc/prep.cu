@@ -34,14 +34,19 @@ __global__ void k_prep_X(const double* __restrict__ X, double* __restrict__ Xc, 
 }
 
 __global__ void k_prep_y(const double* __restrict__ y, double* __restrict__ t, int n, int target,
-                         int require_pos, unsigned long long* maxbits, int* err) {
+                         int require_pos, unsigned long long* maxbits, int* err, int ln_margin_log2) {
   unsigned long long m = 0;
   int e = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double v = y[i];
     if (!isfinite(v)) { e |= kErrNonFinite; v = 1.0; }
     if ((require_pos || target == 1) && !(v > 0.0)) { e |= kErrNonPositive; v = 1.0; }
-    double tv = (target == 1) ? ln_correctly_rounded(v) : v;
+    double tv = v;
+    if (target == 1) {
+      bool certified;
+      tv = ln_cr_checked(v, certified, ln_margin_log2);
+      if (!certified) e |= kErrInexact;  // ln y too close to a rounding boundary (ddlog.cuh)
+    }
     t[i] = tv;
     unsigned long long b = (unsigned long long)__double_as_longlong(fabs(tv));
     m = b > m ? b : m;
@@ -78,7 +83,10 @@ __global__ void k_quant(const double* __restrict__ t, int n, const unsigned long
 
 __global__ void k_ln(const double* y, double* out, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = ln_correctly_rounded(y[i]);
+  {
+    bool certified;
+    out[i] = ln_cr_checked(y[i], certified);
+  }
 }
 
 // ---- presort, small n: one CTA per feature, column in shared memory
@@ -168,6 +176,8 @@ __global__ void k_rank_sorted(const unsigned long long* __restrict__ skeys,
 
 }  // namespace
 
+int g_opt_ln_margin_log2 = 0;
+
 cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int target,
                          int require_pos, int guard, DevData& d, double* scratch_t, cudaStream_t s) {
   unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(scratch_t + n);
@@ -177,7 +187,8 @@ cudaError_t prep_targets(const double* dX, const double* dy, int n, int p, int t
   k_prep_X<<<gx > 0 ? gx : 1, 256, 0, s>>>(dX, d.X, total, d.err);
   note_launch();
   int gy = std::min((n + 255) / 256, 148 * 8);
-  k_prep_y<<<gy > 0 ? gy : 1, 256, 0, s>>>(dy, scratch_t, n, target, require_pos, maxbits, d.err);
+  const int margin = g_opt_ln_margin_log2 ? g_opt_ln_margin_log2 : kLnCertLog2;
+  k_prep_y<<<gy > 0 ? gy : 1, 256, 0, s>>>(dy, scratch_t, n, target, require_pos, maxbits, d.err, margin);
   note_launch();
   k_quant<<<gy > 0 ? gy : 1, 256, 0, s>>>(scratch_t, n, maxbits, guard, d.tq, d.F);
   note_launch();

@@ -6,7 +6,9 @@
 
 namespace rf {
 
-enum : int { kErrNonFinite = 1, kErrNonPositive = 2, kErrOverflow = 4 };
+enum : int { kErrNonFinite = 1, kErrNonPositive = 2, kErrOverflow = 4, kErrInexact = 8 };
+// test switch (rf_debug_set_option "ln_cert_margin_log2"): margin of ln's rounding test, 0 = default
+extern int g_opt_ln_margin_log2;
 
 // Device-resident prepared dataset.
 struct DevData {

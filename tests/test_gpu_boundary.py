@@ -209,3 +209,27 @@ def test_ln_device_bit_exact_wide():
     want = oracle.quantize(y, 1)[0]
     bad = np.nonzero(got.view(np.int64) != want.view(np.int64))[0]
     assert bad.size == 0, (bad.size, y[bad[:5]], got[bad[:5]], want[bad[:5]])
+
+
+def test_ln_uncertified_fails_loudly():
+    """ln's rounding test (ddlog.cuh, R20): a value it cannot certify makes a LOG-target call fail
+    with RF_E_INEXACT instead of quantising a possibly misrounded ln.  A widened margin (test switch)
+    reaches the path; the default margin certifies the same data, and the near-1 hard cases
+    (y = 1 - 2^-52, ...) certify and match the oracle."""
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    rfg.debug_set_option("ln_cert_margin_log2", -20)
+    try:
+        with pytest.raises(rfg.RFError) as ex:
+            rfg.fit(X, y, ntree=2, mtry=3, target=1, seed=1)
+        assert ex.value.code == rfg.E_INEXACT
+        rfg.fit(X, y, ntree=2, mtry=3, target=0, seed=1)  # the identity target takes no ln
+    finally:
+        rfg.debug_set_option("ln_cert_margin_log2", 0)
+    rfg.fit(X, y, ntree=2, mtry=3, target=1, seed=1)
+    hard = np.concatenate([1.0 + np.arange(1, 4000) * 2.0 ** -52, 1.0 - np.arange(1, 4000) * 2.0 ** -53])
+    Xh = np.random.default_rng(5).uniform(0, 1, (hard.size, 3))
+    f = rfg.fit(Xh, hard, ntree=1, mtry=3, target=1, seed=1)  # certified: no RF_E_INEXACT
+    assert f is not None
+    got = rfg.debug_ln(_cuda(hard)).cpu().numpy()
+    want = oracle.quantize(hard, 1)[0]
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))

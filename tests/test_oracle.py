@@ -64,6 +64,8 @@ def test_ln_correctly_rounded():
     rnd = random.Random(3)
     vals = [1.0, 2.0, math.e, 0.5, 1e-300, 1e300, 7.0, 1000.0, 100000.0]
     vals += [10 ** rnd.uniform(-3, 9) for _ in range(3000)]
+    # structured hard cases: ln y within ~2^-105 relative of a rounding midpoint (y = 1 - 2^-52, ...)
+    vals += [1.0 + k * 2.0 ** -52 for k in range(1, 300)] + [1.0 - k * 2.0 ** -53 for k in range(1, 300)]
     for v in vals:
         assert oracle.ln(v) == micro.ln_cr(v), v
 
