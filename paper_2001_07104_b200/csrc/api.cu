@@ -35,26 +35,64 @@ struct rf_forest {
   double* imp = nullptr;           // device [ntree][p] MDI decreases (rf_fit), null if imported
   uint64_t n_rows = 0;
   bool pooled = false;  // nodes / thr_index / tree_off from the device's stream-ordered pool
-  rf::Node8* n8 = nullptr;  // compact copy for batch inference (null if a tree has >= 2^24 nodes)
-  double* val = nullptr;    // [total_nodes] fp64 threshold / leaf value beside n8
+  rf::Node8* n8 = nullptr;  // compact copy for batch inference (null if a tree has >= 2^23 nodes)
+  double* val = nullptr;    // fp64 threshold / leaf value beside n8 (same slots)
+  uint64_t* n8_off = nullptr;  // device [ntree + 1] slot offsets of the blocked layout (null: tree_off)
 };
 
 namespace {
 std::atomic<bool> g_opt_predict_node16{false};  // test switch (rf_debug_set_option "predict_node16")
 
-// compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream
+// compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream: the blocked
+// layout (two-level 32-byte blocks below a BFS prefix, predict.cu) when every tree is BFS-ordered
+// (fitted forests; imported ones if they are), else the BFS-slot copy
 cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
 #ifdef RF_NO_NODE8
   return cudaSuccess;
 #endif
   if (f->p >= 255 || f->total_nodes == 0) return cudaSuccess;
   for (uint32_t t = 0; t < f->ntree; ++t)
-    if (f->h_tree_off[t + 1] - f->h_tree_off[t] >= (1ull << 24)) return cudaSuccess;
-  cudaError_t e = f->pooled ? cudaMallocAsync(&f->n8, f->total_nodes * sizeof(rf::Node8), s)
-                            : cudaMalloc(&f->n8, f->total_nodes * sizeof(rf::Node8));
-  if (e == cudaSuccess)
-    e = f->pooled ? cudaMallocAsync(&f->val, f->total_nodes * sizeof(double), s)
-                  : cudaMalloc(&f->val, f->total_nodes * sizeof(double));
+    if (f->h_tree_off[t + 1] - f->h_tree_off[t] >= (1ull << 23)) return cudaSuccess;
+  auto dalloc = [&](auto** p, size_t bytes) {
+    return f->pooled ? cudaMallocAsync((void**)p, bytes, s) : cudaMalloc((void**)p, bytes);
+  };
+  auto dfree = [&](void* p) { if (p) { if (f->pooled) cudaFreeAsync(p, s); else cudaFree(p); } };
+  const int T = (int)f->ntree;
+#ifndef RF_PRED_NOBLOCKS
+  if (T <= 65536) {
+    uint64_t* slots = nullptr;
+    uint32_t* lev = nullptr;
+    int* nlev = nullptr;
+    int* bad = nullptr;
+    cudaError_t e = dalloc(&slots, (size_t)T * 8);
+    if (e == cudaSuccess) e = dalloc(&lev, (size_t)T * rf::kBlkLevStride * 4);
+    if (e == cudaSuccess) e = dalloc(&nlev, (size_t)T * 4);
+    if (e == cudaSuccess) e = dalloc(&bad, 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, 4, s);
+    if (e == cudaSuccess) e = rf::node8_blocked_count(f->nodes, f->tree_off, T, slots, lev, nlev, bad, s);
+    std::vector<uint64_t> hs((size_t)T + 1, 0);
+    int hbad = 1;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data() + 1, slots, (size_t)T * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && !hbad) {
+      for (int t = 0; t < T; ++t) hs[t + 1] += hs[t];  // exclusive offsets
+      const uint64_t total = hs[T];
+      e = dalloc(&f->n8_off, ((size_t)T + 1) * 8);
+      if (e == cudaSuccess) e = dalloc(&f->n8, total * sizeof(rf::Node8));
+      if (e == cudaSuccess) e = dalloc(&f->val, total * sizeof(double));
+      if (e == cudaSuccess) e = cudaMemcpyAsync(f->n8_off, hs.data(), ((size_t)T + 1) * 8, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(f->n8, 0xFF, total * sizeof(rf::Node8), s);  // padding: leaves
+      if (e == cudaSuccess) e = cudaMemsetAsync(f->val, 0, total * sizeof(double), s);
+      if (e == cudaSuccess) e = rf::node8_blocked_build(f->nodes, f->tree_off, T, f->n8_off, lev, nlev, f->n8, f->val, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // (hs is freed on return)
+    }
+    dfree(slots); dfree(lev); dfree(nlev); dfree(bad);
+    if (e != cudaSuccess || !hbad) return e;
+  }
+#endif
+  cudaError_t e = dalloc(&f->n8, f->total_nodes * sizeof(rf::Node8));
+  if (e == cudaSuccess) e = dalloc(&f->val, f->total_nodes * sizeof(double));
   if (e == cudaSuccess) e = rf::build_node8(f->nodes, f->total_nodes, f->n8, f->val, s);
   return e;
 }
@@ -604,6 +642,7 @@ void rf_forest_free(rf_forest* f) {
     cudaFreeAsync(f->tree_off, s);
     if (f->n8) cudaFreeAsync(f->n8, s);
     if (f->val) cudaFreeAsync(f->val, s);
+    if (f->n8_off) cudaFreeAsync(f->n8_off, s);
     cudaSetDevice(cur);
   } else {
     cudaFree(f->nodes);
@@ -611,6 +650,7 @@ void rf_forest_free(rf_forest* f) {
     cudaFree(f->tree_off);
     cudaFree(f->n8);
     cudaFree(f->val);
+    cudaFree(f->n8_off);
   }
   cudaFree(f->leaf_of_row);
   cudaFree(f->imp);
@@ -677,7 +717,7 @@ static rf_status predict_core(const rf_forest* f, const double* dX, uint64_t n, 
     ProfScope ps("predict", s);
     CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX, (long long)n, (int)p, mode, dout, s,
                           few ? err : nullptr, f->total_nodes, g_opt_predict_node16 ? nullptr : f->n8,
-                          g_opt_predict_node16 ? nullptr : f->val),
+                          g_opt_predict_node16 ? nullptr : f->val, f->n8_off),
        "predict");
   }
   if (host_out) {  // one synchronisation for result and error flag

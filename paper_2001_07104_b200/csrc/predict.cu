@@ -14,6 +14,8 @@
 #include "host_util.cuh"
 #include "predict.cuh"
 
+#include <cub/block/block_scan.cuh>
+
 #include <algorithm>
 
 namespace rf {
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
           const float xf = x_of(x[f * kSmemStrideF]);
           // q decides unless q(x) = q(thr) (monotonic rounding), then the fp64 values do
           const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
-          idx[g] = (nd[g].fl >> 8) + (le ? 0u : 1u);
+          idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? 4u : 1u));
           nd[g] = (kStage > 0 && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
           open = true;
         }
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
       const uint32_t f = nd.fl & 0xFFu;
       const float xf = x_of(x[f * kSmemStrideF]);
       const bool le = xf < nd.tf || (xf == nd.tf && xrow[f] <= val[b0 + id]);
-      id = (nd.fl >> 8) + (le ? 0u : 1u);
+      id = ((nd.fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd.fl >> 31) ? 4u : 1u));
       nd = nodes[b0 + id];
     }
     s += val[b0 + id];
@@ -298,6 +300,128 @@ __global__ void k_build_node8(const Node16* __restrict__ nodes, uint64_t total, 
     c.tf = nd.feat < 0 ? 0.0f : q_thr(nd.v);
     n8[q] = c;
     val[q] = nd.v;
+  }
+}
+
+// ---- blocked compact layout (fitted, BFS-ordered forests).  Per tree: BFS levels 0..6 (<= 127
+// nodes) keep their BFS slots 0..126 (slot 127 is padding); below them the tree is cut into two-level
+// blocks of 4 slots [P, left child, right child, pad] (32 bytes, one DRAM/L2 sector), P a node at a
+// depth 7, 9, 11, ...; the blocks of one level are numbered in BFS order, so sibling blocks are
+// adjacent.  A walk then misses L1 once per two levels below the prefix (the child of P is in P's
+// sector).  Child addressing stays "left + (go right ? stride : 0)": stride 1 inside the prefix and
+// from P to its children, 4 (the next block) from a depth-6 or second-level node to its children,
+// flagged by bit 31 of the node word (left slot < 2^23).
+constexpr int kBlkMaxLevels = kBlkLevStride - 1;
+constexpr uint32_t kBlkPrefix = 128;
+
+__device__ __forceinline__ bool blk_root_depth(int d) { return d >= 7 && ((d - 7) & 1) == 0; }
+
+// level d of a BFS tree: [s_d, s_{d+1}); s_{d+1} - s_d = 2 x (internal nodes of level d - 1).  One CTA
+// per tree: lev[t][d] = s_d (d <= levels), nlev[t] = levels, slots[t] = 128 + 4 x (nodes at
+// block-root depths); bad[0] |= 1 if a tree is not in the BFS order this assumes (children of the
+// j-th internal node of a level at s_{d+1} + 2j), is deeper than kBlkMaxLevels or needs >= 2^23 slots.
+__global__ void __launch_bounds__(256) k_blk_count(const Node16* __restrict__ nodes, const uint64_t* __restrict__ tree_off,
+                                                   uint64_t* __restrict__ slots, uint32_t* __restrict__ lev,
+                                                   int* __restrict__ nlev, int* bad) {
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t s_carry;
+  const int t = blockIdx.x;
+  const uint64_t o0 = tree_off[t], len = tree_off[t + 1] - o0;
+  const Node16* tn = nodes + o0;
+  uint32_t* lv = lev + (size_t)t * (kBlkMaxLevels + 1);
+  uint64_t st = 0, en = 1, roots = 0;
+  bool fail = false;
+  int d = 0;
+  while (st < en) {
+    if (en > len || d >= kBlkMaxLevels) { fail = true; break; }  // (uniform: every thread has st, en)
+    if (threadIdx.x == 0) { s_carry = 0; lv[d] = (uint32_t)st; }
+    __syncthreads();
+    for (uint64_t b = st; b < en; b += 256) {
+      const uint64_t i = b + threadIdx.x;
+      const uint32_t in = (i < en && tn[i].feat >= 0) ? 1u : 0u;
+      uint32_t ex, tot;
+      BS(tmp).ExclusiveSum(in, ex, tot);
+      const uint32_t c0 = s_carry;
+      if (in && tn[i].left != en + 2ull * (c0 + ex)) fail = true;
+      __syncthreads();
+      if (threadIdx.x == 0) s_carry = c0 + tot;
+      __syncthreads();
+    }
+    if (blk_root_depth(d)) roots += en - st;
+    const uint64_t cnt = s_carry;
+    st = en;
+    en = en + 2 * cnt;
+    ++d;
+    __syncthreads();
+  }
+  fail = __syncthreads_or(fail);
+  if (en != len) fail = true;  // every node reached by the level walk
+  const uint64_t sl = kBlkPrefix + 4 * roots;
+  if (sl >= (1ull << 23)) fail = true;
+  if (threadIdx.x == 0) {
+    slots[t] = sl;
+    nlev[t] = d;
+    if (!fail) lv[d] = (uint32_t)st;
+    if (fail) atomicOr(bad, 1);
+  }
+}
+
+// One CTA per tree (after k_blk_count passed): every node of the prefix levels and every block
+// (written by its root's thread, with both children) in parallel, level by level.
+__global__ void __launch_bounds__(256) k_blk_build(const Node16* __restrict__ nodes, const uint64_t* __restrict__ tree_off,
+                                                   const uint64_t* __restrict__ n8_off, const uint32_t* __restrict__ lev,
+                                                   const int* __restrict__ nlev, Node8* __restrict__ n8,
+                                                   double* __restrict__ val) {
+  __shared__ uint32_t s_st[kBlkMaxLevels + 1];   // level starts (tree-local BFS index)
+  __shared__ uint32_t s_blk[kBlkMaxLevels + 1];  // blocks of the block-root levels before level d
+  const int t = blockIdx.x;
+  const Node16* tn = nodes + tree_off[t];
+  Node8* out = n8 + n8_off[t];
+  double* vo = val + n8_off[t];
+  const int nl = nlev[t];
+  const uint32_t* lv = lev + (size_t)t * (kBlkMaxLevels + 1);
+  for (int d = threadIdx.x; d <= nl; d += blockDim.x) s_st[d] = lv[d];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t blk = 0;
+    for (int d = 0; d <= nl; ++d) {
+      s_blk[d] = blk;
+      if (d < nl && blk_root_depth(d)) blk += s_st[d + 1] - s_st[d];
+    }
+  }
+  __syncthreads();
+  // new slot of the j-th node of block-root level d
+  auto root_slot = [&](int d, uint32_t j) { return kBlkPrefix + 4u * (s_blk[d] + j); };
+  auto put = [&](uint32_t slot, const Node16& nd, uint32_t left, uint32_t wide) {
+    Node8 c;
+    c.fl = nd.feat < 0 ? 0xFFu : ((uint32_t)nd.feat | (left << 8) | (wide << 31));
+    c.tf = nd.feat < 0 ? 0.0f : q_thr(nd.v);
+    out[slot] = c;
+    vo[slot] = nd.v;
+  };
+  for (int d = 0; d < nl; ++d) {
+    const uint32_t st = s_st[d], en = s_st[d + 1];
+    if (d < 7) {
+      for (uint32_t i = st + threadIdx.x; i < en; i += blockDim.x) {
+        const Node16 nd = tn[i];
+        if (d < 6 || nd.feat < 0) put(i, nd, nd.left, 0u);
+        else put(i, nd, root_slot(7, nd.left - s_st[7]), 1u);
+      }
+    } else if (blk_root_depth(d)) {
+      for (uint32_t i = st + threadIdx.x; i < en; i += blockDim.x) {
+        const Node16 nd = tn[i];
+        const uint32_t me = root_slot(d, i - st);
+        put(me, nd, me + 1, 0u);
+        if (nd.feat >= 0) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const Node16 ch = tn[nd.left + c];
+            put(me + 1 + c, ch, ch.feat >= 0 ? root_slot(d + 2, ch.left - s_st[d + 2]) : 0u, 1u);
+          }
+        }
+      }
+    }
   }
 }
 
@@ -373,6 +497,20 @@ __global__ void k_check_finite(const double* X, size_t total, int* err) {
 
 }  // namespace
 
+cudaError_t node8_blocked_count(const Node16* nodes, const uint64_t* tree_off, int T, uint64_t* slots, uint32_t* lev,
+                                int* nlev, int* bad, cudaStream_t s) {
+  k_blk_count<<<(unsigned)T, 256, 0, s>>>(nodes, tree_off, slots, lev, nlev, bad);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t node8_blocked_build(const Node16* nodes, const uint64_t* tree_off, int T, const uint64_t* n8_off,
+                                const uint32_t* lev, const int* nlev, Node8* n8, double* val, cudaStream_t s) {
+  k_blk_build<<<(unsigned)T, 256, 0, s>>>(nodes, tree_off, n8_off, lev, nlev, n8, val);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* val, cudaStream_t s) {
   if (!total) return cudaSuccess;
   const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148 * 16);
@@ -383,7 +521,7 @@ cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* 
 
 cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T, const double* X,
                            long long n, int p, int mode, double* out, cudaStream_t s, int* err_few,
-                           uint64_t total_nodes, const Node8* n8, const double* val) {
+                           uint64_t total_nodes, const Node8* n8, const double* val, const uint64_t* n8_off) {
   if (n <= 0) return cudaSuccess;
   if (err_few && n <= kFewRows) {  // latency path: rows checked for finiteness in-kernel
     k_predict_few<<<(unsigned)n, kFewThreads, 0, s>>>(nodes, tree_off, T, X, p, mode, out, err_few);
@@ -396,7 +534,8 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     auto kern = stage ? k_predict_smem8<RF_PRED_STAGE8> : k_predict_smem8<0>;
     cudaError_t e = allow_max_dynamic_smem(kern);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(n8, val, tree_off, T, X, n, p, mode, out);
+    kern<<<(unsigned)((n + kSmemRows - 1) / kSmemRows), kSmemRows, smem, s>>>(n8, val, n8_off ? n8_off : tree_off, T, X,
+                                                                              n, p, mode, out);
     note_launch();
     return cudaGetLastError();
   }

@@ -233,3 +233,61 @@ def test_ln_uncertified_fails_loudly():
     got = rfg.debug_ln(_cuda(hard)).cpu().numpy()
     want = oracle.quantize(hard, 1)[0]
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def _swap_sibling_pairs(e):
+    """Per tree with two internal nodes A, B on one level (depth >= 7 where there is one): swap the
+    records of their child pairs and the two parents' child pointers -- the same trees, no longer in
+    the BFS order the blocked compact layout assumes (its validation must fall back)."""
+    feat, left = e["feature"].copy(), e["left"].copy()
+    val, ti, off = e["value"].copy(), e["thr_index"].copy(), e["tree_off"]
+    swapped = 0
+    for t in range(len(off) - 1):
+        o0, o1 = int(off[t]), int(off[t + 1])
+        depth = np.zeros(o1 - o0, np.int64)
+        for i in range(o1 - o0):
+            if feat[o0 + i] >= 0:
+                depth[left[o0 + i]] = depth[left[o0 + i] + 1] = depth[i] + 1
+        internal = [i for i in range(o1 - o0) if feat[o0 + i] >= 0]
+        for dmin in (7, 1):
+            cand = [i for i in internal if depth[i] >= dmin]
+            pair = next(((a, b) for a in cand for b in cand if a < b and depth[a] == depth[b]), None)
+            if pair:
+                break
+        if not pair:
+            continue
+        a, b = pair
+        ca, cb = int(left[o0 + a]), int(left[o0 + b])
+        for arr in (feat, left, val, ti):
+            x, y_ = arr[o0 + ca:o0 + ca + 2].copy(), arr[o0 + cb:o0 + cb + 2].copy()
+            arr[o0 + ca:o0 + ca + 2], arr[o0 + cb:o0 + cb + 2] = y_, x
+        left[o0 + a], left[o0 + b] = cb, ca
+        swapped += 1
+    return dict(feature=feat, left=left, value=val, thr_index=ti, tree_off=off), swapped
+
+
+@pytest.mark.parametrize("max_depth", [12, -1])
+def test_predict_blocked_layout_and_fallback(max_depth):
+    """Batched inference through the compact copy in its blocked layout (fitted BFS forests: two-level
+    32-byte blocks below the 7-level prefix) and in the BFS-slot layout it falls back to for a forest
+    whose trees are not BFS-ordered (sibling pairs swapped, imported) give the same bits as the
+    16-byte node walk, at depth 12 (staged prefix) and unbounded depth."""
+    X, y = datagen.scaled(30_000, 16)
+    f = rfg.fit(X, y, ntree=12, mtry=5, target=1, seed=4, max_depth=max_depth)
+    Q = datagen.scaled(20_000, 16, seed=9)[0]
+    blocked = rfg.predict(f, Q)
+    rfg.debug_set_option("predict_node16", 1)
+    try:
+        ref = rfg.predict(f, Q)
+    finally:
+        rfg.debug_set_option("predict_node16", 0)
+    assert np.array_equal(blocked.view(np.int64), ref.view(np.int64))
+    e = f.export()
+    d, swapped = _swap_sibling_pairs(e)
+    assert swapped >= 6
+    g = rfg.forest_import(d["feature"], d["left"], d["value"], d["thr_index"], d["tree_off"], e["p"], e["F"],
+                          e["target"])
+    assert np.array_equal(rfg.predict(g, Q).view(np.int64), ref.view(np.int64))
+    imp = rfg.forest_import(e["feature"], e["left"], e["value"], e["thr_index"], e["tree_off"], e["p"], e["F"],
+                            e["target"])  # an imported BFS forest takes the blocked layout too
+    assert np.array_equal(rfg.predict(imp, Q).view(np.int64), ref.view(np.int64))
