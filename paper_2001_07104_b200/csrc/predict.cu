@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
 // 8-byte nodes, the exact threshold (on an fp32 tie) and the leaf value from val[].  The staged
 // BFS prefix holds kStage8 nodes per tree for the same shared memory as the 16-byte layout's
 // kStage (one more tree level in shared memory): 19.2 -> 21.3 M predictions/s on C5 with fp32
-// staging (127 staged nodes beat 63 and 255, 12 trees per thread beat 10 and 16; rd2_43/44).
+// staging (127 staged nodes beat 63 and 255, 12 trees per thread beat 10 and 16; rd2_43/44; with
+// the blocked layout 12 still beats 8 (2.2x slower) and 16 (-13 %), rd2_56_ab_c5.txt).
 #ifndef RF_PRED_STAGE8
 #define RF_PRED_STAGE8 127
 #endif
