@@ -44,7 +44,7 @@ namespace {
 std::atomic<bool> g_opt_predict_node16{false};  // test switch (rf_debug_set_option "predict_node16")
 
 // compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream: the blocked
-// layout (two-level 32-byte blocks below a BFS prefix, predict.cu) when every tree is BFS-ordered
+// layout (three-level 64-byte blocks below a BFS prefix, predict.cu) when every tree is BFS-ordered
 // (fitted forests; imported ones if they are), else the BFS-slot copy
 cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
 #ifdef RF_NO_NODE8

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
 // BFS prefix holds kStage8 nodes per tree for the same shared memory as the 16-byte layout's
 // kStage (one more tree level in shared memory): 19.2 -> 21.3 M predictions/s on C5 with fp32
 // staging (127 staged nodes beat 63 and 255, 12 trees per thread beat 10 and 16; rd2_43/44; with
-// the blocked layout 12 still beats 8 (2.2x slower) and 16 (-13 %), rd2_56_ab_c5.txt).
+// 2-level blocks 12 still beat 8 (2.2x slower) and 16 (-13 %), rd2_56_ab_c5.txt).
 #ifndef RF_PRED_STAGE8
 #define RF_PRED_STAGE8 127
 #endif
@@ -211,6 +211,16 @@ __device__ __forceinline__ XStage q_stage(double v) { return __double2float_rn(v
 __device__ __forceinline__ float x_of(XStage v) { return v; }
 #endif
 __host__ __device__ constexpr size_t xstage_bytes(int p) { return ((size_t)p * kSmemStrideF * sizeof(XStage) + 15) / 16 * 16; }
+
+constexpr uint32_t kBlkPrefix = 128;
+// levels per block (RF_PRED_BLK_LV): 3 -> 8-slot (64-byte) blocks of 7 nodes.  C5 (rd2_55..58):
+// BFS slots 25.7 M predictions/s; 2-level 32-byte blocks 28.5 M; 3-level 30.5 M; 3-level with an L1
+// prefetch of the block's second sector on entry 27.3 M; 4-level (128-byte) 27.4 M.
+#ifndef RF_PRED_BLK_LV
+#define RF_PRED_BLK_LV 3
+#endif
+constexpr int kBlkLv = RF_PRED_BLK_LV;
+constexpr int kBlkSlots = 1 << kBlkLv;
 
 template <int kStage>
 __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __restrict__ nodes,
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
           const float xf = x_of(x[f * kSmemStrideF]);
           // q decides unless q(x) = q(thr) (monotonic rounding), then the fp64 values do
           const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
-          idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? 4u : 1u));
+          idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? (uint32_t)kBlkSlots : 1u));
           nd[g] = (kStage > 0 && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
           open = true;
         }
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
       const uint32_t f = nd.fl & 0xFFu;
       const float xf = x_of(x[f * kSmemStrideF]);
       const bool le = xf < nd.tf || (xf == nd.tf && xrow[f] <= val[b0 + id]);
-      id = ((nd.fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd.fl >> 31) ? 4u : 1u));
+      id = ((nd.fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd.fl >> 31) ? (uint32_t)kBlkSlots : 1u));
       nd = nodes[b0 + id];
     }
     s += val[b0 + id];
@@ -304,18 +314,18 @@ __global__ void k_build_node8(const Node16* __restrict__ nodes, uint64_t total, 
   }
 }
 
-// ---- blocked compact layout (fitted, BFS-ordered forests).  Per tree: BFS levels 0..6 (<= 127
-// nodes) keep their BFS slots 0..126 (slot 127 is padding); below them the tree is cut into two-level
-// blocks of 4 slots [P, left child, right child, pad] (32 bytes, one DRAM/L2 sector), P a node at a
-// depth 7, 9, 11, ...; the blocks of one level are numbered in BFS order, so sibling blocks are
-// adjacent.  A walk then misses L1 once per two levels below the prefix (the child of P is in P's
-// sector).  Child addressing stays "left + (go right ? stride : 0)": stride 1 inside the prefix and
-// from P to its children, 4 (the next block) from a depth-6 or second-level node to its children,
-// flagged by bit 31 of the node word (left slot < 2^23).
+// ---- blocked compact layout (BFS-ordered forests: every fitted one).  Per tree: BFS levels 0..6
+// (<= 127 nodes) keep their BFS slots 0..126 (slot 127 is padding); below them the tree is cut into
+// blocks of kBlkLv levels -- kBlkSlots slots holding a block root P (depth 7, 7 + kBlkLv, ...) and
+// its descendants in heap order (children of offset o at 2o + 1, 2o + 2), 64 bytes for 3 levels;
+// the blocks of one level are numbered in BFS order, so sibling blocks are adjacent.  A walk then
+// fetches one block per three levels below the prefix instead of one node per level.  Child
+// addressing stays "left + (go right ? stride : 0)": stride 1 inside the prefix and inside a block,
+// kBlkSlots (the adjacent block) from a depth-6 node or a block's bottom level, flagged by bit 31 of
+// the node word (left slot < 2^23).
 constexpr int kBlkMaxLevels = kBlkLevStride - 1;
-constexpr uint32_t kBlkPrefix = 128;
 
-__device__ __forceinline__ bool blk_root_depth(int d) { return d >= 7 && ((d - 7) & 1) == 0; }
+__device__ __forceinline__ bool blk_root_depth(int d) { return d >= 7 && (d - 7) % kBlkLv == 0; }
 
 // level d of a BFS tree: [s_d, s_{d+1}); s_{d+1} - s_d = 2 x (internal nodes of level d - 1).  One CTA
 // per tree: lev[t][d] = s_d (d <= levels), nlev[t] = levels, slots[t] = 128 + 4 x (nodes at
@@ -358,7 +368,7 @@ __global__ void __launch_bounds__(256) k_blk_count(const Node16* __restrict__ no
   }
   fail = __syncthreads_or(fail);
   if (en != len) fail = true;  // every node reached by the level walk
-  const uint64_t sl = kBlkPrefix + 4 * roots;
+  const uint64_t sl = kBlkPrefix + (uint64_t)kBlkSlots * roots;
   if (sl >= (1ull << 23)) fail = true;
   if (threadIdx.x == 0) {
     slots[t] = sl;
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(256) k_blk_build(const Node16* __restrict__ no
   }
   __syncthreads();
   // new slot of the j-th node of block-root level d
-  auto root_slot = [&](int d, uint32_t j) { return kBlkPrefix + 4u * (s_blk[d] + j); };
+  auto root_slot = [&](int d, uint32_t j) { return kBlkPrefix + (uint32_t)kBlkSlots * (s_blk[d] + j); };
   auto put = [&](uint32_t slot, const Node16& nd, uint32_t left, uint32_t wide) {
     Node8 c;
     c.fl = nd.feat < 0 ? 0xFFu : ((uint32_t)nd.feat | (left << 8) | (wide << 31));
@@ -410,15 +420,25 @@ __global__ void __launch_bounds__(256) k_blk_build(const Node16* __restrict__ no
         else put(i, nd, root_slot(7, nd.left - s_st[7]), 1u);
       }
     } else if (blk_root_depth(d)) {
+      // the block of root i: heap positions o = 0 .. kBlkSlots - 2 (level l holds o = 2^l - 1 ..),
+      // in-block children of o at 2o + 1, 2o + 2; the bottom level's children are the roots of
+      // adjacent blocks kBlkLv levels down
       for (uint32_t i = st + threadIdx.x; i < en; i += blockDim.x) {
-        const Node16 nd = tn[i];
         const uint32_t me = root_slot(d, i - st);
-        put(me, nd, me + 1, 0u);
-        if (nd.feat >= 0) {
+        int64_t pos[kBlkSlots - 1];
+        pos[0] = i;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const Node16 ch = tn[nd.left + c];
-            put(me + 1 + c, ch, ch.feat >= 0 ? root_slot(d + 2, ch.left - s_st[d + 2]) : 0u, 1u);
+        for (int o = 1; o < kBlkSlots - 1; ++o) pos[o] = -1;
+#pragma unroll
+        for (int o = 0; o < kBlkSlots - 1; ++o) {
+          if (pos[o] < 0) continue;
+          const Node16 nd = tn[pos[o]];
+          const int lvl = 31 - __clz(o + 1);
+          if (lvl < kBlkLv - 1) {
+            if (nd.feat >= 0) { pos[2 * o + 1] = nd.left; pos[2 * o + 2] = nd.left + 1; }
+            put(me + o, nd, me + 2 * o + 1, 0u);
+          } else {
+            put(me + o, nd, nd.feat >= 0 ? root_slot(d + kBlkLv, nd.left - s_st[d + kBlkLv]) : 0u, 1u);
           }
         }
       }

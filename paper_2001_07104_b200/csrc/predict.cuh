@@ -17,7 +17,7 @@ constexpr long long kFewRows = 256;
 // node (threshold or leaf value) beside them.  Trees of < 2^24 nodes, p < 255.
 struct __align__(8) Node8 {
   uint32_t fl;  // feature (0xFF: leaf) | tree-local left child slot << 8 (23 bits) | wide << 31
-                // (right child = left + (wide ? 4 : 1): the blocked layout, predict.cu)
+                // (right child = left + (wide ? 8 : 1): the blocked layout, predict.cu)
   float tf;     // fp32(threshold), round to nearest (exact decisions: see k_predict_smem8)
 };
 cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* val, cudaStream_t s);
