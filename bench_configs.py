@@ -261,11 +261,13 @@ def c4(rfg, torch, flush, cpu=True, e2e=True):
         holder["f"] = rfg.fit(X, y, ntree=C4_TREES, mtry=21, max_depth=12, split_mode=1, target=1, seed=7104)
     rfg.set_profiling(True)
     rfg.row_levels(reset=True)
-    ms, clocks = _timed(torch, run, 1, 1)
-    rl = rfg.row_levels(reset=True) / 2
+    # two timed fits (one alone was exposed to a 13 % outlier in rd2_59 that the A/B of rd2_60 did
+    # not reproduce); the profile and row-levels counters cover the warm-up fit too (3 fits)
+    ms, clocks = _timed(torch, run, 2, 1)
+    rl = rfg.row_levels(reset=True) / 3
     prof = rfg.last_profile()
     rfg.set_profiling(False)
-    kms = {k: v[0] / 2 for k, v in prof.items()}
+    kms = {k: v[0] / 3 for k, v in prof.items()}
     info = holder["f"].info()
     m = 21
     peak, psrc = B.hbm_peak()
@@ -278,7 +280,7 @@ def c4(rfg, torch, flush, cpu=True, e2e=True):
     out = {"workload": "C4 (configs[3]): rf_fit scaled(10,000,000 x 64) generated on the device, 256-bin "
                        "quantile histograms, mtry 21, max_depth 12, 1000 trees, bootstrap, LOG target, 1 GPU",
            "metric": "trees trained/sec", "value": C4_TREES / (ms / 1e3), "unit": "trees/s", "ms_per_step": ms,
-           "steps": 1, "warmup": 1, "l2": "inputs (5.1 GB X, 640 MB bins) larger than L2", "clocks": clocks,
+           "steps": 2, "warmup": 1, "l2": "inputs (5.1 GB X, 640 MB bins) larger than L2", "clocks": clocks,
            "nodes_per_tree": info["total_nodes"] / C4_TREES, "row_levels_per_tree": rl / C4_TREES,
            "kernels_ms_per_fit": kms,
            "whole_fit_hbm": {"algorithmic_bytes": fit_bytes, "achieved": fit_bytes / (ms / 1e3) / 1e9,
