@@ -360,8 +360,9 @@ def c5(rfg, torch, forest, cpu=True, e2e=True):
                         "algorithmic_bytes": "SURVEY 8(d) C5: per query row its 64 fp64 features + the fp64 "
                                              "prediction (520 B)",
                         "peak_source": psrc,
-                        "note": "the node walks (12 dependent 16-B node loads per tree, from L1/L2) bound the "
-                                "kernel, not HBM: SURVEY 8(d) C5"}}
+                        "note": "the node walks bound the kernel, not HBM (SURVEY 8(d) C5): up to 13 dependent 8-B "
+                                "node reads per tree, the top 7 levels from shared memory, the rest as two "
+                                "64-B three-level blocks from L1/L2 (DESIGN.md sec. 5)"}}
     del Q
     # single-query latency (host API, warm): the C4 forest and a 512-tree paper-shaped forest
     q1 = datagen.queries(1, 64)

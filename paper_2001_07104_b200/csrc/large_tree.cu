@@ -2051,7 +2051,14 @@ rf_status grow_batch(Batch& b, const LargePlan& pl, const uint32_t* task_order, 
   if (b.side) LCK(cudaMemsetAsync(b.side, 0, (size_t)b.B * b.n, s));
   if (b.leaf_of_row) LCK(cudaMemsetAsync(b.leaf_of_row, 0xFF, (size_t)b.B * b.n * 4, s));
   {
-    dim3 g(nblk((b.ntr + 1) / 2, 256) > 64 ? 64 : nblk((b.ntr + 1) / 2, 256), b.B);
+#ifndef RF_BOOT_CTAS
+#define RF_BOOT_CTAS 1184
+#endif
+    // CTAs per tree: blocks are scheduled x-fastest, so RF_BOOT_CTAS = the resident CTAs of the GPU
+    // (148 x 8) keeps about one tree's count array (n bytes) hot in L2 at a time for its random
+    // atomics: C4 setup 449 -> 208 ms per fit (64 CTAs per tree kept ~18 trees' 10 MB arrays in
+    // flight), C3 unchanged (profiles/rd2_61_ab_c4.txt, rd2_61_ab_c3.txt)
+    dim3 g(std::min<unsigned>(nblk((b.ntr + 1) / 2, 256), RF_BOOT_CTAS), b.B);
     k_keys_boot<<<g, 256, 0, s>>>(b, seed, task, bootstrap);
     note_launch();
     if (b.wt) {
