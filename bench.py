@@ -307,10 +307,26 @@ def run_ours(args):
     from paper_2001_07104_b200.dist import cv_study_sharded, gather_task_tables
 
     rank, world, local = dist_env()
+    # test hooks of the multi-rank driver on a one-GPU box (tests/test_gpu_dist.py): gloo instead of
+    # NCCL and every rank on cuda:0 -- a functional check of this path, never a measurement
+    backend = os.environ.get("RF_BENCH_BACKEND", "nccl")
+    if os.environ.get("RF_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def all_reduce_(t, op=dist.ReduceOp.SUM):  # gloo: through the host
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
     rfg.lib()
     stream = torch.cuda.current_stream()
     ds = datagen.study(datagen.SEED)
@@ -379,14 +395,14 @@ def run_ours(args):
     rfg.set_profiling(False)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     trees_per_step = len(ds) * reps_total * K_FOLDS * DISTINCT_MTRY * max(NTREES)
     value = trees_per_step / (ms_per_step / 1e3)
     # candidates of all ranks (each rank counts its own)
     ct = torch.tensor([float(cands)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(ct)
+        all_reduce_(ct)
     cands_all = float(ct.item())
 
     # dominant kernel: the small-tree kernel, plain fp64/integer ALU bound
@@ -412,8 +428,10 @@ def run_ours(args):
                                      "candidate (profiles/README.md); the fraction is low by construction"}
 
     e2e = None
-    if not args.no_e2e and rank == 0 and world == 1:
+    if not args.no_e2e and world == 1:
         e2e = measure_e2e(rfg, ds, args, skw)
+    elif not args.no_e2e and strong:
+        e2e = measure_e2e_dist(rfg, ds, args, skw, rank, world, all_reduce_)
     configs = None
     if rank == 0 and world == 1 and not args.no_configs:
         configs = run_configs(rfg, torch, args, dev, flush)
@@ -487,6 +505,69 @@ def measure_e2e(rfg, ds, args, skw):
     return {"value": trees / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": dt * 1e3, "host_threads": len(ds),
             "api": "rf_make_folds + rf_cross_validate_grid (host pointers, pinned inputs)"}
+
+
+def measure_e2e_dist(rfg, ds, args, skw, rank, world, all_reduce_):
+    """e2e at N > 1 (strong scaling): each rank runs its (dataset, task) units of the fixed study
+    (dist.study_units, as the device-timed step) through the host-pointer C ABI from pinned host
+    memory, one host thread per unit, then the owned fold-MAPE columns of all ranks are
+    all-gathered on the host -- every rank ends with the full tables.  Per step: barrier, the
+    rank's wall time, max over ranks; bytes summed over ranks."""
+    import concurrent.futures as cf
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_07104_b200.dist import study_units
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    Xs = [pinned(d["X"]) for d in ds]
+    ys = [pinned(d["y"]) for d in ds]
+    units = study_units([REPS * K_FOLDS] * len(ds), rank, world)
+    G = len(MTRYS) * len(NTREES)
+
+    def one(u):
+        d, lo, hi = u
+        custom = ds[d]["target"] == "time"
+        f = rfg.make_folds(ys[d], K_FOLDS, REPS, seed=SEED + d, custom=custom)
+        fm = rfg.cross_validate_grid(Xs[d], ys[d], K_FOLDS, REPS, NTREES, MTRYS, fold_ids=f,
+                                     target=1 if custom else 0, seed=SEED + d, task_begin=lo, task_end=hi, **skw)
+        cols = fm.reshape(G, -1)[:, lo:hi]
+        return cols, ys[d].nbytes + Xs[d].nbytes + ys[d].nbytes + f.nbytes, f.nbytes + fm.nbytes
+
+    pool = cf.ThreadPoolExecutor(max_workers=max(1, len(units)))
+    io = [0, 0]
+
+    def step():
+        res = list(pool.map(one, units))
+        tables = [None] * world
+        dist.all_gather_object(tables, [r[0] for r in res])  # the full study's tables on every rank
+        io[0], io[1] = sum(r[1] for r in res), sum(r[2] for r in res)
+        return tables
+
+    step()
+    n = max(1, min(args.steps, 3))
+    dts = []
+    for _ in range(n):
+        dist.barrier()
+        t0 = time.perf_counter()
+        step()
+        dts.append(time.perf_counter() - t0)
+    pool.shutdown()
+    t = torch.tensor([sum(dts) / n], dtype=torch.float64, device="cuda")
+    all_reduce_(t, op=dist.ReduceOp.MAX)
+    b = torch.tensor([float(io[0]), float(io[1])], dtype=torch.float64, device="cuda")
+    all_reduce_(b)
+    dt = float(t.item())
+    trees = len(ds) * REPS * K_FOLDS * DISTINCT_MTRY * max(NTREES)
+    return {"value": trees / dt, "unit": UNIT, "h2d_bytes_per_step": int(b[0].item()),
+            "d2h_bytes_per_step": int(b[1].item()), "ms_per_step": dt * 1e3, "host_threads_per_rank": len(units),
+            "api": "rf_make_folds + rf_cross_validate_grid (host pointers, pinned inputs, task ranges per rank), "
+                   "tables all-gathered on the host; max over ranks"}
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one small_tree_kernel launch (one dataset of the

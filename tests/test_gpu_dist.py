@@ -101,3 +101,30 @@ def test_two_ranks_match_one_rank():
             assert np.array_equal(g[key], e[key]), (r, key)
         assert np.array_equal(g["value"].view(np.int64), e["value"].view(np.int64))
         assert np.array_equal(np.load(f"{OUT}/pred_r{r}.npy").view(np.int64), pref.view(np.int64))
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py's N > 1 path (init, strong task sharding, barriers, max over ranks, the host-API e2e
+    with host-side table gathers, rank-0-only JSON line) under torchrun with two ranks.  This box has
+    one GPU, so both ranks run on cuda:0 over gloo (bench.py test hooks RF_BENCH_BACKEND /
+    RF_BENCH_SAME_GPU): a functional check of the driver's scaling-run command, not a measurement."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, RF_BENCH_BACKEND="gloo", RF_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+                        "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-configs", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["trees_per_step"] == 6144000  # the fixed study, split over the ranks
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
