@@ -44,8 +44,8 @@ namespace {
 std::atomic<bool> g_opt_predict_node16{false};  // test switch (rf_debug_set_option "predict_node16")
 
 // compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream: the blocked
-// layout (three-level 64-byte blocks below a BFS prefix, predict.cu) when every tree is BFS-ordered
-// (fitted forests; imported ones if they are), else the BFS-slot copy
+// layout (three-level 64-byte blocks below a BFS prefix, predict.cu) for shallow forests whose
+// trees are all BFS-ordered (fitted forests; imported ones if they are), else the BFS-slot copy
 cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
 #ifdef RF_NO_NODE8
   return cudaSuccess;
@@ -59,7 +59,7 @@ cudaError_t attach_node8(rf_forest* f, cudaStream_t s) {
   auto dfree = [&](void* p) { if (p) { if (f->pooled) cudaFreeAsync(p, s); else cudaFree(p); } };
   const int T = (int)f->ntree;
 #ifndef RF_PRED_NOBLOCKS
-  if (T <= 65536) {
+  if (T <= 65536 && f->total_nodes <= (uint64_t)T * rf::kShallowNodesPerTree) {
     uint64_t* slots = nullptr;
     uint32_t* lev = nullptr;
     int* nlev = nullptr;

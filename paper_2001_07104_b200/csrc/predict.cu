@@ -264,6 +264,28 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
       idx[g] = 0u;
       nd[g] = kStage > 0 ? sn[g * kStage] : nodes[base[g]];
     }
+#ifdef RF_PRED_2PHASE
+    // the descents from depths 0 .. kSmemSteps - 1 stay inside the staged prefix (the nodes of depth
+    // <= 6 are the first <= 127 BFS slots in both layouts): a fixed number of shared-memory steps,
+    // then a walk that reads global memory only (no per-step select between the two)
+    constexpr int kSmemSteps = kStage >= 127 ? 6 : (kStage >= 63 ? 5 : 0);
+#pragma unroll 1
+    for (int st = 0; st < kSmemSteps; ++st) {
+#pragma unroll
+      for (int g = 0; g < kG8; ++g) {
+        const uint32_t f = nd[g].fl & 0xFFu;
+        if (f != 0xFFu) {
+          const float xf = x_of(x[f * kSmemStrideF]);
+          const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
+          idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? (uint32_t)kBlkSlots : 1u));
+          nd[g] = sn[g * kStage + idx[g]];
+        }
+      }
+    }
+    constexpr bool kMixed = kSmemSteps == 0 && kStage > 0;
+#else
+    constexpr bool kMixed = kStage > 0;
+#endif
     bool open = live;
     while (open) {
       open = false;
@@ -275,7 +297,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
           // q decides unless q(x) = q(thr) (monotonic rounding), then the fp64 values do
           const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
           idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? (uint32_t)kBlkSlots : 1u));
-          nd[g] = (kStage > 0 && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
+          nd[g] = (kMixed && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
           open = true;
         }
       }
@@ -550,7 +572,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     return cudaGetLastError();
   }
   if (n8 && val && p <= kSmemMaxP) {
-    const bool stage = RF_PRED_STAGE8 > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * 16384u;
+    const bool stage = RF_PRED_STAGE8 > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * kShallowNodesPerTree;
     const size_t smem = xstage_bytes(p) + (stage ? (size_t)kG8 * RF_PRED_STAGE8 * sizeof(Node8) : 0);
     auto kern = stage ? k_predict_smem8<RF_PRED_STAGE8> : k_predict_smem8<0>;
     cudaError_t e = allow_max_dynamic_smem(kern);
@@ -561,7 +583,7 @@ cudaError_t predict_forest(const Node16* nodes, const uint64_t* tree_off, int T,
     return cudaGetLastError();
   }
   if (p <= kSmemMaxP) {
-    const bool stage = RF_PRED_STAGE > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * 16384u;
+    const bool stage = RF_PRED_STAGE > 0 && total_nodes > 0 && total_nodes <= (uint64_t)T * kShallowNodesPerTree;
     const size_t smem = (size_t)((p * kSmemStrideF + 3) & ~3) * 4 + (stage ? (size_t)kGs * RF_PRED_STAGE * sizeof(Node16) : 0);
     auto kern = stage ? k_predict_smem<RF_PRED_STAGE> : k_predict_smem<0>;
     cudaError_t e = allow_max_dynamic_smem(kern);

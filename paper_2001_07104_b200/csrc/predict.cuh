@@ -25,6 +25,11 @@ cudaError_t build_node8(const Node16* nodes, uint64_t total, Node8* n8, double* 
 // level starts lev [T][kBlkLevStride], nlev[T] (bad |= 1 if the forest does not qualify), then build
 // into n8 / val at n8_off (exclusive sums of slots).
 constexpr int kBlkLevStride = 2049;
+// forests of shallow trees (<= this many nodes per tree on average) take the staged-prefix kernel and
+// the blocked layout; deep forests the BFS-slot copy without staging (the blocked layout measured
+// 28.0 -> 25.6 M predictions/s on the C3 forest, ~126k nodes per tree: its padding outweighs the
+// fewer fetches there, rd2_52/59 bench lines)
+constexpr uint64_t kShallowNodesPerTree = 16384;
 cudaError_t node8_blocked_count(const Node16* nodes, const uint64_t* tree_off, int T, uint64_t* slots, uint32_t* lev,
                                 int* nlev, int* bad, cudaStream_t s);
 cudaError_t node8_blocked_build(const Node16* nodes, const uint64_t* tree_off, int T, const uint64_t* n8_off,

@@ -268,10 +268,10 @@ def _swap_sibling_pairs(e):
 
 @pytest.mark.parametrize("max_depth", [12, -1])
 def test_predict_blocked_layout_and_fallback(max_depth):
-    """Batched inference through the compact copy in its blocked layout (fitted BFS forests: two-level
-    32-byte blocks below the 7-level prefix) and in the BFS-slot layout it falls back to for a forest
-    whose trees are not BFS-ordered (sibling pairs swapped, imported) give the same bits as the
-    16-byte node walk, at depth 12 (staged prefix) and unbounded depth."""
+    """Batched inference through the compact copy in its blocked layout (shallow BFS forests:
+    three-level 64-byte blocks below the 7-level prefix) and in the BFS-slot layout (deep forests,
+    and forests whose trees are not BFS-ordered: sibling pairs swapped, imported) gives the same bits
+    as the 16-byte node walk, at depth 12 (staged prefix, blocked) and unbounded depth (BFS slots)."""
     X, y = datagen.scaled(30_000, 16)
     f = rfg.fit(X, y, ntree=12, mtry=5, target=1, seed=4, max_depth=max_depth)
     Q = datagen.scaled(20_000, 16, seed=9)[0]
