@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem(const Node16* __rest
 // BFS prefix holds kStage8 nodes per tree for the same shared memory as the 16-byte layout's
 // kStage (one more tree level in shared memory): 19.2 -> 21.3 M predictions/s on C5 with fp32
 // staging (127 staged nodes beat 63 and 255, 12 trees per thread beat 10 and 16; rd2_43/44; with
-// 2-level blocks 12 still beat 8 (2.2x slower) and 16 (-13 %), rd2_56_ab_c5.txt).
+// 2-level blocks 12 still beat 8 (2.2x slower) and 16 (-13 %), rd2_56_ab_c5.txt.  Splitting each walk
+// into a fixed count of shared-memory steps (depths 0..5) and a global-only loop, to drop the
+// per-step select, measured 2.3x slower, rd2_65_ab_c5.txt).
 #ifndef RF_PRED_STAGE8
 #define RF_PRED_STAGE8 127
 #endif
@@ -264,28 +266,6 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
       idx[g] = 0u;
       nd[g] = kStage > 0 ? sn[g * kStage] : nodes[base[g]];
     }
-#ifdef RF_PRED_2PHASE
-    // the descents from depths 0 .. kSmemSteps - 1 stay inside the staged prefix (the nodes of depth
-    // <= 6 are the first <= 127 BFS slots in both layouts): a fixed number of shared-memory steps,
-    // then a walk that reads global memory only (no per-step select between the two)
-    constexpr int kSmemSteps = kStage >= 127 ? 6 : (kStage >= 63 ? 5 : 0);
-#pragma unroll 1
-    for (int st = 0; st < kSmemSteps; ++st) {
-#pragma unroll
-      for (int g = 0; g < kG8; ++g) {
-        const uint32_t f = nd[g].fl & 0xFFu;
-        if (f != 0xFFu) {
-          const float xf = x_of(x[f * kSmemStrideF]);
-          const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
-          idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? (uint32_t)kBlkSlots : 1u));
-          nd[g] = sn[g * kStage + idx[g]];
-        }
-      }
-    }
-    constexpr bool kMixed = kSmemSteps == 0 && kStage > 0;
-#else
-    constexpr bool kMixed = kStage > 0;
-#endif
     bool open = live;
     while (open) {
       open = false;
@@ -297,7 +277,7 @@ __global__ void __launch_bounds__(kSmemRows) k_predict_smem8(const Node8* __rest
           // q decides unless q(x) = q(thr) (monotonic rounding), then the fp64 values do
           const bool le = xf < nd[g].tf || (xf == nd[g].tf && __ldg(xrow + f) <= __ldg(val + base[g] + idx[g]));
           idx[g] = ((nd[g].fl >> 8) & 0x7FFFFFu) + (le ? 0u : ((nd[g].fl >> 31) ? (uint32_t)kBlkSlots : 1u));
-          nd[g] = (kMixed && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
+          nd[g] = (kStage > 0 && idx[g] < (uint32_t)kStage) ? sn[g * kStage + idx[g]] : nodes[base[g] + idx[g]];
           open = true;
         }
       }
