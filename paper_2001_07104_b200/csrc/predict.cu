@@ -200,7 +200,8 @@ constexpr int kG8 = RF_PRED_G8;
 // q is monotonic, so q(x) < q(thr) implies x <= thr and q(x) > q(thr) implies x > thr; only
 // q(x) = q(thr) reads the fp64 values.  bf16 halves the staged rows (128 x 64 features: 16 KB) --
 // more resident CTAs -- for a few more fp64 tie reads: 21.3 -> 26.2 M predictions/s on C5
-// (profiles/rd2_44_ab_c5.txt)
+// (profiles/rd2_44_ab_c5.txt).  Staging order-preserving 16-bit keys of the bf16 values instead (two
+// integer compares, no bf16 -> fp32 conversion per step) measured neutral (+0.1 %, rd2_67_ab_c5.txt).
 #ifndef RF_PRED_FP32
 typedef __nv_bfloat16 XStage;
 __device__ __forceinline__ float q_thr(double v) { return __bfloat162float(__float2bfloat16_rn(__double2float_rn(v))); }

@@ -14,7 +14,7 @@ constexpr long long kFewRows = 256;
 // the top BFS nodes of each tree group staged in shared memory (see k_predict_smem).
 // Compact copy of a forest for batch inference: 8-byte nodes (feature | left child << 8, the
 // feature 0xFF marking a leaf; the threshold rounded to fp32) and the exact fp64 value of every
-// node (threshold or leaf value) beside them.  Trees of < 2^24 nodes, p < 255.
+// node (threshold or leaf value) beside them.  Trees of < 2^23 nodes, p < 255.
 struct __align__(8) Node8 {
   uint32_t fl;  // feature (0xFF: leaf) | tree-local left child slot << 8 (23 bits) | wide << 31
                 // (right child = left + (wide ? 8 : 1): the blocked layout, predict.cu)
