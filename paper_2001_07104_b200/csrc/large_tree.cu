@@ -1671,6 +1671,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(Batch b, int cur, c
 // scan, and per split node its distinct left rows (per-thread runs, a warp segmented sum, a CTA
 // table of the tile's first 32 nodes, one global atomic per node and CTA).  The children's
 // (W, S) come from k_hist_best's histogram prefix; their constancy from the next level's build.
+// (Launching the count tiles sorted by their node's split feature -- a key kernel + CUB radix sort per
+// level -- so that concurrent CTAs gather from few L2-resident bin columns: count 458 -> 428 ms per C4
+// fit but the whole fit 5.42 -> 5.70 s, rd2_68_ab_c4.txt; not kept.)
 __global__ void __launch_bounds__(kPartThreads) k_part_count_hist(Batch b, int cur, const uint32_t* tileTab,
                                                                   uint32_t* tileCnt, uint8_t* leftBits) {
   int t, f, k;
