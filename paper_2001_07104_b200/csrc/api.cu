@@ -105,6 +105,7 @@ thread_local std::string g_err;
 struct ProfRec {
   const char* name;
   cudaEvent_t a, b;
+  int dev;  // the device the events belong to (current when the scope ran)
 };
 thread_local std::vector<ProfRec> g_prof;
 thread_local bool g_prof_on = false;
@@ -607,7 +608,26 @@ unsigned long long* candidate_counter() {
   return ptrs[dev];
 }
 bool prof_enabled() { return g_prof_on; }
-void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back(ProfRec{name, a, b}); }
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  g_prof.push_back(ProfRec{name, a, b, dev});
+}
+thread_local std::vector<std::pair<int, cudaEvent_t>> g_evpool;  // (device, event)
+cudaEvent_t prof_event() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (size_t i = g_evpool.size(); i-- > 0;)
+    if (g_evpool[i].first == dev) {
+      cudaEvent_t e = g_evpool[i].second;
+      g_evpool.erase(g_evpool.begin() + (long)i);
+      return e;
+    }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_recycle(cudaEvent_t e, int dev) { g_evpool.emplace_back(dev, e); }
 }  // namespace rf
 
 // ======================================================================= ABI
@@ -1212,7 +1232,7 @@ rf_status rf_forest_import(const int32_t* feature, const uint32_t* left, const d
 }
 
 void rf_set_profiling(int on) {
-  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto& r : g_prof) { rf::prof_recycle(r.a, r.dev); rf::prof_recycle(r.b, r.dev); }
   g_prof.clear();
   g_prof_on = on != 0;
 }

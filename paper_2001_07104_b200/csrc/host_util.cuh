@@ -79,6 +79,9 @@ unsigned long long* candidate_counter();
 // per-kernel event timing (enabled by rf_set_profiling); defined in api.cu
 bool prof_enabled();
 void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b);
+// a timing event of the current device from the thread's pool (created on first need; the records'
+// events return to the pool when profiling is reset, so steady-state scopes create none)
+cudaEvent_t prof_event();
 
 struct ProfScope {
   const char* name;
@@ -87,8 +90,8 @@ struct ProfScope {
   bool on;
   ProfScope(const char* nm, cudaStream_t st) : name(nm), s(st), on(prof_enabled()) {
     if (!on) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+    a = prof_event();
+    b = prof_event();
     cudaEventRecord(a, s);
   }
   ~ProfScope() {
