@@ -25,10 +25,6 @@ inline void retain_pool() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-#ifdef RF_POOL_NO_INTERNAL_DEPS
-    int zero = 0;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
-#endif
   }
   done[dev].store(true, std::memory_order_release);
 }
