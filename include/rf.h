@@ -145,7 +145,10 @@ RF_API rf_status rf_fit_dev(const double* dX, uint64_t n, uint32_t p, const doub
                      const rf_params* prm, void* stream, rf_forest** out);
 
 /* rf_predict: yhat[i] = mean over the forest's trees of the leaf reached by
-   row i (x[f] <= thr goes left), exp() for LOG.
+   row i (x[f] <= thr goes left), exp() for LOG.  Host X
+   [n][p] and yhat [n]; batches above ~1 GB of X are streamed in ~512 MB
+   chunks over two CUDA streams (copies overlap the walks when X is pinned;
+   device memory stays at two chunks).  Synchronous.
    Errors: RF_E_ARITY (p differs), RF_E_NONFINITE. */
 RF_API rf_status rf_predict(const rf_forest* f, const double* X, uint64_t n, uint32_t p, double* yhat);
 RF_API rf_status rf_predict_dev(const rf_forest* f, const double* dX, uint64_t n, uint32_t p,

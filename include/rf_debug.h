@@ -42,8 +42,11 @@ RF_API rf_status rf_debug_phase_cycles(uint64_t* out16, int reset);
    exact; tests run each); 0 restores the default.  "ln_cert_margin_log2" = e
    in [-200, -2] sets the margin of ln's rounding test (ddlog.cuh) to 2^e
    instead of 2^-94, so a wide margin reaches the RF_E_INEXACT path; 0
-   restores the default.  Unknown names, negative caps and margins outside
-   that range return RF_E_ARG. */
+   restores the default.  "predict_chunk_rows" = c > 0 sets the rows per chunk
+   of the pipelined host-pointer rf_predict (batches above two chunks, ~512 MB
+   of X each by default, alternate two streams so that copies overlap the
+   walks); 0 restores the default.  Unknown names, negative caps and margins
+   outside that range return RF_E_ARG. */
 RF_API rf_status rf_debug_set_option(const char* name, int64_t value);
 #ifdef __cplusplus
 }

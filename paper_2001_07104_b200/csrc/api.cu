@@ -42,6 +42,7 @@ struct rf_forest {
 
 namespace {
 std::atomic<bool> g_opt_predict_node16{false};  // test switch (rf_debug_set_option "predict_node16")
+std::atomic<long long> g_opt_predict_chunk{0};     // test switch "predict_chunk_rows" (0: by size)
 
 // compact 8-byte node copy of a forest (predict.cuh Node8) on the forest's stream: the blocked
 // layout (three-level 64-byte blocks below a BFS prefix, predict.cu) for shallow forests whose
@@ -128,11 +129,14 @@ rf_status cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, where); \
   } while (0)
 
-cudaStream_t host_stream(int device) {
+// the calling thread's stream `which` (0, 1) on `device` (host-pointer entry points; 1 = the second
+// stream of the pipelined rf_predict)
+cudaStream_t host_stream(int device, int which = 0) {
   static thread_local std::vector<cudaStream_t> streams;
-  if ((int)streams.size() <= device) streams.resize(device + 1, nullptr);
-  if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
-  return streams[device];
+  const int i = 2 * device + which;
+  if ((int)streams.size() <= i) streams.resize(i + 1, nullptr);
+  if (!streams[i]) cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking);
+  return streams[i];
 }
 
 rf_status check_device() {
@@ -781,12 +785,53 @@ rf_status rf_predict(const rf_forest* f, const double* X, uint64_t n, uint32_t p
   if (n == 0) return RF_OK;
   CK(cudaSetDevice(f->device), "set device");
   cudaStream_t s = host_stream(f->device);
-  Scratch sc(s);
-  double *dX, *dy;
-  CK(sc.alloc(&dX, n * p), "alloc");
-  CK(sc.alloc(&dy, n), "alloc");
-  CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
-  return predict_core(f, dX, n, p, dy, f->target == RF_TARGET_LOG ? 2 : 1, s, yhat);
+  const int mode = f->target == RF_TARGET_LOG ? 2 : 1;
+  // rows per pipeline chunk: ~512 MB of X (test switch "predict_chunk_rows")
+  const uint64_t chunk = g_opt_predict_chunk > 0 ? (uint64_t)g_opt_predict_chunk
+                                                 : std::max<uint64_t>(4096, (512ull << 20) / ((uint64_t)p * 8));
+  if (n <= 2 * chunk) {
+    Scratch sc(s);
+    double *dX, *dy;
+    CK(sc.alloc(&dX, n * p), "alloc");
+    CK(sc.alloc(&dy, n), "alloc");
+    CK(cudaMemcpyAsync(dX, X, n * p * 8, cudaMemcpyHostToDevice, s), "h2d");
+    return predict_core(f, dX, n, p, dy, mode, s, yhat);
+  }
+  // Large batches: chunks alternate between two streams, each doing H2D -> finiteness check ->
+  // walk of its chunk in order, so the copy of one chunk overlaps the walk of the other (with
+  // pinned X the H2D hides behind the kernels).  The predictions of all chunks stay on the device
+  // and come back in one copy at the end (a D2H into pageable memory per chunk would block the
+  // host and serialise the pipeline).
+  cudaStream_t st[2] = {s, host_stream(f->device, 1)};
+  Scratch sc0(st[0]), sc1(st[1]);
+  Scratch* sc[2] = {&sc0, &sc1};
+  double *dX[2], *dy;
+  int* err[2];
+  CK(sc0.alloc(&dy, n), "alloc");
+  for (int b = 0; b < 2; ++b) {
+    CK(sc[b]->alloc(&dX[b], chunk * p), "alloc");
+    CK(sc[b]->alloc(&err[b], 1), "alloc");
+    CK(cudaMemsetAsync(err[b], 0, 4, st[b]), "memset");
+  }
+  int c = 0;
+  for (uint64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
+    const int b = c & 1;
+    const uint64_t cn = std::min(chunk, n - r0);
+    CK(cudaMemcpyAsync(dX[b], X + r0 * p, cn * p * 8, cudaMemcpyHostToDevice, st[b]), "h2d");
+    CK(rf::check_finite(dX[b], cn * p, err[b], st[b]), "check");
+    ProfScope ps("predict", st[b]);
+    CK(rf::predict_forest(f->nodes, f->tree_off, (int)f->ntree, dX[b], (long long)cn, (int)p, mode, dy + r0, st[b],
+                          nullptr, f->total_nodes, g_opt_predict_node16 ? nullptr : f->n8,
+                          g_opt_predict_node16 ? nullptr : f->val, f->n8_off),
+       "predict");
+  }
+  int h[2] = {0, 0};
+  CK(cudaStreamSynchronize(st[1]), "sync");  // stream 1's walks done before stream 0 copies dy
+  CK(cudaMemcpyAsync(yhat, dy, n * 8, cudaMemcpyDeviceToHost, st[0]), "d2h");
+  for (int b = 0; b < 2; ++b) CK(cudaMemcpyAsync(&h[b], err[b], 4, cudaMemcpyDeviceToHost, st[0]), "d2h");
+  CK(cudaStreamSynchronize(st[0]), "sync");
+  if (h[0] | h[1]) return fail(RF_E_NONFINITE, "non-finite value in X");
+  return RF_OK;
 }
 
 rf_status rf_make_folds_dev(const double* dy, uint64_t n, uint32_t k, uint32_t repeats, uint64_t seed,
@@ -1301,6 +1346,11 @@ rf_status rf_debug_set_option(const char* name, int64_t value) {
   }
   if (!strcmp(name, "predict_node16")) {  // batches walk the 16-byte nodes (the compact copy is ignored)
     g_opt_predict_node16 = value != 0;
+    return RF_OK;
+  }
+  if (!strcmp(name, "predict_chunk_rows")) {  // rows per chunk of the pipelined host rf_predict
+    if (value < 0) return fail(RF_E_ARG, "predict_chunk_rows must be >= 0");
+    g_opt_predict_chunk = value;
     return RF_OK;
   }
   if (!strcmp(name, "ln_cert_margin_log2")) {  // widened margin: reaches the RF_E_INEXACT path

@@ -291,3 +291,25 @@ def test_predict_blocked_layout_and_fallback(max_depth):
     imp = rfg.forest_import(e["feature"], e["left"], e["value"], e["thr_index"], e["tree_off"], e["p"], e["F"],
                             e["target"])  # an imported BFS forest takes the blocked layout too
     assert np.array_equal(rfg.predict(imp, Q).view(np.int64), ref.view(np.int64))
+
+
+def test_predict_host_pipelined_chunks():
+    """The host-pointer rf_predict streams large batches in chunks over two CUDA streams: with small
+    chunks forced (test switch), an odd number of chunks and a ragged last one give the same bits as
+    the device entry point; a non-finite value in a late chunk still fails with RF_E_NONFINITE."""
+    X, y = datagen.paper_shaped(189, "K20", "time")
+    f = rfg.fit(X, y, ntree=64, mtry=4, target=1, seed=3)
+    Q = X[np.random.default_rng(2).integers(0, 189, 23_457)] * (1 + np.random.default_rng(3).normal(0, 1e-3, (23_457, 12)))
+    want = rfg.predict(f, _cuda(Q)).cpu().numpy()
+    rfg.debug_set_option("predict_chunk_rows", 5000)
+    try:
+        got = rfg.predict(f, np.ascontiguousarray(Q))
+        assert np.array_equal(got.view(np.int64), want.view(np.int64))
+        Qb = Q.copy()
+        Qb[21_000, 3] = np.nan
+        with pytest.raises(rfg.RFError) as ex:
+            rfg.predict(f, Qb)
+        assert ex.value.code == rfg.E_NONFINITE
+    finally:
+        rfg.debug_set_option("predict_chunk_rows", 0)
+    assert np.array_equal(rfg.predict(f, np.ascontiguousarray(Q)).view(np.int64), want.view(np.int64))
