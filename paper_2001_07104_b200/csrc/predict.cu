@@ -75,8 +75,8 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
   }
 }
 
-// Shared-memory variant (p <= kSmemMaxP): a CTA stages its 128 rows feature-major in
-// shared memory (row stride 129 words: conflict-free when 32 lanes read one feature of 32
+// Shared-memory variant (p <= kSmemMaxP): a CTA stages its kSmemRows rows feature-major in
+// shared memory (row stride kSmemRows + 1 words: conflict-free when 32 lanes read one feature of 32
 // rows), so the L1 serves only the node loads (ncu of the global-memory variants: L1
 // throughput was the limiter, half of it the feature loads).  Same interleaving of trees
 // and tree-order sums.  (A/B: fp32 staging + exact fallback beat fp64 staging by 24 %, 12
@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(256) k_predict(const Node16* __restrict__ node
 #ifndef RF_PRED_SMEM_G
 #define RF_PRED_SMEM_G 12
 #endif
+// rows per CTA: 256 (with the blocked node layout 256 beat 128 by 0.9 % and 64 was 2.3x slower on C5,
+// rd2_80_ab_c5.txt; with the BFS-slot layout 128 had been best)
 #ifndef RF_PRED_ROWS
-#define RF_PRED_ROWS 128
+#define RF_PRED_ROWS 256
 #endif
 constexpr int kSmemRows = RF_PRED_ROWS, kSmemMaxP = 192, kGs = RF_PRED_SMEM_G;
 
